@@ -1,0 +1,252 @@
+/*
+ * moe_b200.h — C-ABI of the B200-native MoE-layer data path (drop-in boundary).
+ *
+ * The reference (MoEless, /root/reference) has no FFI: its boundary is the
+ * value-semantic C++ API in proj/include/moeless/.  This header is the thin
+ * C layer that API's callers reach the GPU through.  Every
+ * entry point names the reference interface it replaces or serves:
+ *
+ *   moe_layer_forward / moe_layer_forward_host
+ *       replaces LayerMetrics layer_forward_time(plan, placement, actual,
+ *       cluster, model)            proj/include/moeless/cost_model.hpp:24-26
+ *       (the analytic alpha*max_share + 2*beta*max_gpu + t_misc becomes a real
+ *       gate -> dispatch -> SwiGLU FFN -> combine on tcgen05 tensor cores).
+ *   moe_gate_topk
+ *       replaces LoadVector route_tokens(...)   proj/include/moeless/workload.hpp:90-92
+ *   moe_predict_loads
+ *       serves LoadVector predict(...)          proj/include/moeless/predictor.hpp:40-43
+ *       (a real gate-shaped predictor kernel)
+ *   moe_set_placement
+ *       consumes ScalingPlan.replica_counts     proj/include/moeless/types.hpp:59
+ *       and Placement.gpu_for                   proj/include/moeless/placer.hpp:17
+ *   moe_plan_scale / moe_plan_place / moe_registry_*
+ *       scale_experts                           proj/include/moeless/scaler.hpp:29-30
+ *       place_experts / update_registry         proj/include/moeless/placer.hpp:74-80
+ *       (host C++; exported so non-C++ callers and the tests reach them too)
+ *
+ * Conventions
+ *   - bf16 tensors are passed as uint16_t bit patterns, row-major.
+ *   - Weights use the nn.Linear layout: W1, W3 [d_ff, d_model], W2 [d_model,
+ *     d_ff], Wg [E, d_model].  FFN_e(x) = W2 (silu(W1 x) * (W3 x)).
+ *   - Status codes: MOE_OK; MOE_EINVAL -> the C++ shim rethrows
+ *     std::invalid_argument; MOE_EINFEASIBLE -> std::runtime_error (message
+ *     keeps the reference wording, e.g. "no GPU has memory for replica (e,r)
+ *     of layer l"); MOE_ECUDA / MOE_ENCCL -> std::runtime_error with the API
+ *     error string.  No exception crosses this boundary; moe_last_error()
+ *     returns the thread-local message of the last failure.
+ *   - A context is single-threaded (one per host thread, mirroring
+ *     run_comparison's one-run-per-thread model, simulator.cpp:303-307) and
+ *     bound to one device = one rank.  Multi-GPU runs use one process per GPU;
+ *     the ranks share an NCCL unique id passed in moe_ctx_desc.
+ *   - Device-pointer entry points take a cudaStream_t as void*; NULL means the
+ *     context's own stream.  There is no CPU fallback: without a usable sm_100
+ *     device moe_ctx_create fails with MOE_ECUDA.
+ */
+#ifndef MOE_B200_H_
+#define MOE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MOE_OK = 0,
+  MOE_EINVAL = 1,
+  MOE_EINFEASIBLE = 2,
+  MOE_ECUDA = 3,
+  MOE_ENCCL = 4,
+  MOE_ESTATE = 5
+};
+
+/* exchange modes for world_size > 1 */
+enum { MOE_EXCHANGE_NCCL = 0, MOE_EXCHANGE_EXTERNAL = 1 };
+
+/* planning modes for moe_layer_forward */
+enum {
+  MOE_PLAN_FIXED = 0, /* use the placement last given to moe_set_placement            */
+  MOE_PLAN_SYNC = 1   /* scale_experts + place_experts on this layer's actual counts
+                         (oracle predictor, distance 0) inside the forward           */
+};
+
+typedef struct moe_ctx moe_ctx;
+
+typedef struct {
+  int num_layers;
+  int num_experts;      /* E  */
+  int top_k;            /* k  */
+  int d_model;          /* multiple of 256 */
+  int d_ff;             /* multiple of 128 */
+  int max_tokens;       /* per-rank token capacity of one forward */
+  int world_size;       /* G (1 = single GPU) */
+  int rank;
+  int device;           /* CUDA ordinal */
+  int exchange_mode;    /* MOE_EXCHANGE_* (ignored when world_size == 1) */
+  const void* nccl_unique_id; /* 128 bytes, same on every rank; NULL if G == 1 or external */
+  int num_predictor_targets;  /* n target layers the fused predictor scores (0 = off) */
+  /* planner knobs used by MOE_PLAN_SYNC (ModelSpec / ScalerConfig / ClusterSpec) */
+  double expert_mem_mb;
+  double layer_mem_cap_mb;
+  double gpu_mem_capacity_mb;
+  double cv_threshold;
+  int keep_alive_iters;
+  int reserved[7];
+} moe_ctx_desc;
+
+typedef struct {
+  /* LayerMetrics-compatible fields (types.hpp:73-80), measured */
+  double compute_ms;   /* grouped GEMMs (K4) */
+  double comm_ms;      /* one direction of the expert all-to-all (mean of both) */
+  double forward_ms;   /* gate -> combine, device time */
+  int replica_count;
+  double mem_mb;
+  /* per-phase device times, ms */
+  double gate_ms, plan_ms, dispatch_ms, a2a_dispatch_ms, gemm1_ms, gemm2_ms, a2a_combine_ms,
+      combine_ms;
+  int64_t rows_local;  /* rows this rank's GEMMs processed */
+  int64_t rows_sent;
+  int warm_count, cold_count;
+  int32_t counts[256];          /* this rank's gate histogram (E <= 256) */
+} moe_layer_stats;
+
+const char* moe_last_error(void);
+const char* moe_version(void);
+
+/* ---------------------------------------------------------------- context */
+int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out);
+int moe_ctx_destroy(moe_ctx* ctx);
+int moe_ctx_stream(moe_ctx* ctx, void** stream_out);
+int moe_ctx_sync(moe_ctx* ctx);
+
+/* ---------------------------------------------------------------- weights */
+/* Host (pinned or pageable) bf16 arrays; copied into the ctx-owned pool.  */
+int moe_load_expert_weights(moe_ctx* ctx, int layer, int expert, const uint16_t* w1,
+                            const uint16_t* w3, const uint16_t* w2);
+int moe_set_gate_weights(moe_ctx* ctx, int layer, const uint16_t* wg);
+/* predictor weights for target `slot` (< num_predictor_targets), scored from
+   layer `layer`'s hidden states: [E, d_model] */
+int moe_set_predictor_weights(moe_ctx* ctx, int layer, int slot, const uint16_t* wp);
+
+/* ------------------------------------------------------------- placement */
+/* replica_counts[E] >= 1; replica_gpu[sum R] flattened (expert, ordinal).   */
+int moe_set_placement(moe_ctx* ctx, int layer, const int32_t* replica_counts,
+                      const int32_t* replica_gpu);
+
+/* ---------------------------------------------------------- device kernels */
+/* K1 (+K2): x_dev [T, d] -> ids [T, k], weights [T, k], counts [E] (zeroed
+   internally).  pred_counts [n_pred, E] may be NULL. */
+int moe_gate_topk(moe_ctx* ctx, int layer, const uint16_t* x_dev, int tokens, int32_t* ids_dev,
+                  float* weights_dev, int32_t* counts_dev, int32_t* pred_counts_dev, void* stream);
+
+/* K2 alone: per-target histograms of the predictor gates on x_dev. */
+int moe_predict_loads(moe_ctx* ctx, int layer, const uint16_t* x_dev, int tokens,
+                      int32_t* pred_counts_dev, void* stream);
+
+/* Full layer: y_dev [T, d] = sum_j w_tj FFN_{e_tj}(x_t).  stats may be NULL. */
+int moe_layer_forward(moe_ctx* ctx, int layer, const uint16_t* x_dev, int tokens, uint16_t* y_dev,
+                      int plan_mode, long iteration, moe_layer_stats* stats, void* stream);
+
+/* Same with HOST buffers: H2D of x and D2H of y happen inside (the e2e path). */
+int moe_layer_forward_host(moe_ctx* ctx, int layer, const uint16_t* x_host, int tokens,
+                           uint16_t* y_host, int plan_mode, long iteration,
+                           moe_layer_stats* stats);
+
+/* Staged forward for MOE_EXCHANGE_EXTERNAL (tests / custom transports):
+   begin = gate + plan + dispatch; expert = both GEMMs over the received rows;
+   end = combine.  Between the stages the caller moves rows between ranks
+   using the buffers and chunk tables below. */
+int moe_forward_begin(moe_ctx* ctx, int layer, const uint16_t* x_dev, int tokens,
+                      const int32_t* counts_all /* [G][E] host, NULL => local only */,
+                      void* stream);
+int moe_forward_expert(moe_ctx* ctx, int layer, void* stream);
+int moe_forward_end(moe_ctx* ctx, uint16_t* y_dev, void* stream);
+/* Device buffers of the staged forward: which = 0 recv/permuted X, 1 send X,
+   2 expert output Y (recv layout), 3 return buffer (send layout), 4 ids,
+   5 weights, 6 row codes, 7 counts.  rows_out = valid rows. */
+int moe_buffer(moe_ctx* ctx, int which, void** ptr_out, int64_t* rows_out);
+/* cudaMemcpyDefault-style copy between any host/device pointers (UVA), on the
+   ctx stream, synchronous on return — the transport hook of the staged API. */
+int moe_memcpy(moe_ctx* ctx, void* dst, const void* src, size_t bytes);
+
+/* ------------------------------------------------ exchange plan (host C++) */
+/* The integer replica split and the row exchange it implies, computed from
+   every rank's gate histogram counts_all[G][E].  Chunks: {peer, replica,
+   row_offset, rows}: sends are offsets into this rank's send buffer, recvs are
+   offsets into its received-rows buffer.  Returns counts through *_n; arrays
+   must hold sum R entries per peer (max_chunks total). */
+typedef struct {
+  int32_t peer;
+  int32_t replica;
+  int64_t row_offset;
+  int64_t rows;
+} moe_chunk;
+
+int moe_exchange_plan(int world_size, int rank, int num_experts, const int32_t* counts_all,
+                      const int32_t* replica_counts, const int32_t* replica_gpu,
+                      moe_chunk* sends, int* n_sends, moe_chunk* recvs, int* n_recvs,
+                      int max_chunks, int64_t* rows_local, int64_t* rows_send,
+                      int64_t* seg_start /* [sum R], -1 if not local */,
+                      int64_t* seg_rows /* [sum R] */);
+
+/* ------------------------------------------------------- planner (host C++) */
+/* scale_experts (scaler.hpp:29-30): counts_out[E]; trace arrays may be NULL. */
+int moe_plan_scale(const int64_t* loads, int num_experts, int layer, double expert_mem_mb,
+                   double layer_mem_cap_mb, double cv_threshold, int exclude_zero,
+                   int32_t* counts_out, double* alloc_mem_out, int* steps_out,
+                   int32_t* split_trace, double* cv_trace, int trace_cap);
+
+typedef struct moe_registry moe_registry;
+int moe_registry_create(int keep_alive_iters, moe_registry** out);
+int moe_registry_destroy(moe_registry* reg);
+int64_t moe_registry_size(const moe_registry* reg);
+
+/* place_experts (placer.hpp:74-76) on a plan whose shares are plan_loads[e] /
+   counts[e]; gpu_out[sum R] flattened (expert, ordinal). */
+int moe_plan_place(moe_registry* reg, const int64_t* plan_loads, const int32_t* counts,
+                   int num_experts, int layer, double expert_mem_mb, int gpus,
+                   double gpu_mem_capacity_mb, long iteration, int load_includes_compute,
+                   double alpha_ms_per_token, double beta_ms_per_token, int32_t* gpu_out,
+                   int* warm_out, int* cold_out);
+/* update_registry (placer.hpp:80) */
+int moe_registry_update(moe_registry* reg, const int32_t* counts, const int32_t* gpu_flat,
+                        int num_experts, int gpus, int layer, long iteration);
+
+/* layer_forward_time (cost_model.hpp:24-26), the analytic model, for
+   calibration: out6 = compute, comm, forward, replicas, mem, cost */
+int moe_model_forward_time(const int64_t* plan_loads, const int32_t* counts,
+                           const int32_t* gpu_flat, const int64_t* actual, int num_experts,
+                           int gpus, double alpha, double beta, double t_misc, double m_misc,
+                           double expert_mem_mb, double* out6);
+
+/* predict (predictor.hpp:40-43): kind 0 oracle, 1 noisy, 2 historical. */
+int moe_plan_predict(int kind, const int64_t* actual, int num_experts, int layer,
+                     const int64_t* history, int history_len, const double* accuracy,
+                     int num_layers, int distance, double decay, int window, long iteration,
+                     uint64_t seed, const double* popularity, int64_t* out, int* fallback);
+double moe_measure_accuracy(const int64_t* predicted, const int64_t* actual, int num_experts);
+double moe_percentile(const double* values, int n, double q);
+
+/* route_tokens (workload.hpp:90-92) and the popularity profile behind it */
+int moe_route_tokens(int64_t tokens, int layer, long iteration, int num_experts, int num_layers,
+                     double zipf_s, uint64_t seed, int top_k, int drift_period,
+                     int64_t* loads_out);
+int moe_popularity(int num_experts, int num_layers, double zipf_s, uint64_t seed, int layer,
+                   long iteration, int drift_period, int32_t* perm_out, double* weights_out);
+
+/* --------------------------------------------------- synthetic inputs (host) */
+/* Deterministic Zipf-skewed gate inputs on an exactly representable grid
+   (DESIGN.md §Synthetic inputs), so ids/counts are bit-exact CPU vs GPU. */
+uint64_t moe_stream_key(uint64_t seed, uint64_t a, uint64_t b, uint64_t tag);
+int moe_synth_tokens(uint64_t key, int64_t first_token, int64_t tokens, int d_model,
+                     int num_experts, uint16_t* x_out);
+int moe_synth_gate(uint64_t key, int d_model, int num_experts, const double* popularity,
+                   const int32_t* noise_perm, uint16_t* wg_out);
+int moe_synth_expert(uint64_t key, int d_model, int d_ff, uint16_t* w1, uint16_t* w3,
+                     uint16_t* w2);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_B200_H_ */

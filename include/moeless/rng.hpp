@@ -1,0 +1,4 @@
+// Forwarding header: the reference include path "moeless/rng.hpp" resolves to
+// the consolidated B200-build API declaration.
+#pragma once
+#include "moeless/api.hpp"

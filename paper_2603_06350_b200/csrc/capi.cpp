@@ -1,0 +1,979 @@
+// capi.cpp — the C-ABI drop-in boundary (include/moe_b200.h).
+//
+// Owns one device's share of the MoE layer: weights pool, workspace, TMA
+// descriptors, streams and (for G > 1) the NCCL communicator, and sequences a
+// layer forward:
+//
+//   K1 gate+topk+hist (+K2 predictor)      gate.cu
+//   [counts all-gather, NCCL]              G > 1
+//   host: plan (scale/place if MOE_PLAN_SYNC) + exchange plan, one H2D upload
+//   block prefix + K3 dispatch             dispatch.cu
+//   [row all-to-all, NCCL grouped p2p]     G > 1
+//   K4 GEMM1 (SwiGLU) + GEMM2              ffn_gemm.cu  (tcgen05/TMEM/TMA)
+//   [row all-to-all back]                  G > 1
+//   K5 combine                             dispatch.cu
+//
+// Replaces layer_forward_time (proj/src/cost_model.cpp:91-122) for callers
+// that want the real layer instead of the analytic model.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "host/exchange_plan.h"
+#include "kernels/dispatch_plan.h"
+#include "moe_b200.h"
+#include "moeless/api.hpp"
+
+namespace moe {
+// kernels
+int gate_num_blocks(int T);
+cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bfloat16* w_all, int E, int n_pred,
+                             int k, int32_t* ids, float* wts, int32_t* counts, int32_t* block_counts,
+                             int32_t* pred_counts, cudaStream_t stream);
+cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, const DevPlan* plan,
+                                int32_t* block_pre, cudaStream_t s);
+cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
+                            const int32_t* block_pre, const DevPlan* plan, __nv_bfloat16* xp_local,
+                            __nv_bfloat16* xp_send, uint32_t* row_code, cudaStream_t s);
+cudaError_t launch_combine(const __nv_bfloat16* y_local, const __nv_bfloat16* y_return, int T, int d, int k,
+                           const uint32_t* row_code, const float* wts, __nv_bfloat16* y, int num_sms,
+                           cudaStream_t s);
+cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
+                                const int* nseg, int n_total, int k_total, int b_rows_per_slot,
+                                __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream);
+// host
+uint64_t stream_key(uint64_t seed, uint64_t a, uint64_t b, uint64_t tag);
+void synth_tokens(uint64_t key, int64_t first, int64_t tokens, int d, int E, uint16_t* x);
+void synth_gate(uint64_t key, int d, int E, const double* pop, const int32_t* noise_perm, uint16_t* wg);
+void synth_expert(uint64_t key, int d, int ff, uint16_t* w1, uint16_t* w3, uint16_t* w2);
+}  // namespace moe
+
+using namespace moe;
+
+// ====================================================================== errors
+namespace {
+thread_local std::string g_last_error;
+
+struct Status : std::runtime_error {
+  int code;
+  Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CU_CHECK(expr)                                                                      \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess)                                                                  \
+      throw Status(MOE_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));          \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MOE_OK;
+  } catch (const Status& s) {
+    g_last_error = s.what();
+    return s.code;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return MOE_EINVAL;
+  } catch (const std::runtime_error& e) {
+    g_last_error = e.what();
+    return MOE_EINFEASIBLE;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return MOE_ESTATE;
+  }
+}
+
+void require(bool ok, const std::string& msg) {
+  if (!ok) throw std::invalid_argument(msg);
+}
+
+// ======================================================================= NCCL
+// Loaded lazily with dlopen so single-GPU use never depends on libnccl.
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+  void load() {
+    if (h) return;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) throw Status(MOE_ENCCL, "cannot dlopen libnccl.so.2");
+    auto sym = [&](const char* s) {
+      void* p = dlsym(h, s);
+      if (!p) throw Status(MOE_ENCCL, std::string("libnccl lacks ") + s);
+      return p;
+    };
+    GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(sym("ncclGetUniqueId"));
+    CommInitRank = reinterpret_cast<decltype(CommInitRank)>(sym("ncclCommInitRank"));
+    CommDestroy = reinterpret_cast<decltype(CommDestroy)>(sym("ncclCommDestroy"));
+    AllGather = reinterpret_cast<decltype(AllGather)>(sym("ncclAllGather"));
+    Send = reinterpret_cast<decltype(Send)>(sym("ncclSend"));
+    Recv = reinterpret_cast<decltype(Recv)>(sym("ncclRecv"));
+    GroupStart = reinterpret_cast<decltype(GroupStart)>(sym("ncclGroupStart"));
+    GroupEnd = reinterpret_cast<decltype(GroupEnd)>(sym("ncclGroupEnd"));
+    GetErrorString = reinterpret_cast<decltype(GetErrorString)>(sym("ncclGetErrorString"));
+  }
+  void check(ncclResult_t r, const char* what) const {
+    if (r != ncclSuccess) throw Status(MOE_ENCCL, std::string(what) + ": " + GetErrorString(r));
+  }
+};
+NcclApi g_nccl;
+
+// ================================================================ TMA maps
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CU_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw Status(MOE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// K-major bf16 matrix [rows, cols], box = box_rows x 64 cols, 128-byte swizzle.
+CUtensorMap make_kmajor_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Status(MOE_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    release();
+    if (count) CU_CHECK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+struct Layer {
+  DevBuf<uint16_t> w13, w2, wg;  // pools
+  CUtensorMap tmB1, tmB2;
+  bool has_gate = false;
+  std::vector<char> expert_loaded;
+  std::vector<int32_t> rep_counts, rep_gpu;  // placement (host)
+  bool has_placement = false;
+};
+
+struct EventSet {
+  static constexpr int N = 10;
+  cudaEvent_t ev[N] = {};
+  void create() {
+    for (auto& e : ev) CU_CHECK(cudaEventCreate(&e));
+  }
+  void destroy() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  float ms(int a, int b) const {
+    float v = 0.0f;
+    cudaEventElapsedTime(&v, ev[a], ev[b]);
+    return v;
+  }
+};
+
+}  // namespace
+
+// =================================================================== context
+struct moe_ctx {
+  moe_ctx_desc desc{};
+  int E = 0, k = 0, d = 0, ff = 0, G = 1, rank = 0, Tmax = 0, n_pred = 0, num_sms = 148;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  std::vector<Layer> layers;
+  // workspace
+  DevBuf<int32_t> ids, counts, counts_all, block_counts, block_pre, pred_counts;
+  DevBuf<float> wts;
+  DevBuf<uint32_t> row_code;
+  DevBuf<uint16_t> xp, h, yp, send, ret, x_in, y_out;
+  DevBuf<DevPlan> dplan;
+  int64_t rows_cap = 0, send_cap = 0;
+  CUtensorMap tmA1, tmA2;
+  // host staging (pinned)
+  DevPlan* hplan = nullptr;
+  int32_t* h_counts = nullptr;  // [G][E]
+  HostPlan plan;
+  moeless::ReplicaRegistry registry{0};
+  EventSet events;
+  // staged-forward state
+  int cur_layer = -1, cur_T = 0;
+  const uint16_t* cur_x = nullptr;
+  std::vector<int64_t> last_counts;
+  int last_warm = 0, last_cold = 0;
+};
+
+namespace {
+
+void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, int32_t* pred_counts) {
+  require(L.has_gate, "gate weights not set for layer");
+  CU_CHECK(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * c->E, s));
+  if (pred_counts && c->n_pred) CU_CHECK(cudaMemsetAsync(pred_counts, 0, sizeof(int32_t) * c->E * c->n_pred, s));
+  CU_CHECK(launch_gate_topk(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
+                            reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, pred_counts ? c->n_pred : 0,
+                            c->k, c->ids.p, c->wts.p, c->counts.p, c->block_counts.p,
+                            pred_counts ? pred_counts : c->pred_counts.p, s));
+}
+
+// Decide the placement for this forward (host), then build + upload the plan.
+void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int32_t* counts_all_host) {
+  Layer& L = c->layers[layer];
+  std::vector<int64_t> all(static_cast<size_t>(c->G) * c->E);
+  for (size_t i = 0; i < all.size(); ++i) all[i] = counts_all_host[i];
+  std::vector<int64_t> total(c->E, 0);
+  for (int s = 0; s < c->G; ++s)
+    for (int e = 0; e < c->E; ++e) total[e] += all[static_cast<size_t>(s) * c->E + e];
+  c->last_counts = total;
+  if (plan_mode == MOE_PLAN_SYNC) {
+    // synchronous MoEless planning on the actual loads (oracle predictor, d = 0):
+    // scale_experts (Alg. 1) -> place_experts (Alg. 2) -> keep-alive registry
+    moeless::ModelSpec ms;
+    ms.num_layers = std::max(1, c->desc.num_layers);
+    ms.experts_per_layer = c->E;
+    ms.top_k = c->k;
+    ms.expert_mem_mb = c->desc.expert_mem_mb > 0 ? c->desc.expert_mem_mb : 3.0 * c->d * c->ff * 2 / 1e6;
+    ms.layer_mem_cap_mb = c->desc.layer_mem_cap_mb;
+    moeless::ScalerConfig sc;
+    sc.cv_threshold = c->desc.cv_threshold;
+    moeless::LoadVector lv{layer, total};
+    auto sp = moeless::scale_experts(lv, ms, sc);
+    moeless::ClusterSpec cl;
+    cl.gpu_count = c->G;
+    cl.gpu_mem_capacity_mb = c->desc.gpu_mem_capacity_mb > 0 ? c->desc.gpu_mem_capacity_mb : 180000.0;
+    auto pr = moeless::place_experts(sp, cl, c->registry, iteration);
+    moeless::update_registry(c->registry, pr.placement, iteration);
+    c->last_warm = pr.warm_count;
+    c->last_cold = pr.cold_count;
+    L.rep_counts.assign(sp.replica_counts.begin(), sp.replica_counts.end());
+    L.rep_gpu.clear();
+    for (auto& v : pr.placement.gpu_for) L.rep_gpu.insert(L.rep_gpu.end(), v.begin(), v.end());
+    L.has_placement = true;
+  } else if (!L.has_placement) {
+    // default: one replica per expert, expert e on GPU e mod G (static_plan, baselines.cpp:32-60)
+    L.rep_counts.assign(c->E, 1);
+    L.rep_gpu.resize(c->E);
+    for (int e = 0; e < c->E; ++e) L.rep_gpu[e] = e % c->G;
+    L.has_placement = true;
+  }
+  build_exchange_plan(c->G, c->rank, c->E, all.data(), L.rep_counts.data(), L.rep_gpu.data(), c->plan);
+  if (c->plan.rows_local > c->rows_cap || c->plan.rows_send > c->send_cap)
+    throw Status(MOE_EINFEASIBLE, "received rows exceed workspace capacity");
+  *c->hplan = c->plan.dev;
+}
+
+void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s) {
+  CU_CHECK(cudaMemcpyAsync(c->dplan.p, c->hplan, sizeof(DevPlan), cudaMemcpyHostToDevice, s));
+  const int nblk = gate_num_blocks(T);
+  CU_CHECK(launch_block_prefix(c->block_counts.p, nblk, c->E, c->dplan.p, c->block_pre.p, s));
+  CU_CHECK(launch_dispatch(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d, c->E, c->k, c->ids.p, c->block_pre.p,
+                           c->dplan.p, reinterpret_cast<__nv_bfloat16*>(c->xp.p),
+                           reinterpret_cast<__nv_bfloat16*>(c->send.p), c->row_code.p, s));
+}
+
+// NCCL grouped p2p for one direction.  forward: my send buffer -> peers'
+// received-rows buffers; backward: my Y rows -> peers' return buffers.
+void stage_exchange(moe_ctx* c, bool forward, cudaStream_t s) {
+  if (c->G == 1 || c->desc.exchange_mode != MOE_EXCHANGE_NCCL) return;
+  const size_t row_bytes = static_cast<size_t>(c->d) * 2;
+  g_nccl.check(g_nccl.GroupStart(), "ncclGroupStart");
+  if (forward) {
+    for (const Chunk& ch : c->plan.sends)
+      g_nccl.check(g_nccl.Send(c->send.p + ch.row_offset * c->d, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
+                   "ncclSend");
+    for (const Chunk& ch : c->plan.recvs)
+      g_nccl.check(g_nccl.Recv(c->xp.p + ch.row_offset * c->d, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
+                   "ncclRecv");
+  } else {
+    for (const Chunk& ch : c->plan.recvs)
+      g_nccl.check(g_nccl.Send(c->yp.p + ch.row_offset * c->d, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
+                   "ncclSend");
+    for (const Chunk& ch : c->plan.sends)
+      g_nccl.check(g_nccl.Recv(c->ret.p + ch.row_offset * c->d, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
+                   "ncclRecv");
+  }
+  g_nccl.check(g_nccl.GroupEnd(), "ncclGroupEnd");
+}
+
+void stage_expert(moe_ctx* c, int layer, cudaStream_t s) {
+  Layer& L = c->layers[layer];
+  const int grid = c->num_sms;
+  CU_CHECK(launch_grouped_gemm(0, &c->tmA1, &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d, 2 * c->ff,
+                               reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, grid, s));
+  CU_CHECK(launch_grouped_gemm(1, &c->tmA2, &L.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
+                               reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, grid, s));
+}
+
+void stage_combine(moe_ctx* c, uint16_t* y, int T, cudaStream_t s) {
+  CU_CHECK(launch_combine(reinterpret_cast<const __nv_bfloat16*>(c->yp.p),
+                          reinterpret_cast<const __nv_bfloat16*>(c->ret.p), T, c->d, c->k, c->row_code.p, c->wts.p,
+                          reinterpret_cast<__nv_bfloat16*>(y), c->num_sms, s));
+}
+
+cudaStream_t pick(moe_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->stream; }
+
+Layer& layer_at(moe_ctx* c, int layer) {
+  require(c != nullptr, "null context");
+  require(layer >= 0 && layer < static_cast<int>(c->layers.size()), "layer out of range");
+  return c->layers[layer];
+}
+
+void ensure_pools(moe_ctx* c, Layer& L) {
+  if (L.w13.p) return;
+  L.w13.alloc(static_cast<size_t>(c->E) * 2 * c->ff * c->d);
+  L.w2.alloc(static_cast<size_t>(c->E) * c->d * c->ff);
+  L.tmB1 = make_kmajor_map(L.w13.p, static_cast<uint64_t>(c->E) * 2 * c->ff, c->d, 256);
+  L.tmB2 = make_kmajor_map(L.w2.p, static_cast<uint64_t>(c->E) * c->d, c->ff, 256);
+  L.expert_loaded.assign(c->E, 0);
+}
+
+void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y, int plan_mode, long iteration,
+                    moe_layer_stats* st, cudaStream_t s) {
+  Layer& L = layer_at(c, layer);
+  require(T >= 0 && T <= c->Tmax, "token count exceeds max_tokens");
+  require(plan_mode == MOE_PLAN_FIXED || plan_mode == MOE_PLAN_SYNC, "unknown plan mode");
+  for (int e = 0; e < c->E; ++e)
+    if (!L.w13.p || !L.expert_loaded[e]) throw std::invalid_argument("expert weights not loaded for layer");
+  EventSet& ev = c->events;
+  const bool timed = st != nullptr;
+  auto mark = [&](int i) {
+    if (timed) CU_CHECK(cudaEventRecord(ev.ev[i], s));
+  };
+  mark(0);
+  stage_gate(c, L, x, T, s, nullptr);
+  if (c->G > 1) {
+    require(c->desc.exchange_mode == MOE_EXCHANGE_NCCL, "staged API required for external exchange");
+    g_nccl.check(g_nccl.AllGather(c->counts.p, c->counts_all.p, c->E, ncclInt32, c->comm, s), "ncclAllGather");
+    CU_CHECK(cudaMemcpyAsync(c->h_counts, c->counts_all.p, sizeof(int32_t) * c->G * c->E, cudaMemcpyDeviceToHost, s));
+  } else {
+    CU_CHECK(cudaMemcpyAsync(c->h_counts, c->counts.p, sizeof(int32_t) * c->E, cudaMemcpyDeviceToHost, s));
+  }
+  mark(1);
+  CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram
+  stage_plan(c, layer, plan_mode, iteration, c->h_counts);
+  mark(2);
+  stage_dispatch(c, x, T, s);
+  mark(3);
+  stage_exchange(c, true, s);
+  mark(4);
+  const int nseg = c->plan.dev.nseg;
+  (void)nseg;
+  Layer& LL = c->layers[layer];
+  CU_CHECK(launch_grouped_gemm(0, &c->tmA1, &LL.tmB1, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d, 2 * c->ff,
+                               reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, c->num_sms, s));
+  mark(5);
+  CU_CHECK(launch_grouped_gemm(1, &c->tmA2, &LL.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
+                               reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s));
+  mark(6);
+  stage_exchange(c, false, s);
+  mark(7);
+  stage_combine(c, y, T, s);
+  mark(8);
+  if (timed) {
+    CU_CHECK(cudaEventSynchronize(ev.ev[8]));
+    st->gate_ms = ev.ms(0, 1);
+    st->plan_ms = ev.ms(1, 2);
+    st->dispatch_ms = ev.ms(2, 3);
+    st->a2a_dispatch_ms = ev.ms(3, 4);
+    st->gemm1_ms = ev.ms(4, 5);
+    st->gemm2_ms = ev.ms(5, 6);
+    st->a2a_combine_ms = ev.ms(6, 7);
+    st->combine_ms = ev.ms(7, 8);
+    st->forward_ms = ev.ms(0, 8);
+    st->compute_ms = st->gemm1_ms + st->gemm2_ms;
+    st->comm_ms = 0.5 * (st->a2a_dispatch_ms + st->a2a_combine_ms);
+    st->replica_count = static_cast<int>(L.rep_gpu.size());
+    st->mem_mb = st->replica_count * (3.0 * c->d * c->ff * 2 / 1e6);
+    st->rows_local = c->plan.rows_local;
+    st->rows_sent = c->plan.rows_send;
+    st->warm_count = c->last_warm;
+    st->cold_count = c->last_cold;
+    for (int e = 0; e < c->E && e < 256; ++e) st->counts[e] = c->h_counts[static_cast<size_t>(c->rank) * c->E + e];
+  }
+}
+
+}  // namespace
+
+// ==================================================================== C ABI
+extern "C" {
+
+const char* moe_last_error(void) { return g_last_error.c_str(); }
+const char* moe_version(void) { return "moe_b200 0.1.0 (sm_100a)"; }
+
+int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
+  return guarded([&] {
+    require(desc && out, "null argument");
+    const moe_ctx_desc& D = *desc;
+    require(D.num_layers >= 1, "num_layers must be >= 1");
+    require(D.num_experts >= 1 && D.num_experts <= kMaxExperts, "num_experts out of range");
+    require(D.top_k >= 1 && D.top_k <= D.num_experts && D.top_k <= 8 && (D.top_k <= 2 || D.top_k % 2 == 0),
+            "top_k must be in {1,2,4,6,8} and <= num_experts");
+    require(D.d_model % 256 == 0 && D.d_model > 0, "d_model must be a positive multiple of 256");
+    require(D.d_ff % 128 == 0 && D.d_ff > 0, "d_ff must be a positive multiple of 128");
+    require(D.max_tokens >= 1, "max_tokens must be >= 1");
+    require(D.world_size >= 1 && D.rank >= 0 && D.rank < D.world_size, "bad world_size / rank");
+    require(D.num_experts * (1 + std::max(0, D.num_predictor_targets)) <= 256, "too many predictor targets");
+    int ndev = 0;
+    CU_CHECK(cudaGetDeviceCount(&ndev));
+    require(D.device >= 0 && D.device < ndev, "device ordinal out of range");
+    CU_CHECK(cudaSetDevice(D.device));
+    cudaDeviceProp prop;
+    CU_CHECK(cudaGetDeviceProperties(&prop, D.device));
+    if (prop.major != 10) throw Status(MOE_ECUDA, "moe_b200 requires an sm_100 (Blackwell) device");
+    auto c = std::make_unique<moe_ctx>();
+    c->desc = D;
+    c->E = D.num_experts;
+    c->k = D.top_k;
+    c->d = D.d_model;
+    c->ff = D.d_ff;
+    c->G = D.world_size;
+    c->rank = D.rank;
+    c->Tmax = D.max_tokens;
+    c->n_pred = std::max(0, D.num_predictor_targets);
+    c->num_sms = prop.multiProcessorCount;
+    c->registry = moeless::ReplicaRegistry(std::max(0, D.keep_alive_iters));
+    c->layers.resize(D.num_layers);
+    CU_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    const int64_t assign = static_cast<int64_t>(c->Tmax) * c->k;
+    c->rows_cap = assign * c->G;  // worst case: every rank routes everything here
+    c->send_cap = c->G > 1 ? assign : 1;
+    const int nblk = gate_num_blocks(c->Tmax);
+    c->ids.alloc(assign);
+    c->wts.alloc(assign);
+    c->row_code.alloc(assign);
+    c->counts.alloc(c->E);
+    c->counts_all.alloc(static_cast<size_t>(c->E) * c->G);
+    c->pred_counts.alloc(static_cast<size_t>(c->E) * std::max(1, c->n_pred));
+    c->block_counts.alloc(static_cast<size_t>(nblk) * c->E);
+    c->block_pre.alloc(static_cast<size_t>(nblk) * c->E);
+    c->xp.alloc(static_cast<size_t>(c->rows_cap) * c->d);
+    c->h.alloc(static_cast<size_t>(c->rows_cap) * c->ff);
+    c->yp.alloc(static_cast<size_t>(c->rows_cap) * c->d);
+    c->send.alloc(static_cast<size_t>(c->send_cap) * c->d);
+    c->ret.alloc(static_cast<size_t>(c->send_cap) * c->d);
+    c->dplan.alloc(1);
+    c->tmA1 = make_kmajor_map(c->xp.p, c->rows_cap, c->d, 128);
+    c->tmA2 = make_kmajor_map(c->h.p, c->rows_cap, c->ff, 128);
+    CU_CHECK(cudaMallocHost(&c->hplan, sizeof(DevPlan)));
+    CU_CHECK(cudaMallocHost(&c->h_counts, sizeof(int32_t) * c->E * c->G));
+    c->events.create();
+    if (c->G > 1 && D.exchange_mode == MOE_EXCHANGE_NCCL) {
+      require(D.nccl_unique_id != nullptr, "nccl_unique_id required for world_size > 1");
+      g_nccl.load();
+      ncclUniqueId id;
+      std::memcpy(&id, D.nccl_unique_id, sizeof(id));
+      g_nccl.check(g_nccl.CommInitRank(&c->comm, c->G, id, c->rank), "ncclCommInitRank");
+    }
+    *out = c.release();
+  });
+}
+
+int moe_ctx_destroy(moe_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->desc.device);
+    cudaStreamSynchronize(c->stream);
+    if (c->comm) g_nccl.CommDestroy(c->comm);
+    c->events.destroy();
+    if (c->hplan) cudaFreeHost(c->hplan);
+    if (c->h_counts) cudaFreeHost(c->h_counts);
+    cudaStreamDestroy(c->stream);
+    delete c;
+  });
+}
+
+int moe_ctx_stream(moe_ctx* c, void** s) {
+  return guarded([&] {
+    require(c && s, "null argument");
+    *s = c->stream;
+  });
+}
+
+int moe_ctx_sync(moe_ctx* c) {
+  return guarded([&] {
+    require(c, "null context");
+    CU_CHECK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int moe_load_expert_weights(moe_ctx* c, int layer, int expert, const uint16_t* w1, const uint16_t* w3,
+                            const uint16_t* w2) {
+  return guarded([&] {
+    Layer& L = layer_at(c, layer);
+    require(expert >= 0 && expert < c->E, "expert out of range");
+    require(w1 && w3 && w2, "null weight pointer");
+    ensure_pools(c, L);
+    // W13 pool: per 128-row block b of the expert, rows [W1[b*128..], W3[b*128..]]
+    const size_t rowb = static_cast<size_t>(c->d) * 2;
+    uint16_t* base = L.w13.p + static_cast<size_t>(expert) * 2 * c->ff * c->d;
+    for (int b = 0; b < c->ff / 128; ++b) {
+      CU_CHECK(cudaMemcpyAsync(base + static_cast<size_t>(b) * 256 * c->d, w1 + static_cast<size_t>(b) * 128 * c->d,
+                               128 * rowb, cudaMemcpyHostToDevice, c->stream));
+      CU_CHECK(cudaMemcpyAsync(base + (static_cast<size_t>(b) * 256 + 128) * c->d,
+                               w3 + static_cast<size_t>(b) * 128 * c->d, 128 * rowb, cudaMemcpyHostToDevice,
+                               c->stream));
+    }
+    CU_CHECK(cudaMemcpyAsync(L.w2.p + static_cast<size_t>(expert) * c->d * c->ff, w2,
+                             static_cast<size_t>(c->d) * c->ff * 2, cudaMemcpyHostToDevice, c->stream));
+    CU_CHECK(cudaStreamSynchronize(c->stream));
+    L.expert_loaded[expert] = 1;
+  });
+}
+
+int moe_set_gate_weights(moe_ctx* c, int layer, const uint16_t* wg) {
+  return guarded([&] {
+    Layer& L = layer_at(c, layer);
+    require(wg != nullptr, "null gate weights");
+    if (!L.wg.p) {
+      L.wg.alloc(static_cast<size_t>(c->E) * c->d * (1 + c->n_pred));
+      CU_CHECK(cudaMemset(L.wg.p, 0, L.wg.n * 2));
+    }
+    CU_CHECK(cudaMemcpy(L.wg.p, wg, static_cast<size_t>(c->E) * c->d * 2, cudaMemcpyHostToDevice));
+    L.has_gate = true;
+  });
+}
+
+int moe_set_predictor_weights(moe_ctx* c, int layer, int slot, const uint16_t* wp) {
+  return guarded([&] {
+    Layer& L = layer_at(c, layer);
+    require(slot >= 0 && slot < c->n_pred, "predictor slot out of range");
+    require(wp != nullptr, "null predictor weights");
+    if (!L.wg.p) {
+      L.wg.alloc(static_cast<size_t>(c->E) * c->d * (1 + c->n_pred));
+      CU_CHECK(cudaMemset(L.wg.p, 0, L.wg.n * 2));
+    }
+    CU_CHECK(cudaMemcpy(L.wg.p + static_cast<size_t>(1 + slot) * c->E * c->d, wp, static_cast<size_t>(c->E) * c->d * 2,
+                        cudaMemcpyHostToDevice));
+  });
+}
+
+int moe_set_placement(moe_ctx* c, int layer, const int32_t* rc, const int32_t* rg) {
+  return guarded([&] {
+    Layer& L = layer_at(c, layer);
+    require(rc && rg, "null placement");
+    int total = 0;
+    for (int e = 0; e < c->E; ++e) {
+      require(rc[e] >= 1, "expert " + std::to_string(e) + " has no replica");
+      total += rc[e];
+    }
+    require(total <= kMaxReplicas, "too many replicas in one layer");
+    for (int i = 0; i < total; ++i)
+      require(rg[i] >= 0 && rg[i] < c->G,
+              "replica placed on invalid GPU " + std::to_string(rg[i]));
+    L.rep_counts.assign(rc, rc + c->E);
+    L.rep_gpu.assign(rg, rg + total);
+    L.has_placement = true;
+  });
+}
+
+int moe_gate_topk(moe_ctx* c, int layer, const uint16_t* x, int T, int32_t* ids, float* w, int32_t* counts,
+                  int32_t* pred_counts, void* stream) {
+  return guarded([&] {
+    Layer& L = layer_at(c, layer);
+    require(T >= 0 && T <= c->Tmax, "token count exceeds max_tokens");
+    require(x && ids && w && counts, "null buffer");
+    cudaStream_t s = pick(c, stream);
+    require(L.has_gate, "gate weights not set for layer");
+    CU_CHECK(cudaMemsetAsync(counts, 0, sizeof(int32_t) * c->E, s));
+    if (pred_counts && c->n_pred) CU_CHECK(cudaMemsetAsync(pred_counts, 0, sizeof(int32_t) * c->E * c->n_pred, s));
+    CU_CHECK(launch_gate_topk(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
+                              reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, pred_counts ? c->n_pred : 0, c->k,
+                              ids, w, counts, c->block_counts.p, pred_counts ? pred_counts : c->pred_counts.p, s));
+  });
+}
+
+int moe_predict_loads(moe_ctx* c, int layer, const uint16_t* x, int T, int32_t* pred_counts, void* stream) {
+  return guarded([&] {
+    Layer& L = layer_at(c, layer);
+    require(c->n_pred > 0, "context has no predictor targets");
+    require(T >= 0 && T <= c->Tmax, "token count exceeds max_tokens");
+    require(x && pred_counts, "null buffer");
+    cudaStream_t s = pick(c, stream);
+    require(L.has_gate, "gate weights not set for layer");
+    // the gate rows ride along (they are in the same stacked matrix); their
+    // outputs go to the ctx scratch so the caller's ids are untouched
+    CU_CHECK(cudaMemsetAsync(pred_counts, 0, sizeof(int32_t) * c->E * c->n_pred, s));
+    CU_CHECK(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * c->E, s));
+    CU_CHECK(launch_gate_topk(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
+                              reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, c->n_pred, c->k, c->ids.p,
+                              c->wts.p, c->counts.p, c->block_counts.p, pred_counts, s));
+  });
+}
+
+int moe_layer_forward(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y, int plan_mode, long iteration,
+                      moe_layer_stats* stats, void* stream) {
+  return guarded([&] {
+    require(c && x && y, "null argument");
+    forward_device(c, layer, x, T, y, plan_mode, iteration, stats, pick(c, stream));
+  });
+}
+
+int moe_layer_forward_host(moe_ctx* c, int layer, const uint16_t* x_host, int T, uint16_t* y_host, int plan_mode,
+                           long iteration, moe_layer_stats* stats) {
+  return guarded([&] {
+    require(c && x_host && y_host, "null argument");
+    require(T >= 0 && T <= c->Tmax, "token count exceeds max_tokens");
+    if (!c->x_in.p) {
+      c->x_in.alloc(static_cast<size_t>(c->Tmax) * c->d);
+      c->y_out.alloc(static_cast<size_t>(c->Tmax) * c->d);
+    }
+    const size_t bytes = static_cast<size_t>(T) * c->d * 2;
+    CU_CHECK(cudaMemcpyAsync(c->x_in.p, x_host, bytes, cudaMemcpyHostToDevice, c->stream));
+    forward_device(c, layer, c->x_in.p, T, c->y_out.p, plan_mode, iteration, stats, c->stream);
+    CU_CHECK(cudaMemcpyAsync(y_host, c->y_out.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CU_CHECK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int moe_forward_begin(moe_ctx* c, int layer, const uint16_t* x, int T, const int32_t* counts_all, void* stream) {
+  return guarded([&] {
+    Layer& L = layer_at(c, layer);
+    require(x != nullptr, "null input");
+    require(T >= 0 && T <= c->Tmax, "token count exceeds max_tokens");
+    cudaStream_t s = pick(c, stream);
+    if (!counts_all) {
+      // stage 1: gate only; caller reads counts (moe_buffer 7), all-gathers, calls again
+      stage_gate(c, L, x, T, s, nullptr);
+      CU_CHECK(cudaStreamSynchronize(s));
+      c->cur_layer = layer;
+      c->cur_T = T;
+      c->cur_x = x;
+      return;
+    }
+    require(c->cur_layer == layer && c->cur_x == x && c->cur_T == T, "forward_begin stage 2 without stage 1");
+    stage_plan(c, layer, MOE_PLAN_FIXED, 0, counts_all);
+    stage_dispatch(c, x, T, s);
+    CU_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int moe_forward_expert(moe_ctx* c, int layer, void* stream) {
+  return guarded([&] {
+    layer_at(c, layer);
+    require(c->cur_layer == layer, "forward_expert without forward_begin");
+    stage_expert(c, layer, pick(c, stream));
+    CU_CHECK(cudaStreamSynchronize(pick(c, stream)));
+  });
+}
+
+int moe_forward_end(moe_ctx* c, uint16_t* y, void* stream) {
+  return guarded([&] {
+    require(c && y, "null argument");
+    require(c->cur_layer >= 0, "forward_end without forward_begin");
+    stage_combine(c, y, c->cur_T, pick(c, stream));
+    CU_CHECK(cudaStreamSynchronize(pick(c, stream)));
+    c->cur_layer = -1;
+  });
+}
+
+int moe_buffer(moe_ctx* c, int which, void** ptr, int64_t* rows) {
+  return guarded([&] {
+    require(c && ptr, "null argument");
+    int64_t r = 0;
+    switch (which) {
+      case 0: *ptr = c->xp.p; r = c->plan.rows_local; break;
+      case 1: *ptr = c->send.p; r = c->plan.rows_send; break;
+      case 2: *ptr = c->yp.p; r = c->plan.rows_local; break;
+      case 3: *ptr = c->ret.p; r = c->plan.rows_send; break;
+      case 4: *ptr = c->ids.p; r = static_cast<int64_t>(c->cur_T) * c->k; break;
+      case 5: *ptr = c->wts.p; r = static_cast<int64_t>(c->cur_T) * c->k; break;
+      case 6: *ptr = c->row_code.p; r = static_cast<int64_t>(c->cur_T) * c->k; break;
+      case 7: *ptr = c->counts.p; r = c->E; break;
+      case 8: *ptr = c->h.p; r = c->plan.rows_local; break;
+      default: throw std::invalid_argument("unknown buffer id");
+    }
+    if (rows) *rows = r;
+  });
+}
+
+int moe_memcpy(moe_ctx* c, void* dst, const void* src, size_t bytes) {
+  return guarded([&] {
+    require(c && dst && src, "null argument");
+    CU_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
+    CU_CHECK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int moe_exchange_plan(int G, int rank, int E, const int32_t* counts_all, const int32_t* rc, const int32_t* rg,
+                      moe_chunk* sends, int* n_sends, moe_chunk* recvs, int* n_recvs, int max_chunks,
+                      int64_t* rows_local, int64_t* rows_send, int64_t* seg_start, int64_t* seg_rows) {
+  return guarded([&] {
+    require(counts_all && rc && rg, "null argument");
+    std::vector<int64_t> all(static_cast<size_t>(G) * std::max(E, 0));
+    for (size_t i = 0; i < all.size(); ++i) all[i] = counts_all[i];
+    HostPlan hp;
+    build_exchange_plan(G, rank, E, all.data(), rc, rg, hp);
+    require(static_cast<int>(hp.sends.size()) <= max_chunks && static_cast<int>(hp.recvs.size()) <= max_chunks,
+            "chunk arrays too small");
+    auto copy = [](const std::vector<Chunk>& v, moe_chunk* dst) {
+      for (size_t i = 0; i < v.size(); ++i) dst[i] = moe_chunk{v[i].peer, v[i].replica, v[i].row_offset, v[i].rows};
+    };
+    if (sends) copy(hp.sends, sends);
+    if (recvs) copy(hp.recvs, recvs);
+    if (n_sends) *n_sends = static_cast<int>(hp.sends.size());
+    if (n_recvs) *n_recvs = static_cast<int>(hp.recvs.size());
+    if (rows_local) *rows_local = hp.rows_local;
+    if (rows_send) *rows_send = hp.rows_send;
+    for (int i = 0; i < hp.dev.R; ++i) {
+      if (seg_start) seg_start[i] = hp.seg_start[i];
+      if (seg_rows) seg_rows[i] = hp.rep_size[i];
+    }
+  });
+}
+
+// ------------------------------------------------------------- planner API
+int moe_plan_scale(const int64_t* loads, int E, int layer, double mem, double cap, double cv, int excl,
+                   int32_t* counts_out, double* alloc_out, int* steps_out, int32_t* split, double* cvt, int cap_n) {
+  return guarded([&] {
+    require(loads && counts_out, "null argument");
+    moeless::ModelSpec m;
+    m.experts_per_layer = E;
+    m.top_k = 1;
+    m.expert_mem_mb = mem;
+    m.layer_mem_cap_mb = cap;
+    moeless::ScalerConfig sc;
+    sc.cv_threshold = cv;
+    sc.exclude_zero_loads_from_cv = excl != 0;
+    moeless::ScaleTrace tr;
+    moeless::LoadVector lv{layer, std::vector<int64_t>(loads, loads + std::max(E, 0))};
+    auto plan = moeless::scale_experts(lv, m, sc, &tr);
+    std::copy(plan.replica_counts.begin(), plan.replica_counts.end(), counts_out);
+    if (alloc_out) *alloc_out = plan.alloc_mem_mb;
+    if (steps_out) *steps_out = static_cast<int>(tr.split_expert.size());
+    for (int i = 0; i < cap_n && i < static_cast<int>(tr.split_expert.size()); ++i) {
+      if (split) split[i] = tr.split_expert[i];
+      if (cvt) cvt[i] = tr.cv[i];
+    }
+  });
+}
+
+struct moe_registry {
+  moeless::ReplicaRegistry reg;
+};
+
+int moe_registry_create(int keep_alive, moe_registry** out) {
+  return guarded([&] {
+    require(out != nullptr, "null argument");
+    *out = new moe_registry{moeless::ReplicaRegistry(keep_alive)};
+  });
+}
+int moe_registry_destroy(moe_registry* r) {
+  delete r;
+  return MOE_OK;
+}
+int64_t moe_registry_size(const moe_registry* r) { return r ? static_cast<int64_t>(r->reg.size()) : -1; }
+
+namespace {
+moeless::ScalingPlan plan_of(const int64_t* loads, const int32_t* counts, int E, int layer, double mem) {
+  moeless::ScalingPlan p;
+  p.layer = layer;
+  p.expert_mem_mb = mem;
+  p.replica_counts.assign(counts, counts + E);
+  int extra = 0;
+  for (int e = 0; e < E; ++e) {
+    extra += counts[e] - 1;
+    for (int r = 0; r < counts[e]; ++r) p.shares.push_back({e, r, moeless::Rational(loads[e], counts[e])});
+  }
+  p.alloc_mem_mb = extra * mem;
+  return p;
+}
+moeless::Placement placement_of(const int32_t* counts, const int32_t* gpu, int E, int G, int layer, double mem) {
+  moeless::Placement p;
+  p.layer = layer;
+  p.per_gpu_mem_mb.assign(G, 0.0);
+  int i = 0;
+  for (int e = 0; e < E; ++e) {
+    p.gpu_for.emplace_back();
+    for (int r = 0; r < counts[e]; ++r, ++i) {
+      p.gpu_for.back().push_back(gpu[i]);
+      if (gpu[i] >= 0 && gpu[i] < G) p.per_gpu_mem_mb[gpu[i]] += mem;
+    }
+  }
+  return p;
+}
+}  // namespace
+
+int moe_plan_place(moe_registry* r, const int64_t* loads, const int32_t* counts, int E, int layer, double mem, int G,
+                   double cap, long it, int incl, double alpha, double beta, int32_t* gpu_out, int* warm, int* cold) {
+  return guarded([&] {
+    require(r && loads && counts && gpu_out, "null argument");
+    for (int e = 0; e < E; ++e) require(counts[e] >= 1, "replica count must be >= 1");
+    auto plan = plan_of(loads, counts, E, layer, mem);
+    moeless::ClusterSpec cl;
+    cl.gpu_count = G;
+    cl.gpu_mem_capacity_mb = cap;
+    moeless::PlacerOptions opt;
+    opt.load_includes_compute = incl != 0;
+    opt.alpha_ms_per_token = alpha;
+    opt.beta_ms_per_token = beta;
+    auto res = moeless::place_experts(plan, cl, r->reg, it, opt);
+    int i = 0;
+    for (int e = 0; e < E; ++e)
+      for (int g : res.placement.gpu_for[e]) gpu_out[i++] = g;
+    if (warm) *warm = res.warm_count;
+    if (cold) *cold = res.cold_count;
+  });
+}
+
+int moe_registry_update(moe_registry* r, const int32_t* counts, const int32_t* gpu, int E, int G, int layer, long it) {
+  return guarded([&] {
+    require(r && counts && gpu, "null argument");
+    moeless::update_registry(r->reg, placement_of(counts, gpu, E, G, layer, 1.0), it);
+  });
+}
+
+int moe_model_forward_time(const int64_t* loads, const int32_t* counts, const int32_t* gpu, const int64_t* actual,
+                           int E, int G, double alpha, double beta, double t_misc, double m_misc, double mem,
+                           double* out6) {
+  return guarded([&] {
+    require(loads && counts && gpu && actual && out6, "null argument");
+    auto plan = plan_of(loads, counts, E, 0, mem);
+    auto pl = placement_of(counts, gpu, E, G, 0, mem);
+    moeless::ClusterSpec cl;
+    cl.gpu_count = G;
+    cl.alpha_ms_per_token = alpha;
+    cl.beta_ms_per_token = beta;
+    cl.t_misc_ms = t_misc;
+    cl.m_misc_mb = m_misc;
+    moeless::ModelSpec ms;
+    ms.experts_per_layer = E;
+    ms.expert_mem_mb = mem;
+    auto m = moeless::layer_forward_time(plan, pl, moeless::LoadVector{0, std::vector<int64_t>(actual, actual + E)}, cl,
+                                         ms);
+    out6[0] = m.compute_ms;
+    out6[1] = m.comm_ms;
+    out6[2] = m.forward_ms;
+    out6[3] = m.replica_count;
+    out6[4] = m.mem_mb;
+    out6[5] = m.cost_mb_ms;
+  });
+}
+
+int moe_plan_predict(int kind, const int64_t* actual, int E, int layer, const int64_t* history, int hlen,
+                     const double* acc, int L, int distance, double decay, int window, long it, uint64_t seed,
+                     const double* pop, int64_t* out, int* fallback) {
+  return guarded([&] {
+    require(actual && out, "null argument");
+    require(kind >= 0 && kind <= 2, "unknown predictor kind");
+    moeless::PredictorProfile p;
+    p.kind = static_cast<moeless::PredictorKind>(kind);
+    p.distance = distance;
+    p.distance_decay = decay;
+    p.history_window = window;
+    if (acc) p.per_layer_accuracy.assign(acc, acc + L);
+    std::vector<moeless::LoadVector> hist;
+    for (int i = 0; i < hlen; ++i)
+      hist.push_back({layer, std::vector<int64_t>(history + static_cast<size_t>(i) * E, history + static_cast<size_t>(i + 1) * E)});
+    std::vector<double> pw;
+    if (pop) pw.assign(pop, pop + E);
+    bool fb = false;
+    auto r = moeless::predict({layer, std::vector<int64_t>(actual, actual + E)}, hist, p, it, seed, pw, &fb);
+    std::copy(r.loads.begin(), r.loads.end(), out);
+    if (fallback) *fallback = fb ? 1 : 0;
+  });
+}
+
+double moe_measure_accuracy(const int64_t* pred, const int64_t* actual, int E) {
+  double v = -1.0;
+  int rc = guarded([&] {
+    v = moeless::measure_accuracy({0, std::vector<int64_t>(pred, pred + E)}, {0, std::vector<int64_t>(actual, actual + E)});
+  });
+  return rc == MOE_OK ? v : -1.0;
+}
+
+double moe_percentile(const double* v, int n, double q) {
+  double out = -1.0;
+  int rc = guarded([&] { out = moeless::percentile(std::vector<double>(v, v + std::max(n, 0)), q); });
+  return rc == MOE_OK ? out : -1.0;
+}
+
+int moe_route_tokens(int64_t T, int layer, long it, int E, int L, double s, uint64_t seed, int k, int drift,
+                     int64_t* loads) {
+  return guarded([&] {
+    require(loads != nullptr, "null argument");
+    auto prof = moeless::make_popularity_profile(E, L, s, seed, false, drift);
+    moeless::IterationBatch b;
+    b.iteration = it;
+    b.token_count = T;
+    auto lv = moeless::route_tokens(b, layer, prof, k, E, seed);
+    std::copy(lv.loads.begin(), lv.loads.end(), loads);
+  });
+}
+
+int moe_popularity(int E, int L, double s, uint64_t seed, int layer, long it, int drift, int32_t* perm, double* w) {
+  return guarded([&] {
+    auto prof = moeless::make_popularity_profile(E, L, s, seed, false, drift);
+    auto p = moeless::effective_permutation(prof, layer, it);
+    if (perm) std::copy(p.begin(), p.end(), perm);
+    if (w) {
+      auto ww = moeless::popularity_weights(prof, layer, it, moeless::Phase::prefill);
+      std::copy(ww.begin(), ww.end(), w);
+    }
+  });
+}
+
+uint64_t moe_stream_key(uint64_t seed, uint64_t a, uint64_t b, uint64_t tag) { return stream_key(seed, a, b, tag); }
+
+int moe_synth_tokens(uint64_t key, int64_t first, int64_t T, int d, int E, uint16_t* x) {
+  return guarded([&] {
+    require(x && T >= 0 && d > E && E >= 1, "bad synth_tokens arguments");
+    synth_tokens(key, first, T, d, E, x);
+  });
+}
+
+int moe_synth_gate(uint64_t key, int d, int E, const double* pop, const int32_t* noise_perm, uint16_t* wg) {
+  return guarded([&] {
+    require(pop && noise_perm && wg && d > E, "bad synth_gate arguments");
+    synth_gate(key, d, E, pop, noise_perm, wg);
+  });
+}
+
+int moe_synth_expert(uint64_t key, int d, int ff, uint16_t* w1, uint16_t* w3, uint16_t* w2) {
+  return guarded([&] {
+    require(w1 && w3 && w2, "null argument");
+    synth_expert(key, d, ff, w1, w3, w2);
+  });
+}
+
+}  // extern "C"

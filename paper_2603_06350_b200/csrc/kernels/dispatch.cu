@@ -1,0 +1,232 @@
+// dispatch.cu — K3: replica-aware token dispatch, and K5: weighted top-k
+// combine / unpermute.
+//
+// The reference's dispatcher is the rational rule "each replica of expert e
+// carries actual[e] / R_e tokens" (proj/src/cost_model.cpp:98-106).  The real
+// dispatcher makes it integer: the n_e assignments of expert
+// e, in global (source rank, token) order, are cut into R_e contiguous ranges,
+// replica r taking floor(n_e/R_e) + [r < n_e mod R_e].  Each rank lays out
+// the rows it receives as segments in (expert, ordinal) order; within a
+// segment, rows keep the global order, so the permutation is stable and
+// bit-reproducible (no atomics decide positions).
+//
+// Pipeline (all on device, no host round trip once the plan is uploaded):
+//   block_prefix_kernel  exclusive scan of the gate's per-32-token-block
+//                        histograms -> each block's per-expert start rank.
+//   dispatch_kernel      one CTA per 32-token block: warp 0 ranks the block's
+//                        (token, slot) assignments with one ballot per expert,
+//                        maps global rank -> replica -> destination row, and
+//                        records a 32-bit row code per assignment (bit 31 =
+//                        row lives in the send buffer of another rank); then
+//                        4 warps stream each token row once from HBM and store
+//                        it k times with 128-bit vector stores.
+//   combine_kernel       y_t = sum_j w_tj * Y[row(t, j)], fp32 accumulate in
+//                        slot order, bf16 out; one warp per token.
+#include <cstdint>
+
+#include "dispatch_plan.h"
+#include "sm100_ptx.cuh"
+
+namespace moe {
+
+// ------------------------------------------------------- block prefix scan
+// block_pre[b][e] = src_off[e] + sum_{b' < b} block_counts[b'][e].  One CTA per
+// expert column; each thread scans a contiguous chunk of blocks.
+__global__ void __launch_bounds__(512)
+block_prefix_kernel(const int32_t* __restrict__ block_counts, int nblk, int E,
+                    const DevPlan* __restrict__ plan, int32_t* __restrict__ block_pre) {
+  const int e = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int per = (nblk + blockDim.x - 1) / blockDim.x;
+  const int b0 = tid * per, b1 = min(nblk, b0 + per);
+  int local = 0;
+  for (int b = b0; b < b1; ++b) local += block_counts[(size_t)b * E + e];
+  // exclusive scan of `local` across the CTA
+  __shared__ int warp_sums[16];
+  const int lane = tid & 31, warp = tid >> 5;
+  int incl = local;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  if (lane == 31) warp_sums[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w += v;
+    }
+    if (lane < (int)(blockDim.x >> 5)) warp_sums[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  int run = plan->src_off[e] + (warp > 0 ? warp_sums[warp - 1] : 0) + incl - local;
+  for (int b = b0; b < b1; ++b) {
+    block_pre[(size_t)b * E + e] = run;
+    run += block_counts[(size_t)b * E + e];
+  }
+}
+
+// ------------------------------------------------------------- dispatch
+__device__ __forceinline__ uint32_t row_code_for(const DevPlan* plan, int e, int gr) {
+  const int n = plan->n_e[e];
+  const int R = plan->rep_base[e + 1] - plan->rep_base[e];
+  const int q = n / R, rem = n % R;
+  const int r = gr < rem * (q + 1) ? gr / (q + 1) : rem + (gr - rem * (q + 1)) / q;
+  const int f = plan->rep_base[e] + r;
+  const uint32_t row = static_cast<uint32_t>(plan->rep_row_base[f] + gr);
+  return row | (plan->rep_remote[f] ? kRemoteBit : 0u);
+}
+
+template <int K>
+__global__ void __launch_bounds__(128)
+dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const int32_t* __restrict__ ids,
+                const int32_t* __restrict__ block_pre, const DevPlan* __restrict__ plan,
+                __nv_bfloat16* __restrict__ xp_local, __nv_bfloat16* __restrict__ xp_send,
+                uint32_t* __restrict__ row_code) {
+  __shared__ uint32_t codes[32 * K];
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int t_base = b * 32;
+  const int ntok = min(32, T - t_base);
+
+  if (warp == 0) {
+    const int t = t_base + lane;
+    const bool live = lane < ntok;
+    int my[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) my[j] = live ? ids[(size_t)t * K + j] : -1;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int e = 0; e < E; ++e) {
+      int slot = -1;
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (my[j] == e) slot = j;
+      const uint32_t m = __ballot_sync(0xffffffffu, slot >= 0);
+      if (m == 0) continue;
+      if (slot >= 0) {
+        const int gr = block_pre[(size_t)b * E + e] + __popc(m & lt);
+        const uint32_t code = row_code_for(plan, e, gr);
+        codes[lane * K + slot] = code;
+        row_code[(size_t)t * K + slot] = code;
+      }
+    }
+  }
+  __syncthreads();
+
+  // stream rows: each warp copies tokens warp, warp+4, ...
+  const int chunks = d / 8;  // 16-byte chunks per row
+  for (int i = warp; i < ntok; i += 4) {
+    const __nv_bfloat16* src = x + (size_t)(t_base + i) * d;
+    __nv_bfloat16* dst[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint32_t c = codes[i * K + j];
+      __nv_bfloat16* base = (c & kRemoteBit) ? xp_send : xp_local;
+      dst[j] = base + (size_t)(c & ~kRemoteBit) * d;
+    }
+    for (int c0 = lane; c0 < chunks; c0 += 32 * 4) {
+      int4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c0 + 32 * u < chunks) v[u] = ld_nc_v4(src + (size_t)(c0 + 32 * u) * 8);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c0 + 32 * u < chunks) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) st_v4(dst[j] + (size_t)(c0 + 32 * u) * 8, v[u]);
+        }
+    }
+  }
+}
+
+// -------------------------------------------------------------- combine
+template <int K>
+__global__ void __launch_bounds__(256)
+combine_kernel(const __nv_bfloat16* __restrict__ y_local, const __nv_bfloat16* __restrict__ y_return, int T,
+               int d, const uint32_t* __restrict__ row_code, const float* __restrict__ wts,
+               __nv_bfloat16* __restrict__ y) {
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  const int chunks = d / 8;
+  for (int t = warp_global; t < T; t += nwarps) {
+    const __nv_bfloat16* src[K];
+    float w[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint32_t c = row_code[(size_t)t * K + j];
+      src[j] = ((c & kRemoteBit) ? y_return : y_local) + (size_t)(c & ~kRemoteBit) * d;
+      w[j] = wts[(size_t)t * K + j];
+    }
+    __nv_bfloat16* out = y + (size_t)t * d;
+    for (int c0 = lane; c0 < chunks; c0 += 32) {
+      int4 v[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) v[j] = ld_nc_v4(src[j] + (size_t)c0 * 8);
+      float acc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const uint32_t* u = reinterpret_cast<const uint32_t*>(&v[j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[2 * i] = fmaf(w[j], bf16lo(u[i]), acc[2 * i]);
+          acc[2 * i + 1] = fmaf(w[j], bf16hi(u[i]), acc[2 * i + 1]);
+        }
+      }
+      int4 o;
+      o.x = pack_bf16(acc[0], acc[1]);
+      o.y = pack_bf16(acc[2], acc[3]);
+      o.z = pack_bf16(acc[4], acc[5]);
+      o.w = pack_bf16(acc[6], acc[7]);
+      st_v4(out + (size_t)c0 * 8, o);
+    }
+  }
+}
+
+// ------------------------------------------------------------- launchers
+cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, const DevPlan* plan,
+                                int32_t* block_pre, cudaStream_t s) {
+  if (nblk <= 0) return cudaSuccess;
+  block_prefix_kernel<<<E, 512, 0, s>>>(block_counts, nblk, E, plan, block_pre);
+  return cudaGetLastError();
+}
+
+#define MOE_SWITCH_K(k, ...)                         \
+  switch (k) {                                        \
+    case 1: { constexpr int KK = 1; __VA_ARGS__; } break; \
+    case 2: { constexpr int KK = 2; __VA_ARGS__; } break; \
+    case 4: { constexpr int KK = 4; __VA_ARGS__; } break; \
+    case 6: { constexpr int KK = 6; __VA_ARGS__; } break; \
+    case 8: { constexpr int KK = 8; __VA_ARGS__; } break; \
+    default: return cudaErrorInvalidValue;            \
+  }
+
+cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
+                            const int32_t* block_pre, const DevPlan* plan, __nv_bfloat16* xp_local,
+                            __nv_bfloat16* xp_send, uint32_t* row_code, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  if (d % 8) return cudaErrorInvalidValue;
+  const int nblk = (T + 31) / 32;
+  MOE_SWITCH_K(k, (dispatch_kernel<KK><<<nblk, 128, 0, s>>>(x, T, d, E, ids, block_pre, plan, xp_local, xp_send,
+                                                           row_code)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(const __nv_bfloat16* y_local, const __nv_bfloat16* y_return, int T, int d, int k,
+                           const uint32_t* row_code, const float* wts, __nv_bfloat16* y, int num_sms,
+                           cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  if (d % 8) return cudaErrorInvalidValue;
+  const int warps_needed = T;
+  int ctas = (warps_needed + 7) / 8;
+  ctas = ctas < num_sms * 8 ? ctas : num_sms * 8;
+  MOE_SWITCH_K(k, (combine_kernel<KK><<<ctas, 256, 0, s>>>(y_local, y_return, T, d, row_code, wts, y)));
+  return cudaGetLastError();
+}
+
+}  // namespace moe

@@ -1,0 +1,35 @@
+// dispatch_plan.h — the per-layer exchange/dispatch plan shared by the host
+// planner (exchange_plan.cpp) and the device kernels (dispatch.cu,
+// ffn_gemm.cu).  Plain-old-data so it is uploaded with one async H2D copy.
+#pragma once
+#include <cstdint>
+
+namespace moe {
+
+constexpr int kMaxExperts = 256;
+constexpr int kMaxReplicas = 512;
+constexpr uint32_t kRemoteBit = 0x80000000u;  // row code: row lives in the send/return buffer
+
+// One GEMM segment = the rows of one replica placed on this rank.
+struct GemmSeg {
+  int row_start;  // first row in the received (permuted) buffer
+  int rows;       // > 0
+  int slot;       // expert whose weights the replica runs
+  int pad;
+};
+
+struct DevPlan {
+  int E, R, G, rank;
+  int nseg;        // GEMM segments on this rank (replicas here with rows > 0)
+  int rows_local;  // rows this rank computes (sum of its segments)
+  int rows_send;   // rows this rank ships to other ranks
+  int pad0;
+  int n_e[kMaxExperts];               // assignments of expert e over all ranks
+  int src_off[kMaxExperts];           // this rank's first global rank in expert e
+  int rep_base[kMaxExperts + 4];      // flat replica id of (e, 0); [E] = R
+  int rep_row_base[kMaxReplicas];     // row(gr) = rep_row_base[f] + gr
+  int rep_remote[kMaxReplicas];       // 1: rows go to the send buffer
+  GemmSeg segs[kMaxReplicas];
+};
+
+}  // namespace moe

@@ -1,0 +1,276 @@
+// ffn_gemm.cu — K4: the expert SwiGLU FFN as two persistent grouped GEMMs on
+// 5th-generation tensor cores (tcgen05 + TMEM), fed by TMA over ragged
+// per-replica segments.
+//
+// It is the real work behind the reference's compute term alpha * max_share
+// (proj/src/cost_model.cpp:115): each replica segment of the permuted token
+// buffer is multiplied by its expert's weights.
+//
+//   GEMM1 (EPI_SWIGLU): H[r, f] = silu(X[r,:] W1[f,:]) * (X[r,:] W3[f,:])
+//       A = X  [rows, d]  K-major;  B = W13 [slot][2ff, d] K-major, W1/W3 rows
+//       interleaved in 128-row blocks so one 128x256 accumulator tile holds the
+//       gate and up projections of the same 128 ff-columns; the epilogue
+//       applies silu(g)*u and writes a 128x128 bf16 tile of H.
+//   GEMM2 (EPI_STORE):  Y[r, n] = H[r,:] W2[n,:]
+//       A = H  [rows, ff] K-major;  B = W2 [slot][d, ff] K-major.
+//
+// Kernel anatomy (one CTA per SM, persistent, 6 warps):
+//   warp 0      TMA producer: 128x64 A tile + 256x64 B tile per stage (48 KB),
+//               4-stage smem ring guarded by full/empty mbarriers.
+//   warp 1      TMEM owner + MMA issuer: one elected thread issues
+//               tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256, K=16) x4 per
+//               stage into a double-buffered TMEM accumulator (2 x 256 cols),
+//               tcgen05.commit frees smem stages and publishes finished tiles.
+//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 32 cols -> registers ->
+//               (silu*mul) -> bf16 -> global; warp w reads TMEM lanes
+//               32*(w%4)..+31 as the hardware requires.
+// Tile order: segments in (expert, ordinal) order; inside a segment, groups of
+// up to 16 m-tiles sweep all n-tiles so concurrently running CTAs share A
+// rows and B columns through L2.
+#include <cstdint>
+#include <cuda.h>
+
+#include "dispatch_plan.h"
+#include "sm100_ptx.cuh"
+
+namespace moe {
+
+constexpr int kMaxSegs = kMaxReplicas;
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int kGroupM = 16;
+constexpr uint32_t kStageBytesA = BM * BK * 2, kStageBytesB = BN * BK * 2;
+constexpr uint32_t kStageBytes = kStageBytesA + kStageBytesB;
+constexpr int kThreads = 192;
+constexpr uint32_t kTmemCols = 512;
+
+enum : int { EPI_SWIGLU = 0, EPI_STORE = 1 };
+
+struct SmemLayout {
+  // offsets relative to the 1024-aligned base
+  static constexpr uint32_t a = 0;
+  static constexpr uint32_t b = a + STAGES * kStageBytesA;
+  static constexpr uint32_t bars = b + STAGES * kStageBytesB;       // 8-byte mbarriers
+  static constexpr uint32_t n_bars = 2 * STAGES + 4;
+  static constexpr uint32_t tmem_slot = bars + n_bars * 8;
+  static constexpr uint32_t seg_tiles = tmem_slot + 16;              // int[kMaxSegs + 1]
+  static constexpr uint32_t segs = seg_tiles + (kMaxSegs + 1) * 4 + 12;  // int4[kMaxSegs]
+  static constexpr uint32_t end = ((segs + 15) / 16) * 16 + kMaxSegs * 16;
+};
+constexpr uint32_t kSmemBytes = SmemLayout::end + 1024;
+
+struct TileCoord {
+  int seg, m, n;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(int t, const int* seg_tiles, const int4* segs, int nseg,
+                                                 int n_tiles) {
+  // binary search: last s with seg_tiles[s] <= t
+  int lo = 0, hi = nseg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (seg_tiles[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  const int s = lo;
+  const int local = t - seg_tiles[s];
+  const int m_tiles = (segs[s].y + BM - 1) / BM;
+  const int per_group = kGroupM * n_tiles;
+  const int g = local / per_group;
+  const int gm = min(kGroupM, m_tiles - g * kGroupM);
+  const int rem = local - g * per_group;
+  TileCoord c;
+  c.seg = s;
+  c.n = rem / gm;
+  c.m = g * kGroupM + rem % gm;
+  return c;
+}
+
+__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total,
+                    int k_total, int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout::bars);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SmemLayout::tmem_slot);
+  int* seg_tiles = reinterpret_cast<int*>(smem + SmemLayout::seg_tiles);
+  int4* segs = reinterpret_cast<int4*>(smem + SmemLayout::segs);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  const int nseg = min(*nseg_g, kMaxSegs);
+  const int n_tiles = n_total / BN;
+
+  for (int i = threadIdx.x; i < nseg; i += kThreads) segs[i] = reinterpret_cast<const int4*>(segs_g)[i];
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int s = 0; s < nseg; ++s) {
+      seg_tiles[s] = acc;
+      acc += ((segs[s].y + BM - 1) / BM) * n_tiles;
+    }
+    seg_tiles[nseg] = acc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_tiles = nseg > 0 ? seg_tiles[nseg] : 0;
+  const int num_kb = k_total / BK;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint64_t pol_b = policy_evict_last();
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const TileCoord c = decode_tile(t, seg_tiles, segs, nseg, n_tiles);
+        const int a_row = segs[c.seg].x + c.m * BM;
+        const int b_row = segs[c.seg].z * b_rows_per_slot + c.n * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], kStageBytes);
+          tma_load_2d(smem + SmemLayout::a + stage * kStageBytesA, &tmA, &full[stage], kb * BK, a_row);
+          tma_load_2d_hint(smem + SmemLayout::b + stage * kStageBytesB, &tmB, &full[stage], kb * BK, b_row,
+                           pol_b);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      const uint32_t a_base = smem_u32(smem + SmemLayout::a);
+      const uint32_t b_base = smem_u32(smem + SmemLayout::b);
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = umma_desc_sw128(a_base + stage * kStageBytesA);
+          const uint64_t bdesc = umma_desc_sw128(b_base + stage * kStageBytesB);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            tc_mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // --------------------------------------------------------- epilogue
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const TileCoord c = decode_tile(t, seg_tiles, segs, nseg, n_tiles);
+      const int4 sg = segs[c.seg];
+      const int row = c.m * BM + quarter * 32 + lane;
+      const bool valid = row < sg.y;
+      const size_t grow = static_cast<size_t>(sg.x + row);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+      if constexpr (EPI == EPI_SWIGLU) {
+        __nv_bfloat16* dst = out + grow * out_ld + c.n * (BN / 2);
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 2 / 32; ++ch) {
+          uint32_t g[32], u[32];
+          tmem_ld_32x32b_x32(taddr + ch * 32, g);
+          tmem_ld_32x32b_x32(taddr + BN / 2 + ch * 32, u);
+          tc_wait_ld();
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float h0 = silu(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
+            const float h1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+            packed[i] = pack_bf16(h0, h1);
+          }
+          if (valid) {
+            int4* p = reinterpret_cast<int4*>(dst + ch * 32);
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              p[v] = make_int4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+          }
+        }
+      } else {
+        __nv_bfloat16* dst = out + grow * out_ld + c.n * BN;
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + ch * 32, r);
+          tc_wait_ld();
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) packed[i] = pack_bf16(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+          if (valid) {
+            int4* p = reinterpret_cast<int4*>(dst + ch * 32);
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              p[v] = make_int4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// --------------------------------------------------------------- host side
+static_assert(kSmemBytes <= 232448, "smem budget");
+
+int gemm_smem_bytes() { return static_cast<int>(kSmemBytes); }
+
+cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
+                                const int* nseg, int n_total, int k_total, int b_rows_per_slot,
+                                __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream) {
+  if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(grouped_gemm_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    configured = true;
+  }
+  if (epi == EPI_SWIGLU)
+    grouped_gemm_kernel<EPI_SWIGLU><<<num_ctas, kThreads, kSmemBytes, stream>>>(
+        *tmA, *tmB, segs, nseg, n_total, k_total, b_rows_per_slot, out, out_ld);
+  else
+    grouped_gemm_kernel<EPI_STORE><<<num_ctas, kThreads, kSmemBytes, stream>>>(
+        *tmA, *tmB, segs, nseg, n_total, k_total, b_rows_per_slot, out, out_ld);
+  return cudaGetLastError();
+}
+
+}  // namespace moe
