@@ -115,6 +115,9 @@ const char* moe_last_error(void);
 const char* moe_version(void);
 
 /* ---------------------------------------------------------------- context */
+/* 128-byte NCCL unique id for moe_ctx_desc.nccl_unique_id (rank 0 creates it,
+   the launcher broadcasts it). */
+int moe_nccl_unique_id(void* out128);
 int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out);
 int moe_ctx_destroy(moe_ctx* ctx);
 int moe_ctx_stream(moe_ctx* ctx, void** stream_out);

@@ -366,6 +366,7 @@ void orc_expert_ffn(const uint16_t* x, int64_t rows, int d, int ff, const uint16
     for (int64_t r = 0; r < rows; ++r) {
       const uint16_t* xr = x + r * d;
       float g = 0.0f, u = 0.0f;
+#pragma omp simd reduction(+ : g, u)
       for (int c = 0; c < d; ++c) {
         float xv = bf2f(xr[c]);
         g += xv * bf2f(a[c]);
@@ -381,6 +382,7 @@ void orc_expert_ffn(const uint16_t* x, int64_t rows, int d, int ff, const uint16
     for (int64_t r = 0; r < rows; ++r) {
       const float* hr = h + r * ff;
       float acc = 0.0f;
+#pragma omp simd reduction(+ : acc)
       for (int f = 0; f < ff; ++f) acc += hr[f] * bf2f(wr[f]);
       y[r * d + n] = round_y ? bf2f(f2bf(acc)) : acc;
     }

@@ -30,7 +30,7 @@ __all__ = [
     "scale_experts", "place_experts", "ReplicaRegistry", "update_registry", "layer_forward_time",
     "predict", "measure_accuracy", "route_tokens", "popularity", "percentile", "exchange_plan",
     "MoELayer", "ScalingPlan", "PlaceResult", "synth_tokens", "synth_gate", "synth_expert",
-    "stream_key", "MoeError", "MOE_PLAN_FIXED", "MOE_PLAN_SYNC", "MOE_EXCHANGE_NCCL",
+    "stream_key", "nccl_unique_id", "MoeError", "MOE_PLAN_FIXED", "MOE_PLAN_SYNC", "MOE_EXCHANGE_NCCL",
     "MOE_EXCHANGE_EXTERNAL", "LIB_PATH",
 ]
 LIB_PATH = _capi.LIB_PATH
@@ -220,6 +220,11 @@ def exchange_plan(world_size: int, rank: int, counts_all: np.ndarray,
 
 
 # ------------------------------------------------------- synthetic inputs
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib.moe_nccl_unique_id(buf))
+    return buf.raw
+
 def stream_key(seed: int, a: int, b: int, tag: int) -> int:
     return int(lib.moe_stream_key(seed, a, b, tag))
 

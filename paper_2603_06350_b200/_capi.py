@@ -62,6 +62,7 @@ def _sig(name, res, *args):
 
 _sig("moe_last_error", C.c_char_p)
 _sig("moe_version", C.c_char_p)
+_sig("moe_nccl_unique_id", C.c_int, vp)
 _sig("moe_ctx_create", C.c_int, P(MoeCtxDesc), P(vp))
 _sig("moe_ctx_destroy", C.c_int, vp)
 _sig("moe_ctx_stream", C.c_int, vp, P(vp))
@@ -103,7 +104,7 @@ _sig("moe_synth_expert", C.c_int, u64, C.c_int, C.c_int, vp, vp, vp)
 
 # Every symbol include/moe_b200.h declares (checked by tests/test_capi_symbols.py).
 EXPORTED = [
-    "moe_last_error", "moe_version", "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_stream",
+    "moe_last_error", "moe_version", "moe_nccl_unique_id", "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_stream",
     "moe_ctx_sync", "moe_load_expert_weights", "moe_set_gate_weights",
     "moe_set_predictor_weights", "moe_set_placement", "moe_gate_topk", "moe_predict_loads",
     "moe_layer_forward", "moe_layer_forward_host", "moe_forward_begin", "moe_forward_expert",

@@ -441,6 +441,17 @@ extern "C" {
 const char* moe_last_error(void) { return g_last_error.c_str(); }
 const char* moe_version(void) { return "moe_b200 0.1.0 (sm_100a)"; }
 
+int moe_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    require(out128 != nullptr, "null argument");
+    g_nccl.load();
+    ncclUniqueId id;
+    g_nccl.check(g_nccl.GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
 int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
   return guarded([&] {
     require(desc && out, "null argument");

@@ -79,7 +79,14 @@ void build_exchange_plan(int G, int rank, int E, const int64_t* counts_all, cons
     if (out.rep_size[id] > 0) {
       int e = 0;
       while (p.rep_base[e + 1] <= id) ++e;
-      p.segs[p.nseg++] = GemmSeg{static_cast<int>(rows), static_cast<int>(out.rep_size[id]), e, 0};
+      // Replicas of one expert that sit on the same GPU share its resident
+      // weights and occupy adjacent rows: schedule them as ONE grouped-GEMM
+      // problem so the weights stream once and only one m-tile is partial.
+      GemmSeg* last = p.nseg > 0 ? &p.segs[p.nseg - 1] : nullptr;
+      if (last && last->slot == e && last->row_start + last->rows == rows)
+        last->rows += static_cast<int>(out.rep_size[id]);
+      else
+        p.segs[p.nseg++] = GemmSeg{static_cast<int>(rows), static_cast<int>(out.rep_size[id]), e, 0};
     }
     rows += out.rep_size[id];
   }

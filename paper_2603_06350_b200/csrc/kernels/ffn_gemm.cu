@@ -37,7 +37,9 @@ namespace moe {
 
 constexpr int kMaxSegs = kMaxReplicas;
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int kGroupM = 16;
+// m-tiles swept per n column: GEMM1 (K = d) keeps a whole expert's A rows L2-resident
+// while its weights stream once; GEMM2 (K = ff, 3.7 MB A tiles) uses a smaller group.
+template <int EPI> constexpr int kGroupM = EPI == 0 ? 32 : 16;
 constexpr uint32_t kStageBytesA = BM * BK * 2, kStageBytesB = BN * BK * 2;
 constexpr uint32_t kStageBytes = kStageBytesA + kStageBytesB;
 constexpr int kThreads = 192;
@@ -62,6 +64,7 @@ struct TileCoord {
   int seg, m, n;
 };
 
+template <int GM>
 __device__ __forceinline__ TileCoord decode_tile(int t, const int* seg_tiles, const int4* segs, int nseg,
                                                  int n_tiles) {
   // binary search: last s with seg_tiles[s] <= t
@@ -73,14 +76,14 @@ __device__ __forceinline__ TileCoord decode_tile(int t, const int* seg_tiles, co
   const int s = lo;
   const int local = t - seg_tiles[s];
   const int m_tiles = (segs[s].y + BM - 1) / BM;
-  const int per_group = kGroupM * n_tiles;
+  const int per_group = GM * n_tiles;
   const int g = local / per_group;
-  const int gm = min(kGroupM, m_tiles - g * kGroupM);
+  const int gm = min(GM, m_tiles - g * GM);
   const int rem = local - g * per_group;
   TileCoord c;
   c.seg = s;
   c.n = rem / gm;
-  c.m = g * kGroupM + rem % gm;
+  c.m = g * GM + rem % gm;
   return c;
 }
 
@@ -139,7 +142,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       uint32_t phase = 0;
       const uint64_t pol_b = policy_evict_last();
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const TileCoord c = decode_tile(t, seg_tiles, segs, nseg, n_tiles);
+        const TileCoord c = decode_tile<kGroupM<EPI>>(t, seg_tiles, segs, nseg, n_tiles);
         const int a_row = segs[c.seg].x + c.m * BM;
         const int b_row = segs[c.seg].z * b_rows_per_slot + c.n * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -187,7 +190,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      const TileCoord c = decode_tile(t, seg_tiles, segs, nseg, n_tiles);
+      const TileCoord c = decode_tile<kGroupM<EPI>>(t, seg_tiles, segs, nseg, n_tiles);
       const int4 sg = segs[c.seg];
       const int row = c.m * BM + quarter * 32 + lane;
       const bool valid = row < sg.y;

@@ -9,14 +9,17 @@
 // restricted to the chosen k (== softmax over the k logits); counts[e] is the
 // histogram of chosen experts (sum == T*k, as route_tokens guarantees).
 //
-// Work decomposition: one warp owns a block of 32 consecutive tokens (this is
-// also the granularity of block_counts[], the stable prefix the dispatch
-// kernel scans).  Each lane owns 8 contiguous columns per 256-column step, so
-// x is read with one 16-byte L1-bypassing load per lane per step (512 B
-// coalesced per warp) and each weight vector is reused for TOKG tokens.
-// Partial sums are all-reduced with xor shuffles; lane (e mod 32) keeps
-// expert e for the arg-max and for the histogram, which is flushed with one
-// global atomicAdd per (block, expert).
+// Work decomposition: one CTA (8 warps) owns a block of 32 consecutive tokens
+// — the granularity of block_counts[], the stable prefix the dispatch kernel
+// scans — and each warp owns TOKG of them.  A lane owns 8 contiguous columns
+// per 256-column step, so x is read with 16-byte L1-bypassing loads (512 B
+// coalesced per warp), unrolled so each lane keeps TOKG x kUnroll loads in
+// flight; the gate rows (64 KB at d=4096, E=8) stay L1-resident and each
+// 16-byte weight vector is reused for TOKG tokens.  Partial sums are
+// all-reduced with xor shuffles; lane (e mod 32) keeps expert e for the
+// warp arg-max.  The block histogram is built with shared-memory atomics and
+// flushed with one global atomicAdd per (block, expert): the atomics-based
+// per-expert load histogram.
 //
 // The predictor weights (n_pred target layers, each [E, d]) are stacked under
 // the gate weights: the same pass over x yields pred_counts[p][E] (histogram
@@ -30,17 +33,18 @@ namespace moe {
 
 namespace {
 
-constexpr int kWarpsPerCta = 4;
-constexpr int kBlockTokens = 32;  // tokens per warp == per block_counts row
+constexpr int kBlockTokens = 32;  // tokens per CTA == per block_counts row
 constexpr int kPerLane = 8;       // stacked experts per lane -> E*(1+n_pred) <= 256
 
 // Top-k over the experts [base, base+E) of a stacked logit vector held as
 // lane l -> stacked index l + 32 s.  Every lane returns the same ids/logits.
 __device__ __forceinline__ void warp_topk(const float (&own)[kPerLane], int base, int E, int k,
-                                          int* ids_out, float* logit_out) {
+                                          int (&ids_out)[8], float (&logit_out)[8]) {
   const int lane = lane_id();
   uint32_t taken = 0;
-  for (int j = 0; j < k; ++j) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j >= k) break;
     float bv = -FLT_MAX;
     int bi = 0x7fffffff;
 #pragma unroll
@@ -67,32 +71,30 @@ __device__ __forceinline__ void warp_topk(const float (&own)[kPerLane], int base
 // x [T, d] bf16; w_all [(1 + n_pred) * E, d] bf16 (rows 0..E-1 = gate).
 // Outputs: ids [T, k] i32, weights [T, k] f32, counts [E] i32 (atomic; caller
 // zeroes), block_counts [ceil(T/32), E] i32, pred_counts [n_pred, E] (atomic).
-template <int TOKG, int EC>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+template <int TOKG, int EC, int kUnroll>
+__global__ void __launch_bounds__(kBlockTokens / TOKG * 32)
 gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d,
                  const __nv_bfloat16* __restrict__ w_all, int E, int n_pred, int k,
                  int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
                  int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts) {
+  constexpr int kWarps = kBlockTokens / TOKG;
+  __shared__ int hist[kPerLane * 32];
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
-  const int blk = blockIdx.x * kWarpsPerCta + warp;
-  const int t_begin = blk * kBlockTokens;
-  if (t_begin >= T) return;
-  const int t_end = min(T, t_begin + kBlockTokens);
+  const int blk = blockIdx.x;
   const int Etot = E * (1 + n_pred);
+  for (int i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
 
-  int hist[kPerLane];  // gate histogram for stacked index lane + 32 s (< E)
+  const int t0 = blk * kBlockTokens + warp * TOKG;
+  const int ntok = max(0, min(TOKG, T - t0));
+  float own[TOKG][kPerLane];
 #pragma unroll
-  for (int s = 0; s < kPerLane; ++s) hist[s] = 0;
+  for (int q = 0; q < TOKG; ++q)
+#pragma unroll
+    for (int s = 0; s < kPerLane; ++s) own[q][s] = -FLT_MAX;
 
-  for (int t0 = t_begin; t0 < t_end; t0 += TOKG) {
-    const int ntok = min(TOKG, t_end - t0);
-    float own[TOKG][kPerLane];
-#pragma unroll
-    for (int q = 0; q < TOKG; ++q)
-#pragma unroll
-      for (int s = 0; s < kPerLane; ++s) own[q][s] = -FLT_MAX;
-
+  if (ntok > 0) {
     for (int e0 = 0; e0 < Etot; e0 += EC) {
       float acc[TOKG][EC];
 #pragma unroll
@@ -100,28 +102,39 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d,
 #pragma unroll
         for (int c = 0; c < EC; ++c) acc[q][c] = 0.0f;
 
-      for (int col = lane * 8; col < d; col += 256) {
-        float xv[TOKG][8];
+      for (int col0 = lane * 8; col0 < d; col0 += 256 * kUnroll) {
+        int4 raw[kUnroll][TOKG];
 #pragma unroll
-        for (int q = 0; q < TOKG; ++q) {
-          int4 raw = make_int4(0, 0, 0, 0);
-          if (q < ntok) raw = ld_nc_v4(x + (size_t)(t0 + q) * d + col);
-          const uint32_t* u = reinterpret_cast<const uint32_t*>(&raw);
+        for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) { xv[q][2 * i] = bf16lo(u[i]); xv[q][2 * i + 1] = bf16hi(u[i]); }
-        }
+          for (int q = 0; q < TOKG; ++q) {
+            const int col = col0 + 256 * u;
+            raw[u][q] = (q < ntok && col < d) ? ld_nc_v4(x + (size_t)(t0 + q) * d + col) : make_int4(0, 0, 0, 0);
+          }
 #pragma unroll
-        for (int c = 0; c < EC; ++c) {
-          if (e0 + c < Etot) {
-            const int4 raw = __ldg(reinterpret_cast<const int4*>(w_all + (size_t)(e0 + c) * d + col));
-            const uint32_t* u = reinterpret_cast<const uint32_t*>(&raw);
-            float wv[8];
+        for (int u = 0; u < kUnroll; ++u) {
+          const int col = col0 + 256 * u;
+          if (col >= d) break;
+          float xv[TOKG][8];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) { wv[2 * i] = bf16lo(u[i]); wv[2 * i + 1] = bf16hi(u[i]); }
+          for (int q = 0; q < TOKG; ++q) {
+            const uint32_t* p = reinterpret_cast<const uint32_t*>(&raw[u][q]);
 #pragma unroll
-            for (int q = 0; q < TOKG; ++q)
+            for (int i = 0; i < 4; ++i) { xv[q][2 * i] = bf16lo(p[i]); xv[q][2 * i + 1] = bf16hi(p[i]); }
+          }
 #pragma unroll
-              for (int i = 0; i < 8; ++i) acc[q][c] = fmaf(xv[q][i], wv[i], acc[q][c]);
+          for (int c = 0; c < EC; ++c) {
+            if (e0 + c < Etot) {
+              const int4 wr = __ldg(reinterpret_cast<const int4*>(w_all + (size_t)(e0 + c) * d + col));
+              const uint32_t* p = reinterpret_cast<const uint32_t*>(&wr);
+              float wv[8];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) { wv[2 * i] = bf16lo(p[i]); wv[2 * i + 1] = bf16hi(p[i]); }
+#pragma unroll
+              for (int q = 0; q < TOKG; ++q)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[q][c] = fmaf(xv[q][i], wv[i], acc[q][c]);
+            }
           }
         }
       }
@@ -149,35 +162,34 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d,
           int sel[8];
           float lg[8];
           warp_topk(own[q], g * E, E, k, sel, lg);
-          if (g == 0) {
-            if (lane == 0) {
+          if (lane == 0) {
+            if (g == 0) {
               float z = 0.0f, p[8];
-              for (int j = 0; j < k; ++j) { p[j] = expf(lg[j] - lg[0]); z += p[j]; }
-              for (int j = 0; j < k; ++j) {
-                ids[(size_t)t * k + j] = sel[j];
-                wts[(size_t)t * k + j] = p[j] / z;
-              }
-            }
-            for (int j = 0; j < k; ++j)
-              if ((sel[j] & 31) == lane) {
 #pragma unroll
-                for (int s = 0; s < kPerLane; ++s)
-                  if ((sel[j] >> 5) == s) hist[s]++;
-              }
-          } else if (lane == 0) {
-            for (int j = 0; j < k; ++j) atomicAdd(pred_counts + (size_t)(g - 1) * E + sel[j], 1);
+              for (int j = 0; j < 8; ++j)
+                if (j < k) { p[j] = expf(lg[j] - lg[0]); z += p[j]; }
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (j < k) {
+                  ids[(size_t)t * k + j] = sel[j];
+                  wts[(size_t)t * k + j] = p[j] / z;
+                  atomicAdd(&hist[sel[j]], 1);
+                }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (j < k) atomicAdd(pred_counts + (size_t)(g - 1) * E + sel[j], 1);
+            }
           }
         }
       }
     }
   }
-#pragma unroll
-  for (int s = 0; s < kPerLane; ++s) {
-    const int e = lane + 32 * s;
-    if (e < E) {
-      block_counts[(size_t)blk * E + e] = hist[s];
-      if (hist[s]) atomicAdd(counts + e, hist[s]);
-    }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int h = hist[e];
+    block_counts[(size_t)blk * E + e] = h;
+    if (h) atomicAdd(counts + e, h);
   }
 }
 
@@ -189,17 +201,16 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
   if (T <= 0) return cudaSuccess;
   if (E * (1 + n_pred) > 32 * kPerLane || k > 8 || (d % 8) != 0) return cudaErrorInvalidValue;
   const int nblk = gate_num_blocks(T);
-  const dim3 grid((nblk + kWarpsPerCta - 1) / kWarpsPerCta), block(kWarpsPerCta * 32);
   const int Etot = E * (1 + n_pred);
   if (Etot <= 8)
-    gate_topk_kernel<4, 8><<<grid, block, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,
-                                                        block_counts, pred_counts);
+    gate_topk_kernel<4, 8, 2><<<nblk, 256, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,
+                                                     block_counts, pred_counts);
   else if (Etot <= 16)
-    gate_topk_kernel<2, 16><<<grid, block, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,
-                                                         block_counts, pred_counts);
+    gate_topk_kernel<2, 16, 4><<<nblk, 512, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,
+                                                      block_counts, pred_counts);
   else
-    gate_topk_kernel<1, 32><<<grid, block, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,
-                                                         block_counts, pred_counts);
+    gate_topk_kernel<2, 16, 4><<<nblk, 512, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,
+                                                       block_counts, pred_counts);
   return cudaGetLastError();
 }
 
