@@ -1,0 +1,72 @@
+"""K2 (batched load predictor fused into the gate's read of x) and the
+synchronous planner inside the forward, on the GPU against the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2603_06350_b200 as pk
+from paper_2603_06350_b200 import MOE_PLAN_SYNC, MoELayer
+from paper_2603_06350_b200 import workload as wl
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("E,k,d,T,npred", [(8, 2, 4096, 2048, 1), (8, 2, 1024, 777, 3), (16, 2, 2048, 512, 2),
+                                           (64, 8, 2048, 256, 1)])
+def test_predictor_counts_bitexact(cuda, E, k, d, T, npred):
+    import torch
+    m = MoELayer(1, E, k, d, 128, max_tokens=T, num_predictor_targets=npred)
+    wg = wl.gate_weights(E, d, 1.2, 1, 0, 0)
+    wps = [wl.gate_weights(E, d, 1.2, 1, 1 + p, 0) for p in range(npred)]
+    m.set_gate(0, wg)
+    for p, wp in enumerate(wps):
+        m.set_predictor(0, p, wp)
+    x = wl.tokens(T, d, E, 1, 9)
+    xd = torch.from_numpy(x.view(np.int16)).to(cuda)
+    ids = torch.zeros((T, k), dtype=torch.int32, device=cuda)
+    w = torch.zeros((T, k), dtype=torch.float32, device=cuda)
+    counts = torch.zeros(E, dtype=torch.int32, device=cuda)
+    pred = torch.zeros((npred, E), dtype=torch.int32, device=cuda)
+    m.gate(0, xd, ids, w, counts, pred)
+    torch.cuda.synchronize()
+    ids_o, _, counts_o = oracle.gate(x, wg, k)
+    assert np.array_equal(ids.cpu().numpy(), ids_o) and np.array_equal(counts.cpu().numpy(), counts_o)
+    for p, wp in enumerate(wps):
+        assert np.array_equal(pred[p].cpu().numpy(), oracle.gate(x, wp, k)[2])
+    pred2 = torch.zeros((npred, E), dtype=torch.int32, device=cuda)
+    m.predict_loads(0, xd, pred2)
+    torch.cuda.synchronize()
+    assert torch.equal(pred, pred2)
+    # predictor accuracy metric (predictor.cpp:168-186) on the predicted vs actual loads
+    acc = pk.measure_accuracy(pred[0].cpu().numpy(), counts.cpu().numpy())
+    assert 0.0 <= acc <= 1.0
+    m.close()
+
+
+def test_sync_planner_inside_forward_matches_host_planner(cuda):
+    import torch
+    E, k, d, ff, T = 8, 2, 1024, 1408, 1024
+    mem = 3.0 * d * ff * 2 / 1e6
+    m = MoELayer(1, E, k, d, ff, max_tokens=T, expert_mem_mb=mem, layer_mem_cap_mb=4 * mem, keep_alive_iters=50)
+    wg = wl.gate_weights(E, d, 1.2, 1, 0, 0)
+    experts = [wl.expert_weights(d, ff, 1, 0, e) for e in range(E)]
+    m.set_gate(0, wg)
+    for e, w in enumerate(experts):
+        m.load_expert(0, e, *w)
+    reg = pk.ReplicaRegistry(50)
+    for it in range(3):
+        x = wl.tokens(T, d, E, 1, it)
+        xd = torch.from_numpy(x.view(np.int16)).to(cuda)
+        yd = torch.zeros((T, d), dtype=torch.int16, device=cuda)
+        st = m.forward(0, xd, yd, MOE_PLAN_SYNC, it, stats=True)
+        counts = np.array(st.counts[:E])
+        plan = pk.scale_experts(counts, mem, 4 * mem, 0.2)
+        placed = pk.place_experts(plan, 1, 180000.0, reg, it)
+        pk.update_registry(reg, plan.replica_counts, placed.flat(), 1, 0, it)
+        assert st.replica_count == plan.total_replicas()
+        assert (st.warm_count, st.cold_count) == (placed.warm_count, placed.cold_count)
+        y = oracle.bf16_to_f32(yd.cpu().numpy().view(np.uint16))
+        idx = np.arange(0, T, 37)
+        y_ref = oracle.layer_forward(x[idx], wg, experts, [1] * E, k)[0]
+        assert float(np.max(np.abs(y[idx] - y_ref)) / np.max(np.abs(y_ref))) <= 2e-2
+    m.close()
