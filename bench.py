@@ -291,18 +291,28 @@ def run_ours(args):
     # e2e through the host-buffer C-ABI entry point
     e2e = None
     if not args.no_e2e:
-        xh = torch.from_numpy(pool_host[0].view(np.int16)).pin_memory()
-        yh = torch.empty((T, d), dtype=torch.int16).pin_memory()
+        # pinned host batches in, pinned host outputs out, pipelined C-ABI calls
+        xh = [torch.from_numpy(x.view(np.int16)).pin_memory() for x in pool_host]
+        yh = [torch.empty((T, d), dtype=torch.int16).pin_memory() for _ in range(3)]
+        tickets = []
+        for i in range(2):  # warm the staging buffers / streams
+            m.set_gate(0, gates[i])
+            tickets.append(m.forward_host_async(0, xh[i % len(xh)], yh[i % 3], MOE_PLAN_SYNC, i))
+        for t in tickets:
+            m.wait(t)
         barrier()
-        e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e_start.record(stream)
+        tickets = []
+        t0 = time.perf_counter()
         for i in range(args.steps):
             it = total_iters + i
+            if i >= 3:
+                m.wait(tickets[i - 3])  # its output buffer is about to be reused
             m.set_gate(0, gates[it])
-            m.forward_host(0, xh, yh, MOE_PLAN_SYNC, it)
-        e_end.record(stream)
+            tickets.append(m.forward_host_async(0, xh[i % len(xh)], yh[i % 3], MOE_PLAN_SYNC, it))
+        for t in tickets[-3:]:
+            m.wait(t)
+        e2e_ms = (time.perf_counter() - t0) * 1e3  # host-visible: every result is in host memory
         barrier()
-        e2e_ms = e_start.elapsed_time(e_end)
         e2e = {"ms": e2e_ms}
 
     # max over ranks
@@ -332,7 +342,9 @@ def run_ours(args):
                        "planner": "MOE_PLAN_SYNC (scale_experts + place_experts on actual loads)"},
             "p50_ms": p50, "p99_ms": p99,
             "phase_ms_median": phases, "replicas_median": replicas,
-            "gpu_launches": 6 * args.steps,
+            # per step: gate-weight SM copy, K1 gate, counts SM copy, plan SM copy,
+            # block prefix, K3 dispatch, K4 GEMM1, K4 GEMM2, K5 combine
+            "gpu_launches": 9 * args.steps,
             "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel (GEMM1 SwiGLU + GEMM2)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "peak_source": peak_src + ", bf16 sustained", "burst_peak": peaks.get("bf16_tflops"),
@@ -346,7 +358,9 @@ def run_ours(args):
             line["e2e"] = {"value": G * T * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s",
                            "h2d_bytes_per_step": xb, "d2h_bytes_per_step": T * d * 2,
                            "ms_per_step": e2e_ms / args.steps,
-                           "api": "moe_layer_forward_host (C-ABI, pinned host buffers)"}
+                           "api": "moe_layer_forward_host_async + moe_wait (C-ABI, pinned host buffers; "
+                                  "H2D/D2H of neighbouring steps overlap the layer), wall clock over all steps "
+                                  "until the last result is in host memory"}
         if G == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = run_cpu_baseline(args.cpu_sample_tokens)
         print(json.dumps(line), flush=True)

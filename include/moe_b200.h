@@ -156,6 +156,21 @@ int moe_layer_forward_host(moe_ctx* ctx, int layer, const uint16_t* x_host, int 
                            uint16_t* y_host, int plan_mode, long iteration,
                            moe_layer_stats* stats);
 
+/* Pipelined host-buffer forward for serving loops: enqueues H2D(x) on a copy
+   stream, the layer on the compute stream and D2H(y) on a second copy stream,
+   and returns once the layer's device work is enqueued (it blocks only while
+   the host planner waits for this step's gate histogram).  Consecutive calls
+   therefore overlap step i+1's upload and step i-1's download with step i's
+   GEMMs.  x_host/y_host must be pinned and stay valid until moe_wait(ticket)
+   returns.  At most 2 calls may be in flight; *ticket identifies the call. */
+int moe_layer_forward_host_async(moe_ctx* ctx, int layer, const uint16_t* x_host, int tokens,
+                                 uint16_t* y_host, int plan_mode, long iteration,
+                                 int64_t* ticket);
+int moe_wait(moe_ctx* ctx, int64_t ticket);
+/* Page-locked host buffers for the pipelined API (portable + mapped). */
+int moe_host_alloc(size_t bytes, void** out);
+int moe_host_free(void* p);
+
 /* Staged forward for MOE_EXCHANGE_EXTERNAL (tests / custom transports):
    begin = gate + plan + dispatch; expert = both GEMMs over the received rows;
    end = combine.  Between the stages the caller moves rows between ranks

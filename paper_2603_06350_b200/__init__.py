@@ -30,7 +30,7 @@ __all__ = [
     "scale_experts", "place_experts", "ReplicaRegistry", "update_registry", "layer_forward_time",
     "predict", "measure_accuracy", "route_tokens", "popularity", "percentile", "exchange_plan",
     "MoELayer", "ScalingPlan", "PlaceResult", "synth_tokens", "synth_gate", "synth_expert",
-    "stream_key", "nccl_unique_id", "MoeError", "MOE_PLAN_FIXED", "MOE_PLAN_SYNC", "MOE_EXCHANGE_NCCL",
+    "stream_key", "nccl_unique_id", "PinnedArray", "MoeError", "MOE_PLAN_FIXED", "MOE_PLAN_SYNC", "MOE_EXCHANGE_NCCL",
     "MOE_EXCHANGE_EXTERNAL", "LIB_PATH",
 ]
 LIB_PATH = _capi.LIB_PATH
@@ -220,6 +220,24 @@ def exchange_plan(world_size: int, rank: int, counts_all: np.ndarray,
 
 
 # ------------------------------------------------------- synthetic inputs
+class PinnedArray:
+    """numpy view of a page-locked host buffer from the library's allocator."""
+
+    def __init__(self, shape, dtype):
+        self.dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * self.dtype.itemsize
+        p = C.c_void_p()
+        check(lib.moe_host_alloc(max(nbytes, 16), C.byref(p)))
+        self._p = p
+        buf = (C.c_uint8 * max(nbytes, 16)).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=self.dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def __del__(self):
+        if getattr(self, "_p", None):
+            lib.moe_host_free(self._p)
+            self._p = None
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(lib.moe_nccl_unique_id(buf))
@@ -350,6 +368,19 @@ class MoELayer:
                                          C.c_void_p(yp), plan_mode, iteration,
                                          C.byref(st) if st is not None else None))
         return st
+
+    def forward_host_async(self, layer: int, x_host, y_host, plan_mode: int = MOE_PLAN_FIXED,
+                           iteration: int = 0) -> int:
+        """Pipelined e2e call (pinned host buffers); returns a ticket for wait()."""
+        xp = x_host.ctypes.data if isinstance(x_host, np.ndarray) else x_host.data_ptr()
+        yp = y_host.ctypes.data if isinstance(y_host, np.ndarray) else y_host.data_ptr()
+        t = C.c_int64()
+        check(lib.moe_layer_forward_host_async(self._h, layer, C.c_void_p(xp), int(x_host.shape[0]),
+                                               C.c_void_p(yp), plan_mode, iteration, C.byref(t)))
+        return t.value
+
+    def wait(self, ticket: int) -> None:
+        check(lib.moe_wait(self._h, ticket))
 
     # staged forward (external exchange) ------------------------------
     def begin(self, layer: int, x, counts_all: Optional[np.ndarray] = None) -> None:

@@ -75,6 +75,10 @@ _sig("moe_gate_topk", C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp)
 _sig("moe_predict_loads", C.c_int, vp, C.c_int, vp, C.c_int, vp, vp)
 _sig("moe_layer_forward", C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int, C.c_long, P(MoeLayerStats), vp)
 _sig("moe_layer_forward_host", C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int, C.c_long, P(MoeLayerStats))
+_sig("moe_layer_forward_host_async", C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int, C.c_long, P(i64))
+_sig("moe_wait", C.c_int, vp, i64)
+_sig("moe_host_alloc", C.c_int, C.c_size_t, P(vp))
+_sig("moe_host_free", C.c_int, vp)
 _sig("moe_forward_begin", C.c_int, vp, C.c_int, vp, C.c_int, vp, vp)
 _sig("moe_forward_expert", C.c_int, vp, C.c_int, vp)
 _sig("moe_forward_end", C.c_int, vp, vp, vp)
@@ -107,7 +111,9 @@ EXPORTED = [
     "moe_last_error", "moe_version", "moe_nccl_unique_id", "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_stream",
     "moe_ctx_sync", "moe_load_expert_weights", "moe_set_gate_weights",
     "moe_set_predictor_weights", "moe_set_placement", "moe_gate_topk", "moe_predict_loads",
-    "moe_layer_forward", "moe_layer_forward_host", "moe_forward_begin", "moe_forward_expert",
+    "moe_layer_forward", "moe_layer_forward_host", "moe_layer_forward_host_async", "moe_wait",
+    "moe_host_alloc", "moe_host_free",
+    "moe_forward_begin", "moe_forward_expert",
     "moe_forward_end", "moe_buffer", "moe_memcpy", "moe_exchange_plan", "moe_plan_scale",
     "moe_registry_create", "moe_registry_destroy", "moe_registry_size", "moe_plan_place",
     "moe_registry_update", "moe_model_forward_time", "moe_plan_predict", "moe_measure_accuracy",

@@ -44,6 +44,7 @@ cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, co
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
                             const int32_t* block_pre, const DevPlan* plan, __nv_bfloat16* xp_local,
                             __nv_bfloat16* xp_send, uint32_t* row_code, cudaStream_t s);
+cudaError_t launch_small_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
 cudaError_t launch_combine(const __nv_bfloat16* y_local, const __nv_bfloat16* y_return, int T, int d, int k,
                            const uint32_t* row_code, const float* wts, __nv_bfloat16* y, int num_sms,
                            cudaStream_t s);
@@ -94,6 +95,9 @@ int guarded(F&& f) {
     return MOE_ESTATE;
   }
 }
+
+constexpr size_t pad16(size_t b) { return (b + 15) & ~size_t(15); }
+static_assert(sizeof(DevPlan) % 16 == 0, "DevPlan is copied in 16-byte words");
 
 void require(bool ok, const std::string& msg) {
   if (!ok) throw std::invalid_argument(msg);
@@ -229,12 +233,21 @@ struct moe_ctx {
   DevBuf<float> wts;
   DevBuf<uint32_t> row_code;
   DevBuf<uint16_t> xp, h, yp, send, ret, x_in, y_out;
+  // pipelined host-buffer forward: two slots of staging buffers + events
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  DevBuf<uint16_t> xa[2], ya[2];
+  cudaEvent_t ev_x_ready[2] = {}, ev_x_free[2] = {}, ev_y_ready[2] = {}, ev_done[2] = {};
+  static constexpr int kTicketRing = 16;
+  cudaEvent_t ev_ticket[kTicketRing] = {};  // per-call completion (result in host memory)
+  int64_t next_ticket = 0;
   DevBuf<DevPlan> dplan;
   int64_t rows_cap = 0, send_cap = 0;
   CUtensorMap tmA1, tmA2;
   // host staging (pinned)
   DevPlan* hplan = nullptr;
   int32_t* h_counts = nullptr;  // [G][E]
+  uint16_t* wg_stage = nullptr;  // pinned staging for stream-ordered gate updates
+  cudaEvent_t ev_wg_staged = nullptr;
   HostPlan plan;
   moeless::ReplicaRegistry registry{0};
   EventSet events;
@@ -304,7 +317,7 @@ void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int3
 }
 
 void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s) {
-  CU_CHECK(cudaMemcpyAsync(c->dplan.p, c->hplan, sizeof(DevPlan), cudaMemcpyHostToDevice, s));
+  CU_CHECK(launch_small_copy(c->dplan.p, c->hplan, sizeof(DevPlan), s));  // SM copy from mapped pinned memory
   const int nblk = gate_num_blocks(T);
   CU_CHECK(launch_block_prefix(c->block_counts.p, nblk, c->E, c->dplan.p, c->block_pre.p, s));
   CU_CHECK(launch_dispatch(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d, c->E, c->k, c->ids.p, c->block_pre.p,
@@ -369,7 +382,7 @@ void ensure_pools(moe_ctx* c, Layer& L) {
 }
 
 void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y, int plan_mode, long iteration,
-                    moe_layer_stats* st, cudaStream_t s) {
+                    moe_layer_stats* st, cudaStream_t s, cudaEvent_t x_consumed = nullptr) {
   Layer& L = layer_at(c, layer);
   require(T >= 0 && T <= c->Tmax, "token count exceeds max_tokens");
   require(plan_mode == MOE_PLAN_FIXED || plan_mode == MOE_PLAN_SYNC, "unknown plan mode");
@@ -385,15 +398,16 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   if (c->G > 1) {
     require(c->desc.exchange_mode == MOE_EXCHANGE_NCCL, "staged API required for external exchange");
     g_nccl.check(g_nccl.AllGather(c->counts.p, c->counts_all.p, c->E, ncclInt32, c->comm, s), "ncclAllGather");
-    CU_CHECK(cudaMemcpyAsync(c->h_counts, c->counts_all.p, sizeof(int32_t) * c->G * c->E, cudaMemcpyDeviceToHost, s));
+    CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * c->E), s));
   } else {
-    CU_CHECK(cudaMemcpyAsync(c->h_counts, c->counts.p, sizeof(int32_t) * c->E, cudaMemcpyDeviceToHost, s));
+    CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * c->E), s));
   }
   mark(1);
   CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram
   stage_plan(c, layer, plan_mode, iteration, c->h_counts);
   mark(2);
   stage_dispatch(c, x, T, s);
+  if (x_consumed) CU_CHECK(cudaEventRecord(x_consumed, s));  // x is not read after dispatch
   mark(3);
   stage_exchange(c, true, s);
   mark(4);
@@ -493,8 +507,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->ids.alloc(assign);
     c->wts.alloc(assign);
     c->row_code.alloc(assign);
-    c->counts.alloc(c->E);
-    c->counts_all.alloc(static_cast<size_t>(c->E) * c->G);
+    c->counts.alloc(pad16(sizeof(int32_t) * c->E) / 4);
+    c->counts_all.alloc(pad16(sizeof(int32_t) * c->E * c->G) / 4);
     c->pred_counts.alloc(static_cast<size_t>(c->E) * std::max(1, c->n_pred));
     c->block_counts.alloc(static_cast<size_t>(nblk) * c->E);
     c->block_pre.alloc(static_cast<size_t>(nblk) * c->E);
@@ -506,8 +520,9 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->dplan.alloc(1);
     c->tmA1 = make_kmajor_map(c->xp.p, c->rows_cap, c->d, 128);
     c->tmA2 = make_kmajor_map(c->h.p, c->rows_cap, c->ff, 128);
-    CU_CHECK(cudaMallocHost(&c->hplan, sizeof(DevPlan)));
-    CU_CHECK(cudaMallocHost(&c->h_counts, sizeof(int32_t) * c->E * c->G));
+    // mapped pinned control buffers, read/written by small SM copies (UVA pointers)
+    CU_CHECK(cudaHostAlloc(&c->hplan, sizeof(DevPlan), cudaHostAllocMapped));
+    CU_CHECK(cudaHostAlloc(&c->h_counts, pad16(sizeof(int32_t) * c->E * c->G), cudaHostAllocMapped));
     c->events.create();
     if (c->G > 1 && D.exchange_mode == MOE_EXCHANGE_NCCL) {
       require(D.nccl_unique_id != nullptr, "nccl_unique_id required for world_size > 1");
@@ -529,6 +544,19 @@ int moe_ctx_destroy(moe_ctx* c) {
     c->events.destroy();
     if (c->hplan) cudaFreeHost(c->hplan);
     if (c->h_counts) cudaFreeHost(c->h_counts);
+    if (c->wg_stage) cudaFreeHost(c->wg_stage);
+    if (c->ev_wg_staged) cudaEventDestroy(c->ev_wg_staged);
+    if (c->h2d) {
+      cudaStreamSynchronize(c->h2d);
+      cudaStreamSynchronize(c->d2h);
+      for (int i = 0; i < 2; ++i)
+        for (cudaEvent_t e : {c->ev_x_ready[i], c->ev_x_free[i], c->ev_y_ready[i], c->ev_done[i]})
+          if (e) cudaEventDestroy(e);
+      for (cudaEvent_t e : c->ev_ticket)
+        if (e) cudaEventDestroy(e);
+      cudaStreamDestroy(c->h2d);
+      cudaStreamDestroy(c->d2h);
+    }
     cudaStreamDestroy(c->stream);
     delete c;
   });
@@ -578,9 +606,20 @@ int moe_set_gate_weights(moe_ctx* c, int layer, const uint16_t* wg) {
     require(wg != nullptr, "null gate weights");
     if (!L.wg.p) {
       L.wg.alloc(static_cast<size_t>(c->E) * c->d * (1 + c->n_pred));
-      CU_CHECK(cudaMemset(L.wg.p, 0, L.wg.n * 2));
+      CU_CHECK(cudaMemsetAsync(L.wg.p, 0, L.wg.n * 2, c->stream));
     }
-    CU_CHECK(cudaMemcpy(L.wg.p, wg, static_cast<size_t>(c->E) * c->d * 2, cudaMemcpyHostToDevice));
+    // Stream-ordered update through a pinned staging buffer: forwards already
+    // enqueued keep the old weights, later ones see the new — no device sync.
+    const size_t bytes = static_cast<size_t>(c->E) * c->d * 2;
+    if (!c->wg_stage) {
+      CU_CHECK(cudaHostAlloc(&c->wg_stage, bytes, cudaHostAllocMapped));
+      CU_CHECK(cudaEventCreateWithFlags(&c->ev_wg_staged, cudaEventDisableTiming));
+    } else {
+      CU_CHECK(cudaEventSynchronize(c->ev_wg_staged));  // previous upload has left the staging buffer
+    }
+    std::memcpy(c->wg_stage, wg, bytes);
+    CU_CHECK(launch_small_copy(L.wg.p, c->wg_stage, bytes, c->stream));
+    CU_CHECK(cudaEventRecord(c->ev_wg_staged, c->stream));
     L.has_gate = true;
   });
 }
@@ -592,8 +631,9 @@ int moe_set_predictor_weights(moe_ctx* c, int layer, int slot, const uint16_t* w
     require(wp != nullptr, "null predictor weights");
     if (!L.wg.p) {
       L.wg.alloc(static_cast<size_t>(c->E) * c->d * (1 + c->n_pred));
-      CU_CHECK(cudaMemset(L.wg.p, 0, L.wg.n * 2));
+      CU_CHECK(cudaMemsetAsync(L.wg.p, 0, L.wg.n * 2, c->stream));
     }
+    CU_CHECK(cudaStreamSynchronize(c->stream));  // no enqueued forward may see a half-written gate
     CU_CHECK(cudaMemcpy(L.wg.p + static_cast<size_t>(1 + slot) * c->E * c->d, wp, static_cast<size_t>(c->E) * c->d * 2,
                         cudaMemcpyHostToDevice));
   });
@@ -674,6 +714,69 @@ int moe_layer_forward_host(moe_ctx* c, int layer, const uint16_t* x_host, int T,
     forward_device(c, layer, c->x_in.p, T, c->y_out.p, plan_mode, iteration, stats, c->stream);
     CU_CHECK(cudaMemcpyAsync(y_host, c->y_out.p, bytes, cudaMemcpyDeviceToHost, c->stream));
     CU_CHECK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int moe_layer_forward_host_async(moe_ctx* c, int layer, const uint16_t* x_host, int T, uint16_t* y_host,
+                                 int plan_mode, long iteration, int64_t* ticket) {
+  return guarded([&] {
+    require(c && x_host && y_host, "null argument");
+    require(T >= 0 && T <= c->Tmax, "token count exceeds max_tokens");
+    if (!c->h2d) {
+      CU_CHECK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+      CU_CHECK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        c->xa[i].alloc(static_cast<size_t>(c->Tmax) * c->d);
+        c->ya[i].alloc(static_cast<size_t>(c->Tmax) * c->d);
+        for (cudaEvent_t* e : {&c->ev_x_ready[i], &c->ev_x_free[i], &c->ev_y_ready[i], &c->ev_done[i]}) {
+          CU_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+          CU_CHECK(cudaEventRecord(*e, c->stream));  // "already satisfied" for the first use
+        }
+      }
+      for (cudaEvent_t& e : c->ev_ticket) CU_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int64_t tk = c->next_ticket++;
+    const int slot = static_cast<int>(tk & 1);
+    const size_t bytes = static_cast<size_t>(T) * c->d * 2;
+    // upload: wait until the call two steps back has finished reading this slot
+    CU_CHECK(cudaStreamWaitEvent(c->h2d, c->ev_x_free[slot], 0));
+    CU_CHECK(cudaMemcpyAsync(c->xa[slot].p, x_host, bytes, cudaMemcpyHostToDevice, c->h2d));
+    CU_CHECK(cudaEventRecord(c->ev_x_ready[slot], c->h2d));
+    // compute: this slot's output buffer must have been downloaded (call tk-2)
+    CU_CHECK(cudaStreamWaitEvent(c->stream, c->ev_x_ready[slot], 0));
+    CU_CHECK(cudaStreamWaitEvent(c->stream, c->ev_done[slot], 0));
+    forward_device(c, layer, c->xa[slot].p, T, c->ya[slot].p, plan_mode, iteration, nullptr, c->stream,
+                   c->ev_x_free[slot]);
+    CU_CHECK(cudaEventRecord(c->ev_y_ready[slot], c->stream));
+    // download on its own stream so it overlaps the next step's layer
+    CU_CHECK(cudaStreamWaitEvent(c->d2h, c->ev_y_ready[slot], 0));
+    CU_CHECK(cudaMemcpyAsync(y_host, c->ya[slot].p, bytes, cudaMemcpyDeviceToHost, c->d2h));
+    CU_CHECK(cudaEventRecord(c->ev_done[slot], c->d2h));
+    CU_CHECK(cudaEventRecord(c->ev_ticket[tk % moe_ctx::kTicketRing], c->d2h));
+    if (ticket) *ticket = tk;
+  });
+}
+
+int moe_host_alloc(size_t bytes, void** out) {
+  return guarded([&] {
+    require(out != nullptr, "null argument");
+    CU_CHECK(cudaHostAlloc(out, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
+  });
+}
+
+int moe_host_free(void* p) {
+  return guarded([&] {
+    if (p) CU_CHECK(cudaFreeHost(p));
+  });
+}
+
+int moe_wait(moe_ctx* c, int64_t ticket) {
+  return guarded([&] {
+    require(c != nullptr, "null context");
+    require(ticket >= 0 && ticket < c->next_ticket, "unknown ticket");
+    // this call's own completion event (a ticket more than kTicketRing calls old
+    // shares its event with a later call, which completes later: conservative)
+    CU_CHECK(cudaEventSynchronize(c->ev_ticket[ticket % moe_ctx::kTicketRing]));
   });
 }
 

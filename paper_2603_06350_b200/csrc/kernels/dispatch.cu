@@ -188,6 +188,25 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_local, const __nv_bfloat16* _
   }
 }
 
+// ------------------------------------------------------- small SM copies
+// Copies a few KB between device memory and MAPPED pinned host memory with
+// the SMs instead of a copy engine, so control data (gate histogram out,
+// exchange plan / gate weights in) never queues behind the 100+ MB token
+// uploads and result downloads that the pipelined host API keeps in flight.
+__global__ void __launch_bounds__(256) small_copy_kernel(int4* __restrict__ dst, const int4* __restrict__ src, int n16) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+
+cudaError_t launch_small_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return cudaSuccess;
+  if ((bytes & 15) || (reinterpret_cast<uintptr_t>(dst) & 15) || (reinterpret_cast<uintptr_t>(src) & 15))
+    return cudaErrorInvalidValue;
+  const int n16 = static_cast<int>(bytes / 16);
+  const int blocks = n16 / 256 + 1 < 64 ? n16 / 256 + 1 : 64;
+  small_copy_kernel<<<blocks, 256, 0, s>>>(static_cast<int4*>(dst), static_cast<const int4*>(src), n16);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------- launchers
 cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, const DevPlan* plan,
                                 int32_t* block_pre, cudaStream_t s) {
