@@ -83,57 +83,58 @@ def ncu_traffic():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled with NVML every 20 ms in a
+    background thread DURING the timed region (nvidia-smi's fields: clocks.sm,
+    clocks.max.sm, power.draw, clocks_event_reasons.*)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("nvmlClocksEventReasonHwSlowdown", "hw_slowdown"),
+               ("nvmlClocksEventReasonHwThermalSlowdown", "hw_thermal_slowdown"),
+               ("nvmlClocksEventReasonSwThermalSlowdown", "sw_thermal_slowdown"),
+               ("nvmlClocksEventReasonSwPowerCap", "sw_power_cap"),
+               ("nvmlClocksEventReasonHwPowerBrakeSlowdown", "hw_power_brake_slowdown"))
 
-    def __init__(self, gpu_index):
-        self.gpu = gpu_index
-        self.proc = None
+    def __init__(self, gpu_index, period_s=0.02):
+        self.gpu, self.period = gpu_index, period_s
+        self.rows, self.err = [], None
+
+    def _loop(self):
+        import pynvml as N
+        try:
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.gpu)
+            smax = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            while not self.stop.is_set():
+                reasons = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append(dict(sm=N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM), smax=smax,
+                                      power=N.nvmlDeviceGetPowerUsage(h) / 1000.0, reasons=reasons))
+                self.stop.wait(self.period)
+        except Exception as e:  # no NVML: report unsampled
+            self.err = repr(e)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.proc = None
+        import threading
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self._loop, daemon=True)
+        self.th.start()
         return self
 
     def __exit__(self, *a):
-        self.out = ""
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.out, _ = self.proc.communicate(timeout=5)
-            except Exception:
-                self.proc.kill()
-                self.out = ""
+        self.stop.set()
+        self.th.join(timeout=5)
 
     def summary(self):
-        rows = []
-        for line in (getattr(self, "out", "") or "").strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                rows.append(dict(sm=float(f[1]), smax=float(f[2]), power=float(f[3]),
-                                 hw=f[5], hwt=f[6], swt=f[7], swp=f[8]))
-            except ValueError:
-                continue
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        loaded = [r for r in rows if r["power"] > 200] or rows
+        import pynvml as N
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0, "error": self.err}
+        loaded = [r for r in self.rows if r["power"] > 300] or self.rows
         reasons = set()
         for r in loaded:
-            for key, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"),
-                              ("swt", "sw_thermal_slowdown"), ("swp", "sw_power_cap")):
-                if r[key].lower().startswith("active"):
+            for attr, name in self.REASONS:
+                if r["reasons"] & getattr(N, attr, 0):
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(r["sm"] for r in loaded), "sm_max_mhz": max(r["smax"] for r in rows),
-                "reasons": sorted(reasons), "samples": len(loaded)}
+        return {"sm_mhz": statistics.median(r["sm"] for r in loaded), "sm_max_mhz": max(r["smax"] for r in self.rows),
+                "reasons": sorted(reasons), "samples": len(loaded),
+                "power_w_median": statistics.median(r["power"] for r in loaded), "source": "NVML, 20 ms period"}
 
 
 def nearest_rank(values, q):
@@ -341,6 +342,7 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (2.8 GB weights + 134 MB tokens per step)",
                        "planner": "MOE_PLAN_SYNC (scale_experts + place_experts on actual loads)"},
             "p50_ms": p50, "p99_ms": p99,
+            "step_ms": [round(v, 3) for v in lat],
             "phase_ms_median": phases, "replicas_median": replicas,
             # per step: gate-weight SM copy, K1 gate, counts SM copy, plan SM copy,
             # block prefix, K3 dispatch, K4 GEMM1, K4 GEMM2, K5 combine

@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -48,6 +49,9 @@ cudaError_t launch_small_copy(void* dst, const void* src, size_t bytes, cudaStre
 cudaError_t launch_combine(const __nv_bfloat16* y_local, const __nv_bfloat16* y_return, int T, int d, int k,
                            const uint32_t* row_code, const float* wts, __nv_bfloat16* y, int num_sms,
                            cudaStream_t s);
+cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
+                                    const int* nseg, int n_total, int k_total, int b_rows_per_slot,
+                                    __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream);
 cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                 __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream);
@@ -195,7 +199,8 @@ struct DevBuf {
 
 struct Layer {
   DevBuf<uint16_t> w13, w2, wg;  // pools
-  CUtensorMap tmB1, tmB2;
+  CUtensorMap tmB1, tmB2;    // 256-row boxes (1-SM kernel: whole N tile per CTA)
+  CUtensorMap tmB1h, tmB2h;  // 128-row boxes (2-SM kernel: each CTA stages half of N)
   bool has_gate = false;
   std::vector<char> expert_loaded;
   std::vector<int32_t> rep_counts, rep_gpu;  // placement (host)
@@ -225,6 +230,7 @@ struct EventSet {
 struct moe_ctx {
   moe_ctx_desc desc{};
   int E = 0, k = 0, d = 0, ff = 0, G = 1, rank = 0, Tmax = 0, n_pred = 0, num_sms = 148;
+  int gemm_variant = 0;  // 0 auto, 1 force 1-SM, 2 force 2-SM (env MOE_GEMM_VARIANT=1sm|2sm)
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
   std::vector<Layer> layers;
@@ -349,13 +355,27 @@ void stage_exchange(moe_ctx* c, bool forward, cudaStream_t s) {
   g_nccl.check(g_nccl.GroupEnd(), "ncclGroupEnd");
 }
 
-void stage_expert(moe_ctx* c, int layer, cudaStream_t s) {
+// K4: which = 0 -> GEMM1 (X -> H, SwiGLU epilogue), 1 -> GEMM2 (H -> Y).
+// Default: the 1-SM kernel.  The 2-SM (cta_group::2, 256-row tile) kernel
+// reaches ~88% tensor-pipe utilisation per clock vs ~80%, but under the
+// B200's 1 kW cap it settles ~190 MHz lower and nets ~4% less throughput on
+// the Mixtral layer (profiles/ab_gemm_variants_r01.md), so it is opt-in
+// (MOE_GEMM_VARIANT=2sm) until it is made more energy-efficient.
+void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s) {
   Layer& L = c->layers[layer];
-  const int grid = c->num_sms;
-  CU_CHECK(launch_grouped_gemm(0, &c->tmA1, &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d, 2 * c->ff,
-                               reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, grid, s));
-  CU_CHECK(launch_grouped_gemm(1, &c->tmA2, &L.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
-                               reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, grid, s));
+  const bool two_sm = c->gemm_variant == 2;
+  auto fn = two_sm ? launch_grouped_gemm_2sm : launch_grouped_gemm;
+  if (which == 0)
+    CU_CHECK(fn(0, &c->tmA1, two_sm ? &L.tmB1h : &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d, 2 * c->ff,
+                reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, c->num_sms, s));
+  else
+    CU_CHECK(fn(1, &c->tmA2, two_sm ? &L.tmB2h : &L.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
+                reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s));
+}
+
+void stage_expert(moe_ctx* c, int layer, cudaStream_t s) {
+  launch_ffn_gemm(c, layer, 0, s);
+  launch_ffn_gemm(c, layer, 1, s);
 }
 
 void stage_combine(moe_ctx* c, uint16_t* y, int T, cudaStream_t s) {
@@ -378,6 +398,8 @@ void ensure_pools(moe_ctx* c, Layer& L) {
   L.w2.alloc(static_cast<size_t>(c->E) * c->d * c->ff);
   L.tmB1 = make_kmajor_map(L.w13.p, static_cast<uint64_t>(c->E) * 2 * c->ff, c->d, 256);
   L.tmB2 = make_kmajor_map(L.w2.p, static_cast<uint64_t>(c->E) * c->d, c->ff, 256);
+  L.tmB1h = make_kmajor_map(L.w13.p, static_cast<uint64_t>(c->E) * 2 * c->ff, c->d, 128);
+  L.tmB2h = make_kmajor_map(L.w2.p, static_cast<uint64_t>(c->E) * c->d, c->ff, 128);
   L.expert_loaded.assign(c->E, 0);
 }
 
@@ -411,14 +433,9 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   mark(3);
   stage_exchange(c, true, s);
   mark(4);
-  const int nseg = c->plan.dev.nseg;
-  (void)nseg;
-  Layer& LL = c->layers[layer];
-  CU_CHECK(launch_grouped_gemm(0, &c->tmA1, &LL.tmB1, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d, 2 * c->ff,
-                               reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, c->num_sms, s));
+  launch_ffn_gemm(c, layer, 0, s);
   mark(5);
-  CU_CHECK(launch_grouped_gemm(1, &c->tmA2, &LL.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
-                               reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s));
+  launch_ffn_gemm(c, layer, 1, s);
   mark(6);
   stage_exchange(c, false, s);
   mark(7);
@@ -497,6 +514,10 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->Tmax = D.max_tokens;
     c->n_pred = std::max(0, D.num_predictor_targets);
     c->num_sms = prop.multiProcessorCount;
+    if (const char* v = std::getenv("MOE_GEMM_VARIANT")) {
+      const std::string s(v);
+      c->gemm_variant = s == "1sm" ? 1 : (s == "2sm" ? 2 : 0);
+    }
     c->registry = moeless::ReplicaRegistry(std::max(0, D.keep_alive_iters));
     c->layers.resize(D.num_layers);
     CU_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));

@@ -64,7 +64,7 @@ struct TileCoord {
   int seg, m, n;
 };
 
-template <int GM>
+template <int GM, int TILE_M = BM>
 __device__ __forceinline__ TileCoord decode_tile(int t, const int* seg_tiles, const int4* segs, int nseg,
                                                  int n_tiles) {
   // binary search: last s with seg_tiles[s] <= t
@@ -75,7 +75,7 @@ __device__ __forceinline__ TileCoord decode_tile(int t, const int* seg_tiles, co
   }
   const int s = lo;
   const int local = t - seg_tiles[s];
-  const int m_tiles = (segs[s].y + BM - 1) / BM;
+  const int m_tiles = (segs[s].y + TILE_M - 1) / TILE_M;
   const int per_group = GM * n_tiles;
   const int g = local / per_group;
   const int gm = min(GM, m_tiles - g * GM);
@@ -252,8 +252,227 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   }
 }
 
+// ===================================================================
+// 2-CTA variant: a cluster of 2 SMs computes a 256x256 tile with
+// tcgen05.mma.cta_group::2 (M=256).  Each CTA stages its own 128 A rows and
+// HALF of the 256 B rows (the W1 block on CTA 0, the W3 block on CTA 1 for
+// GEMM1), so per SM and k-block it moves 32 KB instead of 48 KB through
+// L2 -> smem for the same MMA work; both CTAs' TMA bytes land on the leader's
+// full barrier, the leader's single MMA thread issues for the pair, commits
+// multicast to both CTAs' empty / tmem-full barriers, and both CTAs' epilogue
+// warps (each reading its own TMEM: 128 rows x 256 cols) release the
+// accumulator on the leader's tmem-empty barrier (8 arrivals).
+constexpr int BM2 = 256;                 // rows per cluster tile
+constexpr int STAGES2 = 6;
+constexpr uint32_t kHalfA = 128 * BK * 2, kHalfB = 128 * BK * 2;  // 16 KB each, per CTA
+constexpr uint32_t kStage2 = kHalfA + kHalfB;
+
+template <int EPI> constexpr int kGroupM2 = EPI == 0 ? 16 : 8;  // in 256-row tiles
+
+struct SmemLayout2 {
+  static constexpr uint32_t a = 0;
+  static constexpr uint32_t b = a + STAGES2 * kHalfA;
+  static constexpr uint32_t bars = b + STAGES2 * kHalfB;
+  static constexpr uint32_t n_bars = 2 * STAGES2 + 4;
+  static constexpr uint32_t tmem_slot = bars + n_bars * 8;
+  static constexpr uint32_t seg_tiles = tmem_slot + 16;
+  static constexpr uint32_t segs = seg_tiles + (kMaxSegs + 1) * 4 + 12;
+  static constexpr uint32_t end = ((segs + 15) / 16) * 16 + kMaxSegs * 16;
+};
+constexpr uint32_t kSmemBytes2 = SmemLayout2::end + 1024;
+static_assert(kSmemBytes2 <= 232448, "smem budget (2-CTA)");
+
+template <int EPI>
+__device__ __forceinline__ void store_accumulator(uint32_t taddr, __nv_bfloat16* __restrict__ out, size_t grow,
+                                                  bool valid, int n, int out_ld) {
+  if constexpr (EPI == EPI_SWIGLU) {
+    __nv_bfloat16* dst = out + grow * out_ld + n * (BN / 2);
+#pragma unroll 1
+    for (int ch = 0; ch < BN / 2 / 32; ++ch) {
+      uint32_t g[32], u[32];
+      tmem_ld_32x32b_x32(taddr + ch * 32, g);
+      tmem_ld_32x32b_x32(taddr + BN / 2 + ch * 32, u);
+      tc_wait_ld();
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float h0 = silu(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
+        const float h1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+        packed[i] = pack_bf16(h0, h1);
+      }
+      if (valid) {
+        int4* p = reinterpret_cast<int4*>(dst + ch * 32);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) p[v] = make_int4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+      }
+    }
+  } else {
+    __nv_bfloat16* dst = out + grow * out_ld + n * BN;
+#pragma unroll 1
+    for (int ch = 0; ch < BN / 32; ++ch) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(taddr + ch * 32, r);
+      tc_wait_ld();
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) packed[i] = pack_bf16(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+      if (valid) {
+        int4* p = reinterpret_cast<int4*>(dst + ch * 32);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) p[v] = make_int4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+      }
+    }
+  }
+}
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total, int k_total,
+                        int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout2::bars);
+  uint64_t* full = bars;                      // used on the leader only
+  uint64_t* empty = bars + STAGES2;           // per CTA
+  uint64_t* tfull = bars + 2 * STAGES2;       // per CTA
+  uint64_t* tempty = bars + 2 * STAGES2 + 2;  // used on the leader only (8 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SmemLayout2::tmem_slot);
+  int* seg_tiles = reinterpret_cast<int*>(smem + SmemLayout2::seg_tiles);
+  int4* segs = reinterpret_cast<int4*>(smem + SmemLayout2::segs);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1, num_clusters = gridDim.x >> 1;
+  const int nseg = min(*nseg_g, kMaxSegs);
+  const int n_tiles = n_total / BN;
+
+  for (int i = threadIdx.x; i < nseg; i += kThreads) segs[i] = reinterpret_cast<const int4*>(segs_g)[i];
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_2sm<kTmemCols>(tmem_slot);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int s = 0; s < nseg; ++s) {
+      seg_tiles[s] = acc;
+      acc += ((segs[s].y + BM2 - 1) / BM2) * n_tiles;
+    }
+    seg_tiles[nseg] = acc;
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised before any remote arrive / TMA
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_tiles = nseg > 0 ? seg_tiles[nseg] : 0;
+  const int num_kb = k_total / BK;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- producer (both CTAs)
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+      for (int t = cluster; t < total_tiles; t += num_clusters) {
+        const TileCoord c = decode_tile<kGroupM2<EPI>, BM2>(t, seg_tiles, segs, nseg, n_tiles);
+        const int a_row = segs[c.seg].x + c.m * BM2 + static_cast<int>(rank) * 128;
+        const int b_row = segs[c.seg].z * b_rows_per_slot + c.n * BN + static_cast<int>(rank) * 128;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStage2);
+          tma_load_2d_2sm(smem + SmemLayout2::a + stage * kHalfA, &tmA, &full[stage], kb * BK, a_row, pol_a);
+          tma_load_2d_2sm(smem + SmemLayout2::b + stage * kHalfB, &tmB, &full[stage], kb * BK, b_row, pol_b);
+          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer (leader)
+    if (leader && elect_one()) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM2, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      const uint32_t a_base = smem_u32(smem + SmemLayout2::a);
+      const uint32_t b_base = smem_u32(smem + SmemLayout2::b);
+      for (int t = cluster; t < total_tiles; t += num_clusters) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = umma_desc_sw128(a_base + stage * kHalfA);
+          const uint64_t bdesc = umma_desc_sw128(b_base + stage * kHalfB);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            tc_mma_bf16_2sm(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          tc_commit_2sm_mc(&empty[stage], 0x3);
+          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_2sm_mc(&tfull[acc], 0x3);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // --------------------------------------------------------- epilogue (both CTAs)
+    const int quarter = warp & 3;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = cluster; t < total_tiles; t += num_clusters) {
+      const TileCoord c = decode_tile<kGroupM2<EPI>, BM2>(t, seg_tiles, segs, nseg, n_tiles);
+      const int4 sg = segs[c.seg];
+      const int row = c.m * BM2 + static_cast<int>(rank) * 128 + quarter * 32 + lane;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+      store_accumulator<EPI>(taddr, out, static_cast<size_t>(sg.x + row), row < sg.y, c.n, out_ld);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer must not exit while the leader still multicasts to it
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2sm<kTmemCols>(tmem_base);
+  }
+}
+
 // --------------------------------------------------------------- host side
 static_assert(kSmemBytes <= 232448, "smem budget");
+
+cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
+                                    const int* nseg, int n_total, int k_total, int b_rows_per_slot,
+                                    __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream) {
+  if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(grouped_gemm_2sm_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes2);
+    cudaFuncSetAttribute(grouped_gemm_2sm_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes2);
+    configured = true;
+  }
+  const int grid = num_ctas & ~1;
+  if (epi == EPI_SWIGLU)
+    grouped_gemm_2sm_kernel<EPI_SWIGLU><<<grid, kThreads, kSmemBytes2, stream>>>(
+        *tmA, *tmB, segs, nseg, n_total, k_total, b_rows_per_slot, out, out_ld);
+  else
+    grouped_gemm_2sm_kernel<EPI_STORE><<<grid, kThreads, kSmemBytes2, stream>>>(
+        *tmA, *tmB, segs, nseg, n_total, k_total, b_rows_per_slot, out, out_ld);
+  return cudaGetLastError();
+}
 
 int gemm_smem_bytes() { return static_cast<int>(kSmemBytes); }
 
