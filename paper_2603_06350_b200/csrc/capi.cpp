@@ -46,6 +46,7 @@ cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, 
                             const int32_t* block_pre, const DevPlan* plan, __nv_bfloat16* xp_local,
                             __nv_bfloat16* xp_send, uint32_t* row_code, cudaStream_t s);
 cudaError_t launch_small_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
+cudaError_t launch_plan_local(const int32_t* counts, int E, DevPlan* plan, cudaStream_t s);
 cudaError_t launch_combine(const __nv_bfloat16* y_local, const __nv_bfloat16* y_return, int T, int d, int k,
                            const uint32_t* row_code, const float* wts, __nv_bfloat16* y, int num_sms,
                            cudaStream_t s);
@@ -207,6 +208,12 @@ struct Layer {
   bool has_placement = false;
 };
 
+struct PendingPlan {
+  bool active = false;
+  int layer = 0, mode = 0;
+  long iteration = 0;
+};
+
 struct EventSet {
   static constexpr int N = 10;
   cudaEvent_t ev[N] = {};
@@ -262,6 +269,9 @@ struct moe_ctx {
   const uint16_t* cur_x = nullptr;
   std::vector<int64_t> last_counts;
   int last_warm = 0, last_cold = 0;
+  // single-GPU forward: host planner work deferred until the histogram lands
+  PendingPlan pending;
+  cudaEvent_t ev_counts = nullptr;
 };
 
 namespace {
@@ -322,8 +332,9 @@ void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int3
   *c->hplan = c->plan.dev;
 }
 
-void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s) {
-  CU_CHECK(launch_small_copy(c->dplan.p, c->hplan, sizeof(DevPlan), s));  // SM copy from mapped pinned memory
+void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool upload_plan = true) {
+  if (upload_plan)
+    CU_CHECK(launch_small_copy(c->dplan.p, c->hplan, sizeof(DevPlan), s));  // SM copy from mapped pinned memory
   const int nblk = gate_num_blocks(T);
   CU_CHECK(launch_block_prefix(c->block_counts.p, nblk, c->E, c->dplan.p, c->block_pre.p, s));
   CU_CHECK(launch_dispatch(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d, c->E, c->k, c->ids.p, c->block_pre.p,
@@ -386,6 +397,15 @@ void stage_combine(moe_ctx* c, uint16_t* y, int T, cudaStream_t s) {
 
 cudaStream_t pick(moe_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->stream; }
 
+// Run the host planner for the last single-GPU forward once its histogram is
+// in mapped host memory (waits only for that forward's gate kernel).
+void flush_pending_plan(moe_ctx* c) {
+  if (!c->pending.active) return;
+  c->pending.active = false;
+  CU_CHECK(cudaEventSynchronize(c->ev_counts));
+  stage_plan(c, c->pending.layer, c->pending.mode, c->pending.iteration, c->h_counts);
+}
+
 Layer& layer_at(moe_ctx* c, int layer) {
   require(c != nullptr, "null context");
   require(layer >= 0 && layer < static_cast<int>(c->layers.size()), "layer out of range");
@@ -415,20 +435,34 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   auto mark = [&](int i) {
     if (timed) CU_CHECK(cudaEventRecord(ev.ev[i], s));
   };
+  flush_pending_plan(c);  // the previous call's deferred planner work (G = 1)
   mark(0);
   stage_gate(c, L, x, T, s, nullptr);
   if (c->G > 1) {
+    // NCCL needs every chunk size on the host: one round trip per layer.
     require(c->desc.exchange_mode == MOE_EXCHANGE_NCCL, "staged API required for external exchange");
     g_nccl.check(g_nccl.AllGather(c->counts.p, c->counts_all.p, c->E, ncclInt32, c->comm, s), "ncclAllGather");
     CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * c->E), s));
+    mark(1);
+    CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram
+    stage_plan(c, layer, plan_mode, iteration, c->h_counts);
+    mark(2);
+    stage_dispatch(c, x, T, s);
   } else {
+    // One GPU: the device builds the dispatch plan from its own histogram and
+    // the layer never waits for the host.  The MoEless planner (scale_experts
+    // / place_experts / registry, MOE_PLAN_SYNC) runs on the histogram as soon
+    // as it lands in mapped host memory — its replica decisions cannot change
+    // single-GPU work (co-located replicas share one GEMM segment), so running
+    // it off the critical path keeps the reference's per-layer semantics.
     CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * c->E), s));
+    CU_CHECK(cudaEventRecord(c->ev_counts, s));
+    mark(1);
+    CU_CHECK(launch_plan_local(c->counts.p, c->E, c->dplan.p, s));
+    c->pending = PendingPlan{true, layer, plan_mode, iteration};
+    mark(2);
+    stage_dispatch(c, x, T, s, /*upload_plan=*/false);
   }
-  mark(1);
-  CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram
-  stage_plan(c, layer, plan_mode, iteration, c->h_counts);
-  mark(2);
-  stage_dispatch(c, x, T, s);
   if (x_consumed) CU_CHECK(cudaEventRecord(x_consumed, s));  // x is not read after dispatch
   mark(3);
   stage_exchange(c, true, s);
@@ -443,6 +477,7 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   mark(8);
   if (timed) {
     CU_CHECK(cudaEventSynchronize(ev.ev[8]));
+    flush_pending_plan(c);
     st->gate_ms = ev.ms(0, 1);
     st->plan_ms = ev.ms(1, 2);
     st->dispatch_ms = ev.ms(2, 3);
@@ -545,6 +580,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     CU_CHECK(cudaHostAlloc(&c->hplan, sizeof(DevPlan), cudaHostAllocMapped));
     CU_CHECK(cudaHostAlloc(&c->h_counts, pad16(sizeof(int32_t) * c->E * c->G), cudaHostAllocMapped));
     c->events.create();
+    CU_CHECK(cudaEventCreateWithFlags(&c->ev_counts, cudaEventDisableTiming));
     if (c->G > 1 && D.exchange_mode == MOE_EXCHANGE_NCCL) {
       require(D.nccl_unique_id != nullptr, "nccl_unique_id required for world_size > 1");
       g_nccl.load();
@@ -567,6 +603,7 @@ int moe_ctx_destroy(moe_ctx* c) {
     if (c->h_counts) cudaFreeHost(c->h_counts);
     if (c->wg_stage) cudaFreeHost(c->wg_stage);
     if (c->ev_wg_staged) cudaEventDestroy(c->ev_wg_staged);
+    if (c->ev_counts) cudaEventDestroy(c->ev_counts);
     if (c->h2d) {
       cudaStreamSynchronize(c->h2d);
       cudaStreamSynchronize(c->d2h);
@@ -594,6 +631,7 @@ int moe_ctx_sync(moe_ctx* c) {
   return guarded([&] {
     require(c, "null context");
     CU_CHECK(cudaStreamSynchronize(c->stream));
+    flush_pending_plan(c);
   });
 }
 
@@ -798,6 +836,7 @@ int moe_wait(moe_ctx* c, int64_t ticket) {
     // this call's own completion event (a ticket more than kTicketRing calls old
     // shares its event with a later call, which completes later: conservative)
     CU_CHECK(cudaEventSynchronize(c->ev_ticket[ticket % moe_ctx::kTicketRing]));
+    flush_pending_plan(c);
   });
 }
 
@@ -807,6 +846,7 @@ int moe_forward_begin(moe_ctx* c, int layer, const uint16_t* x, int T, const int
     require(x != nullptr, "null input");
     require(T >= 0 && T <= c->Tmax, "token count exceeds max_tokens");
     cudaStream_t s = pick(c, stream);
+    flush_pending_plan(c);
     if (!counts_all) {
       // stage 1: gate only; caller reads counts (moe_buffer 7), all-gathers, calls again
       stage_gate(c, L, x, T, s, nullptr);
@@ -845,6 +885,7 @@ int moe_forward_end(moe_ctx* c, uint16_t* y, void* stream) {
 int moe_buffer(moe_ctx* c, int which, void** ptr, int64_t* rows) {
   return guarded([&] {
     require(c && ptr, "null argument");
+    flush_pending_plan(c);
     int64_t r = 0;
     switch (which) {
       case 0: *ptr = c->xp.p; r = c->plan.rows_local; break;

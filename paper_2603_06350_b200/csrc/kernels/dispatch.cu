@@ -188,6 +188,53 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_local, const __nv_bfloat16* _
   }
 }
 
+// ------------------------------------------------------- on-device plan (G = 1)
+// Single GPU: every replica is local and co-located replicas of an expert are
+// one GEMM segment, so the dispatch plan is an exclusive scan of the gate
+// histogram — built on the device, no host round trip.  Row placement is
+// identical to the host plan's (expert e's rows start at sum_{e'<e} n_e').
+__global__ void __launch_bounds__(256) plan_local_kernel(const int32_t* __restrict__ counts, int E,
+                                                         DevPlan* __restrict__ plan) {
+  __shared__ int base[kMaxExperts + 1];
+  __shared__ int seg_idx[kMaxExperts + 1];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int acc = 0, ns = 0;
+    for (int e = 0; e < E; ++e) {
+      base[e] = acc;
+      seg_idx[e] = ns;
+      const int n = counts[e];
+      acc += n;
+      ns += n > 0 ? 1 : 0;
+    }
+    base[E] = acc;
+    seg_idx[E] = ns;
+    plan->E = E;
+    plan->R = E;
+    plan->G = 1;
+    plan->rank = 0;
+    plan->nseg = ns;
+    plan->rows_local = acc;
+    plan->rows_send = 0;
+    plan->rep_base[E] = E;
+  }
+  __syncthreads();
+  for (int e = tid; e < E; e += blockDim.x) {
+    const int n = counts[e];
+    plan->n_e[e] = n;
+    plan->src_off[e] = 0;
+    plan->rep_base[e] = e;  // one (merged) replica per expert
+    plan->rep_row_base[e] = base[e];
+    plan->rep_remote[e] = 0;
+    if (n > 0) plan->segs[seg_idx[e]] = GemmSeg{base[e], n, e, 0};
+  }
+}
+
+cudaError_t launch_plan_local(const int32_t* counts, int E, DevPlan* plan, cudaStream_t s) {
+  plan_local_kernel<<<1, 256, 0, s>>>(counts, E, plan);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------- small SM copies
 // Copies a few KB between device memory and MAPPED pinned host memory with
 // the SMs instead of a copy engine, so control data (gate histogram out,
