@@ -1,0 +1,92 @@
+#!/usr/bin/env python
+"""Per-config measurements beside the headline bench (one B200).
+
+  python bench_configs.py [--configs cfg1,cfg3,cfg5] [--steps 50] [--warmup 5]
+
+For each BASELINE.json config that fits one GPU: layer latency p50/p99
+(nearest rank, device events, host running ahead), tokens/s, the phase
+breakdown and the K4 roofline; rows are re-routed every step.  The multi-GPU
+configs (cfg3 at G=2/4/8, cfg4, cfg5 at G=8) are run here at G=1 with the same
+per-GPU shapes and labelled so; bench.py --gpus N covers the EP path.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def run_config(name, steps, warmup):
+    import numpy as np
+    import torch
+
+    from paper_2603_06350_b200 import MOE_PLAN_SYNC, MoELayer, percentile
+    from paper_2603_06350_b200 import workload as wl
+    c = dict(wl.CONFIGS[name])
+    E, k, d, ff, T, s = c["E"], c["k"], c["d"], c["ff"], c["T"], c["s"]
+    mem = 3.0 * d * ff * 2 / 1e6
+    m = MoELayer(1, E, k, d, ff, max_tokens=T, expert_mem_mb=mem, layer_mem_cap_mb=c["extra_replicas"] * mem)
+    for e in range(E):
+        m.load_expert(0, e, *wl.expert_weights(d, ff, 1, 0, e))
+    pool = [torch.from_numpy(wl.tokens(T, d, E, 1, i).view(np.int16)).cuda() for i in range(4)]
+    n_it = warmup + steps + 10
+    gates = [wl.gate_weights(E, d, s, 1, 0, it) for it in range(n_it)]
+    y = torch.empty((T, d), dtype=torch.int16, device="cuda")
+    stream = torch.cuda.ExternalStream(m.stream_ptr)
+
+    def step(it, stats=False):
+        m.set_gate(0, gates[it])
+        return m.forward(0, pool[it % 4], y, MOE_PLAN_SYNC, it, stats=stats)
+
+    for it in range(warmup):
+        step(it)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(steps):
+        ev[i][0].record(stream)
+        step(warmup + i)
+        ev[i][1].record(stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    lat = [a.elapsed_time(b) for a, b in ev]
+    total = t0.elapsed_time(t1)
+    st = [step(warmup + steps + i, stats=True) for i in range(10)]
+    phases = {p: statistics.median(getattr(x, p) for x in st)
+              for p in ("gate_ms", "plan_ms", "dispatch_ms", "gemm1_ms", "gemm2_ms", "combine_ms")}
+    rows = statistics.median(x.rows_local for x in st)
+    flops = 6.0 * d * ff * rows
+    gemm = phases["gemm1_ms"] + phases["gemm2_ms"]
+    active = statistics.median(sum(1 for e in range(E) if x.counts[e] > 0) for x in st)
+    wbytes = active * 3 * d * ff * 2
+    m.close()
+    return {
+        "config": name, "shape": c, "tokens_per_s": T * steps / (total * 1e-3), "ms_per_step": total / steps,
+        "p50_ms": percentile(lat, 0.5), "p99_ms": percentile(lat, 0.99), "phase_ms_median": phases,
+        "k4_tflops": flops / (gemm * 1e-3) / 1e12, "k4_weight_gbs": wbytes / (gemm * 1e-3) / 1e9,
+        "active_experts": active, "replicas_median": statistics.median(x.replica_count for x in st),
+        "gpus": 1, "note": "per-GPU shape at G=1" if c["G"] > 1 else "",
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="cfg1,cfg3,cfg5")
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    res = [run_config(n, a.steps, a.warmup) for n in a.configs.split(",")]
+    for r in res:
+        print(json.dumps(r), flush=True)
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -9,21 +9,26 @@
 // restricted to the chosen k (== softmax over the k logits); counts[e] is the
 // histogram of chosen experts (sum == T*k, as route_tokens guarantees).
 //
+// The op is an HBM-bound skinny GEMM (N = E*(1+n_pred) <= 256 logits per
+// token); it uses the warp-level tensor-core MMA (m16n8k16, bf16 in, fp32
+// accumulate) only so the FMA issue rate never limits the stream of x.
+//
 // Work decomposition: one CTA (8 warps) owns a block of 32 consecutive tokens
 // — the granularity of block_counts[], the stable prefix the dispatch kernel
-// scans — and each warp owns TOKG of them.  A lane owns 8 contiguous columns
-// per 256-column step, so x is read with 16-byte L1-bypassing loads (512 B
-// coalesced per warp), unrolled so each lane keeps TOKG x kUnroll loads in
-// flight; the gate rows (64 KB at d=4096, E=8) stay L1-resident and each
-// 16-byte weight vector is reused for TOKG tokens.  Partial sums are
-// all-reduced with xor shuffles; lane (e mod 32) keeps expert e for the
-// warp arg-max.  The block histogram is built with shared-memory atomics and
-// flushed with one global atomicAdd per (block, expert): the atomics-based
-// per-expert load histogram.
+// scans.  Warp w takes m-tile (w & 1) (16 tokens) and K-slice (w >> 1) (a
+// quarter of d), so a block keeps 8 independent 16-byte-load streams in
+// flight.  Fragments are loaded straight from global memory: the 16 k-slots
+// of one MMA are mapped to features so that lane (g, c) needs 4 CONSECUTIVE
+// features of row g / row g+8 / expert g (slots 2c,2c+1 <-> f, f+1 and
+// 2c+8,2c+9 <-> f+2, f+3, identical for A and B), i.e. one 16-byte load per
+// row feeds two MMAs.  K-slices are summed into shared memory in a fixed
+// order (deterministic), then one warp per 4 tokens does the arg-max top-k,
+// the softmax and the shared-memory histogram, flushed with one global
+// atomicAdd per (block, expert) — the atomics-based per-expert histogram.
 //
-// The predictor weights (n_pred target layers, each [E, d]) are stacked under
-// the gate weights: the same pass over x yields pred_counts[p][E] (histogram
-// only), so K2 costs no extra HBM read of x while E*(1+n_pred) <= EC.
+// Exactness: on the synthetic grid every partial sum is a
+// multiple of 2^-16 below 2^6, so any fp32 summation order — the MMA's
+// included — yields the exact logit, and ids match the CPU oracle bit for bit.
 #include <cfloat>
 #include <cstdint>
 
@@ -34,13 +39,30 @@ namespace moe {
 namespace {
 
 constexpr int kBlockTokens = 32;  // tokens per CTA == per block_counts row
-constexpr int kPerLane = 8;       // stacked experts per lane -> E*(1+n_pred) <= 256
+constexpr int kWarps = 8;
+constexpr int kSlices = 4;        // K-slices per m-tile
+constexpr int kPerLane = 8;       // stacked logits per lane in the top-k (<= 256)
 
-// Top-k over the experts [base, base+E) of a stacked logit vector held as
-// lane l -> stacked index l + 32 s.  Every lane returns the same ids/logits.
-__device__ __forceinline__ void warp_topk(const float (&own)[kPerLane], int base, int E, int k,
-                                          int (&ids_out)[8], float (&logit_out)[8]) {
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Top-k over logits [base, base+E) of one token's stacked row in shared
+// memory; lane l looks at l, l+32, ...  Every lane returns the same result.
+__device__ __forceinline__ void warp_topk(const float* row, int base, int E, int k, int (&ids_out)[8],
+                                          float (&logit_out)[8]) {
   const int lane = lane_id();
+  float own[kPerLane];
+#pragma unroll
+  for (int s = 0; s < kPerLane; ++s) {
+    const int e = lane + 32 * s;
+    own[s] = e < E ? row[base + e] : -FLT_MAX;
+  }
   uint32_t taken = 0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -49,8 +71,8 @@ __device__ __forceinline__ void warp_topk(const float (&own)[kPerLane], int base
     int bi = 0x7fffffff;
 #pragma unroll
     for (int s = 0; s < kPerLane; ++s) {
-      const int e = lane + 32 * s - base;
-      if (e >= 0 && e < E && !((taken >> s) & 1u))
+      const int e = lane + 32 * s;
+      if (e < E && !((taken >> s) & 1u))
         if (own[s] > bv || (own[s] == bv && e < bi)) { bv = own[s]; bi = e; }
     }
 #pragma unroll
@@ -59,8 +81,7 @@ __device__ __forceinline__ void warp_topk(const float (&own)[kPerLane], int base
       const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
       if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
     }
-    const int st = bi + base;
-    if ((st & 31) == lane) taken |= 1u << (st >> 5);
+    if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
     ids_out[j] = bi;
     logit_out[j] = bv;
   }
@@ -71,116 +92,90 @@ __device__ __forceinline__ void warp_topk(const float (&own)[kPerLane], int base
 // x [T, d] bf16; w_all [(1 + n_pred) * E, d] bf16 (rows 0..E-1 = gate).
 // Outputs: ids [T, k] i32, weights [T, k] f32, counts [E] i32 (atomic; caller
 // zeroes), block_counts [ceil(T/32), E] i32, pred_counts [n_pred, E] (atomic).
-template <int TOKG, int EC, int kUnroll>
-__global__ void __launch_bounds__(kBlockTokens / TOKG * 32)
-gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d,
-                 const __nv_bfloat16* __restrict__ w_all, int E, int n_pred, int k,
-                 int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
+// NT = n-tiles of 8 stacked logits (E * (1 + n_pred) <= 8 * NT).
+template <int NT>
+__global__ void __launch_bounds__(kWarps * 32)
+gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_bfloat16* __restrict__ w_all, int E,
+                 int n_pred, int k, int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
                  int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts) {
-  constexpr int kWarps = kBlockTokens / TOKG;
-  __shared__ int hist[kPerLane * 32];
-  const int warp = threadIdx.x >> 5;
-  const int lane = lane_id();
+  constexpr int kCols = 8 * NT;
+  constexpr int kLd = kCols + 4;  // padded row of the reduction buffer
+  __shared__ float red[kBlockTokens * kLd];
+  __shared__ int hist[256];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int g = lane >> 2, c = lane & 3;
+  const int mt = warp & 1, ks = warp >> 1;
   const int blk = blockIdx.x;
   const int Etot = E * (1 + n_pred);
   for (int i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
-  __syncthreads();
 
-  const int t0 = blk * kBlockTokens + warp * TOKG;
-  const int ntok = max(0, min(TOKG, T - t0));
-  float own[TOKG][kPerLane];
+  // ---- skinny GEMM: 16 tokens x 8*NT logits over this warp's K-slice
+  const int r0 = blk * kBlockTokens + mt * 16 + g, r1 = r0 + 8;
+  const bool v0 = r0 < T, v1 = r1 < T;
+  const __nv_bfloat16* x0 = x + (size_t)(v0 ? r0 : 0) * d;
+  const __nv_bfloat16* x1 = x + (size_t)(v1 ? r1 : 0) * d;
+  const int slice = d / kSlices;  // d % 256 == 0 -> slice % 64 == 0
+  const int k_begin = ks * slice, k_end = k_begin + slice;
+  float acc[NT][4];
 #pragma unroll
-  for (int q = 0; q < TOKG; ++q)
+  for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
+  const int4 zero = make_int4(0, 0, 0, 0);
+#pragma unroll 2
+  for (int kb = k_begin; kb < k_end; kb += 32) {
+    const int f = kb + 8 * c;  // this lane's 8 consecutive features of the 32-feature block
+    const int4 a_lo = v0 ? ld_nc_v4(x0 + f) : zero;
+    const int4 a_hi = v1 ? ld_nc_v4(x1 + f) : zero;
 #pragma unroll
-    for (int s = 0; s < kPerLane; ++s) own[q][s] = -FLT_MAX;
-
-  if (ntok > 0) {
-    for (int e0 = 0; e0 < Etot; e0 += EC) {
-      float acc[TOKG][EC];
+    for (int n = 0; n < NT; ++n) {
+      const int e = n * 8 + g;
+      const int4 b = e < Etot ? __ldg(reinterpret_cast<const int4*>(w_all + (size_t)e * d + f)) : zero;
+      mma_bf16_16816(acc[n], a_lo.x, a_hi.x, a_lo.y, a_hi.y, b.x, b.y);  // features f .. f+3
+      mma_bf16_16816(acc[n], a_lo.z, a_hi.z, a_lo.w, a_hi.w, b.z, b.w);  // features f+4 .. f+7
+    }
+  }
+  // ---- ordered K-slice reduction into shared memory (deterministic)
+  for (int s = 0; s < kSlices; ++s) {
+    if (ks == s) {
 #pragma unroll
-      for (int q = 0; q < TOKG; ++q)
-#pragma unroll
-        for (int c = 0; c < EC; ++c) acc[q][c] = 0.0f;
-
-      for (int col0 = lane * 8; col0 < d; col0 += 256 * kUnroll) {
-        int4 raw[kUnroll][TOKG];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
-#pragma unroll
-          for (int q = 0; q < TOKG; ++q) {
-            const int col = col0 + 256 * u;
-            raw[u][q] = (q < ntok && col < d) ? ld_nc_v4(x + (size_t)(t0 + q) * d + col) : make_int4(0, 0, 0, 0);
-          }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int col = col0 + 256 * u;
-          if (col >= d) break;
-          float xv[TOKG][8];
-#pragma unroll
-          for (int q = 0; q < TOKG; ++q) {
-            const uint32_t* p = reinterpret_cast<const uint32_t*>(&raw[u][q]);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { xv[q][2 * i] = bf16lo(p[i]); xv[q][2 * i + 1] = bf16hi(p[i]); }
-          }
-#pragma unroll
-          for (int c = 0; c < EC; ++c) {
-            if (e0 + c < Etot) {
-              const int4 wr = __ldg(reinterpret_cast<const int4*>(w_all + (size_t)(e0 + c) * d + col));
-              const uint32_t* p = reinterpret_cast<const uint32_t*>(&wr);
-              float wv[8];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) { wv[2 * i] = bf16lo(p[i]); wv[2 * i + 1] = bf16hi(p[i]); }
-#pragma unroll
-              for (int q = 0; q < TOKG; ++q)
-#pragma unroll
-                for (int i = 0; i < 8; ++i) acc[q][c] = fmaf(xv[q][i], wv[i], acc[q][c]);
-            }
-          }
+      for (int n = 0; n < NT; ++n) {
+        float* p0 = red + (mt * 16 + g) * kLd + n * 8 + 2 * c;
+        float* p1 = p0 + 8 * kLd;
+        if (s == 0) {
+          p0[0] = acc[n][0]; p0[1] = acc[n][1]; p1[0] = acc[n][2]; p1[1] = acc[n][3];
+        } else {
+          p0[0] += acc[n][0]; p0[1] += acc[n][1]; p1[0] += acc[n][2]; p1[1] += acc[n][3];
         }
       }
-#pragma unroll
-      for (int q = 0; q < TOKG; ++q)
-#pragma unroll
-        for (int c = 0; c < EC; ++c) {
-          float v = acc[q][c];
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-          const int st = e0 + c;
-          if (st < Etot && (st & 31) == lane) {
-#pragma unroll
-            for (int s = 0; s < kPerLane; ++s)
-              if ((st >> 5) == s) own[q][s] = v;
-          }
-        }
     }
-
+    __syncthreads();
+  }
+  // ---- top-k, softmax, histograms: warp w handles tokens 4w .. 4w+3
+  for (int q = 0; q < kBlockTokens / kWarps; ++q) {
+    const int lt = warp * (kBlockTokens / kWarps) + q;
+    const int t = blk * kBlockTokens + lt;
+    if (t >= T) break;
+    const float* row = red + lt * kLd;
+    for (int gi = 0; gi <= n_pred; ++gi) {
+      int sel[8];
+      float lg[8];
+      warp_topk(row, gi * E, E, k, sel, lg);
+      if (lane == 0) {
+        if (gi == 0) {
+          float z = 0.0f, p[8];
 #pragma unroll
-    for (int q = 0; q < TOKG; ++q) {
-      if (q < ntok) {
-        const int t = t0 + q;
-        for (int g = 0; g <= n_pred; ++g) {
-          int sel[8];
-          float lg[8];
-          warp_topk(own[q], g * E, E, k, sel, lg);
-          if (lane == 0) {
-            if (g == 0) {
-              float z = 0.0f, p[8];
+          for (int j = 0; j < 8; ++j)
+            if (j < k) { p[j] = expf(lg[j] - lg[0]); z += p[j]; }
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                if (j < k) { p[j] = expf(lg[j] - lg[0]); z += p[j]; }
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                if (j < k) {
-                  ids[(size_t)t * k + j] = sel[j];
-                  wts[(size_t)t * k + j] = p[j] / z;
-                  atomicAdd(&hist[sel[j]], 1);
-                }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                if (j < k) atomicAdd(pred_counts + (size_t)(g - 1) * E + sel[j], 1);
+          for (int j = 0; j < 8; ++j)
+            if (j < k) {
+              ids[(size_t)t * k + j] = sel[j];
+              wts[(size_t)t * k + j] = p[j] / z;
+              atomicAdd(&hist[sel[j]], 1);
             }
-          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < k) atomicAdd(pred_counts + (size_t)(gi - 1) * E + sel[j], 1);
         }
       }
     }
@@ -199,19 +194,24 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
                              int n_pred, int k, int32_t* ids, float* wts, int32_t* counts,
                              int32_t* block_counts, int32_t* pred_counts, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  if (E * (1 + n_pred) > 32 * kPerLane || k > 8 || (d % 8) != 0) return cudaErrorInvalidValue;
-  const int nblk = gate_num_blocks(T);
   const int Etot = E * (1 + n_pred);
-  if (Etot <= 8)
-    gate_topk_kernel<4, 8, 2><<<nblk, 256, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,
-                                                     block_counts, pred_counts);
-  else if (Etot <= 16)
-    gate_topk_kernel<2, 16, 4><<<nblk, 512, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,
-                                                      block_counts, pred_counts);
-  else
-    gate_topk_kernel<2, 16, 4><<<nblk, 512, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,
-                                                       block_counts, pred_counts);
-  return cudaGetLastError();
+  if (Etot > 32 * kPerLane || k > 8 || (d % 256) != 0) return cudaErrorInvalidValue;
+  const int nblk = gate_num_blocks(T);
+  const dim3 grid(nblk), block(kWarps * 32);
+#define MOE_GATE_CASE(NT_)                                                                                  \
+  if (Etot <= 8 * NT_) {                                                                                    \
+    gate_topk_kernel<NT_><<<grid, block, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,       \
+                                                      block_counts, pred_counts);                          \
+    return cudaGetLastError();                                                                              \
+  }
+  MOE_GATE_CASE(1)
+  MOE_GATE_CASE(2)
+  MOE_GATE_CASE(4)
+  MOE_GATE_CASE(8)
+  MOE_GATE_CASE(16)
+  MOE_GATE_CASE(32)
+#undef MOE_GATE_CASE
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace moe
