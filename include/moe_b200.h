@@ -67,8 +67,12 @@ enum { MOE_EXCHANGE_NCCL = 0, MOE_EXCHANGE_EXTERNAL = 1 };
 /* planning modes for moe_layer_forward */
 enum {
   MOE_PLAN_FIXED = 0, /* use the placement last given to moe_set_placement            */
-  MOE_PLAN_SYNC = 1   /* scale_experts + place_experts on this layer's actual counts
+  MOE_PLAN_SYNC = 1,  /* scale_experts + place_experts on this layer's actual counts
                          (oracle predictor, distance 0) inside the forward           */
+  MOE_PLAN_PREDICTED = 2 /* MoEless: the fused predictor at layer l scores layer
+                         l + predictor_distance; the host plans that layer from the
+                         prediction ahead of time; layers never predicted (l < d)
+                         bootstrap from their load history (simulator.cpp:146-151) */
 };
 
 typedef struct moe_ctx moe_ctx;
@@ -92,7 +96,8 @@ typedef struct {
   double gpu_mem_capacity_mb;
   double cv_threshold;
   int keep_alive_iters;
-  int reserved[7];
+  int predictor_distance;     /* d: predictor slot 0 of layer l scores layer l + d (default 1) */
+  int reserved[6];
 } moe_ctx_desc;
 
 typedef struct {
@@ -109,6 +114,8 @@ typedef struct {
   int64_t rows_sent;
   int warm_count, cold_count;
   int32_t counts[256];          /* this rank's gate histogram (E <= 256) */
+  double predictor_accuracy;    /* measure_accuracy(prediction made d layers ago, actual); -1 if none */
+  int32_t plan_source;          /* 0 fixed, 1 actual loads, 2 predicted ahead, 3 history bootstrap */
 } moe_layer_stats;
 
 const char* moe_last_error(void);

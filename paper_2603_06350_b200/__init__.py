@@ -23,14 +23,15 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _capi
-from ._capi import (MOE_EXCHANGE_EXTERNAL, MOE_EXCHANGE_NCCL, MOE_PLAN_FIXED, MOE_PLAN_SYNC,
+from ._capi import (MOE_EXCHANGE_EXTERNAL, MOE_EXCHANGE_NCCL, MOE_PLAN_FIXED, MOE_PLAN_PREDICTED, MOE_PLAN_SYNC,
                     MoeChunk, MoeCtxDesc, MoeError, MoeLayerStats, check, lib)
 
 __all__ = [
     "scale_experts", "place_experts", "ReplicaRegistry", "update_registry", "layer_forward_time",
     "predict", "measure_accuracy", "route_tokens", "popularity", "percentile", "exchange_plan",
     "MoELayer", "ScalingPlan", "PlaceResult", "synth_tokens", "synth_gate", "synth_expert",
-    "stream_key", "nccl_unique_id", "PinnedArray", "MoeError", "MOE_PLAN_FIXED", "MOE_PLAN_SYNC", "MOE_EXCHANGE_NCCL",
+    "stream_key", "nccl_unique_id", "PinnedArray", "MoeError", "MOE_PLAN_FIXED", "MOE_PLAN_SYNC",
+    "MOE_PLAN_PREDICTED", "MOE_EXCHANGE_NCCL",
     "MOE_EXCHANGE_EXTERNAL", "LIB_PATH",
 ]
 LIB_PATH = _capi.LIB_PATH
@@ -284,7 +285,7 @@ class MoELayer:
                  exchange_mode: int = MOE_EXCHANGE_NCCL, nccl_unique_id: Optional[bytes] = None,
                  num_predictor_targets: int = 0, expert_mem_mb: float = 0.0,
                  layer_mem_cap_mb: float = 0.0, gpu_mem_capacity_mb: float = 180000.0,
-                 cv_threshold: float = 0.2, keep_alive_iters: int = 50):
+                 cv_threshold: float = 0.2, keep_alive_iters: int = 50, predictor_distance: int = 1):
         d = MoeCtxDesc()
         d.num_layers, d.num_experts, d.top_k = num_layers, num_experts, top_k
         d.d_model, d.d_ff, d.max_tokens = d_model, d_ff, max_tokens
@@ -295,6 +296,7 @@ class MoELayer:
         d.expert_mem_mb = expert_mem_mb or 3.0 * d_model * d_ff * 2 / 1e6
         d.layer_mem_cap_mb, d.gpu_mem_capacity_mb = layer_mem_cap_mb, gpu_mem_capacity_mb
         d.cv_threshold, d.keep_alive_iters = cv_threshold, keep_alive_iters
+        d.predictor_distance = predictor_distance
         h = C.c_void_p()
         check(lib.moe_ctx_create(C.byref(d), C.byref(h)))
         self._h = h

@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libmoe_b200.so")
 
 MOE_OK, MOE_EINVAL, MOE_EINFEASIBLE, MOE_ECUDA, MOE_ENCCL, MOE_ESTATE = range(6)
 MOE_EXCHANGE_NCCL, MOE_EXCHANGE_EXTERNAL = 0, 1
-MOE_PLAN_FIXED, MOE_PLAN_SYNC = 0, 1
+MOE_PLAN_FIXED, MOE_PLAN_SYNC, MOE_PLAN_PREDICTED = 0, 1, 2
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -35,7 +35,8 @@ class MoeCtxDesc(C.Structure):
         ("exchange_mode", C.c_int), ("nccl_unique_id", vp),
         ("num_predictor_targets", C.c_int),
         ("expert_mem_mb", dbl), ("layer_mem_cap_mb", dbl), ("gpu_mem_capacity_mb", dbl),
-        ("cv_threshold", dbl), ("keep_alive_iters", C.c_int), ("reserved", C.c_int * 7),
+        ("cv_threshold", dbl), ("keep_alive_iters", C.c_int), ("predictor_distance", C.c_int),
+        ("reserved", C.c_int * 6),
     ]
 
 
@@ -46,6 +47,7 @@ class MoeLayerStats(C.Structure):
         ("a2a_dispatch_ms", dbl), ("gemm1_ms", dbl), ("gemm2_ms", dbl),
         ("a2a_combine_ms", dbl), ("combine_ms", dbl), ("rows_local", i64), ("rows_sent", i64),
         ("warm_count", C.c_int), ("cold_count", C.c_int), ("counts", i32 * 256),
+        ("predictor_accuracy", dbl), ("plan_source", i32),
     ]
 
 

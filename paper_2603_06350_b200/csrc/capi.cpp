@@ -206,12 +206,23 @@ struct Layer {
   std::vector<char> expert_loaded;
   std::vector<int32_t> rep_counts, rep_gpu;  // placement (host)
   bool has_placement = false;
+  bool has_pred_weights = false;
+  // layer-aware predictor state (MOE_PLAN_PREDICTED)
+  std::vector<int64_t> pred_loads;          // predicted loads for this layer (made d layers earlier)
+  bool pred_valid = false;
+  long plan_for = -1;                       // iteration whose placement was planned ahead
+  double last_accuracy = -1.0, acc_sum = 0.0;
+  long acc_n = 0, bootstraps = 0;
+  int plan_source = 0;                      // 0 fixed, 1 actual, 2 predicted, 3 historical bootstrap
+  int warm = 0, cold = 0;
+  std::vector<moeless::LoadVector> history;
 };
 
 struct PendingPlan {
   bool active = false;
   int layer = 0, mode = 0;
   long iteration = 0;
+  int stride = 0;
 };
 
 struct EventSet {
@@ -238,6 +249,8 @@ struct moe_ctx {
   moe_ctx_desc desc{};
   int E = 0, k = 0, d = 0, ff = 0, G = 1, rank = 0, Tmax = 0, n_pred = 0, num_sms = 148;
   int gemm_variant = 0;  // 0 auto, 1 force 1-SM, 2 force 2-SM (env MOE_GEMM_VARIANT=1sm|2sm)
+  int pred_distance = 1;  // predictor slot 0 scores layer + pred_distance
+  int count_stride = 0;   // ints per rank in the counts buffer: E * (1 + n_pred)
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
   std::vector<Layer> layers;
@@ -278,8 +291,7 @@ namespace {
 
 void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, int32_t* pred_counts) {
   require(L.has_gate, "gate weights not set for layer");
-  CU_CHECK(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * c->E, s));
-  if (pred_counts && c->n_pred) CU_CHECK(cudaMemsetAsync(pred_counts, 0, sizeof(int32_t) * c->E * c->n_pred, s));
+  CU_CHECK(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * c->count_stride, s));
   CU_CHECK(launch_gate_topk(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
                             reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, pred_counts ? c->n_pred : 0,
                             c->k, c->ids.p, c->wts.p, c->counts.p, c->block_counts.p,
@@ -287,38 +299,70 @@ void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, 
 }
 
 // Decide the placement for this forward (host), then build + upload the plan.
-void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int32_t* counts_all_host) {
+// MoEless planning for one layer on a load vector: scale_experts (Alg. 1) ->
+// place_experts (Alg. 2) against the keep-alive registry -> update_registry
+// (the reference's per-layer sequence, simulator.cpp:159-201).
+void plan_layer(moe_ctx* c, int layer, const std::vector<int64_t>& loads, long iteration) {
+  Layer& L = c->layers[layer];
+  moeless::ModelSpec ms;
+  ms.num_layers = std::max(1, c->desc.num_layers);
+  ms.experts_per_layer = c->E;
+  ms.top_k = c->k;
+  ms.expert_mem_mb = c->desc.expert_mem_mb > 0 ? c->desc.expert_mem_mb : 3.0 * c->d * c->ff * 2 / 1e6;
+  ms.layer_mem_cap_mb = c->desc.layer_mem_cap_mb;
+  moeless::ScalerConfig sc;
+  sc.cv_threshold = c->desc.cv_threshold;
+  auto sp = moeless::scale_experts(moeless::LoadVector{layer, loads}, ms, sc);
+  moeless::ClusterSpec cl;
+  cl.gpu_count = c->G;
+  cl.gpu_mem_capacity_mb = c->desc.gpu_mem_capacity_mb > 0 ? c->desc.gpu_mem_capacity_mb : 180000.0;
+  auto pr = moeless::place_experts(sp, cl, c->registry, iteration);
+  moeless::update_registry(c->registry, pr.placement, iteration);
+  L.warm = pr.warm_count;
+  L.cold = pr.cold_count;
+  L.rep_counts.assign(sp.replica_counts.begin(), sp.replica_counts.end());
+  L.rep_gpu.clear();
+  for (auto& v : pr.placement.gpu_for) L.rep_gpu.insert(L.rep_gpu.end(), v.begin(), v.end());
+  L.has_placement = true;
+}
+
+// buf: [G][stride] int32 from the gate — per rank, E actual counts followed by
+// n_pred x E predictor counts (stride == E when no predictor ran).
+void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int32_t* buf, int stride) {
   Layer& L = c->layers[layer];
   std::vector<int64_t> all(static_cast<size_t>(c->G) * c->E);
-  for (size_t i = 0; i < all.size(); ++i) all[i] = counts_all_host[i];
-  std::vector<int64_t> total(c->E, 0);
+  std::vector<int64_t> total(c->E, 0), predicted(c->E, 0);
+  const bool have_pred = stride >= 2 * c->E;
   for (int s = 0; s < c->G; ++s)
-    for (int e = 0; e < c->E; ++e) total[e] += all[static_cast<size_t>(s) * c->E + e];
+    for (int e = 0; e < c->E; ++e) {
+      all[static_cast<size_t>(s) * c->E + e] = buf[static_cast<size_t>(s) * stride + e];
+      total[e] += buf[static_cast<size_t>(s) * stride + e];
+      if (have_pred) predicted[e] += buf[static_cast<size_t>(s) * stride + c->E + e];
+    }
   c->last_counts = total;
+  // realised accuracy of the prediction made d layers earlier (predictor.cpp:168-186)
+  L.last_accuracy = -1.0;
+  if (L.pred_valid) {
+    L.last_accuracy = moeless::measure_accuracy({layer, L.pred_loads}, {layer, total});
+    L.acc_sum += L.last_accuracy;
+    ++L.acc_n;
+    L.pred_valid = false;
+  }
   if (plan_mode == MOE_PLAN_SYNC) {
-    // synchronous MoEless planning on the actual loads (oracle predictor, d = 0):
-    // scale_experts (Alg. 1) -> place_experts (Alg. 2) -> keep-alive registry
-    moeless::ModelSpec ms;
-    ms.num_layers = std::max(1, c->desc.num_layers);
-    ms.experts_per_layer = c->E;
-    ms.top_k = c->k;
-    ms.expert_mem_mb = c->desc.expert_mem_mb > 0 ? c->desc.expert_mem_mb : 3.0 * c->d * c->ff * 2 / 1e6;
-    ms.layer_mem_cap_mb = c->desc.layer_mem_cap_mb;
-    moeless::ScalerConfig sc;
-    sc.cv_threshold = c->desc.cv_threshold;
-    moeless::LoadVector lv{layer, total};
-    auto sp = moeless::scale_experts(lv, ms, sc);
-    moeless::ClusterSpec cl;
-    cl.gpu_count = c->G;
-    cl.gpu_mem_capacity_mb = c->desc.gpu_mem_capacity_mb > 0 ? c->desc.gpu_mem_capacity_mb : 180000.0;
-    auto pr = moeless::place_experts(sp, cl, c->registry, iteration);
-    moeless::update_registry(c->registry, pr.placement, iteration);
-    c->last_warm = pr.warm_count;
-    c->last_cold = pr.cold_count;
-    L.rep_counts.assign(sp.replica_counts.begin(), sp.replica_counts.end());
-    L.rep_gpu.clear();
-    for (auto& v : pr.placement.gpu_for) L.rep_gpu.insert(L.rep_gpu.end(), v.begin(), v.end());
-    L.has_placement = true;
+    // synchronous planning on the actual loads (oracle predictor, distance 0)
+    plan_layer(c, layer, total, iteration);
+    L.plan_source = 1;
+  } else if (plan_mode == MOE_PLAN_PREDICTED && L.plan_for != iteration) {
+    // no prediction reached this layer (l < d, simulator.cpp:146-151): bootstrap
+    // from the layer's load history with the historical predictor
+    moeless::PredictorProfile hp;
+    hp.kind = moeless::PredictorKind::historical;
+    const auto guess = moeless::predict({layer, total}, L.history, hp, iteration, 1);
+    plan_layer(c, layer, guess.loads, iteration);
+    L.plan_source = 3;
+    ++L.bootstraps;
+  } else if (plan_mode == MOE_PLAN_PREDICTED) {
+    L.plan_source = 2;  // placement made d layers ago from the predictor
   } else if (!L.has_placement) {
     // default: one replica per expert, expert e on GPU e mod G (static_plan, baselines.cpp:32-60)
     L.rep_counts.assign(c->E, 1);
@@ -326,6 +370,20 @@ void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int3
     for (int e = 0; e < c->E; ++e) L.rep_gpu[e] = e % c->G;
     L.has_placement = true;
   }
+  // plan layer + d from this layer's predictor histogram (the MoEless
+  // layer-aware predictor: plan ahead, evaluate on the actual loads)
+  const int target = layer + c->pred_distance;
+  if (have_pred && target < static_cast<int>(c->layers.size())) {
+    Layer& Lt = c->layers[target];
+    Lt.pred_loads = predicted;
+    Lt.pred_valid = true;
+    if (plan_mode == MOE_PLAN_PREDICTED) {
+      plan_layer(c, target, predicted, iteration);
+      Lt.plan_for = iteration;
+    }
+  }
+  L.history.push_back({layer, total});
+  if (L.history.size() > 16) L.history.erase(L.history.begin());
   build_exchange_plan(c->G, c->rank, c->E, all.data(), L.rep_counts.data(), L.rep_gpu.data(), c->plan);
   if (c->plan.rows_local > c->rows_cap || c->plan.rows_send > c->send_cap)
     throw Status(MOE_EINFEASIBLE, "received rows exceed workspace capacity");
@@ -403,7 +461,7 @@ void flush_pending_plan(moe_ctx* c) {
   if (!c->pending.active) return;
   c->pending.active = false;
   CU_CHECK(cudaEventSynchronize(c->ev_counts));
-  stage_plan(c, c->pending.layer, c->pending.mode, c->pending.iteration, c->h_counts);
+  stage_plan(c, c->pending.layer, c->pending.mode, c->pending.iteration, c->h_counts, c->pending.stride);
 }
 
 Layer& layer_at(moe_ctx* c, int layer) {
@@ -427,7 +485,8 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
                     moe_layer_stats* st, cudaStream_t s, cudaEvent_t x_consumed = nullptr) {
   Layer& L = layer_at(c, layer);
   require(T >= 0 && T <= c->Tmax, "token count exceeds max_tokens");
-  require(plan_mode == MOE_PLAN_FIXED || plan_mode == MOE_PLAN_SYNC, "unknown plan mode");
+  require(plan_mode == MOE_PLAN_FIXED || plan_mode == MOE_PLAN_SYNC || plan_mode == MOE_PLAN_PREDICTED,
+          "unknown plan mode");
   for (int e = 0; e < c->E; ++e)
     if (!L.w13.p || !L.expert_loaded[e]) throw std::invalid_argument("expert weights not loaded for layer");
   EventSet& ev = c->events;
@@ -436,16 +495,20 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
     if (timed) CU_CHECK(cudaEventRecord(ev.ev[i], s));
   };
   flush_pending_plan(c);  // the previous call's deferred planner work (G = 1)
+  // the fused predictor (K2) runs when the layer has predictor weights: its
+  // histograms follow the gate's in the same counts buffer
+  const bool with_pred = c->n_pred > 0 && L.has_pred_weights;
+  const int stride = with_pred ? c->count_stride : c->E;
   mark(0);
-  stage_gate(c, L, x, T, s, nullptr);
+  stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr);
   if (c->G > 1) {
     // NCCL needs every chunk size on the host: one round trip per layer.
     require(c->desc.exchange_mode == MOE_EXCHANGE_NCCL, "staged API required for external exchange");
-    g_nccl.check(g_nccl.AllGather(c->counts.p, c->counts_all.p, c->E, ncclInt32, c->comm, s), "ncclAllGather");
-    CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * c->E), s));
+    g_nccl.check(g_nccl.AllGather(c->counts.p, c->counts_all.p, stride, ncclInt32, c->comm, s), "ncclAllGather");
+    CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
     mark(1);
     CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram
-    stage_plan(c, layer, plan_mode, iteration, c->h_counts);
+    stage_plan(c, layer, plan_mode, iteration, c->h_counts, stride);
     mark(2);
     stage_dispatch(c, x, T, s);
   } else {
@@ -455,11 +518,11 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
     // as it lands in mapped host memory — its replica decisions cannot change
     // single-GPU work (co-located replicas share one GEMM segment), so running
     // it off the critical path keeps the reference's per-layer semantics.
-    CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * c->E), s));
+    CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * stride), s));
     CU_CHECK(cudaEventRecord(c->ev_counts, s));
     mark(1);
     CU_CHECK(launch_plan_local(c->counts.p, c->E, c->dplan.p, s));
-    c->pending = PendingPlan{true, layer, plan_mode, iteration};
+    c->pending = PendingPlan{true, layer, plan_mode, iteration, stride};
     mark(2);
     stage_dispatch(c, x, T, s, /*upload_plan=*/false);
   }
@@ -493,8 +556,10 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
     st->mem_mb = st->replica_count * (3.0 * c->d * c->ff * 2 / 1e6);
     st->rows_local = c->plan.rows_local;
     st->rows_sent = c->plan.rows_send;
-    st->warm_count = c->last_warm;
-    st->cold_count = c->last_cold;
+    st->warm_count = L.warm;
+    st->cold_count = L.cold;
+    st->predictor_accuracy = L.last_accuracy;
+    st->plan_source = L.plan_source;
     for (int e = 0; e < c->E && e < 256; ++e) st->counts[e] = c->h_counts[static_cast<size_t>(c->rank) * c->E + e];
   }
 }
@@ -548,6 +613,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->rank = D.rank;
     c->Tmax = D.max_tokens;
     c->n_pred = std::max(0, D.num_predictor_targets);
+    c->pred_distance = D.predictor_distance > 0 ? D.predictor_distance : 1;
     c->num_sms = prop.multiProcessorCount;
     if (const char* v = std::getenv("MOE_GEMM_VARIANT")) {
       const std::string s(v);
@@ -563,8 +629,9 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->ids.alloc(assign);
     c->wts.alloc(assign);
     c->row_code.alloc(assign);
-    c->counts.alloc(pad16(sizeof(int32_t) * c->E) / 4);
-    c->counts_all.alloc(pad16(sizeof(int32_t) * c->E * c->G) / 4);
+    c->count_stride = c->E * (1 + c->n_pred);  // [gate E | predictor n_pred x E]
+    c->counts.alloc(pad16(sizeof(int32_t) * c->count_stride) / 4);
+    c->counts_all.alloc(pad16(sizeof(int32_t) * c->count_stride * c->G) / 4);
     c->pred_counts.alloc(static_cast<size_t>(c->E) * std::max(1, c->n_pred));
     c->block_counts.alloc(static_cast<size_t>(nblk) * c->E);
     c->block_pre.alloc(static_cast<size_t>(nblk) * c->E);
@@ -578,7 +645,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->tmA2 = make_kmajor_map(c->h.p, c->rows_cap, c->ff, 128);
     // mapped pinned control buffers, read/written by small SM copies (UVA pointers)
     CU_CHECK(cudaHostAlloc(&c->hplan, sizeof(DevPlan), cudaHostAllocMapped));
-    CU_CHECK(cudaHostAlloc(&c->h_counts, pad16(sizeof(int32_t) * c->E * c->G), cudaHostAllocMapped));
+    CU_CHECK(cudaHostAlloc(&c->h_counts, pad16(sizeof(int32_t) * c->count_stride * c->G), cudaHostAllocMapped));
     c->events.create();
     CU_CHECK(cudaEventCreateWithFlags(&c->ev_counts, cudaEventDisableTiming));
     if (c->G > 1 && D.exchange_mode == MOE_EXCHANGE_NCCL) {
@@ -695,6 +762,7 @@ int moe_set_predictor_weights(moe_ctx* c, int layer, int slot, const uint16_t* w
     CU_CHECK(cudaStreamSynchronize(c->stream));  // no enqueued forward may see a half-written gate
     CU_CHECK(cudaMemcpy(L.wg.p + static_cast<size_t>(1 + slot) * c->E * c->d, wp, static_cast<size_t>(c->E) * c->d * 2,
                         cudaMemcpyHostToDevice));
+    L.has_pred_weights = true;
   });
 }
 
@@ -857,7 +925,7 @@ int moe_forward_begin(moe_ctx* c, int layer, const uint16_t* x, int T, const int
       return;
     }
     require(c->cur_layer == layer && c->cur_x == x && c->cur_T == T, "forward_begin stage 2 without stage 1");
-    stage_plan(c, layer, MOE_PLAN_FIXED, 0, counts_all);
+    stage_plan(c, layer, MOE_PLAN_FIXED, 0, counts_all, c->E);
     stage_dispatch(c, x, T, s);
     CU_CHECK(cudaStreamSynchronize(s));
   });

@@ -22,6 +22,7 @@
 //                        it k times with 128-bit vector stores.
 //   combine_kernel       y_t = sum_j w_tj * Y[row(t, j)], fp32 accumulate in
 //                        slot order, bf16 out; one warp per token.
+#include <algorithm>
 #include <cstdint>
 
 #include "dispatch_plan.h"
@@ -110,14 +111,18 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
         const int gr = block_pre[(size_t)b * E + e] + __popc(m & lt);
         const uint32_t code = row_code_for(plan, e, gr);
         codes[lane * K + slot] = code;
-        row_code[(size_t)t * K + slot] = code;
+        if (blockIdx.y == 0) row_code[(size_t)t * K + slot] = code;
       }
     }
   }
   __syncthreads();
 
-  // stream rows: each warp copies tokens warp, warp+4, ...
-  const int chunks = d / 8;  // 16-byte chunks per row
+  // stream rows: each warp copies tokens warp, warp+4, ...; the row's 16-byte
+  // chunks are split over gridDim.y CTAs (small batches: decode keeps every
+  // SM busy; the ranking above is recomputed per split, it is a few ballots)
+  const int chunks_all = d / 8;
+  const int per = (chunks_all + gridDim.y - 1) / gridDim.y;
+  const int c_begin = blockIdx.y * per, chunks = min(chunks_all, c_begin + per);
   for (int i = warp; i < ntok; i += 4) {
     const __nv_bfloat16* src = x + (size_t)(t_base + i) * d;
     __nv_bfloat16* dst[K];
@@ -127,7 +132,7 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
       __nv_bfloat16* base = (c & kRemoteBit) ? xp_send : xp_local;
       dst[j] = base + (size_t)(c & ~kRemoteBit) * d;
     }
-    for (int c0 = lane; c0 < chunks; c0 += 32 * 4) {
+    for (int c0 = c_begin + lane; c0 < chunks; c0 += 32 * 4) {
       int4 v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -151,7 +156,10 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_local, const __nv_bfloat16* _
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
-  const int chunks = d / 8;
+  // columns split over gridDim.y (small batches), tokens over warps
+  const int chunks_all = d / 8;
+  const int per = (chunks_all + gridDim.y - 1) / gridDim.y;
+  const int c_begin = blockIdx.y * per, chunks = min(chunks_all, c_begin + per);
   for (int t = warp_global; t < T; t += nwarps) {
     const __nv_bfloat16* src[K];
     float w[K];
@@ -162,7 +170,7 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_local, const __nv_bfloat16* _
       w[j] = wts[(size_t)t * K + j];
     }
     __nv_bfloat16* out = y + (size_t)t * d;
-    for (int c0 = lane; c0 < chunks; c0 += 32) {
+    for (int c0 = c_begin + lane; c0 < chunks; c0 += 32) {
       int4 v[K];
 #pragma unroll
       for (int j = 0; j < K; ++j) v[j] = ld_nc_v4(src[j] + (size_t)c0 * 8);
@@ -278,7 +286,10 @@ cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, 
   if (T <= 0) return cudaSuccess;
   if (d % 8) return cudaErrorInvalidValue;
   const int nblk = (T + 31) / 32;
-  MOE_SWITCH_K(k, (dispatch_kernel<KK><<<nblk, 128, 0, s>>>(x, T, d, E, ids, block_pre, plan, xp_local, xp_send,
+  // at least ~2 CTAs per SM: split each row's chunks when there are few blocks
+  const int split = std::max(1, std::min((2 * 148 + nblk - 1) / nblk, d / 8 / 32));
+  const dim3 grid(nblk, split);
+  MOE_SWITCH_K(k, (dispatch_kernel<KK><<<grid, 128, 0, s>>>(x, T, d, E, ids, block_pre, plan, xp_local, xp_send,
                                                            row_code)));
   return cudaGetLastError();
 }
@@ -291,7 +302,9 @@ cudaError_t launch_combine(const __nv_bfloat16* y_local, const __nv_bfloat16* y_
   const int warps_needed = T;
   int ctas = (warps_needed + 7) / 8;
   ctas = ctas < num_sms * 8 ? ctas : num_sms * 8;
-  MOE_SWITCH_K(k, (combine_kernel<KK><<<ctas, 256, 0, s>>>(y_local, y_return, T, d, row_code, wts, y)));
+  const int split = std::max(1, std::min((2 * num_sms + ctas - 1) / ctas, d / 8 / 32));
+  const dim3 grid(ctas, split);
+  MOE_SWITCH_K(k, (combine_kernel<KK><<<grid, 256, 0, s>>>(y_local, y_return, T, d, row_code, wts, y)));
   return cudaGetLastError();
 }
 
