@@ -73,6 +73,59 @@ def run_config(name, steps, warmup):
     }
 
 
+def run_stack(name, iters, warmup, layers=None):
+    """cfg4: the 32-layer Mixtral-shape MoE stack with the layer-aware predictor
+    and planner-driven scaling/placement (MOE_PLAN_PREDICTED, distance 1)."""
+    import numpy as np
+    import torch
+
+    from paper_2603_06350_b200 import percentile
+    from paper_2603_06350_b200 import workload as wl
+    from paper_2603_06350_b200.stack import MoEStack
+    c = dict(wl.CONFIGS[name])
+    L = layers or c.get("L", 32)
+    E, k, d, ff, T = c["E"], c["k"], c["d"], c["ff"], c["T"]
+    st = MoEStack(L, E, k, d, ff, T, extra_replicas=c["extra_replicas"], zipf_s=c["s"], distance=1)
+    pool = [torch.from_numpy(wl.tokens(T, d, E, 1, i).view(np.int16)).cuda() for i in range(4)]
+    ys = [torch.empty((T, d), dtype=torch.int16, device="cuda") for _ in range(2)]
+    stream = torch.cuda.ExternalStream(st.layer.stream_ptr)
+
+    def xs_for(it):  # layer l reads its own batch: predictions are made on other tokens
+        return [pool[(it + l) % 4] for l in range(L)]
+
+    for it in range(warmup):
+        st.forward(xs_for(it), [ys[l % 2] for l in range(L)], it)
+    torch.cuda.synchronize()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
+          for _ in range(iters)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(iters):
+        it = warmup + i
+        xs = xs_for(it)
+        for l in range(L):
+            ev[i][l][0].record(stream)
+            st.layer.forward(l, xs[l], ys[l % 2], 2, it)
+            ev[i][l][1].record(stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    lat = [a.elapsed_time(b) for row in ev for a, b in row]  # all (iteration, layer) samples
+    total = t0.elapsed_time(t1)
+    stats = st.forward(xs_for(warmup + iters), [ys[l % 2] for l in range(L)], warmup + iters, stats=True)
+    acc = [s.predictor_accuracy for s in stats[1:]]
+    res = {
+        "config": name, "layers": L, "gpus": 1, "shape": c, "iterations": iters,
+        "ms_per_stack": total / iters, "ms_per_layer_mean": total / iters / L,
+        "p50_layer_ms": percentile(lat, 0.5), "p99_layer_ms": percentile(lat, 0.99),
+        "tokens_per_s_per_layer": T * iters * L / (total * 1e-3),
+        "predictor_accuracy_mean": sum(acc) / len(acc), "predictor_accuracy_min": min(acc),
+        "plan_sources": [s.plan_source for s in stats], "replicas": [s.replica_count for s in stats],
+        "note": "per-GPU shape at G=1 (named config is G=8); planning from the fused predictor, distance 1",
+    }
+    st.close()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="cfg1,cfg3,cfg5")
@@ -80,7 +133,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
-    res = [run_config(n, a.steps, a.warmup) for n in a.configs.split(",")]
+    res = [run_stack(n, max(2, a.steps // 10), 1) if n == "cfg4" else run_config(n, a.steps, a.warmup)
+           for n in a.configs.split(",")]
     for r in res:
         print(json.dumps(r), flush=True)
     if a.out:
