@@ -45,7 +45,7 @@ FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--pool", type=int, default=4, help="distinct token batches cycled per rank")
@@ -93,7 +93,7 @@ class ClockSampler:
                ("nvmlClocksEventReasonSwPowerCap", "sw_power_cap"),
                ("nvmlClocksEventReasonHwPowerBrakeSlowdown", "hw_power_brake_slowdown"))
 
-    def __init__(self, gpu_index, period_s=0.02):
+    def __init__(self, gpu_index, period_s=0.01):
         self.gpu, self.period = gpu_index, period_s
         self.rows, self.err = [], None
 
@@ -126,7 +126,9 @@ class ClockSampler:
         import pynvml as N
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0, "error": self.err}
-        loaded = [r for r in self.rows if r["power"] > 300] or self.rows
+        # every sample lies inside the timed region (NVML power is a ~1 s
+        # average, so it is not used to select "loaded" samples)
+        loaded = self.rows
         reasons = set()
         for r in loaded:
             for attr, name in self.REASONS:
@@ -134,7 +136,7 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(r["sm"] for r in loaded), "sm_max_mhz": max(r["smax"] for r in self.rows),
                 "reasons": sorted(reasons), "samples": len(loaded),
-                "power_w_median": statistics.median(r["power"] for r in loaded), "source": "NVML, 20 ms period"}
+                "power_w_median": statistics.median(r["power"] for r in loaded), "source": "NVML, 10 ms period"}
 
 
 def nearest_rank(values, q):
@@ -281,11 +283,14 @@ def run_ours(args):
         barrier()
     total_ms = t_start.elapsed_time(t_end)
     lat = [a.elapsed_time(b) for a, b in ev]
-    # phase breakdown (per-phase CUDA events inside the C-ABI) from a short
-    # untimed pass; these per-kernel times feed the roofline
+    # K4 times of the TIMED steps: CUDA events the C-ABI records around the two
+    # grouped GEMMs of every forward on its stream (no host sync in the loop)
+    g1, g2, grows = m.gemm_times(min(args.steps, 64))
+    gemm_ms = [float(a + b) for a, b in zip(g1, g2)]
+    rows = [int(r) for r in grows]
+    # phase breakdown (per-phase events + host sync per call) from a short
+    # untimed pass after the timed region
     stats = [step(args.warmup + args.steps + i, stats=True) for i in range(min(args.steps, 10))]
-    gemm_ms = [s.gemm1_ms + s.gemm2_ms for s in stats]
-    rows = [s.rows_local for s in stats]
     phases = {name: statistics.median(getattr(s, name) for s in stats)
               for name in ("gate_ms", "plan_ms", "dispatch_ms", "a2a_dispatch_ms", "gemm1_ms", "gemm2_ms",
                            "a2a_combine_ms", "combine_ms")}
@@ -353,6 +358,9 @@ def run_ours(args):
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "peak_source": peak_src + ", bf16 sustained", "burst_peak": peaks.get("bf16_tflops"),
                          "algorithmic_flops_per_step": statistics.median(gflop),
+                         "kernel_ms_per_step": statistics.median(gemm_ms),
+                         "timing": "CUDA events around GEMM1/GEMM2 of each timed step on the ctx stream "
+                                   "(moe_gemm_times); achieved = 6*d*ff*rows / (GEMM1+GEMM2), median over steps",
                          "traffic": (traffic or {}).get("dram_bytes_per_step"),
                          "traffic_source": (traffic or {}).get("source")},
             "clocks": clk.summary(),

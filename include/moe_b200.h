@@ -174,6 +174,12 @@ int moe_layer_forward_host_async(moe_ctx* ctx, int layer, const uint16_t* x_host
                                  uint16_t* y_host, int plan_mode, long iteration,
                                  int64_t* ticket);
 int moe_wait(moe_ctx* ctx, int64_t ticket);
+/* K4 device times of the most recent forwards (<= 64), oldest first, measured
+   with CUDA events recorded around the two grouped GEMMs of EVERY forward
+   (no host synchronisation inside the forward).  Synchronises the ctx
+   stream, then fills up to max_n entries and *n_out. */
+int moe_gemm_times(moe_ctx* ctx, int max_n, float* gemm1_ms, float* gemm2_ms, int64_t* rows, int* n_out);
+
 /* Page-locked host buffers for the pipelined API (portable + mapped). */
 int moe_host_alloc(size_t bytes, void** out);
 int moe_host_free(void* p);

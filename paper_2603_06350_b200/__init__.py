@@ -381,6 +381,14 @@ class MoELayer:
                                                C.c_void_p(yp), plan_mode, iteration, C.byref(t)))
         return t.value
 
+    def gemm_times(self, max_n: int = 64):
+        """(gemm1_ms, gemm2_ms, rows) of the most recent forwards (event ring, no per-step sync)."""
+        g1, g2 = np.zeros(max_n, np.float32), np.zeros(max_n, np.float32)
+        rows = np.zeros(max_n, np.int64)
+        n = C.c_int()
+        check(lib.moe_gemm_times(self._h, max_n, _p(g1), _p(g2), _p(rows), C.byref(n)))
+        return g1[:n.value], g2[:n.value], rows[:n.value]
+
     def wait(self, ticket: int) -> None:
         check(lib.moe_wait(self._h, ticket))
 

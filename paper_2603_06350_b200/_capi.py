@@ -80,6 +80,7 @@ _sig("moe_layer_forward_host", C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int, C
 _sig("moe_layer_forward_host_async", C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int, C.c_long, P(i64))
 _sig("moe_wait", C.c_int, vp, i64)
 _sig("moe_host_alloc", C.c_int, C.c_size_t, P(vp))
+_sig("moe_gemm_times", C.c_int, vp, C.c_int, vp, vp, vp, P(C.c_int))
 _sig("moe_host_free", C.c_int, vp)
 _sig("moe_forward_begin", C.c_int, vp, C.c_int, vp, C.c_int, vp, vp)
 _sig("moe_forward_expert", C.c_int, vp, C.c_int, vp)
@@ -114,7 +115,7 @@ EXPORTED = [
     "moe_ctx_sync", "moe_load_expert_weights", "moe_set_gate_weights",
     "moe_set_predictor_weights", "moe_set_placement", "moe_gate_topk", "moe_predict_loads",
     "moe_layer_forward", "moe_layer_forward_host", "moe_layer_forward_host_async", "moe_wait",
-    "moe_host_alloc", "moe_host_free",
+    "moe_host_alloc", "moe_host_free", "moe_gemm_times",
     "moe_forward_begin", "moe_forward_expert",
     "moe_forward_end", "moe_buffer", "moe_memcpy", "moe_exchange_plan", "moe_plan_scale",
     "moe_registry_create", "moe_registry_destroy", "moe_registry_size", "moe_plan_place",

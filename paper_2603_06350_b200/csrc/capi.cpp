@@ -251,6 +251,11 @@ struct moe_ctx {
   int gemm_variant = 0;  // 0 auto, 1 force 1-SM, 2 force 2-SM (env MOE_GEMM_VARIANT=1sm|2sm)
   int pred_distance = 1;  // predictor slot 0 scores layer + pred_distance
   int count_stride = 0;   // ints per rank in the counts buffer: E * (1 + n_pred)
+  // K4 timing ring: events around GEMM1 / GEMM2 of every forward (no sync)
+  static constexpr int kGemmRing = 64;
+  cudaEvent_t gemm_ev[kGemmRing][3] = {};
+  int64_t gemm_rows[kGemmRing] = {};
+  int64_t gemm_seq = 0;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
   std::vector<Layer> layers;
@@ -530,9 +535,15 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   mark(3);
   stage_exchange(c, true, s);
   mark(4);
+  const int gslot = static_cast<int>(c->gemm_seq % moe_ctx::kGemmRing);
+  CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][0], s));
   launch_ffn_gemm(c, layer, 0, s);
+  CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][1], s));
   mark(5);
   launch_ffn_gemm(c, layer, 1, s);
+  CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][2], s));
+  c->gemm_rows[gslot] = c->G == 1 ? static_cast<int64_t>(T) * c->k : c->plan.rows_local;
+  ++c->gemm_seq;
   mark(6);
   stage_exchange(c, false, s);
   mark(7);
@@ -648,6 +659,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     CU_CHECK(cudaHostAlloc(&c->h_counts, pad16(sizeof(int32_t) * c->count_stride * c->G), cudaHostAllocMapped));
     c->events.create();
     CU_CHECK(cudaEventCreateWithFlags(&c->ev_counts, cudaEventDisableTiming));
+    for (auto& tri : c->gemm_ev)
+      for (cudaEvent_t& e : tri) CU_CHECK(cudaEventCreate(&e));
     if (c->G > 1 && D.exchange_mode == MOE_EXCHANGE_NCCL) {
       require(D.nccl_unique_id != nullptr, "nccl_unique_id required for world_size > 1");
       g_nccl.load();
@@ -671,6 +684,9 @@ int moe_ctx_destroy(moe_ctx* c) {
     if (c->wg_stage) cudaFreeHost(c->wg_stage);
     if (c->ev_wg_staged) cudaEventDestroy(c->ev_wg_staged);
     if (c->ev_counts) cudaEventDestroy(c->ev_counts);
+    for (auto& tri : c->gemm_ev)
+      for (cudaEvent_t e : tri)
+        if (e) cudaEventDestroy(e);
     if (c->h2d) {
       cudaStreamSynchronize(c->h2d);
       cudaStreamSynchronize(c->d2h);
@@ -881,6 +897,25 @@ int moe_layer_forward_host_async(moe_ctx* c, int layer, const uint16_t* x_host, 
     CU_CHECK(cudaEventRecord(c->ev_done[slot], c->d2h));
     CU_CHECK(cudaEventRecord(c->ev_ticket[tk % moe_ctx::kTicketRing], c->d2h));
     if (ticket) *ticket = tk;
+  });
+}
+
+int moe_gemm_times(moe_ctx* c, int max_n, float* g1, float* g2, int64_t* rows, int* n_out) {
+  return guarded([&] {
+    require(c && n_out, "null argument");
+    CU_CHECK(cudaStreamSynchronize(c->stream));
+    const int64_t avail = std::min<int64_t>(c->gemm_seq, moe_ctx::kGemmRing);
+    const int n = static_cast<int>(std::min<int64_t>(avail, std::max(0, max_n)));
+    for (int i = 0; i < n; ++i) {
+      const int slot = static_cast<int>((c->gemm_seq - n + i) % moe_ctx::kGemmRing);
+      float a = 0.0f, b = 0.0f;
+      CU_CHECK(cudaEventElapsedTime(&a, c->gemm_ev[slot][0], c->gemm_ev[slot][1]));
+      CU_CHECK(cudaEventElapsedTime(&b, c->gemm_ev[slot][1], c->gemm_ev[slot][2]));
+      if (g1) g1[i] = a;
+      if (g2) g2[i] = b;
+      if (rows) rows[i] = c->gemm_rows[slot];
+    }
+    *n_out = n;
   });
 }
 
