@@ -97,8 +97,15 @@ typedef struct {
   double cv_threshold;
   int keep_alive_iters;
   int predictor_distance;     /* d: predictor slot 0 of layer l scores layer l + d (default 1) */
-  int reserved[6];
+  int precision;              /* MOE_PRECISION_BF16 (default) or MOE_PRECISION_FP32 */
+  int reserved[5];
 } moe_ctx_desc;
+
+/* precision of activations, weights and outputs.  BF16: bf16 in/out, fp32
+   accumulate on tcgen05 (tolerance 2e-2).  FP32: fp32 in/out, fp32 FFMA
+   (tolerance 1e-4); activation/output buffers are float, weights are loaded
+   with the *_f32 entry points. */
+enum { MOE_PRECISION_BF16 = 0, MOE_PRECISION_FP32 = 1 };
 
 typedef struct {
   /* LayerMetrics-compatible fields (types.hpp:73-80), measured */
@@ -135,6 +142,10 @@ int moe_ctx_sync(moe_ctx* ctx);
 int moe_load_expert_weights(moe_ctx* ctx, int layer, int expert, const uint16_t* w1,
                             const uint16_t* w3, const uint16_t* w2);
 int moe_set_gate_weights(moe_ctx* ctx, int layer, const uint16_t* wg);
+/* fp32-mode counterparts (MOE_PRECISION_FP32 contexts only) */
+int moe_load_expert_weights_f32(moe_ctx* ctx, int layer, int expert, const float* w1, const float* w3,
+                                const float* w2);
+int moe_set_gate_weights_f32(moe_ctx* ctx, int layer, const float* wg);
 /* predictor weights for target `slot` (< num_predictor_targets), scored from
    layer `layer`'s hidden states: [E, d_model] */
 int moe_set_predictor_weights(moe_ctx* ctx, int layer, int slot, const uint16_t* wp);

@@ -285,7 +285,8 @@ class MoELayer:
                  exchange_mode: int = MOE_EXCHANGE_NCCL, nccl_unique_id: Optional[bytes] = None,
                  num_predictor_targets: int = 0, expert_mem_mb: float = 0.0,
                  layer_mem_cap_mb: float = 0.0, gpu_mem_capacity_mb: float = 180000.0,
-                 cv_threshold: float = 0.2, keep_alive_iters: int = 50, predictor_distance: int = 1):
+                 cv_threshold: float = 0.2, keep_alive_iters: int = 50, predictor_distance: int = 1,
+                 precision: int = 0):
         d = MoeCtxDesc()
         d.num_layers, d.num_experts, d.top_k = num_layers, num_experts, top_k
         d.d_model, d.d_ff, d.max_tokens = d_model, d_ff, max_tokens
@@ -297,6 +298,8 @@ class MoELayer:
         d.layer_mem_cap_mb, d.gpu_mem_capacity_mb = layer_mem_cap_mb, gpu_mem_capacity_mb
         d.cv_threshold, d.keep_alive_iters = cv_threshold, keep_alive_iters
         d.predictor_distance = predictor_distance
+        d.precision = precision
+        self.fp32 = precision == 1
         h = C.c_void_p()
         check(lib.moe_ctx_create(C.byref(d), C.byref(h)))
         self._h = h
@@ -325,15 +328,19 @@ class MoELayer:
         check(lib.moe_ctx_sync(self._h))
 
     def load_expert(self, layer: int, expert: int, w1: np.ndarray, w3: np.ndarray, w2: np.ndarray):
+        dt = np.float32 if self.fp32 else np.uint16
         for w, shape in ((w1, (self.ff, self.d)), (w3, (self.ff, self.d)), (w2, (self.d, self.ff))):
-            if w.dtype != np.uint16 or w.shape != shape or not w.flags.c_contiguous:
-                raise ValueError(f"expert weight must be C-contiguous uint16 {shape}")
-        check(lib.moe_load_expert_weights(self._h, layer, expert, _p(w1), _p(w3), _p(w2)))
+            if w.dtype != dt or w.shape != shape or not w.flags.c_contiguous:
+                raise ValueError(f"expert weight must be C-contiguous {np.dtype(dt).name} {shape}")
+        fn = lib.moe_load_expert_weights_f32 if self.fp32 else lib.moe_load_expert_weights
+        check(fn(self._h, layer, expert, _p(w1), _p(w3), _p(w2)))
 
     def set_gate(self, layer: int, wg: np.ndarray) -> None:
-        if wg.dtype != np.uint16 or wg.shape != (self.E, self.d) or not wg.flags.c_contiguous:
-            raise ValueError("gate weight must be C-contiguous uint16 [E, d_model]")
-        check(lib.moe_set_gate_weights(self._h, layer, _p(wg)))
+        dt = np.float32 if self.fp32 else np.uint16
+        if wg.dtype != dt or wg.shape != (self.E, self.d) or not wg.flags.c_contiguous:
+            raise ValueError(f"gate weight must be C-contiguous {np.dtype(dt).name} [E, d_model]")
+        fn = lib.moe_set_gate_weights_f32 if self.fp32 else lib.moe_set_gate_weights
+        check(fn(self._h, layer, _p(wg)))
 
     def set_predictor(self, layer: int, slot: int, wp: np.ndarray) -> None:
         check(lib.moe_set_predictor_weights(self._h, layer, slot, _p(np.ascontiguousarray(wp))))

@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libmoe_b200.so")
 MOE_OK, MOE_EINVAL, MOE_EINFEASIBLE, MOE_ECUDA, MOE_ENCCL, MOE_ESTATE = range(6)
 MOE_EXCHANGE_NCCL, MOE_EXCHANGE_EXTERNAL = 0, 1
 MOE_PLAN_FIXED, MOE_PLAN_SYNC, MOE_PLAN_PREDICTED = 0, 1, 2
+MOE_PRECISION_BF16, MOE_PRECISION_FP32 = 0, 1
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -36,7 +37,7 @@ class MoeCtxDesc(C.Structure):
         ("num_predictor_targets", C.c_int),
         ("expert_mem_mb", dbl), ("layer_mem_cap_mb", dbl), ("gpu_mem_capacity_mb", dbl),
         ("cv_threshold", dbl), ("keep_alive_iters", C.c_int), ("predictor_distance", C.c_int),
-        ("reserved", C.c_int * 6),
+        ("precision", C.c_int), ("reserved", C.c_int * 5),
     ]
 
 
@@ -71,6 +72,8 @@ _sig("moe_ctx_stream", C.c_int, vp, P(vp))
 _sig("moe_ctx_sync", C.c_int, vp)
 _sig("moe_load_expert_weights", C.c_int, vp, C.c_int, C.c_int, vp, vp, vp)
 _sig("moe_set_gate_weights", C.c_int, vp, C.c_int, vp)
+_sig("moe_load_expert_weights_f32", C.c_int, vp, C.c_int, C.c_int, vp, vp, vp)
+_sig("moe_set_gate_weights_f32", C.c_int, vp, C.c_int, vp)
 _sig("moe_set_predictor_weights", C.c_int, vp, C.c_int, C.c_int, vp)
 _sig("moe_set_placement", C.c_int, vp, C.c_int, vp, vp)
 _sig("moe_gate_topk", C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp)
@@ -113,6 +116,7 @@ _sig("moe_synth_expert", C.c_int, u64, C.c_int, C.c_int, vp, vp, vp)
 EXPORTED = [
     "moe_last_error", "moe_version", "moe_nccl_unique_id", "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_stream",
     "moe_ctx_sync", "moe_load_expert_weights", "moe_set_gate_weights",
+    "moe_load_expert_weights_f32", "moe_set_gate_weights_f32",
     "moe_set_predictor_weights", "moe_set_placement", "moe_gate_topk", "moe_predict_loads",
     "moe_layer_forward", "moe_layer_forward_host", "moe_layer_forward_host_async", "moe_wait",
     "moe_host_alloc", "moe_host_free", "moe_gemm_times",

@@ -47,6 +47,15 @@ cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, 
                             __nv_bfloat16* xp_send, uint32_t* row_code, cudaStream_t s);
 cudaError_t launch_small_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
 cudaError_t launch_plan_local(const int32_t* counts, int E, DevPlan* plan, cudaStream_t s);
+// K7 fp32 path
+cudaError_t launch_gate_f32(const float* x, int T, int d, const float* wg, int E, int k, int32_t* ids, float* wts,
+                            int32_t* counts, int32_t* block_counts, cudaStream_t s);
+cudaError_t launch_grouped_sgemm(const float* A, int lda, const float* Bpool, int b_rows_per_slot, int ldb,
+                                 const GemmSeg* segs, const int* nseg, int N, int K, float* C, int ldc, int num_sms,
+                                 cudaStream_t s);
+cudaError_t launch_swiglu_f32(const float* C, int rows, int ff, float* H, cudaStream_t s);
+cudaError_t launch_combine_f32(const float* y_local, const float* y_return, int T, int d, int k,
+                               const uint32_t* row_code, const float* wts, float* y, cudaStream_t s);
 cudaError_t launch_combine(const __nv_bfloat16* y_local, const __nv_bfloat16* y_return, int T, int d, int k,
                            const uint32_t* row_code, const float* wts, __nv_bfloat16* y, int num_sms,
                            cudaStream_t s);
@@ -251,6 +260,10 @@ struct moe_ctx {
   int gemm_variant = 0;  // 0 auto, 1 force 1-SM, 2 force 2-SM (env MOE_GEMM_VARIANT=1sm|2sm)
   int pred_distance = 1;  // predictor slot 0 scores layer + pred_distance
   int count_stride = 0;   // ints per rank in the counts buffer: E * (1 + n_pred)
+  bool fp32 = false;      // MOE_PRECISION_FP32: SIMT fp32 path (K7)
+  int elem = 1;           // 16-bit units per element (2 in fp32 mode)
+  int xw = 0;             // one activation row in 16-bit units (d_model * elem)
+  DevBuf<float> gu_f32;   // fp32 GEMM1 output [rows_cap][2 ff]
   // K4 timing ring: events around GEMM1 / GEMM2 of every forward (no sync)
   static constexpr int kGemmRing = 64;
   cudaEvent_t gemm_ev[kGemmRing][3] = {};
@@ -278,6 +291,7 @@ struct moe_ctx {
   DevPlan* hplan = nullptr;
   int32_t* h_counts = nullptr;  // [G][E]
   uint16_t* wg_stage = nullptr;  // pinned staging for stream-ordered gate updates
+  size_t wg_stage_bytes = 0;
   cudaEvent_t ev_wg_staged = nullptr;
   HostPlan plan;
   moeless::ReplicaRegistry registry{0};
@@ -297,6 +311,11 @@ namespace {
 void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, int32_t* pred_counts) {
   require(L.has_gate, "gate weights not set for layer");
   CU_CHECK(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * c->count_stride, s));
+  if (c->fp32) {
+    CU_CHECK(launch_gate_f32(reinterpret_cast<const float*>(x), T, c->d, reinterpret_cast<const float*>(L.wg.p), c->E,
+                             c->k, c->ids.p, c->wts.p, c->counts.p, c->block_counts.p, s));
+    return;
+  }
   CU_CHECK(launch_gate_topk(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
                             reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, pred_counts ? c->n_pred : 0,
                             c->k, c->ids.p, c->wts.p, c->counts.p, c->block_counts.p,
@@ -400,7 +419,8 @@ void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool u
     CU_CHECK(launch_small_copy(c->dplan.p, c->hplan, sizeof(DevPlan), s));  // SM copy from mapped pinned memory
   const int nblk = gate_num_blocks(T);
   CU_CHECK(launch_block_prefix(c->block_counts.p, nblk, c->E, c->dplan.p, c->block_pre.p, s));
-  CU_CHECK(launch_dispatch(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d, c->E, c->k, c->ids.p, c->block_pre.p,
+  // rows move as opaque 16-byte chunks: the row width in 16-bit units covers fp32 rows too
+  CU_CHECK(launch_dispatch(reinterpret_cast<const __nv_bfloat16*>(x), T, c->xw, c->E, c->k, c->ids.p, c->block_pre.p,
                            c->dplan.p, reinterpret_cast<__nv_bfloat16*>(c->xp.p),
                            reinterpret_cast<__nv_bfloat16*>(c->send.p), c->row_code.p, s));
 }
@@ -409,21 +429,22 @@ void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool u
 // received-rows buffers; backward: my Y rows -> peers' return buffers.
 void stage_exchange(moe_ctx* c, bool forward, cudaStream_t s) {
   if (c->G == 1 || c->desc.exchange_mode != MOE_EXCHANGE_NCCL) return;
-  const size_t row_bytes = static_cast<size_t>(c->d) * 2;
+  const size_t w = static_cast<size_t>(c->xw);  // row width in 16-bit units (bf16 or fp32 rows)
+  const size_t row_bytes = w * 2;
   g_nccl.check(g_nccl.GroupStart(), "ncclGroupStart");
   if (forward) {
     for (const Chunk& ch : c->plan.sends)
-      g_nccl.check(g_nccl.Send(c->send.p + ch.row_offset * c->d, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
+      g_nccl.check(g_nccl.Send(c->send.p + ch.row_offset * w, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
                    "ncclSend");
     for (const Chunk& ch : c->plan.recvs)
-      g_nccl.check(g_nccl.Recv(c->xp.p + ch.row_offset * c->d, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
+      g_nccl.check(g_nccl.Recv(c->xp.p + ch.row_offset * w, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
                    "ncclRecv");
   } else {
     for (const Chunk& ch : c->plan.recvs)
-      g_nccl.check(g_nccl.Send(c->yp.p + ch.row_offset * c->d, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
+      g_nccl.check(g_nccl.Send(c->yp.p + ch.row_offset * w, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
                    "ncclSend");
     for (const Chunk& ch : c->plan.sends)
-      g_nccl.check(g_nccl.Recv(c->ret.p + ch.row_offset * c->d, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
+      g_nccl.check(g_nccl.Recv(c->ret.p + ch.row_offset * w, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
                    "ncclRecv");
   }
   g_nccl.check(g_nccl.GroupEnd(), "ncclGroupEnd");
@@ -435,8 +456,23 @@ void stage_exchange(moe_ctx* c, bool forward, cudaStream_t s) {
 // B200's 1 kW cap it settles ~190 MHz lower and nets ~4% less throughput on
 // the Mixtral layer (profiles/ab_gemm_variants_r01.md), so it is opt-in
 // (MOE_GEMM_VARIANT=2sm) until it is made more energy-efficient.
-void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s) {
+void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t rows = 0) {
   Layer& L = c->layers[layer];
+  if (c->fp32) {  // K7: SIMT fp32 grouped GEMMs (+ SwiGLU pass between them)
+    const GemmSeg* segs = c->dplan.p->segs;
+    const int* nseg = &c->dplan.p->nseg;
+    if (which == 0) {
+      CU_CHECK(launch_grouped_sgemm(reinterpret_cast<const float*>(c->xp.p), c->d,
+                                    reinterpret_cast<const float*>(L.w13.p), 2 * c->ff, c->d, segs, nseg, 2 * c->ff,
+                                    c->d, c->gu_f32.p, 2 * c->ff, c->num_sms, s));
+      CU_CHECK(launch_swiglu_f32(c->gu_f32.p, static_cast<int>(rows), c->ff, reinterpret_cast<float*>(c->h.p), s));
+    } else {
+      CU_CHECK(launch_grouped_sgemm(reinterpret_cast<const float*>(c->h.p), c->ff,
+                                    reinterpret_cast<const float*>(L.w2.p), c->d, c->ff, segs, nseg, c->d, c->ff,
+                                    reinterpret_cast<float*>(c->yp.p), c->d, c->num_sms, s));
+    }
+    return;
+  }
   const bool two_sm = c->gemm_variant == 2;
   auto fn = two_sm ? launch_grouped_gemm_2sm : launch_grouped_gemm;
   if (which == 0)
@@ -448,11 +484,16 @@ void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s) {
 }
 
 void stage_expert(moe_ctx* c, int layer, cudaStream_t s) {
-  launch_ffn_gemm(c, layer, 0, s);
-  launch_ffn_gemm(c, layer, 1, s);
+  launch_ffn_gemm(c, layer, 0, s, c->plan.rows_local);
+  launch_ffn_gemm(c, layer, 1, s, c->plan.rows_local);
 }
 
 void stage_combine(moe_ctx* c, uint16_t* y, int T, cudaStream_t s) {
+  if (c->fp32) {
+    CU_CHECK(launch_combine_f32(reinterpret_cast<const float*>(c->yp.p), reinterpret_cast<const float*>(c->ret.p), T,
+                                c->d, c->k, c->row_code.p, c->wts.p, reinterpret_cast<float*>(y), s));
+    return;
+  }
   CU_CHECK(launch_combine(reinterpret_cast<const __nv_bfloat16*>(c->yp.p),
                           reinterpret_cast<const __nv_bfloat16*>(c->ret.p), T, c->d, c->k, c->row_code.p, c->wts.p,
                           reinterpret_cast<__nv_bfloat16*>(y), c->num_sms, s));
@@ -477,8 +518,10 @@ Layer& layer_at(moe_ctx* c, int layer) {
 
 void ensure_pools(moe_ctx* c, Layer& L) {
   if (L.w13.p) return;
-  L.w13.alloc(static_cast<size_t>(c->E) * 2 * c->ff * c->d);
-  L.w2.alloc(static_cast<size_t>(c->E) * c->d * c->ff);
+  L.w13.alloc(static_cast<size_t>(c->E) * 2 * c->ff * c->d * c->elem);
+  L.w2.alloc(static_cast<size_t>(c->E) * c->d * c->ff * c->elem);
+  L.expert_loaded.assign(c->E, 0);
+  if (c->fp32) return;  // SIMT fp32 path: no tensor maps
   L.tmB1 = make_kmajor_map(L.w13.p, static_cast<uint64_t>(c->E) * 2 * c->ff, c->d, 256);
   L.tmB2 = make_kmajor_map(L.w2.p, static_cast<uint64_t>(c->E) * c->d, c->ff, 256);
   L.tmB1h = make_kmajor_map(L.w13.p, static_cast<uint64_t>(c->E) * 2 * c->ff, c->d, 128);
@@ -536,13 +579,14 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   stage_exchange(c, true, s);
   mark(4);
   const int gslot = static_cast<int>(c->gemm_seq % moe_ctx::kGemmRing);
+  const int64_t rows_here = c->G == 1 ? static_cast<int64_t>(T) * c->k : c->plan.rows_local;
   CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][0], s));
-  launch_ffn_gemm(c, layer, 0, s);
+  launch_ffn_gemm(c, layer, 0, s, rows_here);
   CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][1], s));
   mark(5);
-  launch_ffn_gemm(c, layer, 1, s);
+  launch_ffn_gemm(c, layer, 1, s, rows_here);
   CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][2], s));
-  c->gemm_rows[gslot] = c->G == 1 ? static_cast<int64_t>(T) * c->k : c->plan.rows_local;
+  c->gemm_rows[gslot] = rows_here;
   ++c->gemm_seq;
   mark(6);
   stage_exchange(c, false, s);
@@ -632,6 +676,10 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     }
     c->registry = moeless::ReplicaRegistry(std::max(0, D.keep_alive_iters));
     c->layers.resize(D.num_layers);
+    require(D.precision == MOE_PRECISION_BF16 || D.precision == MOE_PRECISION_FP32, "unknown precision");
+    c->fp32 = D.precision == MOE_PRECISION_FP32;
+    c->elem = c->fp32 ? 2 : 1;
+    require(!c->fp32 || c->n_pred == 0, "the fp32 mode has no fused predictor");
     CU_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     const int64_t assign = static_cast<int64_t>(c->Tmax) * c->k;
     c->rows_cap = assign * c->G;  // worst case: every rank routes everything here
@@ -646,14 +694,20 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->pred_counts.alloc(static_cast<size_t>(c->E) * std::max(1, c->n_pred));
     c->block_counts.alloc(static_cast<size_t>(nblk) * c->E);
     c->block_pre.alloc(static_cast<size_t>(nblk) * c->E);
-    c->xp.alloc(static_cast<size_t>(c->rows_cap) * c->d);
-    c->h.alloc(static_cast<size_t>(c->rows_cap) * c->ff);
-    c->yp.alloc(static_cast<size_t>(c->rows_cap) * c->d);
-    c->send.alloc(static_cast<size_t>(c->send_cap) * c->d);
-    c->ret.alloc(static_cast<size_t>(c->send_cap) * c->d);
+    // row buffers in 16-bit units: one row = d_model * elem units (elem 2 for fp32)
+    c->xw = c->d * c->elem;
+    c->xp.alloc(static_cast<size_t>(c->rows_cap) * c->xw);
+    c->h.alloc(static_cast<size_t>(c->rows_cap) * c->ff * c->elem);
+    c->yp.alloc(static_cast<size_t>(c->rows_cap) * c->xw);
+    c->send.alloc(static_cast<size_t>(c->send_cap) * c->xw);
+    c->ret.alloc(static_cast<size_t>(c->send_cap) * c->xw);
     c->dplan.alloc(1);
-    c->tmA1 = make_kmajor_map(c->xp.p, c->rows_cap, c->d, 128);
-    c->tmA2 = make_kmajor_map(c->h.p, c->rows_cap, c->ff, 128);
+    if (c->fp32) {
+      c->gu_f32.alloc(static_cast<size_t>(c->rows_cap) * 2 * c->ff);  // GEMM1 output before SwiGLU
+    } else {
+      c->tmA1 = make_kmajor_map(c->xp.p, c->rows_cap, c->d, 128);
+      c->tmA2 = make_kmajor_map(c->h.p, c->rows_cap, c->ff, 128);
+    }
     // mapped pinned control buffers, read/written by small SM copies (UVA pointers)
     CU_CHECK(cudaHostAlloc(&c->hplan, sizeof(DevPlan), cudaHostAllocMapped));
     CU_CHECK(cudaHostAlloc(&c->h_counts, pad16(sizeof(int32_t) * c->count_stride * c->G), cudaHostAllocMapped));
@@ -718,52 +772,82 @@ int moe_ctx_sync(moe_ctx* c) {
   });
 }
 
+namespace {
+// elem: 16-bit units per element of the caller's arrays (1 bf16, 2 fp32)
+void load_expert_impl(moe_ctx* c, int layer, int expert, const void* w1v, const void* w3v, const void* w2v,
+                      int elem) {
+  Layer& L = layer_at(c, layer);
+  require(elem == c->elem, elem == 2 ? "fp32 weights need a MOE_PRECISION_FP32 context"
+                                     : "bf16 weights need a MOE_PRECISION_BF16 context");
+  require(expert >= 0 && expert < c->E, "expert out of range");
+  require(w1v && w3v && w2v, "null weight pointer");
+  ensure_pools(c, L);
+  const uint16_t* w1 = static_cast<const uint16_t*>(w1v);
+  const uint16_t* w3 = static_cast<const uint16_t*>(w3v);
+  const uint16_t* w2 = static_cast<const uint16_t*>(w2v);
+  // W13 pool: per 128-row block b of the expert, rows [W1[b*128..], W3[b*128..]]
+  const size_t row = static_cast<size_t>(c->d) * elem;  // one weight row in 16-bit units
+  uint16_t* base = L.w13.p + static_cast<size_t>(expert) * 2 * c->ff * row;
+  for (int b = 0; b < c->ff / 128; ++b) {
+    CU_CHECK(cudaMemcpyAsync(base + static_cast<size_t>(b) * 256 * row, w1 + static_cast<size_t>(b) * 128 * row,
+                             128 * row * 2, cudaMemcpyHostToDevice, c->stream));
+    CU_CHECK(cudaMemcpyAsync(base + (static_cast<size_t>(b) * 256 + 128) * row, w3 + static_cast<size_t>(b) * 128 * row,
+                             128 * row * 2, cudaMemcpyHostToDevice, c->stream));
+  }
+  CU_CHECK(cudaMemcpyAsync(L.w2.p + static_cast<size_t>(expert) * c->d * c->ff * elem, w2,
+                           static_cast<size_t>(c->d) * c->ff * 2 * elem, cudaMemcpyHostToDevice, c->stream));
+  CU_CHECK(cudaStreamSynchronize(c->stream));
+  L.expert_loaded[expert] = 1;
+}
+}  // namespace
+
 int moe_load_expert_weights(moe_ctx* c, int layer, int expert, const uint16_t* w1, const uint16_t* w3,
                             const uint16_t* w2) {
-  return guarded([&] {
-    Layer& L = layer_at(c, layer);
-    require(expert >= 0 && expert < c->E, "expert out of range");
-    require(w1 && w3 && w2, "null weight pointer");
-    ensure_pools(c, L);
-    // W13 pool: per 128-row block b of the expert, rows [W1[b*128..], W3[b*128..]]
-    const size_t rowb = static_cast<size_t>(c->d) * 2;
-    uint16_t* base = L.w13.p + static_cast<size_t>(expert) * 2 * c->ff * c->d;
-    for (int b = 0; b < c->ff / 128; ++b) {
-      CU_CHECK(cudaMemcpyAsync(base + static_cast<size_t>(b) * 256 * c->d, w1 + static_cast<size_t>(b) * 128 * c->d,
-                               128 * rowb, cudaMemcpyHostToDevice, c->stream));
-      CU_CHECK(cudaMemcpyAsync(base + (static_cast<size_t>(b) * 256 + 128) * c->d,
-                               w3 + static_cast<size_t>(b) * 128 * c->d, 128 * rowb, cudaMemcpyHostToDevice,
-                               c->stream));
-    }
-    CU_CHECK(cudaMemcpyAsync(L.w2.p + static_cast<size_t>(expert) * c->d * c->ff, w2,
-                             static_cast<size_t>(c->d) * c->ff * 2, cudaMemcpyHostToDevice, c->stream));
-    CU_CHECK(cudaStreamSynchronize(c->stream));
-    L.expert_loaded[expert] = 1;
-  });
+  return guarded([&] { load_expert_impl(c, layer, expert, w1, w3, w2, 1); });
+}
+
+int moe_load_expert_weights_f32(moe_ctx* c, int layer, int expert, const float* w1, const float* w3,
+                                const float* w2) {
+  return guarded([&] { load_expert_impl(c, layer, expert, w1, w3, w2, 2); });
+}
+
+namespace {
+void set_gate_impl(moe_ctx* c, int layer, const void* wg, int elem) {
+  Layer& L = layer_at(c, layer);
+  require(wg != nullptr, "null gate weights");
+  require(elem == c->elem, "gate weight precision does not match the context");
+  if (!L.wg.p) {
+    L.wg.alloc(static_cast<size_t>(c->E) * c->d * (1 + c->n_pred) * elem);
+    CU_CHECK(cudaMemsetAsync(L.wg.p, 0, L.wg.n * 2, c->stream));
+  }
+  // Stream-ordered update through a pinned staging buffer: forwards already
+  // enqueued keep the old weights, later ones see the new — no device sync.
+  const size_t bytes = static_cast<size_t>(c->E) * c->d * 2 * elem;
+  if (c->wg_stage && c->wg_stage_bytes < bytes) {
+    CU_CHECK(cudaEventSynchronize(c->ev_wg_staged));
+    CU_CHECK(cudaFreeHost(c->wg_stage));
+    c->wg_stage = nullptr;
+  }
+  if (!c->wg_stage) {
+    CU_CHECK(cudaHostAlloc(&c->wg_stage, bytes, cudaHostAllocMapped));
+    c->wg_stage_bytes = bytes;
+    if (!c->ev_wg_staged) CU_CHECK(cudaEventCreateWithFlags(&c->ev_wg_staged, cudaEventDisableTiming));
+  } else {
+    CU_CHECK(cudaEventSynchronize(c->ev_wg_staged));  // previous upload has left the staging buffer
+  }
+  std::memcpy(c->wg_stage, wg, bytes);
+  CU_CHECK(launch_small_copy(L.wg.p, c->wg_stage, bytes, c->stream));
+  CU_CHECK(cudaEventRecord(c->ev_wg_staged, c->stream));
+  L.has_gate = true;
+}
+}  // namespace
+
+int moe_set_gate_weights_f32(moe_ctx* c, int layer, const float* wg) {
+  return guarded([&] { set_gate_impl(c, layer, wg, 2); });
 }
 
 int moe_set_gate_weights(moe_ctx* c, int layer, const uint16_t* wg) {
-  return guarded([&] {
-    Layer& L = layer_at(c, layer);
-    require(wg != nullptr, "null gate weights");
-    if (!L.wg.p) {
-      L.wg.alloc(static_cast<size_t>(c->E) * c->d * (1 + c->n_pred));
-      CU_CHECK(cudaMemsetAsync(L.wg.p, 0, L.wg.n * 2, c->stream));
-    }
-    // Stream-ordered update through a pinned staging buffer: forwards already
-    // enqueued keep the old weights, later ones see the new — no device sync.
-    const size_t bytes = static_cast<size_t>(c->E) * c->d * 2;
-    if (!c->wg_stage) {
-      CU_CHECK(cudaHostAlloc(&c->wg_stage, bytes, cudaHostAllocMapped));
-      CU_CHECK(cudaEventCreateWithFlags(&c->ev_wg_staged, cudaEventDisableTiming));
-    } else {
-      CU_CHECK(cudaEventSynchronize(c->ev_wg_staged));  // previous upload has left the staging buffer
-    }
-    std::memcpy(c->wg_stage, wg, bytes);
-    CU_CHECK(launch_small_copy(L.wg.p, c->wg_stage, bytes, c->stream));
-    CU_CHECK(cudaEventRecord(c->ev_wg_staged, c->stream));
-    L.has_gate = true;
-  });
+  return guarded([&] { set_gate_impl(c, layer, wg, 1); });
 }
 
 int moe_set_predictor_weights(moe_ctx* c, int layer, int slot, const uint16_t* wp) {
@@ -849,10 +933,10 @@ int moe_layer_forward_host(moe_ctx* c, int layer, const uint16_t* x_host, int T,
     require(c && x_host && y_host, "null argument");
     require(T >= 0 && T <= c->Tmax, "token count exceeds max_tokens");
     if (!c->x_in.p) {
-      c->x_in.alloc(static_cast<size_t>(c->Tmax) * c->d);
-      c->y_out.alloc(static_cast<size_t>(c->Tmax) * c->d);
+      c->x_in.alloc(static_cast<size_t>(c->Tmax) * c->xw);
+      c->y_out.alloc(static_cast<size_t>(c->Tmax) * c->xw);
     }
-    const size_t bytes = static_cast<size_t>(T) * c->d * 2;
+    const size_t bytes = static_cast<size_t>(T) * c->xw * 2;
     CU_CHECK(cudaMemcpyAsync(c->x_in.p, x_host, bytes, cudaMemcpyHostToDevice, c->stream));
     forward_device(c, layer, c->x_in.p, T, c->y_out.p, plan_mode, iteration, stats, c->stream);
     CU_CHECK(cudaMemcpyAsync(y_host, c->y_out.p, bytes, cudaMemcpyDeviceToHost, c->stream));
@@ -869,8 +953,8 @@ int moe_layer_forward_host_async(moe_ctx* c, int layer, const uint16_t* x_host, 
       CU_CHECK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
       CU_CHECK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
       for (int i = 0; i < 2; ++i) {
-        c->xa[i].alloc(static_cast<size_t>(c->Tmax) * c->d);
-        c->ya[i].alloc(static_cast<size_t>(c->Tmax) * c->d);
+        c->xa[i].alloc(static_cast<size_t>(c->Tmax) * c->xw);
+        c->ya[i].alloc(static_cast<size_t>(c->Tmax) * c->xw);
         for (cudaEvent_t* e : {&c->ev_x_ready[i], &c->ev_x_free[i], &c->ev_y_ready[i], &c->ev_done[i]}) {
           CU_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
           CU_CHECK(cudaEventRecord(*e, c->stream));  // "already satisfied" for the first use
@@ -880,7 +964,7 @@ int moe_layer_forward_host_async(moe_ctx* c, int layer, const uint16_t* x_host, 
     }
     const int64_t tk = c->next_ticket++;
     const int slot = static_cast<int>(tk & 1);
-    const size_t bytes = static_cast<size_t>(T) * c->d * 2;
+    const size_t bytes = static_cast<size_t>(T) * c->xw * 2;
     // upload: wait until the call two steps back has finished reading this slot
     CU_CHECK(cudaStreamWaitEvent(c->h2d, c->ev_x_free[slot], 0));
     CU_CHECK(cudaMemcpyAsync(c->xa[slot].p, x_host, bytes, cudaMemcpyHostToDevice, c->h2d));

@@ -1,0 +1,217 @@
+// fp32_path.cu — K7: the fp32 mode of the MoE layer (north_star: outputs
+// within 1e-4 of the fp32 reference).  TF32 tensor cores (10-bit mantissa)
+// cannot meet that bar, so the expert FFN runs as grouped SIMT SGEMMs with
+// fp32 FFMA accumulation; gate and combine are fp32 end to end.  Dispatch is
+// shared with the bf16 path (it moves rows as opaque 16-byte chunks).
+//
+//   gate_f32_kernel       one warp per token: fp32 logits x Wg^T, top-k with
+//                         lowest-index ties, softmax over the chosen k,
+//                         per-32-token block histogram (same contract as K1)
+//   grouped_sgemm_kernel  C[r, n] = sum_k A[r, k] B[slot][n, k] over ragged
+//                         segments; 128x128 tiles, BK = 16, 8x8 per thread,
+//                         operands staged transposed in smem
+//   swiglu_f32_kernel     H[r, f] = silu(C[r, gate f]) * C[r, up f] with the
+//                         W1/W3 128-row-block interleave of the weight pool
+//   combine_f32_kernel    y_t = sum_j w_tj Y[row(t, j)] in slot order
+#include <cfloat>
+#include <cstdint>
+
+#include "dispatch_plan.h"
+#include "sm100_ptx.cuh"
+
+namespace moe {
+
+// ------------------------------------------------------------------ gate
+__global__ void __launch_bounds__(256)
+gate_f32_kernel(const float* __restrict__ x, int T, int d, const float* __restrict__ wg, int E, int k,
+                int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
+                int32_t* __restrict__ block_counts) {
+  __shared__ int hist[256];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  for (int i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  // CTA = 32 tokens (one block_counts row), 8 warps x 4 tokens
+  for (int q = 0; q < 4; ++q) {
+    const int t = blockIdx.x * 32 + warp * 4 + q;
+    if (t >= T) break;
+    const float* xr = x + (size_t)t * d;
+    float own[8];
+    for (int s = 0; s < 8; ++s) own[s] = -FLT_MAX;
+    for (int e = 0; e < E; ++e) {
+      const float* wr = wg + (size_t)e * d;
+      float acc = 0.0f;
+      for (int c = lane; c < d; c += 32) acc = fmaf(xr[c], wr[c], acc);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if ((e & 31) == lane) own[e >> 5] = acc;
+    }
+    uint32_t taken = 0;
+    float lg[8];
+    int sel[8];
+    for (int j = 0; j < k; ++j) {
+      float bv = -FLT_MAX;
+      int bi = 0x7fffffff;
+      for (int s = 0; s < 8; ++s) {
+        const int e = lane + 32 * s;
+        if (e < E && !((taken >> s) & 1u) && (own[s] > bv || (own[s] == bv && e < bi))) { bv = own[s]; bi = e; }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+      sel[j] = bi;
+      lg[j] = bv;
+    }
+    if (lane == 0) {
+      float z = 0.0f, p[8];
+      for (int j = 0; j < k; ++j) { p[j] = expf(lg[j] - lg[0]); z += p[j]; }
+      for (int j = 0; j < k; ++j) {
+        ids[(size_t)t * k + j] = sel[j];
+        wts[(size_t)t * k + j] = p[j] / z;
+        atomicAdd(&hist[sel[j]], 1);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    block_counts[(size_t)blockIdx.x * E + e] = hist[e];
+    if (hist[e]) atomicAdd(counts + e, hist[e]);
+  }
+}
+
+// ---------------------------------------------------------- grouped SGEMM
+constexpr int SG_BM = 128, SG_BN = 128, SG_BK = 16;
+
+// grid: persistent CTAs; tiles enumerated over segments x m-tiles x n-tiles.
+__global__ void __launch_bounds__(256)
+grouped_sgemm_kernel(const float* __restrict__ A, int lda, const float* __restrict__ Bpool, int b_rows_per_slot,
+                     int ldb, const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int N, int K,
+                     float* __restrict__ C, int ldc) {
+  __shared__ float As[SG_BK][SG_BM + 4];
+  __shared__ float Bs[SG_BK][SG_BN + 4];
+  __shared__ int seg_tiles[kMaxReplicas + 1];
+  const int nseg = min(*nseg_g, kMaxReplicas);
+  const int n_tiles = N / SG_BN;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int s = 0; s < nseg; ++s) {
+      seg_tiles[s] = acc;
+      acc += ((segs_g[s].rows + SG_BM - 1) / SG_BM) * n_tiles;
+    }
+    seg_tiles[nseg] = acc;
+  }
+  __syncthreads();
+  const int total = nseg > 0 ? seg_tiles[nseg] : 0;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 8 x 8 outputs each
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    int s = 0;
+    while (s + 1 < nseg && seg_tiles[s + 1] <= t) ++s;
+    const GemmSeg sg = segs_g[s];
+    const int local = t - seg_tiles[s];
+    const int m0 = (local / n_tiles) * SG_BM, n0 = (local % n_tiles) * SG_BN;
+    const float* Ab = A + (size_t)(sg.row_start + m0) * lda;
+    const float* Bb = Bpool + ((size_t)sg.slot * b_rows_per_slot + n0) * ldb;
+    const int mrows = min(SG_BM, sg.rows - m0);
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+    for (int k0 = 0; k0 < K; k0 += SG_BK) {
+      // 256 threads load 128 x 16 of A and of B (8 floats each), transposed into smem
+      for (int i = threadIdx.x; i < SG_BM * SG_BK; i += 256) {
+        const int r = i / SG_BK, kk = i % SG_BK;
+        As[kk][r] = r < mrows ? Ab[(size_t)r * lda + k0 + kk] : 0.0f;
+        Bs[kk][r] = Bb[(size_t)r * ldb + k0 + kk];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < SG_BK; ++kk) {
+        float a[8], b[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = As[kk][ty * 8 + i];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) b[j] = Bs[kk][tx * 8 + j];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = ty * 8 + i;
+      if (r < mrows) {
+        float* cr = C + (size_t)(sg.row_start + m0 + r) * ldc + n0 + tx * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cr[j] = acc[i][j];
+      }
+    }
+  }
+}
+
+// gate/up interleave: C row = [W1 blk 0 (128) | W3 blk 0 (128) | W1 blk 1 | ...]
+__global__ void swiglu_f32_kernel(const float* __restrict__ C, int rows, int ff, float* __restrict__ H) {
+  const size_t n = (size_t)rows * ff;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / ff;
+    const int f = static_cast<int>(i % ff);
+    const int blk = f >> 7, j = f & 127;
+    const float g = C[r * 2 * ff + blk * 256 + j];
+    const float u = C[r * 2 * ff + blk * 256 + 128 + j];
+    H[i] = g / (1.0f + expf(-g)) * u;
+  }
+}
+
+__global__ void combine_f32_kernel(const float* __restrict__ y_local, const float* __restrict__ y_return, int T,
+                                   int d, int k, const uint32_t* __restrict__ row_code, const float* __restrict__ wts,
+                                   float* __restrict__ y) {
+  const size_t n = (size_t)T * d;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t t = i / d;
+    const int c = static_cast<int>(i % d);
+    float acc = 0.0f;
+    for (int j = 0; j < k; ++j) {
+      const uint32_t code = row_code[t * k + j];
+      const float* src = ((code & kRemoteBit) ? y_return : y_local) + (size_t)(code & ~kRemoteBit) * d;
+      acc = fmaf(wts[t * k + j], src[c], acc);
+    }
+    y[i] = acc;
+  }
+}
+
+// --------------------------------------------------------------- launchers
+cudaError_t launch_gate_f32(const float* x, int T, int d, const float* wg, int E, int k, int32_t* ids, float* wts,
+                            int32_t* counts, int32_t* block_counts, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  if (E > 256 || k > 8) return cudaErrorInvalidValue;
+  gate_f32_kernel<<<(T + 31) / 32, 256, 0, s>>>(x, T, d, wg, E, k, ids, wts, counts, block_counts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grouped_sgemm(const float* A, int lda, const float* Bpool, int b_rows_per_slot, int ldb,
+                                 const GemmSeg* segs, const int* nseg, int N, int K, float* C, int ldc, int num_sms,
+                                 cudaStream_t s) {
+  if (N % SG_BN || K % SG_BK) return cudaErrorInvalidValue;
+  grouped_sgemm_kernel<<<num_sms * 2, 256, 0, s>>>(A, lda, Bpool, b_rows_per_slot, ldb, segs, nseg, N, K, C, ldc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_swiglu_f32(const float* C, int rows, int ff, float* H, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  swiglu_f32_kernel<<<1184, 256, 0, s>>>(C, rows, ff, H);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine_f32(const float* y_local, const float* y_return, int T, int d, int k,
+                               const uint32_t* row_code, const float* wts, float* y, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  combine_f32_kernel<<<1184, 256, 0, s>>>(y_local, y_return, T, d, k, row_code, wts, y);
+  return cudaGetLastError();
+}
+
+}  // namespace moe
