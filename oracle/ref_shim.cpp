@@ -15,7 +15,11 @@
 #include <string>
 #include <vector>
 
+#include <algorithm>
+
 #include "moeless/baselines.hpp"
+#include "moeless/config.hpp"
+#include "moeless/simulator.hpp"
 #include "moeless/cost_model.hpp"
 #include "moeless/placer.hpp"
 #include "moeless/predictor.hpp"
@@ -249,6 +253,23 @@ int ref_static_plan(const std::int64_t* loads, int experts, int gpus, double exp
     c.gpu_mem_capacity_mb = gpu_mem_mb;
     auto r = static_plan(lv(loads, experts), m, c);
     for (int e = 0; e < experts; ++e) gpu_out[e] = r.second.gpu_for[e][0];
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// The reference simulator end to end (config.cpp:90 parse_config_text ->
+// workload.cpp:90 parse_trace -> simulator.cpp:71 run -> report.cpp:48
+// summary_json), for driving it with B200-calibrated alpha/beta/t_misc.
+// Writes the summary JSON into out (NUL-terminated, truncated to cap).
+int ref_simulate(const char* config_text, const char* trace_path, char* out, int cap) {
+  try {
+    SimConfig cfg = parse_config_text(config_text, "<calibrated>");
+    auto trace = parse_trace(trace_path);
+    auto rep = run(cfg, trace);
+    const std::string js = summary_json(rep);
+    const int n = std::min<int>(cap - 1, static_cast<int>(js.size()));
+    std::memcpy(out, js.data(), n);
+    out[n] = 0;
     return 0;
   } catch (const std::exception& e) { return fail(e); }
 }
