@@ -274,6 +274,20 @@ int ref_simulate(const char* config_text, const char* trace_path, char* out, int
   } catch (const std::exception& e) { return fail(e); }
 }
 
+// parse_trace + batch_requests (workload.cpp:90-186): writes up to cap
+// (iteration, phase 0/1, token_count) triples, returns the batch count.
+long ref_batch_trace(const char* trace_path, long* out, long cap) {
+  try {
+    auto b = batch_requests(parse_trace(trace_path));
+    for (long i = 0; i < static_cast<long>(b.size()) && i < cap; ++i) {
+      out[3 * i] = b[i].iteration;
+      out[3 * i + 1] = b[i].phase == Phase::decode ? 1 : 0;
+      out[3 * i + 2] = static_cast<long>(b[i].token_count);
+    }
+    return static_cast<long>(b.size());
+  } catch (const std::exception& e) { fail(e); return -1; }
+}
+
 // The reference's per-layer CPU path, exactly as run() sequences it
 // (simulator.cpp:116-201): route_tokens -> predict -> scale_experts ->
 // place_experts -> layer_forward_time -> update_registry.  Runs `iters`
