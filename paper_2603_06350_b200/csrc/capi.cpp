@@ -39,7 +39,7 @@ namespace moe {
 int gate_num_blocks(int T);
 cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bfloat16* w_all, int E, int n_pred,
                              int k, int32_t* ids, float* wts, int32_t* counts, int32_t* block_counts,
-                             int32_t* pred_counts, cudaStream_t stream);
+                             int32_t* pred_counts, float* partial, cudaStream_t stream);
 cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, const DevPlan* plan,
                                 int32_t* block_pre, cudaStream_t s);
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
@@ -264,6 +264,7 @@ struct moe_ctx {
   int elem = 1;           // 16-bit units per element (2 in fp32 mode)
   int xw = 0;             // one activation row in 16-bit units (d_model * elem)
   DevBuf<float> gu_f32;   // fp32 GEMM1 output [rows_cap][2 ff]
+  DevBuf<float> gate_partial;  // split-K gate scratch (small batches)
   // K4 timing ring: events around GEMM1 / GEMM2 of every forward (no sync)
   static constexpr int kGemmRing = 64;
   cudaEvent_t gemm_ev[kGemmRing][3] = {};
@@ -319,7 +320,7 @@ void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, 
   CU_CHECK(launch_gate_topk(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
                             reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, pred_counts ? c->n_pred : 0,
                             c->k, c->ids.p, c->wts.p, c->counts.p, c->block_counts.p,
-                            pred_counts ? pred_counts : c->pred_counts.p, s));
+                            pred_counts ? pred_counts : c->pred_counts.p, c->gate_partial.p, s));
 }
 
 // Decide the placement for this forward (host), then build + upload the plan.
@@ -702,6 +703,11 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->send.alloc(static_cast<size_t>(c->send_cap) * c->xw);
     c->ret.alloc(static_cast<size_t>(c->send_cap) * c->xw);
     c->dplan.alloc(1);
+    {  // split-K gate scratch: <= 296 (block, split) CTAs x 32 tokens x padded logits
+      int nt = 1;
+      while (8 * nt < c->count_stride) nt *= 2;
+      c->gate_partial.alloc(static_cast<size_t>(296) * 32 * 8 * nt);
+    }
     if (c->fp32) {
       c->gu_f32.alloc(static_cast<size_t>(c->rows_cap) * 2 * c->ff);  // GEMM1 output before SwiGLU
     } else {
@@ -897,7 +903,8 @@ int moe_gate_topk(moe_ctx* c, int layer, const uint16_t* x, int T, int32_t* ids,
     if (pred_counts && c->n_pred) CU_CHECK(cudaMemsetAsync(pred_counts, 0, sizeof(int32_t) * c->E * c->n_pred, s));
     CU_CHECK(launch_gate_topk(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
                               reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, pred_counts ? c->n_pred : 0, c->k,
-                              ids, w, counts, c->block_counts.p, pred_counts ? pred_counts : c->pred_counts.p, s));
+                              ids, w, counts, c->block_counts.p, pred_counts ? pred_counts : c->pred_counts.p,
+                              c->gate_partial.p, s));
   });
 }
 
@@ -915,7 +922,7 @@ int moe_predict_loads(moe_ctx* c, int layer, const uint16_t* x, int T, int32_t* 
     CU_CHECK(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * c->E, s));
     CU_CHECK(launch_gate_topk(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
                               reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, c->n_pred, c->k, c->ids.p,
-                              c->wts.p, c->counts.p, c->block_counts.p, pred_counts, s));
+                              c->wts.p, c->counts.p, c->block_counts.p, pred_counts, c->gate_partial.p, s));
   });
 }
 

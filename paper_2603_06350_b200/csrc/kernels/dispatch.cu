@@ -71,16 +71,6 @@ block_prefix_kernel(const int32_t* __restrict__ block_counts, int nblk, int E,
 }
 
 // ------------------------------------------------------------- dispatch
-__device__ __forceinline__ uint32_t row_code_for(const DevPlan* plan, int e, int gr) {
-  const int n = plan->n_e[e];
-  const int R = plan->rep_base[e + 1] - plan->rep_base[e];
-  const int q = n / R, rem = n % R;
-  const int r = gr < rem * (q + 1) ? gr / (q + 1) : rem + (gr - rem * (q + 1)) / q;
-  const int f = plan->rep_base[e] + r;
-  const uint32_t row = static_cast<uint32_t>(plan->rep_row_base[f] + gr);
-  return row | (plan->rep_remote[f] ? kRemoteBit : 0u);
-}
-
 template <int K>
 __global__ void __launch_bounds__(128)
 dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const int32_t* __restrict__ ids,
@@ -88,10 +78,27 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
                 __nv_bfloat16* __restrict__ xp_local, __nv_bfloat16* __restrict__ xp_send,
                 uint32_t* __restrict__ row_code) {
   __shared__ uint32_t codes[32 * K];
+  // the block's prefix row and the plan tables the ranking loop reads, staged
+  // once (coalesced) so the per-expert loop below never waits on L2
+  __shared__ int s_pre[kMaxExperts], s_n[kMaxExperts], s_rbase[kMaxExperts + 1];
+  __shared__ int s_rrow[kMaxReplicas];
+  __shared__ unsigned char s_rrem[kMaxReplicas];
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int t_base = b * 32;
   const int ntok = min(32, T - t_base);
+  const int R = plan->R;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {
+    s_pre[i] = block_pre[(size_t)b * E + i];
+    s_n[i] = plan->n_e[i];
+    s_rbase[i] = plan->rep_base[i];
+  }
+  if (threadIdx.x == 0) s_rbase[E] = plan->rep_base[E];
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    s_rrow[i] = plan->rep_row_base[i];
+    s_rrem[i] = plan->rep_remote[i] ? 1 : 0;
+  }
+  __syncthreads();
 
   if (warp == 0) {
     const int t = t_base + lane;
@@ -108,8 +115,13 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
       const uint32_t m = __ballot_sync(0xffffffffu, slot >= 0);
       if (m == 0) continue;
       if (slot >= 0) {
-        const int gr = block_pre[(size_t)b * E + e] + __popc(m & lt);
-        const uint32_t code = row_code_for(plan, e, gr);
+        const int gr = s_pre[e] + __popc(m & lt);
+        // integer replica split: replica r owns floor(n/R) + [r < n mod R] ranks
+        const int n = s_n[e], Re = s_rbase[e + 1] - s_rbase[e];
+        const int q = n / Re, rem = n % Re;
+        const int r = gr < rem * (q + 1) ? gr / (q + 1) : rem + (gr - rem * (q + 1)) / q;
+        const int f = s_rbase[e] + r;
+        const uint32_t code = static_cast<uint32_t>(s_rrow[f] + gr) | (s_rrem[f] ? kRemoteBit : 0u);
         codes[lane * K + slot] = code;
         if (blockIdx.y == 0) row_code[(size_t)t * K + slot] = code;
       }

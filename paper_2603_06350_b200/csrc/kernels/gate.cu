@@ -15,16 +15,20 @@
 //
 // Work decomposition: one CTA (8 warps) owns a block of 32 consecutive tokens
 // — the granularity of block_counts[], the stable prefix the dispatch kernel
-// scans.  Warp w takes m-tile (w & 1) (16 tokens) and K-slice (w >> 1) (a
-// quarter of d), so a block keeps 8 independent 16-byte-load streams in
-// flight.  Fragments are loaded straight from global memory: the 16 k-slots
-// of one MMA are mapped to features so that lane (g, c) needs 4 CONSECUTIVE
-// features of row g / row g+8 / expert g (slots 2c,2c+1 <-> f, f+1 and
-// 2c+8,2c+9 <-> f+2, f+3, identical for A and B), i.e. one 16-byte load per
-// row feeds two MMAs.  K-slices are summed into shared memory in a fixed
-// order (deterministic), then one warp per 4 tokens does the arg-max top-k,
-// the softmax and the shared-memory histogram, flushed with one global
-// atomicAdd per (block, expert) — the atomics-based per-expert histogram.
+// scans.  Warp w takes m-tile (w & 1) (16 tokens) and K-slice (w >> 1), so a
+// block keeps 8 independent 16-byte-load streams in flight.  Fragments are
+// loaded straight from global memory: the 16 k-slots of one MMA are mapped to
+// features so that lane (g, c) needs 4 CONSECUTIVE features of row g / row
+// g+8 / expert g (slots 2c,2c+1 <-> f, f+1 and 2c+8,2c+9 <-> f+2, f+3,
+// identical for A and B), i.e. one 16-byte load per row feeds two MMAs.
+// K-slices are summed into shared memory in a fixed order (deterministic),
+// then one warp per 4 tokens does the arg-max top-k, the softmax and the
+// shared-memory histogram, flushed with one global atomicAdd per (block,
+// expert) — the atomics-based per-expert histogram.
+//
+// Small batches (decode: 256 tokens = 8 blocks) split K over gridDim.y CTAs
+// per block as well; each CTA publishes its partial logits and
+// gate_finish_kernel sums the slices in order before the same top-k.
 //
 // Exactness: on the synthetic grid every partial sum is a
 // multiple of 2^-16 below 2^6, so any fp32 summation order — the MMA's
@@ -40,7 +44,7 @@ namespace {
 
 constexpr int kBlockTokens = 32;  // tokens per CTA == per block_counts row
 constexpr int kWarps = 8;
-constexpr int kSlices = 4;        // K-slices per m-tile
+constexpr int kSlices = 4;        // K-slices per m-tile inside a CTA
 constexpr int kPerLane = 8;       // stacked logits per lane in the top-k (<= 256)
 
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
@@ -87,74 +91,19 @@ __device__ __forceinline__ void warp_topk(const float* row, int base, int E, int
   }
 }
 
-}  // namespace
-
-// x [T, d] bf16; w_all [(1 + n_pred) * E, d] bf16 (rows 0..E-1 = gate).
-// Outputs: ids [T, k] i32, weights [T, k] f32, counts [E] i32 (atomic; caller
-// zeroes), block_counts [ceil(T/32), E] i32, pred_counts [n_pred, E] (atomic).
-// NT = n-tiles of 8 stacked logits (E * (1 + n_pred) <= 8 * NT).
-template <int NT>
-__global__ void __launch_bounds__(kWarps * 32)
-gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_bfloat16* __restrict__ w_all, int E,
-                 int n_pred, int k, int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
-                 int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts) {
-  constexpr int kCols = 8 * NT;
-  constexpr int kLd = kCols + 4;  // padded row of the reduction buffer
-  __shared__ float red[kBlockTokens * kLd];
-  __shared__ int hist[256];
+// top-k, softmax and histograms for one 32-token block whose stacked logits
+// sit in shared memory (row stride LD); warp w handles tokens 4w .. 4w+3.
+template <int LD>
+__device__ __forceinline__ void select_and_count(const float* red, int* hist, int blk, int T, int E, int n_pred,
+                                                 int k, int32_t* __restrict__ ids, float* __restrict__ wts,
+                                                 int32_t* __restrict__ counts, int32_t* __restrict__ block_counts,
+                                                 int32_t* __restrict__ pred_counts) {
   const int warp = threadIdx.x >> 5, lane = lane_id();
-  const int g = lane >> 2, c = lane & 3;
-  const int mt = warp & 1, ks = warp >> 1;
-  const int blk = blockIdx.x;
-  const int Etot = E * (1 + n_pred);
-  for (int i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
-
-  // ---- skinny GEMM: 16 tokens x 8*NT logits over this warp's K-slice
-  const int r0 = blk * kBlockTokens + mt * 16 + g, r1 = r0 + 8;
-  const bool v0 = r0 < T, v1 = r1 < T;
-  const __nv_bfloat16* x0 = x + (size_t)(v0 ? r0 : 0) * d;
-  const __nv_bfloat16* x1 = x + (size_t)(v1 ? r1 : 0) * d;
-  const int slice = d / kSlices;  // d % 256 == 0 -> slice % 64 == 0
-  const int k_begin = ks * slice, k_end = k_begin + slice;
-  float acc[NT][4];
-#pragma unroll
-  for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
-  const int4 zero = make_int4(0, 0, 0, 0);
-#pragma unroll 2
-  for (int kb = k_begin; kb < k_end; kb += 32) {
-    const int f = kb + 8 * c;  // this lane's 8 consecutive features of the 32-feature block
-    const int4 a_lo = v0 ? ld_nc_v4(x0 + f) : zero;
-    const int4 a_hi = v1 ? ld_nc_v4(x1 + f) : zero;
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      const int e = n * 8 + g;
-      const int4 b = e < Etot ? __ldg(reinterpret_cast<const int4*>(w_all + (size_t)e * d + f)) : zero;
-      mma_bf16_16816(acc[n], a_lo.x, a_hi.x, a_lo.y, a_hi.y, b.x, b.y);  // features f .. f+3
-      mma_bf16_16816(acc[n], a_lo.z, a_hi.z, a_lo.w, a_hi.w, b.z, b.w);  // features f+4 .. f+7
-    }
-  }
-  // ---- ordered K-slice reduction into shared memory (deterministic)
-  for (int s = 0; s < kSlices; ++s) {
-    if (ks == s) {
-#pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        float* p0 = red + (mt * 16 + g) * kLd + n * 8 + 2 * c;
-        float* p1 = p0 + 8 * kLd;
-        if (s == 0) {
-          p0[0] = acc[n][0]; p0[1] = acc[n][1]; p1[0] = acc[n][2]; p1[1] = acc[n][3];
-        } else {
-          p0[0] += acc[n][0]; p0[1] += acc[n][1]; p1[0] += acc[n][2]; p1[1] += acc[n][3];
-        }
-      }
-    }
-    __syncthreads();
-  }
-  // ---- top-k, softmax, histograms: warp w handles tokens 4w .. 4w+3
   for (int q = 0; q < kBlockTokens / kWarps; ++q) {
     const int lt = warp * (kBlockTokens / kWarps) + q;
     const int t = blk * kBlockTokens + lt;
     if (t >= T) break;
-    const float* row = red + lt * kLd;
+    const float* row = red + lt * LD;
     for (int gi = 0; gi <= n_pred; ++gi) {
       int sel[8];
       float lg[8];
@@ -188,20 +137,135 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_b
   }
 }
 
+}  // namespace
+
+// x [T, d] bf16; w_all [(1 + n_pred) * E, d] bf16 (rows 0..E-1 = gate).
+// Outputs: ids [T, k] i32, weights [T, k] f32, counts [E] i32 (atomic; caller
+// zeroes), block_counts [ceil(T/32), E] i32, pred_counts [n_pred, E] (atomic).
+// NT = n-tiles of 8 stacked logits (E * (1 + n_pred) <= 8 * NT).  With
+// gridDim.y > 1 the CTA covers a 1/gridDim.y share of d and writes its
+// partial logits to `partial` instead of selecting.
+template <int NT>
+__global__ void __launch_bounds__(kWarps * 32)
+gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_bfloat16* __restrict__ w_all, int E,
+                 int n_pred, int k, int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
+                 int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts, float* __restrict__ partial) {
+  constexpr int kCols = 8 * NT;
+  constexpr int kLd = kCols + 4;  // padded row of the reduction buffer
+  __shared__ float red[kBlockTokens * kLd];
+  __shared__ int hist[256];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int g = lane >> 2, c = lane & 3;
+  const int mt = warp & 1, ks = warp >> 1;
+  const int blk = blockIdx.x;
+  const int Etot = E * (1 + n_pred);
+  for (int i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
+
+  // ---- skinny GEMM: 16 tokens x 8*NT logits over this warp's K-slice
+  const int r0 = blk * kBlockTokens + mt * 16 + g, r1 = r0 + 8;
+  const bool v0 = r0 < T, v1 = r1 < T;
+  const __nv_bfloat16* x0 = x + (size_t)(v0 ? r0 : 0) * d;
+  const __nv_bfloat16* x1 = x + (size_t)(v1 ? r1 : 0) * d;
+  const int slice = d / (kSlices * gridDim.y);  // multiple of 32 (checked by the launcher)
+  const int k_begin = (blockIdx.y * kSlices + ks) * slice, k_end = k_begin + slice;
+  float acc[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
+  const int4 zero = make_int4(0, 0, 0, 0);
+#pragma unroll 2
+  for (int kb = k_begin; kb < k_end; kb += 32) {
+    const int f = kb + 8 * c;  // this lane's 8 consecutive features of the 32-feature block
+    const int4 a_lo = v0 ? ld_nc_v4(x0 + f) : zero;
+    const int4 a_hi = v1 ? ld_nc_v4(x1 + f) : zero;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int e = n * 8 + g;
+      const int4 b = e < Etot ? __ldg(reinterpret_cast<const int4*>(w_all + (size_t)e * d + f)) : zero;
+      mma_bf16_16816(acc[n], a_lo.x, a_hi.x, a_lo.y, a_hi.y, b.x, b.y);  // features f .. f+3
+      mma_bf16_16816(acc[n], a_lo.z, a_hi.z, a_lo.w, a_hi.w, b.z, b.w);  // features f+4 .. f+7
+    }
+  }
+  // ---- ordered K-slice reduction into shared memory (deterministic)
+  for (int s = 0; s < kSlices; ++s) {
+    if (ks == s) {
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        float* p0 = red + (mt * 16 + g) * kLd + n * 8 + 2 * c;
+        float* p1 = p0 + 8 * kLd;
+        if (s == 0) {
+          p0[0] = acc[n][0]; p0[1] = acc[n][1]; p1[0] = acc[n][2]; p1[1] = acc[n][3];
+        } else {
+          p0[0] += acc[n][0]; p0[1] += acc[n][1]; p1[0] += acc[n][2]; p1[1] += acc[n][3];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (gridDim.y > 1) {
+    float* dst = partial + ((size_t)blockIdx.y * gridDim.x + blk) * kBlockTokens * kCols;
+    for (int i = threadIdx.x; i < kBlockTokens * kCols; i += blockDim.x) dst[i] = red[(i / kCols) * kLd + i % kCols];
+    return;
+  }
+  select_and_count<kLd>(red, hist, blk, T, E, n_pred, k, ids, wts, counts, block_counts, pred_counts);
+}
+
+// Sums the split-K partial logits of one 32-token block in slice order
+// (deterministic), then top-k / softmax / histograms as in the fused kernel.
+template <int NT>
+__global__ void __launch_bounds__(kWarps * 32)
+gate_finish_kernel(const float* __restrict__ partial, int splits, int T, int E, int n_pred, int k,
+                   int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
+                   int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts) {
+  constexpr int kCols = 8 * NT;
+  constexpr int kLd = kCols + 4;
+  __shared__ float red[kBlockTokens * kLd];
+  __shared__ int hist[256];
+  const int blk = blockIdx.x;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
+  for (int i = threadIdx.x; i < kBlockTokens * kCols; i += blockDim.x) {
+    float v = 0.0f;
+    for (int s = 0; s < splits; ++s) v += partial[((size_t)s * gridDim.x + blk) * kBlockTokens * kCols + i];
+    red[(i / kCols) * kLd + i % kCols] = v;
+  }
+  __syncthreads();
+  select_and_count<kLd>(red, hist, blk, T, E, n_pred, k, ids, wts, counts, block_counts, pred_counts);
+}
+
 int gate_num_blocks(int T) { return (T + kBlockTokens - 1) / kBlockTokens; }
+
+// K-splits for a batch: enough CTAs to cover the SMs twice, d/(4 S) a
+// multiple of 32, at most 16.
+int gate_splits(int T, int d) {
+  const int nblk = gate_num_blocks(T);
+  int s = 1;
+  while (s < 16 && nblk * s * 2 <= 2 * 148 && d % (kSlices * 32 * s * 2) == 0) s *= 2;
+  return s;
+}
+
+// floats of split-K scratch a launch with these sizes needs
+size_t gate_partial_floats(int T, int d, int Etot) {
+  const int s = gate_splits(T, d);
+  int nt = 1;
+  while (8 * nt < Etot) nt *= 2;
+  return s > 1 ? static_cast<size_t>(s) * gate_num_blocks(T) * kBlockTokens * 8 * nt : 0;
+}
 
 cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bfloat16* w_all, int E,
                              int n_pred, int k, int32_t* ids, float* wts, int32_t* counts,
-                             int32_t* block_counts, int32_t* pred_counts, cudaStream_t stream) {
+                             int32_t* block_counts, int32_t* pred_counts, float* partial, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
   const int Etot = E * (1 + n_pred);
   if (Etot > 32 * kPerLane || k > 8 || (d % 256) != 0) return cudaErrorInvalidValue;
   const int nblk = gate_num_blocks(T);
-  const dim3 grid(nblk), block(kWarps * 32);
+  const int splits = partial ? gate_splits(T, d) : 1;
+  const dim3 grid(nblk, splits), block(kWarps * 32);
 #define MOE_GATE_CASE(NT_)                                                                                  \
   if (Etot <= 8 * NT_) {                                                                                    \
     gate_topk_kernel<NT_><<<grid, block, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,       \
-                                                      block_counts, pred_counts);                          \
+                                                      block_counts, pred_counts, partial);                 \
+    if (splits > 1)                                                                                         \
+      gate_finish_kernel<NT_><<<nblk, block, 0, stream>>>(partial, splits, T, E, n_pred, k, ids, wts,       \
+                                                          counts, block_counts, pred_counts);               \
     return cudaGetLastError();                                                                              \
   }
   MOE_GATE_CASE(1)
