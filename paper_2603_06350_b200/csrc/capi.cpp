@@ -59,6 +59,9 @@ cudaError_t launch_combine_f32(const float* y_local, const float* y_return, int 
 cudaError_t launch_combine(const __nv_bfloat16* y_local, const __nv_bfloat16* y_return, int T, int d, int k,
                            const uint32_t* row_code, const float* wts, __nv_bfloat16* y, int num_sms,
                            cudaStream_t s);
+cudaError_t launch_grouped_gemm_m256(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
+                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
+                                     __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream);
 cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                     __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream);
@@ -287,7 +290,8 @@ struct moe_ctx {
   int64_t next_ticket = 0;
   DevBuf<DevPlan> dplan;
   int64_t rows_cap = 0, send_cap = 0;
-  CUtensorMap tmA1, tmA2;
+  CUtensorMap tmA1, tmA2;    // 128-row boxes
+  CUtensorMap tmA1w, tmA2w;  // 256-row boxes (256-row single-CTA K4 variant)
   // host staging (pinned)
   DevPlan* hplan = nullptr;
   int32_t* h_counts = nullptr;  // [G][E]
@@ -474,13 +478,15 @@ void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t r
     }
     return;
   }
-  const bool two_sm = c->gemm_variant == 2;
-  auto fn = two_sm ? launch_grouped_gemm_2sm : launch_grouped_gemm;
+  const bool two_sm = c->gemm_variant == 2, m256 = c->gemm_variant == 3;
+  auto fn = two_sm ? launch_grouped_gemm_2sm : (m256 ? launch_grouped_gemm_m256 : launch_grouped_gemm);
+  const CUtensorMap* a1 = m256 ? &c->tmA1w : &c->tmA1;
+  const CUtensorMap* a2 = m256 ? &c->tmA2w : &c->tmA2;
   if (which == 0)
-    CU_CHECK(fn(0, &c->tmA1, two_sm ? &L.tmB1h : &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d, 2 * c->ff,
+    CU_CHECK(fn(0, a1, two_sm ? &L.tmB1h : &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d, 2 * c->ff,
                 reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, c->num_sms, s));
   else
-    CU_CHECK(fn(1, &c->tmA2, two_sm ? &L.tmB2h : &L.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
+    CU_CHECK(fn(1, a2, two_sm ? &L.tmB2h : &L.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
                 reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s));
 }
 
@@ -673,7 +679,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->num_sms = prop.multiProcessorCount;
     if (const char* v = std::getenv("MOE_GEMM_VARIANT")) {
       const std::string s(v);
-      c->gemm_variant = s == "1sm" ? 1 : (s == "2sm" ? 2 : 0);
+      c->gemm_variant = s == "1sm" ? 1 : (s == "2sm" ? 2 : (s == "m256" ? 3 : 0));
     }
     c->registry = moeless::ReplicaRegistry(std::max(0, D.keep_alive_iters));
     c->layers.resize(D.num_layers);
@@ -713,6 +719,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     } else {
       c->tmA1 = make_kmajor_map(c->xp.p, c->rows_cap, c->d, 128);
       c->tmA2 = make_kmajor_map(c->h.p, c->rows_cap, c->ff, 128);
+      c->tmA1w = make_kmajor_map(c->xp.p, c->rows_cap, c->d, 256);
+      c->tmA2w = make_kmajor_map(c->h.p, c->rows_cap, c->ff, 256);
     }
     // mapped pinned control buffers, read/written by small SM copies (UVA pointers)
     CU_CHECK(cudaHostAlloc(&c->hplan, sizeof(DevPlan), cudaHostAllocMapped));

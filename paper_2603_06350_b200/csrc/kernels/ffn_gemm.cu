@@ -451,6 +451,173 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
   }
 }
 
+// ===================================================================
+// Single-CTA 256-row variant: per k-block the CTA stages a 256x64 A tile and
+// a 256x64 B tile (64 KB, 3 stages) and issues two M=128 MMAs (top and
+// bottom row halves) that share the B operand, accumulating into the two
+// halves of TMEM (2 x 256 columns, single-buffered).  Per FLOP it moves 1/3
+// less data from L2 than the 128-row kernel and keeps more bytes in flight
+// per MMA cycle, with no cross-SM operand traffic; the price is that the
+// epilogue of tile i is not overlapped with the MMAs of tile i+1.
+constexpr int BM4 = 256, STAGES4 = 3;
+constexpr uint32_t kStageA4 = BM4 * BK * 2, kStageB4 = BN * BK * 2, kStage4 = kStageA4 + kStageB4;
+
+struct SmemLayout4 {
+  static constexpr uint32_t a = 0;
+  static constexpr uint32_t b = a + STAGES4 * kStageA4;
+  static constexpr uint32_t bars = b + STAGES4 * kStageB4;
+  static constexpr uint32_t n_bars = 2 * STAGES4 + 2;
+  static constexpr uint32_t tmem_slot = bars + n_bars * 8;
+  static constexpr uint32_t seg_tiles = tmem_slot + 16;
+  static constexpr uint32_t segs = seg_tiles + (kMaxSegs + 1) * 4 + 12;
+  static constexpr uint32_t end = ((segs + 15) / 16) * 16 + kMaxSegs * 16;
+};
+constexpr uint32_t kSmemBytes4 = SmemLayout4::end + 1024;
+static_assert(kSmemBytes4 <= 232448, "smem budget (256-row variant)");
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+grouped_gemm_m256_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total, int k_total,
+                         int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout4::bars);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES4;
+  uint64_t* tfull = bars + 2 * STAGES4;
+  uint64_t* tempty = bars + 2 * STAGES4 + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SmemLayout4::tmem_slot);
+  int* seg_tiles = reinterpret_cast<int*>(smem + SmemLayout4::seg_tiles);
+  int4* segs = reinterpret_cast<int4*>(smem + SmemLayout4::segs);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  const int nseg = min(*nseg_g, kMaxSegs);
+  const int n_tiles = n_total / BN;
+
+  for (int i = threadIdx.x; i < nseg; i += kThreads) segs[i] = reinterpret_cast<const int4*>(segs_g)[i];
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES4; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int s = 0; s < nseg; ++s) {
+      seg_tiles[s] = acc;
+      acc += ((segs[s].y + BM4 - 1) / BM4) * n_tiles;
+    }
+    seg_tiles[nseg] = acc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_tiles = nseg > 0 ? seg_tiles[nseg] : 0;
+  const int num_kb = k_total / BK;
+  constexpr int GM4 = EPI == EPI_SWIGLU ? 16 : 8;  // 256-row tiles per n sweep
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint64_t pol_b = policy_evict_last();
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const TileCoord c = decode_tile<GM4, BM4>(t, seg_tiles, segs, nseg, n_tiles);
+        const int a_row = segs[c.seg].x + c.m * BM4;
+        const int b_row = segs[c.seg].z * b_rows_per_slot + c.n * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], kStage4);
+          tma_load_2d(smem + SmemLayout4::a + stage * kStageA4, &tmA, &full[stage], kb * BK, a_row);
+          tma_load_2d_hint(smem + SmemLayout4::b + stage * kStageB4, &tmB, &full[stage], kb * BK, b_row, pol_b);
+          if (++stage == STAGES4) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      const uint32_t a_base = smem_u32(smem + SmemLayout4::a);
+      const uint32_t b_base = smem_u32(smem + SmemLayout4::b);
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        mbar_wait(tempty, acc_phase ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_st = a_base + stage * kStageA4;
+          const uint64_t a_top = umma_desc_sw128(a_st);
+          const uint64_t a_bot = umma_desc_sw128(a_st + BM * 128);  // rows 128..255: +16 KB
+          const uint64_t bdesc = umma_desc_sw128(b_base + stage * kStageB4);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint32_t acc = (kb | k) != 0 ? 1u : 0u;
+            tc_mma_bf16(tmem_base, a_top + 2 * k, bdesc + 2 * k, idesc, acc);
+            tc_mma_bf16(tmem_base + BN, a_bot + 2 * k, bdesc + 2 * k, idesc, acc);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES4) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(tfull);
+        acc_phase ^= 1;
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const TileCoord c = decode_tile<GM4, BM4>(t, seg_tiles, segs, nseg, n_tiles);
+      const int4 sg = segs[c.seg];
+      mbar_wait(tfull, acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        const int row = c.m * BM4 + half * BM + quarter * 32 + lane;
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + half * BN;
+        store_accumulator<EPI>(taddr, out, static_cast<size_t>(sg.x + row), row < sg.y, c.n, out_ld);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+      acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+cudaError_t launch_grouped_gemm_m256(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
+                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
+                                     __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream) {
+  if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(grouped_gemm_m256_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes4);
+    cudaFuncSetAttribute(grouped_gemm_m256_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes4);
+    configured = true;
+  }
+  if (epi == EPI_SWIGLU)
+    grouped_gemm_m256_kernel<EPI_SWIGLU><<<num_ctas, kThreads, kSmemBytes4, stream>>>(
+        *tmA, *tmB, segs, nseg, n_total, k_total, b_rows_per_slot, out, out_ld);
+  else
+    grouped_gemm_m256_kernel<EPI_STORE><<<num_ctas, kThreads, kSmemBytes4, stream>>>(
+        *tmA, *tmB, segs, nseg, n_total, k_total, b_rows_per_slot, out, out_ld);
+  return cudaGetLastError();
+}
+
 // --------------------------------------------------------------- host side
 static_assert(kSmemBytes <= 232448, "smem budget");
 

@@ -1,5 +1,5 @@
-"""Both K4 kernels — 1-SM (M=128 tiles) and 2-SM cta_group::2 (M=256 tiles
-across an SM pair) — against the oracle and against each other, on ragged
+"""The K4 kernels — 1-SM (M=128 tiles), 2-SM cta_group::2 (M=256 tiles across
+an SM pair) and single-CTA M=256 (two MMAs sharing B) — against the oracle and against each other, on ragged
 segments (partial tiles, single-row segments, replicas co-located)."""
 import os
 
@@ -44,9 +44,10 @@ def _run(cuda, variant, E, k, d, ff, T, rc, seed=21):
 def test_variants_agree_and_match_oracle(cuda, E, k, d, ff, T, rc):
     x, wg, experts, y1 = _run(cuda, "1sm", E, k, d, ff, T, rc)
     _, _, _, y2 = _run(cuda, "2sm", E, k, d, ff, T, rc)
+    _, _, _, y3 = _run(cuda, "m256", E, k, d, ff, T, rc)
     y_ref = oracle.layer_forward(x, wg, experts, rc, k)[0]
-    for y in (y1, y2):
+    for y in (y1, y2, y3):
         err = float(np.max(np.abs(y - y_ref)) / np.max(np.abs(y_ref)))
         assert err <= 2e-2, err
-    # same tiles along K, same fp32 accumulation order: bit-identical outputs
-    assert np.array_equal(y1, y2)
+    # same K order per output element, same fp32 accumulation: bit-identical outputs
+    assert np.array_equal(y1, y2) and np.array_equal(y1, y3)
