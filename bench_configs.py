@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 
-def run_config(name, steps, warmup):
+def run_config(name, steps, warmup, graphs=False):
     import numpy as np
     import torch
 
@@ -28,7 +28,8 @@ def run_config(name, steps, warmup):
     c = dict(wl.CONFIGS[name])
     E, k, d, ff, T, s = c["E"], c["k"], c["d"], c["ff"], c["T"], c["s"]
     mem = 3.0 * d * ff * 2 / 1e6
-    m = MoELayer(1, E, k, d, ff, max_tokens=T, expert_mem_mb=mem, layer_mem_cap_mb=c["extra_replicas"] * mem)
+    m = MoELayer(1, E, k, d, ff, max_tokens=T, expert_mem_mb=mem, layer_mem_cap_mb=c["extra_replicas"] * mem,
+                 cuda_graphs=graphs)
     for e in range(E):
         m.load_expert(0, e, *wl.expert_weights(d, ff, 1, 0, e))
     pool = [torch.from_numpy(wl.tokens(T, d, E, 1, i).view(np.int16)).cuda() for i in range(4)]
@@ -69,7 +70,7 @@ def run_config(name, steps, warmup):
         "p50_ms": percentile(lat, 0.5), "p99_ms": percentile(lat, 0.99), "phase_ms_median": phases,
         "k4_tflops": flops / (gemm * 1e-3) / 1e12, "k4_weight_gbs": wbytes / (gemm * 1e-3) / 1e9,
         "active_experts": active, "replicas_median": statistics.median(x.replica_count for x in st),
-        "gpus": 1, "note": "per-GPU shape at G=1" if c["G"] > 1 else "",
+        "gpus": 1, "note": "per-GPU shape at G=1" if c["G"] > 1 else "", "cuda_graphs": graphs,
     }
 
 
@@ -132,8 +133,9 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--out", default="")
+    ap.add_argument("--graphs", action="store_true", help="replay single-GPU forwards as CUDA graphs")
     a = ap.parse_args()
-    res = [run_stack(n, max(2, a.steps // 10), 1) if n == "cfg4" else run_config(n, a.steps, a.warmup)
+    res = [run_stack(n, max(2, a.steps // 10), 1) if n == "cfg4" else run_config(n, a.steps, a.warmup, a.graphs)
            for n in a.configs.split(",")]
     for r in res:
         print(json.dumps(r), flush=True)

@@ -98,7 +98,9 @@ typedef struct {
   int keep_alive_iters;
   int predictor_distance;     /* d: predictor slot 0 of layer l scores layer l + d (default 1) */
   int precision;              /* MOE_PRECISION_BF16 (default) or MOE_PRECISION_FP32 */
-  int reserved[5];
+  int use_cuda_graphs;        /* 1: single-GPU forwards are captured once per (layer, tokens,
+                                 buffers) and replayed as one CUDA graph launch */
+  int reserved[4];
 } moe_ctx_desc;
 
 /* precision of activations, weights and outputs.  BF16: bf16 in/out, fp32

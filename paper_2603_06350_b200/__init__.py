@@ -286,7 +286,7 @@ class MoELayer:
                  num_predictor_targets: int = 0, expert_mem_mb: float = 0.0,
                  layer_mem_cap_mb: float = 0.0, gpu_mem_capacity_mb: float = 180000.0,
                  cv_threshold: float = 0.2, keep_alive_iters: int = 50, predictor_distance: int = 1,
-                 precision: int = 0):
+                 precision: int = 0, cuda_graphs: bool = False):
         d = MoeCtxDesc()
         d.num_layers, d.num_experts, d.top_k = num_layers, num_experts, top_k
         d.d_model, d.d_ff, d.max_tokens = d_model, d_ff, max_tokens
@@ -299,6 +299,7 @@ class MoELayer:
         d.cv_threshold, d.keep_alive_iters = cv_threshold, keep_alive_iters
         d.predictor_distance = predictor_distance
         d.precision = precision
+        d.use_cuda_graphs = int(cuda_graphs)
         self.fp32 = precision == 1
         h = C.c_void_p()
         check(lib.moe_ctx_create(C.byref(d), C.byref(h)))

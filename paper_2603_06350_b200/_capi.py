@@ -37,7 +37,7 @@ class MoeCtxDesc(C.Structure):
         ("num_predictor_targets", C.c_int),
         ("expert_mem_mb", dbl), ("layer_mem_cap_mb", dbl), ("gpu_mem_capacity_mb", dbl),
         ("cv_threshold", dbl), ("keep_alive_iters", C.c_int), ("predictor_distance", C.c_int),
-        ("precision", C.c_int), ("reserved", C.c_int * 5),
+        ("precision", C.c_int), ("use_cuda_graphs", C.c_int), ("reserved", C.c_int * 4),
     ]
 
 

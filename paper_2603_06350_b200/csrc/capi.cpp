@@ -24,7 +24,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <tuple>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -230,6 +232,16 @@ struct Layer {
   std::vector<moeless::LoadVector> history;
 };
 
+struct GraphKey {
+  int layer, T;
+  const void* x;
+  const void* y;
+  cudaEvent_t x_consumed;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(layer, T, x, y, x_consumed) < std::tie(o.layer, o.T, o.x, o.y, o.x_consumed);
+  }
+};
+
 struct PendingPlan {
   bool active = false;
   int layer = 0, mode = 0;
@@ -268,6 +280,8 @@ struct moe_ctx {
   int xw = 0;             // one activation row in 16-bit units (d_model * elem)
   DevBuf<float> gu_f32;   // fp32 GEMM1 output [rows_cap][2 ff]
   DevBuf<float> gate_partial;  // split-K gate scratch (small batches)
+  bool use_graphs = false;     // replay single-GPU forwards as CUDA graphs
+  std::map<GraphKey, cudaGraphExec_t> graphs;
   // K4 timing ring: events around GEMM1 / GEMM2 of every forward (no sync)
   static constexpr int kGemmRing = 64;
   cudaEvent_t gemm_ev[kGemmRing][3] = {};
@@ -536,6 +550,26 @@ void ensure_pools(moe_ctx* c, Layer& L) {
   L.expert_loaded.assign(c->E, 0);
 }
 
+// The single-GPU device sequence of one forward (no host synchronisation):
+// gate (+predictor) -> histogram to mapped host memory -> on-device plan ->
+// dispatch -> GEMM1 -> GEMM2 -> combine.  Used for CUDA-graph capture.
+void enqueue_local_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, uint16_t* y, cudaStream_t s,
+                           bool with_pred, int stride, cudaEvent_t x_consumed) {
+  // events recorded inside a capture must be external record nodes, so each
+  // replay signals them for the host (flush_pending_plan, x reuse)
+  const unsigned rec = cudaEventRecordExternal;
+  stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr);
+  CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * stride), s));
+  CU_CHECK(cudaEventRecordWithFlags(c->ev_counts, s, rec));
+  CU_CHECK(launch_plan_local(c->counts.p, c->E, c->dplan.p, s));
+  stage_dispatch(c, x, T, s, /*upload_plan=*/false);
+  if (x_consumed) CU_CHECK(cudaEventRecordWithFlags(x_consumed, s, rec));
+  const int64_t rows = static_cast<int64_t>(T) * c->k;
+  launch_ffn_gemm(c, layer, 0, s, rows);
+  launch_ffn_gemm(c, layer, 1, s, rows);
+  stage_combine(c, y, T, s);
+}
+
 void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y, int plan_mode, long iteration,
                     moe_layer_stats* st, cudaStream_t s, cudaEvent_t x_consumed = nullptr) {
   Layer& L = layer_at(c, layer);
@@ -554,6 +588,27 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   // histograms follow the gate's in the same counts buffer
   const bool with_pred = c->n_pred > 0 && L.has_pred_weights;
   const int stride = with_pred ? c->count_stride : c->E;
+  if (c->use_graphs && c->G == 1 && !timed) {
+    // Replay the layer's whole device sequence (8-10 kernels) as one CUDA
+    // graph: captured once per (layer, tokens, buffers), then launched with a
+    // single call — the launch-bound decode regime pays one launch, not ten.
+    const GraphKey key{layer, T, x, y, x_consumed};
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+      CU_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      enqueue_local_forward(c, L, layer, x, T, y, s, with_pred, stride, x_consumed);
+      cudaGraph_t g = nullptr;
+      CU_CHECK(cudaStreamEndCapture(s, &g));
+      cudaGraphExec_t ex = nullptr;
+      const cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+      cudaGraphDestroy(g);
+      CU_CHECK(e);
+      it = c->graphs.emplace(key, ex).first;
+    }
+    CU_CHECK(cudaGraphLaunch(it->second, s));
+    c->pending = PendingPlan{true, layer, plan_mode, iteration, stride};
+    return;
+  }
   mark(0);
   stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr);
   if (c->G > 1) {
@@ -676,6 +731,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->Tmax = D.max_tokens;
     c->n_pred = std::max(0, D.num_predictor_targets);
     c->pred_distance = D.predictor_distance > 0 ? D.predictor_distance : 1;
+    c->use_graphs = D.use_cuda_graphs != 0;
+    if (const char* v = std::getenv("MOE_CUDA_GRAPHS")) c->use_graphs = std::string(v) == "1";
     c->num_sms = prop.multiProcessorCount;
     if (const char* v = std::getenv("MOE_GEMM_VARIANT")) {
       const std::string s(v);
@@ -752,6 +809,7 @@ int moe_ctx_destroy(moe_ctx* c) {
     if (c->wg_stage) cudaFreeHost(c->wg_stage);
     if (c->ev_wg_staged) cudaEventDestroy(c->ev_wg_staged);
     if (c->ev_counts) cudaEventDestroy(c->ev_counts);
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     for (auto& tri : c->gemm_ev)
       for (cudaEvent_t e : tri)
         if (e) cudaEventDestroy(e);
