@@ -61,8 +61,14 @@ enum {
   MOE_ESTATE = 5
 };
 
-/* exchange modes for world_size > 1 */
-enum { MOE_EXCHANGE_NCCL = 0, MOE_EXCHANGE_EXTERNAL = 1 };
+/* exchange modes for world_size > 1.
+   NCCL:     counts all-gather + grouped ncclSend/ncclRecv of row chunks.
+   EXTERNAL: the staged API; the caller moves the chunks.
+   P2P:      peer memory over NVLink (or ranks sharing one device): dispatch
+             stores rows straight into the owning rank's receive buffer and
+             combine reads expert outputs from the owner; flags in device
+             memory order the phases.  Requires moe_p2p_export/import. */
+enum { MOE_EXCHANGE_NCCL = 0, MOE_EXCHANGE_EXTERNAL = 1, MOE_EXCHANGE_P2P = 2 };
 
 /* planning modes for moe_layer_forward */
 enum {
@@ -135,6 +141,24 @@ const char* moe_version(void);
    the launcher broadcasts it). */
 int moe_nccl_unique_id(void* out128);
 int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out);
+
+/* Peer-memory exchange (MOE_EXCHANGE_P2P).  Each rank exports a handle to its
+   exchange slab, the launcher all-gathers the handles (any transport: MPI,
+   torch.distributed, a file), and every rank imports all G of them, indexed by
+   rank.  Handles from the same process are used as plain device pointers
+   (several ranks may share one device); others are opened with CUDA IPC.
+   Every rank must then issue the same sequence of moe_layer_forward calls. */
+typedef struct {
+  unsigned char ipc[64]; /* cudaIpcMemHandle_t of the slab */
+  uint64_t pid;          /* exporting process */
+  uint64_t base;         /* slab address in the exporting process */
+  uint64_t bytes;        /* slab size */
+  uint64_t off_flags, off_counts, off_xp, off_yp;
+  int32_t device, rank, world_size, version;
+  unsigned char reserved[56];
+} moe_p2p_handle;        /* 192 bytes */
+int moe_p2p_export(moe_ctx* ctx, moe_p2p_handle* out);
+int moe_p2p_import(moe_ctx* ctx, const moe_p2p_handle* handles, int n);
 int moe_ctx_destroy(moe_ctx* ctx);
 int moe_ctx_stream(moe_ctx* ctx, void** stream_out);
 int moe_ctx_sync(moe_ctx* ctx);

@@ -23,8 +23,8 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _capi
-from ._capi import (MOE_EXCHANGE_EXTERNAL, MOE_EXCHANGE_NCCL, MOE_PLAN_FIXED, MOE_PLAN_PREDICTED, MOE_PLAN_SYNC,
-                    MoeChunk, MoeCtxDesc, MoeError, MoeLayerStats, check, lib)
+from ._capi import (MOE_EXCHANGE_EXTERNAL, MOE_EXCHANGE_NCCL, MOE_EXCHANGE_P2P, MOE_PLAN_FIXED, MOE_PLAN_PREDICTED,
+                    MOE_PLAN_SYNC, MoeChunk, MoeCtxDesc, MoeError, MoeLayerStats, MoeP2PHandle, check, lib)
 
 __all__ = [
     "scale_experts", "place_experts", "ReplicaRegistry", "update_registry", "layer_forward_time",
@@ -32,7 +32,7 @@ __all__ = [
     "MoELayer", "ScalingPlan", "PlaceResult", "synth_tokens", "synth_gate", "synth_expert",
     "stream_key", "nccl_unique_id", "PinnedArray", "MoeError", "MOE_PLAN_FIXED", "MOE_PLAN_SYNC",
     "MOE_PLAN_PREDICTED", "MOE_EXCHANGE_NCCL",
-    "MOE_EXCHANGE_EXTERNAL", "LIB_PATH",
+    "MOE_EXCHANGE_EXTERNAL", "MOE_EXCHANGE_P2P", "LIB_PATH",
 ]
 LIB_PATH = _capi.LIB_PATH
 
@@ -327,6 +327,21 @@ class MoELayer:
 
     def sync(self) -> None:
         check(lib.moe_ctx_sync(self._h))
+
+    def p2p_export(self) -> bytes:
+        """This rank's peer-memory handle (MOE_EXCHANGE_P2P): 192 opaque bytes
+        to all-gather over any transport."""
+        h = MoeP2PHandle()
+        check(lib.moe_p2p_export(self._h, C.byref(h)))
+        return C.string_at(C.addressof(h), C.sizeof(h))
+
+    def p2p_import(self, handles: Sequence[bytes]) -> None:
+        """Map every rank's slab (handles indexed by rank, this rank's included)."""
+        arr = (MoeP2PHandle * len(handles))()
+        for i, b in enumerate(handles):
+            assert len(b) == C.sizeof(MoeP2PHandle)
+            C.memmove(C.addressof(arr[i]), b, len(b))
+        check(lib.moe_p2p_import(self._h, arr, len(handles)))
 
     def load_expert(self, layer: int, expert: int, w1: np.ndarray, w3: np.ndarray, w2: np.ndarray):
         dt = np.float32 if self.fp32 else np.uint16

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmoe_b200.so")
 
 MOE_OK, MOE_EINVAL, MOE_EINFEASIBLE, MOE_ECUDA, MOE_ENCCL, MOE_ESTATE = range(6)
-MOE_EXCHANGE_NCCL, MOE_EXCHANGE_EXTERNAL = 0, 1
+MOE_EXCHANGE_NCCL, MOE_EXCHANGE_EXTERNAL, MOE_EXCHANGE_P2P = 0, 1, 2
 MOE_PLAN_FIXED, MOE_PLAN_SYNC, MOE_PLAN_PREDICTED = 0, 1, 2
 MOE_PRECISION_BF16, MOE_PRECISION_FP32 = 0, 1
 
@@ -52,6 +52,18 @@ class MoeLayerStats(C.Structure):
     ]
 
 
+class MoeP2PHandle(C.Structure):
+    _fields_ = [
+        ("ipc", C.c_ubyte * 64), ("pid", u64), ("base", u64), ("bytes", u64),
+        ("off_flags", u64), ("off_counts", u64), ("off_xp", u64), ("off_yp", u64),
+        ("device", i32), ("rank", i32), ("world_size", i32), ("version", i32),
+        ("reserved", C.c_ubyte * 56),
+    ]
+
+
+assert C.sizeof(MoeP2PHandle) == 192
+
+
 class MoeChunk(C.Structure):
     _fields_ = [("peer", i32), ("replica", i32), ("row_offset", i64), ("rows", i64)]
 
@@ -70,6 +82,8 @@ _sig("moe_ctx_create", C.c_int, P(MoeCtxDesc), P(vp))
 _sig("moe_ctx_destroy", C.c_int, vp)
 _sig("moe_ctx_stream", C.c_int, vp, P(vp))
 _sig("moe_ctx_sync", C.c_int, vp)
+_sig("moe_p2p_export", C.c_int, vp, P(MoeP2PHandle))
+_sig("moe_p2p_import", C.c_int, vp, P(MoeP2PHandle), C.c_int)
 _sig("moe_load_expert_weights", C.c_int, vp, C.c_int, C.c_int, vp, vp, vp)
 _sig("moe_set_gate_weights", C.c_int, vp, C.c_int, vp)
 _sig("moe_load_expert_weights_f32", C.c_int, vp, C.c_int, C.c_int, vp, vp, vp)
@@ -115,7 +129,7 @@ _sig("moe_synth_expert", C.c_int, u64, C.c_int, C.c_int, vp, vp, vp)
 # Every symbol include/moe_b200.h declares (checked by tests/test_capi_symbols.py).
 EXPORTED = [
     "moe_last_error", "moe_version", "moe_nccl_unique_id", "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_stream",
-    "moe_ctx_sync", "moe_load_expert_weights", "moe_set_gate_weights",
+    "moe_ctx_sync", "moe_p2p_export", "moe_p2p_import", "moe_load_expert_weights", "moe_set_gate_weights",
     "moe_load_expert_weights_f32", "moe_set_gate_weights_f32",
     "moe_set_predictor_weights", "moe_set_placement", "moe_gate_topk", "moe_predict_loads",
     "moe_layer_forward", "moe_layer_forward_host", "moe_layer_forward_host_async", "moe_wait",

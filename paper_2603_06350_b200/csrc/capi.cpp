@@ -28,6 +28,7 @@
 #include <memory>
 #include <tuple>
 #include <stdexcept>
+#include <unistd.h>
 #include <string>
 #include <vector>
 
@@ -45,8 +46,20 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
 cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, const DevPlan* plan,
                                 int32_t* block_pre, cudaStream_t s);
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
-                            const int32_t* block_pre, const DevPlan* plan, __nv_bfloat16* xp_local,
-                            __nv_bfloat16* xp_send, uint32_t* row_code, cudaStream_t s);
+                            const int32_t* block_pre, const DevPlan* plan, const RowTargets& targets,
+                            uint32_t* row_code, cudaStream_t s);
+// K6 over peer memory (p2p.cu)
+constexpr int kMaxRanks = 8;
+enum { kFlagCounts = 0, kFlagRows = 1, kFlagOutputs = 2, kFlagKinds = 4 };
+struct PeerSlabs {
+  uint32_t* flags[kMaxRanks];
+  const int32_t* counts[kMaxRanks];
+};
+cudaError_t launch_p2p_signal(const PeerSlabs& peers, int G, int kind, int src, uint32_t epoch, cudaStream_t s);
+cudaError_t launch_p2p_wait(const uint32_t* my_flags, int G, int kind, uint32_t epoch, uint64_t timeout_ns, int* err,
+                            cudaStream_t s);
+cudaError_t launch_p2p_counts(const PeerSlabs& peers, int G, int rank, int stride, uint32_t epoch,
+                              uint64_t timeout_ns, int* err, int32_t* counts_all, cudaStream_t s);
 cudaError_t launch_small_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
 cudaError_t launch_plan_local(const int32_t* counts, int E, DevPlan* plan, cudaStream_t s);
 // K7 fp32 path
@@ -56,11 +69,10 @@ cudaError_t launch_grouped_sgemm(const float* A, int lda, const float* Bpool, in
                                  const GemmSeg* segs, const int* nseg, int N, int K, float* C, int ldc, int num_sms,
                                  cudaStream_t s);
 cudaError_t launch_swiglu_f32(const float* C, int rows, int ff, float* H, cudaStream_t s);
-cudaError_t launch_combine_f32(const float* y_local, const float* y_return, int T, int d, int k,
-                               const uint32_t* row_code, const float* wts, float* y, cudaStream_t s);
-cudaError_t launch_combine(const __nv_bfloat16* y_local, const __nv_bfloat16* y_return, int T, int d, int k,
-                           const uint32_t* row_code, const float* wts, __nv_bfloat16* y, int num_sms,
-                           cudaStream_t s);
+cudaError_t launch_combine_f32(const RowTargets& sources, int T, int d, int k, const uint32_t* row_code,
+                               const float* wts, float* y, cudaStream_t s);
+cudaError_t launch_combine(const RowTargets& sources, int T, int d, int k, const uint32_t* row_code,
+                           const float* wts, __nv_bfloat16* y, int num_sms, cudaStream_t s);
 cudaError_t launch_grouped_gemm_m256(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                      const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                      __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream);
@@ -199,13 +211,21 @@ template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool owned = true;
   void alloc(size_t count) {
     release();
     if (count) CU_CHECK(cudaMalloc(&p, count * sizeof(T)));
     n = count;
+    owned = true;
+  }
+  void view(void* q, size_t count) {  // a window into another allocation (the P2P slab)
+    release();
+    p = static_cast<T*>(q);
+    n = count;
+    owned = false;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p && owned) cudaFree(p);
     p = nullptr;
     n = 0;
   }
@@ -323,6 +343,16 @@ struct moe_ctx {
   // single-GPU forward: host planner work deferred until the histogram lands
   PendingPlan pending;
   cudaEvent_t ev_counts = nullptr;
+  // peer-memory exchange (MOE_EXCHANGE_P2P): one exported slab per rank
+  bool p2p = false, p2p_ready = false;
+  DevBuf<uint8_t> slab;
+  size_t off_flags = 0, off_counts = 0, off_xp = 0, off_yp = 0;
+  std::vector<void*> ipc_opened;  // peer slabs opened with cudaIpcOpenMemHandle
+  PeerSlabs peers{};
+  RowTargets xp_targets{}, yp_targets{};  // rank g -> g's xp / yp
+  uint32_t epoch = 0;                      // forwards issued; the flag value of the current one
+  int* p2p_err = nullptr;                  // mapped pinned: first timed-out wait (1 + kind*8 + rank)
+  uint64_t p2p_timeout_ns = 10000000000ull;
 };
 
 namespace {
@@ -427,8 +457,8 @@ void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int3
   }
   L.history.push_back({layer, total});
   if (L.history.size() > 16) L.history.erase(L.history.begin());
-  build_exchange_plan(c->G, c->rank, c->E, all.data(), L.rep_counts.data(), L.rep_gpu.data(), c->plan);
-  if (c->plan.rows_local > c->rows_cap || c->plan.rows_send > c->send_cap)
+  build_exchange_plan(c->G, c->rank, c->E, all.data(), L.rep_counts.data(), L.rep_gpu.data(), c->plan, c->p2p);
+  if (c->plan.rows_local > c->rows_cap || (!c->p2p && c->plan.rows_send > c->send_cap))
     throw Status(MOE_EINFEASIBLE, "received rows exceed workspace capacity");
   *c->hplan = c->plan.dev;
 }
@@ -439,15 +469,31 @@ void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool u
   const int nblk = gate_num_blocks(T);
   CU_CHECK(launch_block_prefix(c->block_counts.p, nblk, c->E, c->dplan.p, c->block_pre.p, s));
   // rows move as opaque 16-byte chunks: the row width in 16-bit units covers fp32 rows too
+  RowTargets t{};
+  if (c->p2p) {
+    t = c->xp_targets;  // rows go straight into the owning rank's received-rows buffer
+  } else {
+    t.base[0] = c->xp.p;
+    t.base[kSendTarget] = c->send.p;
+  }
   CU_CHECK(launch_dispatch(reinterpret_cast<const __nv_bfloat16*>(x), T, c->xw, c->E, c->k, c->ids.p, c->block_pre.p,
-                           c->dplan.p, reinterpret_cast<__nv_bfloat16*>(c->xp.p),
-                           reinterpret_cast<__nv_bfloat16*>(c->send.p), c->row_code.p, s));
+                           c->dplan.p, t, c->row_code.p, s));
 }
 
-// NCCL grouped p2p for one direction.  forward: my send buffer -> peers'
-// received-rows buffers; backward: my Y rows -> peers' return buffers.
+// The exchange step of one direction.  NCCL: grouped send/recv, forward: my
+// send buffer -> peers' received-rows buffers; backward: my Y rows -> peers'
+// return buffers.  Peer memory: the rows already moved inside dispatch (and
+// combine reads peers' outputs in place), so only the flag handshake is left:
+// forward = "my rows are in your buffer", backward = "my outputs are ready".
 void stage_exchange(moe_ctx* c, bool forward, cudaStream_t s) {
-  if (c->G == 1 || c->desc.exchange_mode != MOE_EXCHANGE_NCCL) return;
+  if (c->G == 1) return;
+  if (c->p2p) {
+    const int kind = forward ? kFlagRows : kFlagOutputs;
+    CU_CHECK(launch_p2p_signal(c->peers, c->G, kind, c->rank, c->epoch, s));
+    CU_CHECK(launch_p2p_wait(c->peers.flags[c->rank], c->G, kind, c->epoch, c->p2p_timeout_ns, c->p2p_err, s));
+    return;
+  }
+  if (c->desc.exchange_mode != MOE_EXCHANGE_NCCL) return;
   const size_t w = static_cast<size_t>(c->xw);  // row width in 16-bit units (bf16 or fp32 rows)
   const size_t row_bytes = w * 2;
   g_nccl.check(g_nccl.GroupStart(), "ncclGroupStart");
@@ -510,14 +556,27 @@ void stage_expert(moe_ctx* c, int layer, cudaStream_t s) {
 }
 
 void stage_combine(moe_ctx* c, uint16_t* y, int T, cudaStream_t s) {
+  RowTargets t{};
+  if (c->p2p) {
+    t = c->yp_targets;  // expert outputs are read where they were computed
+  } else {
+    t.base[0] = c->yp.p;
+    t.base[kSendTarget] = c->ret.p;
+  }
   if (c->fp32) {
-    CU_CHECK(launch_combine_f32(reinterpret_cast<const float*>(c->yp.p), reinterpret_cast<const float*>(c->ret.p), T,
-                                c->d, c->k, c->row_code.p, c->wts.p, reinterpret_cast<float*>(y), s));
+    CU_CHECK(launch_combine_f32(t, T, c->d, c->k, c->row_code.p, c->wts.p, reinterpret_cast<float*>(y), s));
     return;
   }
-  CU_CHECK(launch_combine(reinterpret_cast<const __nv_bfloat16*>(c->yp.p),
-                          reinterpret_cast<const __nv_bfloat16*>(c->ret.p), T, c->d, c->k, c->row_code.p, c->wts.p,
-                          reinterpret_cast<__nv_bfloat16*>(y), c->num_sms, s));
+  CU_CHECK(launch_combine(t, T, c->d, c->k, c->row_code.p, c->wts.p, reinterpret_cast<__nv_bfloat16*>(y),
+                          c->num_sms, s));
+}
+
+void check_p2p(moe_ctx* c) {
+  if (!c->p2p || !c->p2p_err || *reinterpret_cast<volatile int*>(c->p2p_err) == 0) return;
+  const int v = *c->p2p_err - 1;
+  static const char* kinds[] = {"gate counts", "dispatched rows", "expert outputs", "?"};
+  throw Status(MOE_ESTATE, std::string("peer exchange timed out waiting for ") + kinds[(v / kMaxRanks) & 3] +
+                               " of rank " + std::to_string(v % kMaxRanks) + " (ranks out of step?)");
 }
 
 cudaStream_t pick(moe_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->stream; }
@@ -573,6 +632,7 @@ void enqueue_local_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, i
 void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y, int plan_mode, long iteration,
                     moe_layer_stats* st, cudaStream_t s, cudaEvent_t x_consumed = nullptr) {
   Layer& L = layer_at(c, layer);
+  CU_CHECK(cudaSetDevice(c->desc.device));  // callers may drive ranks from several host threads
   require(T >= 0 && T <= c->Tmax, "token count exceeds max_tokens");
   require(plan_mode == MOE_PLAN_FIXED || plan_mode == MOE_PLAN_SYNC || plan_mode == MOE_PLAN_PREDICTED,
           "unknown plan mode");
@@ -611,7 +671,23 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   }
   mark(0);
   stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr);
-  if (c->G > 1) {
+  if (c->G > 1 && c->p2p) {
+    // peer memory: every rank reads every histogram from its owner; the host
+    // plans as in the NCCL path (one round trip), then dispatch writes rows
+    // directly into the owners' buffers
+    require(c->p2p_ready, "moe_p2p_import must be called before a peer-memory forward");
+    check_p2p(c);
+    const uint32_t ep = ++c->epoch;
+    CU_CHECK(launch_p2p_counts(c->peers, c->G, c->rank, stride, ep, c->p2p_timeout_ns, c->p2p_err,
+                               c->counts_all.p, s));
+    CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
+    mark(1);
+    CU_CHECK(cudaStreamSynchronize(s));
+    check_p2p(c);
+    stage_plan(c, layer, plan_mode, iteration, c->h_counts, stride);
+    mark(2);
+    stage_dispatch(c, x, T, s);  // rows land in their owners' buffers
+  } else if (c->G > 1) {
     // NCCL needs every chunk size on the host: one round trip per layer.
     require(c->desc.exchange_mode == MOE_EXCHANGE_NCCL, "staged API required for external exchange");
     g_nccl.check(g_nccl.AllGather(c->counts.p, c->counts_all.p, stride, ncclInt32, c->comm, s), "ncclAllGather");
@@ -765,6 +841,25 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->yp.alloc(static_cast<size_t>(c->rows_cap) * c->xw);
     c->send.alloc(static_cast<size_t>(c->send_cap) * c->xw);
     c->ret.alloc(static_cast<size_t>(c->send_cap) * c->xw);
+    if (c->G > 1 && D.exchange_mode == MOE_EXCHANGE_P2P) {
+      // one exported slab: flags | counts | received rows (xp) | expert outputs (yp)
+      require(c->G <= kMaxRanks, "the peer-memory exchange supports up to 8 ranks");
+      c->p2p = true;
+      auto up = [](size_t b) { return (b + 4095) & ~size_t(4095); };
+      const size_t rows_bytes = static_cast<size_t>(c->rows_cap) * c->xw * 2;
+      c->off_flags = 0;
+      c->off_counts = up(sizeof(uint32_t) * kFlagKinds * kMaxRanks);
+      c->off_xp = c->off_counts + up(sizeof(int32_t) * c->count_stride);
+      c->off_yp = c->off_xp + up(rows_bytes);
+      c->slab.alloc(c->off_yp + up(rows_bytes));
+      CU_CHECK(cudaMemset(c->slab.p, 0, c->off_xp));  // flags start at epoch 0
+      c->counts.view(c->slab.p + c->off_counts, pad16(sizeof(int32_t) * c->count_stride) / 4);
+      c->xp.view(c->slab.p + c->off_xp, static_cast<size_t>(c->rows_cap) * c->xw);
+      c->yp.view(c->slab.p + c->off_yp, static_cast<size_t>(c->rows_cap) * c->xw);
+      CU_CHECK(cudaHostAlloc(&c->p2p_err, sizeof(int) * 4, cudaHostAllocMapped));
+      *c->p2p_err = 0;
+      if (const char* v = std::getenv("MOE_P2P_TIMEOUT_MS")) c->p2p_timeout_ns = std::strtoull(v, nullptr, 10) * 1000000ull;
+    }
     c->dplan.alloc(1);
     {  // split-K gate scratch: <= 296 (block, split) CTAs x 32 tokens x padded logits
       int nt = 1;
@@ -803,6 +898,8 @@ int moe_ctx_destroy(moe_ctx* c) {
     cudaSetDevice(c->desc.device);
     cudaStreamSynchronize(c->stream);
     if (c->comm) g_nccl.CommDestroy(c->comm);
+    for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
+    if (c->p2p_err) cudaFreeHost(c->p2p_err);
     c->events.destroy();
     if (c->hplan) cudaFreeHost(c->hplan);
     if (c->h_counts) cudaFreeHost(c->h_counts);
@@ -841,6 +938,79 @@ int moe_ctx_sync(moe_ctx* c) {
     require(c, "null context");
     CU_CHECK(cudaStreamSynchronize(c->stream));
     flush_pending_plan(c);
+  });
+}
+
+int moe_p2p_export(moe_ctx* c, moe_p2p_handle* out) {
+  return guarded([&] {
+    require(c && out, "null argument");
+    require(c->p2p, "context was not created with MOE_EXCHANGE_P2P and world_size > 1");
+    static_assert(sizeof(moe_p2p_handle) == 192, "moe_p2p_handle layout");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    moe_p2p_handle h{};
+    cudaIpcMemHandle_t ipc;
+    CU_CHECK(cudaIpcGetMemHandle(&ipc, c->slab.p));
+    std::memcpy(h.ipc, &ipc, sizeof(ipc));
+    h.pid = static_cast<uint64_t>(getpid());
+    h.base = reinterpret_cast<uint64_t>(c->slab.p);
+    h.bytes = c->slab.n;
+    h.off_flags = c->off_flags;
+    h.off_counts = c->off_counts;
+    h.off_xp = c->off_xp;
+    h.off_yp = c->off_yp;
+    h.device = c->desc.device;
+    h.rank = c->rank;
+    h.world_size = c->G;
+    h.version = 1;
+    *out = h;
+  });
+}
+
+int moe_p2p_import(moe_ctx* c, const moe_p2p_handle* hs, int n) {
+  return guarded([&] {
+    require(c && hs, "null argument");
+    require(c->p2p, "context was not created with MOE_EXCHANGE_P2P and world_size > 1");
+    require(!c->p2p_ready, "peer slabs already imported");
+    require(n == c->G, "need one handle per rank");
+    CU_CHECK(cudaSetDevice(c->desc.device));
+    for (int g = 0; g < n; ++g) {
+      const moe_p2p_handle& h = hs[g];
+      require(h.version == 1 && h.rank == g && h.world_size == c->G, "handle " + std::to_string(g) +
+                                                                          " is not rank " + std::to_string(g) +
+                                                                          " of this world");
+      require(h.bytes == c->slab.n && h.off_xp == c->off_xp && h.off_yp == c->off_yp &&
+                  h.off_counts == c->off_counts,
+              "rank " + std::to_string(g) + " was created with a different shape");
+      uint8_t* base = nullptr;
+      if (g == c->rank) {
+        base = c->slab.p;
+      } else if (h.pid == static_cast<uint64_t>(getpid())) {
+        // same process (ranks driven by threads): the pointer is valid here; a
+        // different device needs peer access
+        if (h.device != c->desc.device) {
+          int ok = 0;
+          CU_CHECK(cudaDeviceCanAccessPeer(&ok, c->desc.device, h.device));
+          require(ok != 0, "device " + std::to_string(c->desc.device) + " cannot access device " +
+                               std::to_string(h.device));
+          const cudaError_t e = cudaDeviceEnablePeerAccess(h.device, 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          else CU_CHECK(e);
+        }
+        base = reinterpret_cast<uint8_t*>(h.base);
+      } else {
+        cudaIpcMemHandle_t ipc;
+        std::memcpy(&ipc, h.ipc, sizeof(ipc));
+        void* q = nullptr;
+        CU_CHECK(cudaIpcOpenMemHandle(&q, ipc, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened.push_back(q);
+        base = static_cast<uint8_t*>(q);
+      }
+      c->peers.flags[g] = reinterpret_cast<uint32_t*>(base + h.off_flags);
+      c->peers.counts[g] = reinterpret_cast<const int32_t*>(base + h.off_counts);
+      c->xp_targets.base[g] = base + h.off_xp;
+      c->yp_targets.base[g] = base + h.off_yp;
+    }
+    c->p2p_ready = true;
   });
 }
 
@@ -995,7 +1165,8 @@ int moe_predict_loads(moe_ctx* c, int layer, const uint16_t* x, int T, int32_t* 
 int moe_layer_forward(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y, int plan_mode, long iteration,
                       moe_layer_stats* stats, void* stream) {
   return guarded([&] {
-    require(c && x && y, "null argument");
+    // a rank with no tokens still takes part in the exchange (x, y may be null)
+    require(c && (T == 0 || (x && y)), "null argument");
     forward_device(c, layer, x, T, y, plan_mode, iteration, stats, pick(c, stream));
   });
 }
@@ -1105,6 +1276,7 @@ int moe_forward_begin(moe_ctx* c, int layer, const uint16_t* x, int T, const int
     Layer& L = layer_at(c, layer);
     require(x != nullptr, "null input");
     require(T >= 0 && T <= c->Tmax, "token count exceeds max_tokens");
+    require(!c->p2p, "the staged API is for the NCCL / external exchange, not MOE_EXCHANGE_P2P");
     cudaStream_t s = pick(c, stream);
     flush_pending_plan(c);
     if (!counts_all) {

@@ -24,7 +24,7 @@
 namespace moe {
 
 void build_exchange_plan(int G, int rank, int E, const int64_t* counts_all, const int32_t* R,
-                         const int32_t* gpu_of, HostPlan& out) {
+                         const int32_t* gpu_of, HostPlan& out, bool direct) {
   if (G < 1 || rank < 0 || rank >= G) throw std::invalid_argument("bad world size / rank");
   if (E < 1 || E > kMaxExperts) throw std::invalid_argument("num_experts out of range");
   DevPlan& p = out.dev;
@@ -91,7 +91,6 @@ void build_exchange_plan(int G, int rank, int E, const int64_t* counts_all, cons
     rows += out.rep_size[id];
   }
   out.rows_local = rows;
-  // sends: my rows bound to replicas elsewhere, peer-major then replica order
   out.sends.clear();
   out.recvs.clear();
   int64_t send_rows = 0;
@@ -101,6 +100,33 @@ void build_exchange_plan(int G, int rank, int E, const int64_t* counts_all, cons
     lo = std::max(out.rep_start[id], so);
     hi = std::min(out.rep_start[id] + out.rep_size[id], so + sc);
   };
+  if (direct) {
+    // every GPU lays out its segments the same way (replica order), so each
+    // rank can compute where its rows land in any peer's buffer
+    std::vector<int64_t> fill(G, 0);
+    for (int id = 0; id < f; ++id) {
+      const int g = gpu_of[id];
+      const int64_t seg = fill[g];
+      fill[g] += out.rep_size[id];
+      p.rep_remote[id] = g;
+      if (g == rank) continue;  // local replicas keep their segment base from above
+      if (seg - out.rep_start[id] < INT32_MIN || seg > INT32_MAX)
+        throw std::invalid_argument("row count exceeds 2^31");
+      p.rep_row_base[id] = static_cast<int>(seg - out.rep_start[id]);
+      int e = 0;
+      while (p.rep_base[e + 1] <= id) ++e;
+      int64_t lo, hi;
+      my_range(rank, e, id, lo, hi);
+      if (hi > lo) send_rows += hi - lo;
+    }
+    for (int g = 0; g < G; ++g)
+      if (fill[g] > kRowMask) throw std::invalid_argument("row count exceeds the row-code range");
+    out.rows_send = send_rows;
+    p.rows_local = static_cast<int>(rows);
+    p.rows_send = static_cast<int>(send_rows);
+    return;
+  }
+  // sends: my rows bound to replicas elsewhere, peer-major then replica order
   for (int peer = 0; peer < G; ++peer) {
     if (peer == rank) continue;
     for (int e = 0; e < E; ++e)
@@ -108,7 +134,7 @@ void build_exchange_plan(int G, int rank, int E, const int64_t* counts_all, cons
         if (gpu_of[id] != peer) continue;
         int64_t lo, hi;
         my_range(rank, e, id, lo, hi);
-        p.rep_remote[id] = 1;
+        p.rep_remote[id] = kSendTarget;
         p.rep_row_base[id] = static_cast<int>(send_rows - lo);
         if (hi > lo) {
           out.sends.push_back({peer, id, send_rows, hi - lo});
@@ -128,7 +154,7 @@ void build_exchange_plan(int G, int rank, int E, const int64_t* counts_all, cons
         if (hi > lo) out.recvs.push_back({peer, id, out.seg_start[id] + (lo - out.rep_start[id]), hi - lo});
       }
   }
-  if (rows > INT32_MAX || send_rows > INT32_MAX) throw std::invalid_argument("row count exceeds 2^31");
+  if (rows > kRowMask || send_rows > kRowMask) throw std::invalid_argument("row count exceeds the row-code range");
   p.rows_local = static_cast<int>(rows);
   p.rows_send = static_cast<int>(send_rows);
 }

@@ -22,7 +22,13 @@ struct HostPlan {
 };
 
 // counts_all: [G][E]; R: [E]; gpu_of: [sum R] flattened (expert, ordinal).
+// direct = false: remote rows go to this rank's send buffer (row-code target
+// kSendTarget) for the NCCL / external exchange, described by sends/recvs.
+// direct = true (peer-memory exchange): every row code names the destination
+// rank and the row inside THAT rank's received-rows buffer, so dispatch
+// stores each row straight into its final place on the owning GPU; no chunk
+// lists, rows_send counts the rows that leave this GPU.
 void build_exchange_plan(int G, int rank, int E, const int64_t* counts_all, const int32_t* R,
-                         const int32_t* gpu_of, HostPlan& out);
+                         const int32_t* gpu_of, HostPlan& out, bool direct = false);
 
 }  // namespace moe

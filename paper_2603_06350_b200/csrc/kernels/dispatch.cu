@@ -75,14 +75,14 @@ template <int K>
 __global__ void __launch_bounds__(128)
 dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const int32_t* __restrict__ ids,
                 const int32_t* __restrict__ block_pre, const DevPlan* __restrict__ plan,
-                __nv_bfloat16* __restrict__ xp_local, __nv_bfloat16* __restrict__ xp_send,
-                uint32_t* __restrict__ row_code) {
+                const RowTargets targets, uint32_t* __restrict__ row_code) {
   __shared__ uint32_t codes[32 * K];
   // the block's prefix row and the plan tables the ranking loop reads, staged
   // once (coalesced) so the per-expert loop below never waits on L2
   __shared__ int s_pre[kMaxExperts], s_n[kMaxExperts], s_rbase[kMaxExperts + 1];
   __shared__ int s_rrow[kMaxReplicas];
   __shared__ unsigned char s_rrem[kMaxReplicas];
+  __shared__ __nv_bfloat16* s_tgt[kMaxTargets];
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int t_base = b * 32;
@@ -96,8 +96,9 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
   if (threadIdx.x == 0) s_rbase[E] = plan->rep_base[E];
   for (int i = threadIdx.x; i < R; i += blockDim.x) {
     s_rrow[i] = plan->rep_row_base[i];
-    s_rrem[i] = plan->rep_remote[i] ? 1 : 0;
+    s_rrem[i] = static_cast<unsigned char>(plan->rep_remote[i]);
   }
+  if (threadIdx.x < kMaxTargets) s_tgt[threadIdx.x] = static_cast<__nv_bfloat16*>(targets.base[threadIdx.x]);
   __syncthreads();
 
   if (warp == 0) {
@@ -121,7 +122,7 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
         const int q = n / Re, rem = n % Re;
         const int r = gr < rem * (q + 1) ? gr / (q + 1) : rem + (gr - rem * (q + 1)) / q;
         const int f = s_rbase[e] + r;
-        const uint32_t code = static_cast<uint32_t>(s_rrow[f] + gr) | (s_rrem[f] ? kRemoteBit : 0u);
+        const uint32_t code = static_cast<uint32_t>(s_rrow[f] + gr) | (static_cast<uint32_t>(s_rrem[f]) << kTargetShift);
         codes[lane * K + slot] = code;
         if (blockIdx.y == 0) row_code[(size_t)t * K + slot] = code;
       }
@@ -141,8 +142,7 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       const uint32_t c = codes[i * K + j];
-      __nv_bfloat16* base = (c & kRemoteBit) ? xp_send : xp_local;
-      dst[j] = base + (size_t)(c & ~kRemoteBit) * d;
+      dst[j] = s_tgt[c >> kTargetShift] + (size_t)(c & kRowMask) * d;  // local, send buffer or a peer's rows
     }
     for (int c0 = c_begin + lane; c0 < chunks; c0 += 32 * 4) {
       int4 v[4];
@@ -162,9 +162,11 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
 // -------------------------------------------------------------- combine
 template <int K>
 __global__ void __launch_bounds__(256)
-combine_kernel(const __nv_bfloat16* __restrict__ y_local, const __nv_bfloat16* __restrict__ y_return, int T,
-               int d, const uint32_t* __restrict__ row_code, const float* __restrict__ wts,
-               __nv_bfloat16* __restrict__ y) {
+combine_kernel(const RowTargets sources, int T, int d, const uint32_t* __restrict__ row_code,
+               const float* __restrict__ wts, __nv_bfloat16* __restrict__ y) {
+  __shared__ const __nv_bfloat16* s_src[kMaxTargets];
+  if (threadIdx.x < kMaxTargets) s_src[threadIdx.x] = static_cast<const __nv_bfloat16*>(sources.base[threadIdx.x]);
+  __syncthreads();
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
@@ -178,7 +180,7 @@ combine_kernel(const __nv_bfloat16* __restrict__ y_local, const __nv_bfloat16* _
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       const uint32_t c = row_code[(size_t)t * K + j];
-      src[j] = ((c & kRemoteBit) ? y_return : y_local) + (size_t)(c & ~kRemoteBit) * d;
+      src[j] = s_src[c >> kTargetShift] + (size_t)(c & kRowMask) * d;  // local, return buffer or a peer's outputs
       w[j] = wts[(size_t)t * K + j];
     }
     __nv_bfloat16* out = y + (size_t)t * d;
@@ -293,22 +295,20 @@ cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, co
   }
 
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
-                            const int32_t* block_pre, const DevPlan* plan, __nv_bfloat16* xp_local,
-                            __nv_bfloat16* xp_send, uint32_t* row_code, cudaStream_t s) {
+                            const int32_t* block_pre, const DevPlan* plan, const RowTargets& targets,
+                            uint32_t* row_code, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   if (d % 8) return cudaErrorInvalidValue;
   const int nblk = (T + 31) / 32;
   // at least ~2 CTAs per SM: split each row's chunks when there are few blocks
   const int split = std::max(1, std::min((2 * 148 + nblk - 1) / nblk, d / 8 / 32));
   const dim3 grid(nblk, split);
-  MOE_SWITCH_K(k, (dispatch_kernel<KK><<<grid, 128, 0, s>>>(x, T, d, E, ids, block_pre, plan, xp_local, xp_send,
-                                                           row_code)));
+  MOE_SWITCH_K(k, (dispatch_kernel<KK><<<grid, 128, 0, s>>>(x, T, d, E, ids, block_pre, plan, targets, row_code)));
   return cudaGetLastError();
 }
 
-cudaError_t launch_combine(const __nv_bfloat16* y_local, const __nv_bfloat16* y_return, int T, int d, int k,
-                           const uint32_t* row_code, const float* wts, __nv_bfloat16* y, int num_sms,
-                           cudaStream_t s) {
+cudaError_t launch_combine(const RowTargets& sources, int T, int d, int k, const uint32_t* row_code,
+                           const float* wts, __nv_bfloat16* y, int num_sms, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   if (d % 8) return cudaErrorInvalidValue;
   const int warps_needed = T;
@@ -316,7 +316,7 @@ cudaError_t launch_combine(const __nv_bfloat16* y_local, const __nv_bfloat16* y_
   ctas = ctas < num_sms * 8 ? ctas : num_sms * 8;
   const int split = std::max(1, std::min((2 * num_sms + ctas - 1) / ctas, d / 8 / 32));
   const dim3 grid(ctas, split);
-  MOE_SWITCH_K(k, (combine_kernel<KK><<<grid, 256, 0, s>>>(y_local, y_return, T, d, row_code, wts, y)));
+  MOE_SWITCH_K(k, (combine_kernel<KK><<<grid, 256, 0, s>>>(sources, T, d, row_code, wts, y)));
   return cudaGetLastError();
 }
 

@@ -8,7 +8,19 @@ namespace moe {
 
 constexpr int kMaxExperts = 256;
 constexpr int kMaxReplicas = 512;
-constexpr uint32_t kRemoteBit = 0x80000000u;  // row code: row lives in the send/return buffer
+// Row code = (target << 28) | row.  The target indexes a table of row
+// buffers (RowTargets): 0 = this rank's received rows / expert outputs,
+// 8 = the send / return buffer of the NCCL exchange (kRemoteBit), and in the
+// peer-memory exchange g = rank g's buffers, written / read over NVLink.
+constexpr int kTargetShift = 28;
+constexpr uint32_t kRowMask = (1u << kTargetShift) - 1u;
+constexpr uint32_t kRemoteBit = 0x80000000u;  // target 8: the NCCL send/return buffer
+constexpr int kSendTarget = 8;
+constexpr int kMaxTargets = 16;
+
+struct RowTargets {
+  void* base[kMaxTargets];
+};
 
 // One GEMM segment = the rows of one replica placed on this rank.
 struct GemmSeg {
@@ -28,7 +40,7 @@ struct DevPlan {
   int src_off[kMaxExperts];           // this rank's first global rank in expert e
   int rep_base[kMaxExperts + 4];      // flat replica id of (e, 0); [E] = R
   int rep_row_base[kMaxReplicas];     // row(gr) = rep_row_base[f] + gr
-  int rep_remote[kMaxReplicas];       // 1: rows go to the send buffer
+  int rep_remote[kMaxReplicas];       // row-code target of replica f's rows (0 local)
   GemmSeg segs[kMaxReplicas];
 };
 

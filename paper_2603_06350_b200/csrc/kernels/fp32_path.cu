@@ -167,9 +167,12 @@ __global__ void swiglu_f32_kernel(const float* __restrict__ C, int rows, int ff,
   }
 }
 
-__global__ void combine_f32_kernel(const float* __restrict__ y_local, const float* __restrict__ y_return, int T,
-                                   int d, int k, const uint32_t* __restrict__ row_code, const float* __restrict__ wts,
+__global__ void combine_f32_kernel(const RowTargets sources, int T, int d, int k,
+                                   const uint32_t* __restrict__ row_code, const float* __restrict__ wts,
                                    float* __restrict__ y) {
+  __shared__ const float* s_src[kMaxTargets];
+  if (threadIdx.x < kMaxTargets) s_src[threadIdx.x] = static_cast<const float*>(sources.base[threadIdx.x]);
+  __syncthreads();
   const size_t n = (size_t)T * d;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const size_t t = i / d;
@@ -177,7 +180,7 @@ __global__ void combine_f32_kernel(const float* __restrict__ y_local, const floa
     float acc = 0.0f;
     for (int j = 0; j < k; ++j) {
       const uint32_t code = row_code[t * k + j];
-      const float* src = ((code & kRemoteBit) ? y_return : y_local) + (size_t)(code & ~kRemoteBit) * d;
+      const float* src = s_src[code >> kTargetShift] + (size_t)(code & kRowMask) * d;
       acc = fmaf(wts[t * k + j], src[c], acc);
     }
     y[i] = acc;
@@ -207,10 +210,10 @@ cudaError_t launch_swiglu_f32(const float* C, int rows, int ff, float* H, cudaSt
   return cudaGetLastError();
 }
 
-cudaError_t launch_combine_f32(const float* y_local, const float* y_return, int T, int d, int k,
-                               const uint32_t* row_code, const float* wts, float* y, cudaStream_t s) {
+cudaError_t launch_combine_f32(const RowTargets& sources, int T, int d, int k, const uint32_t* row_code,
+                               const float* wts, float* y, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
-  combine_f32_kernel<<<1184, 256, 0, s>>>(y_local, y_return, T, d, k, row_code, wts, y);
+  combine_f32_kernel<<<1184, 256, 0, s>>>(sources, T, d, k, row_code, wts, y);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,163 @@
+"""Peer-memory expert parallelism (MOE_EXCHANGE_P2P) with G ranks sharing ONE
+B200 (the pool has one GPU per call).
+
+Each rank is a full context: its dispatch kernel stores rows straight into the
+owning rank's received-rows buffer, its combine reads expert outputs from the
+owner, and device flags order the phases — the same code that runs over
+NVLink between GPUs.  Ranks are driven by host threads (one process, plain
+pointers) and by separate processes (CUDA IPC handles).
+
+A row's expert output does not depend on which rank computes it (the GEMM's
+per-row K loop is the same wherever the row lands), so every rank's output
+must be BIT-IDENTICAL to a single-GPU forward on its own tokens, whatever
+the placement; ids and counts are checked against the oracle.
+"""
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2603_06350_b200 import (MOE_EXCHANGE_P2P, MOE_PLAN_FIXED, MOE_PLAN_SYNC, MoeError, MoELayer)
+from paper_2603_06350_b200 import workload as wl
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ranks(G, E, k, d, ff, Tmax, cap_replicas=0, **kw):
+    mem = 3.0 * d * ff * 2 / 1e6
+    ms = [MoELayer(1, E, k, d, ff, max_tokens=Tmax, world_size=G, rank=r, exchange_mode=MOE_EXCHANGE_P2P,
+                   expert_mem_mb=mem, layer_mem_cap_mb=(E + cap_replicas) * mem, **kw) for r in range(G)]
+    handles = [m.p2p_export() for m in ms]
+    for m in ms:
+        m.p2p_import(handles)
+    return ms
+
+
+def _single(E, k, d, ff, Tmax):
+    mem = 3.0 * d * ff * 2 / 1e6
+    return MoELayer(1, E, k, d, ff, max_tokens=Tmax, expert_mem_mb=mem, layer_mem_cap_mb=E * mem)
+
+
+def _parallel(ms, fn):
+    with ThreadPoolExecutor(len(ms)) as ex:
+        return list(ex.map(fn, range(len(ms))))
+
+
+@pytest.mark.parametrize("G,E,k,d,ff,tokens,rc,rg", [
+    (2, 8, 2, 1024, 1408, [256, 200], [1] * 8, [0, 1, 0, 1, 0, 1, 0, 1]),
+    (2, 8, 2, 1024, 1408, [300, 1], [2, 1, 1, 3, 1, 1, 1, 1], [0, 1, 1, 0, 1, 0, 1, 0, 0, 1, 1]),
+    (4, 16, 2, 1024, 1408, [128, 64, 0, 200], [1] * 16, [e % 4 for e in range(16)]),
+    (4, 64, 8, 2048, 1408, [64, 64, 64, 64], [1] * 62 + [3, 2], [e % 4 for e in range(62)] + [0, 1, 2, 3, 3]),
+])
+def test_p2p_fixed_placement_bit_identical(cuda, G, E, k, d, ff, tokens, rc, rg):
+    import torch
+    wg = wl.gate_weights(E, d, 1.2, 1, 0, 0)
+    experts = [wl.expert_weights(d, ff, 1, 0, e) for e in range(E)]
+    Tmax = max(max(tokens), 1)
+    ms = _ranks(G, E, k, d, ff, Tmax)
+    one = _single(E, k, d, ff, Tmax)
+    for m in ms + [one]:
+        m.set_gate(0, wg)
+        for e, w in enumerate(experts):
+            m.load_expert(0, e, *w)
+    for m in ms:
+        m.set_placement(0, rc, rg)
+    xs = [wl.tokens(tokens[r], d, E, 1, 70 + r) for r in range(G)]
+    xd = [torch.from_numpy(x.view(np.int16)).to(cuda) for x in xs]
+    yd = [torch.zeros((max(t, 1), d), dtype=torch.int16, device=cuda)[:t] for t in tokens]
+    for it in range(3):  # repeated forwards exercise the epoch flags and buffer reuse
+        sts = _parallel(ms, lambda r: ms[r].forward(0, xd[r], yd[r], MOE_PLAN_FIXED, it, stats=True))
+        torch.cuda.synchronize()
+        assert sum(st.rows_local for st in sts) == k * sum(tokens)
+        for r in range(G):
+            T = tokens[r]
+            if T == 0:
+                continue
+            y1 = torch.zeros_like(yd[r])
+            one.forward(0, xd[r], y1, MOE_PLAN_FIXED, it)
+            one.sync()
+            assert torch.equal(yd[r], y1), (it, r)
+            ids = ms[r].read_buffer(4, np.int32, (T, k))
+            y_ref, ids_o, _, counts_o = oracle.layer_forward(xs[r], wg, experts, [1] * E, k)
+            assert np.array_equal(ids, ids_o)
+            assert np.array_equal(np.array(sts[r].counts[:E]), counts_o)
+            y = oracle.bf16_to_f32(yd[r].cpu().numpy().view(np.uint16))
+            assert float(np.max(np.abs(y - y_ref)) / np.max(np.abs(y_ref))) <= 2e-2
+    for m in ms + [one]:
+        m.close()
+
+
+def test_p2p_sync_planner_replicas(cuda):
+    """MOE_PLAN_SYNC at G=4: every rank runs scale/place on the all-gathered
+    histogram (identical decisions), straggler replicas split hot experts over
+    ranks, gates change every iteration; outputs stay bit-identical to G=1."""
+    import torch
+    G, E, k, d, ff, T = 4, 16, 2, 1024, 1408, 192
+    ms = _ranks(G, E, k, d, ff, T, cap_replicas=6)
+    one = _single(E, k, d, ff, T)
+    for m in ms + [one]:
+        for e in range(E):
+            m.load_expert(0, e, *wl.expert_weights(d, ff, 1, 0, e))
+    xd = [torch.from_numpy(wl.tokens(T, d, E, 1, 90 + r).view(np.int16)).to(cuda) for r in range(G)]
+    yd = [torch.zeros((T, d), dtype=torch.int16, device=cuda) for _ in range(G)]
+    replicas = []
+    for it in range(4):
+        wg = wl.gate_weights(E, d, 1.6, 1, 0, it)
+        for m in ms + [one]:
+            m.set_gate(0, wg)
+        sts = _parallel(ms, lambda r: ms[r].forward(0, xd[r], yd[r], MOE_PLAN_SYNC, it, stats=True))
+        torch.cuda.synchronize()
+        assert len({st.replica_count for st in sts}) == 1  # same plan on every rank
+        replicas.append(sts[0].replica_count)
+        assert sum(st.rows_local for st in sts) == k * G * T
+        for r in range(G):
+            y1 = torch.zeros_like(yd[r])
+            one.forward(0, xd[r], y1, MOE_PLAN_FIXED, it)
+            one.sync()
+            assert torch.equal(yd[r], y1), (it, r)
+    assert max(replicas) > E  # the planner did add straggler replicas
+    for m in ms + [one]:
+        m.close()
+
+
+def test_p2p_rank_out_of_step_times_out(cuda, monkeypatch):
+    """A rank whose peers never arrive fails the call instead of hanging."""
+    import torch
+    monkeypatch.setenv("MOE_P2P_TIMEOUT_MS", "300")
+    E, k, d, ff, T = 8, 2, 256, 256, 64
+    ms = _ranks(2, E, k, d, ff, T)
+    for m in ms:
+        m.set_gate(0, wl.gate_weights(E, d, 1.2, 1, 0, 0))
+        for e in range(E):
+            m.load_expert(0, e, *wl.expert_weights(d, ff, 1, 0, e))
+    x = torch.from_numpy(wl.tokens(T, d, E, 1, 0).view(np.int16)).to(cuda)
+    y = torch.zeros((T, d), dtype=torch.int16, device=cuda)
+    with pytest.raises(MoeError, match="timed out"):
+        ms[0].forward(0, x, y, MOE_PLAN_FIXED, 0)
+    ms[0].close()
+    ms[1].close()
+
+
+def test_p2p_two_processes_ipc(cuda, tmp_path):
+    """Two processes on the same device, slabs shared with CUDA IPC handles
+    exchanged over gloo (tests/p2p_worker.py); each checks itself against a
+    single-GPU forward."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29731", PYTHONPATH=ROOT)
+    procs = [subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "p2p_worker.py"), str(r), "2"],
+                              env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT) for r in range(2)]
+    outs = []
+    for p in procs:
+        try:
+            out, _ = p.communicate(timeout=240)
+        except subprocess.TimeoutExpired:
+            p.kill()
+            out, _ = p.communicate()
+        outs.append(out.decode(errors="replace"))
+    for p, o in zip(procs, outs):
+        assert p.returncode == 0, o[-3000:]
+        assert "P2P-IPC OK" in o, o[-3000:]
