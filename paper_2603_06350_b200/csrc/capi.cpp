@@ -47,7 +47,7 @@ cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, co
                                 int32_t* block_pre, cudaStream_t s);
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
                             const int32_t* block_pre, const DevPlan* plan, const RowTargets& targets,
-                            uint32_t* row_code, cudaStream_t s);
+                            uint32_t* row_code, const PeerSignal& sig, cudaStream_t s);
 // K6 over peer memory (p2p.cu)
 constexpr int kMaxRanks = 8;
 enum { kFlagCounts = 0, kFlagRows = 1, kFlagOutputs = 2, kFlagKinds = 4 };
@@ -352,6 +352,7 @@ struct moe_ctx {
   RowTargets xp_targets{}, yp_targets{};  // rank g -> g's xp / yp
   uint32_t epoch = 0;                      // forwards issued; the flag value of the current one
   int* p2p_err = nullptr;                  // mapped pinned: first timed-out wait (1 + kind*8 + rank)
+  DevBuf<uint32_t> dispatch_counter;       // CTAs of the signalling dispatch grid that finished
   uint64_t p2p_timeout_ns = 10000000000ull;
 };
 
@@ -470,14 +471,23 @@ void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool u
   CU_CHECK(launch_block_prefix(c->block_counts.p, nblk, c->E, c->dplan.p, c->block_pre.p, s));
   // rows move as opaque 16-byte chunks: the row width in 16-bit units covers fp32 rows too
   RowTargets t{};
+  PeerSignal sig{};
   if (c->p2p) {
     t = c->xp_targets;  // rows go straight into the owning rank's received-rows buffer
+    if (T > 0) {        // the dispatch grid itself publishes "my rows are delivered"
+      for (int g = 0; g < c->G; ++g) sig.flags[g] = c->peers.flags[g];
+      sig.counter = c->dispatch_counter.p;
+      sig.G = c->G;
+      sig.src = c->rank;
+      sig.kind = kFlagRows;
+      sig.epoch = c->epoch;
+    }
   } else {
     t.base[0] = c->xp.p;
     t.base[kSendTarget] = c->send.p;
   }
   CU_CHECK(launch_dispatch(reinterpret_cast<const __nv_bfloat16*>(x), T, c->xw, c->E, c->k, c->ids.p, c->block_pre.p,
-                           c->dplan.p, t, c->row_code.p, s));
+                           c->dplan.p, t, c->row_code.p, sig, s));
 }
 
 // The exchange step of one direction.  NCCL: grouped send/recv, forward: my
@@ -489,7 +499,9 @@ void stage_exchange(moe_ctx* c, bool forward, cudaStream_t s) {
   if (c->G == 1) return;
   if (c->p2p) {
     const int kind = forward ? kFlagRows : kFlagOutputs;
-    CU_CHECK(launch_p2p_signal(c->peers, c->G, kind, c->rank, c->epoch, s));
+    // the rows signal is fused into the dispatch kernel (a rank without tokens
+    // launches no dispatch and signals here)
+    if (!forward || c->cur_T == 0) CU_CHECK(launch_p2p_signal(c->peers, c->G, kind, c->rank, c->epoch, s));
     CU_CHECK(launch_p2p_wait(c->peers.flags[c->rank], c->G, kind, c->epoch, c->p2p_timeout_ns, c->p2p_err, s));
     return;
   }
@@ -634,6 +646,7 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   Layer& L = layer_at(c, layer);
   CU_CHECK(cudaSetDevice(c->desc.device));  // callers may drive ranks from several host threads
   require(T >= 0 && T <= c->Tmax, "token count exceeds max_tokens");
+  c->cur_T = T;
   require(plan_mode == MOE_PLAN_FIXED || plan_mode == MOE_PLAN_SYNC || plan_mode == MOE_PLAN_PREDICTED,
           "unknown plan mode");
   for (int e = 0; e < c->E; ++e)
@@ -857,6 +870,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
       c->xp.view(c->slab.p + c->off_xp, static_cast<size_t>(c->rows_cap) * c->xw);
       c->yp.view(c->slab.p + c->off_yp, static_cast<size_t>(c->rows_cap) * c->xw);
       CU_CHECK(cudaHostAlloc(&c->p2p_err, sizeof(int) * 4, cudaHostAllocMapped));
+      c->dispatch_counter.alloc(4);
+      CU_CHECK(cudaMemset(c->dispatch_counter.p, 0, 16));
       *c->p2p_err = 0;
       if (const char* v = std::getenv("MOE_P2P_TIMEOUT_MS")) c->p2p_timeout_ns = std::strtoull(v, nullptr, 10) * 1000000ull;
     }

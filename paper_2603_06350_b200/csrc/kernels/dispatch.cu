@@ -13,13 +13,15 @@
 // Pipeline (all on device, no host round trip once the plan is uploaded):
 //   block_prefix_kernel  exclusive scan of the gate's per-32-token-block
 //                        histograms -> each block's per-expert start rank.
-//   dispatch_kernel      one CTA per 32-token block: warp 0 ranks the block's
-//                        (token, slot) assignments with one ballot per expert,
-//                        maps global rank -> replica -> destination row, and
-//                        records a 32-bit row code per assignment (bit 31 =
-//                        row lives in the send buffer of another rank); then
-//                        4 warps stream each token row once from HBM and store
-//                        it k times with 128-bit vector stores.
+//   dispatch_kernel      one CTA per 32-token block (x gridDim.y column
+//                        splits for small batches): warp 0 ranks the block's
+//                        (token, slot) assignments from per-expert token
+//                        bitmasks (shared-memory atomicOr + popc), maps global
+//                        rank -> replica -> destination row, and records a
+//                        32-bit row code per assignment (target << 28 | row:
+//                        local rows, the NCCL send buffer, or a peer's
+//                        received rows); then all 4 warps stream the rows
+//                        once from HBM and store each k times (128-bit).
 //   combine_kernel       y_t = sum_j w_tj * Y[row(t, j)], fp32 accumulate in
 //                        slot order, bf16 out; one warp per token.
 #include <algorithm>
@@ -75,11 +77,13 @@ template <int K>
 __global__ void __launch_bounds__(128)
 dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const int32_t* __restrict__ ids,
                 const int32_t* __restrict__ block_pre, const DevPlan* __restrict__ plan,
-                const RowTargets targets, uint32_t* __restrict__ row_code) {
+                const __grid_constant__ RowTargets targets, uint32_t* __restrict__ row_code,
+                const __grid_constant__ PeerSignal sig) {
   __shared__ uint32_t codes[32 * K];
-  // the block's prefix row and the plan tables the ranking loop reads, staged
-  // once (coalesced) so the per-expert loop below never waits on L2
+  // the block's prefix row and the plan tables the ranking reads, staged once
+  // (coalesced) so the ranking never waits on L2
   __shared__ int s_pre[kMaxExperts], s_n[kMaxExperts], s_rbase[kMaxExperts + 1];
+  __shared__ uint32_t s_mask[kMaxExperts];  // tokens of this block that chose expert e
   __shared__ int s_rrow[kMaxReplicas];
   __shared__ unsigned char s_rrem[kMaxReplicas];
   __shared__ __nv_bfloat16* s_tgt[kMaxTargets];
@@ -92,69 +96,102 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
     s_pre[i] = block_pre[(size_t)b * E + i];
     s_n[i] = plan->n_e[i];
     s_rbase[i] = plan->rep_base[i];
+    s_mask[i] = 0u;
   }
   if (threadIdx.x == 0) s_rbase[E] = plan->rep_base[E];
   for (int i = threadIdx.x; i < R; i += blockDim.x) {
     s_rrow[i] = plan->rep_row_base[i];
     s_rrem[i] = static_cast<unsigned char>(plan->rep_remote[i]);
   }
-  if (threadIdx.x < kMaxTargets) s_tgt[threadIdx.x] = static_cast<__nv_bfloat16*>(targets.base[threadIdx.x]);
+#pragma unroll
+  for (int i = 0; i < kMaxTargets; ++i)  // constant indices: the table stays in parameter space
+    if (threadIdx.x == i) s_tgt[i] = static_cast<__nv_bfloat16*>(targets.base[i]);
   __syncthreads();
 
   if (warp == 0) {
+    // stable rank of (token, expert) inside the block = number of EARLIER
+    // tokens of the block that chose the same expert: one bit per token
     const int t = t_base + lane;
     const bool live = lane < ntok;
     int my[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) my[j] = live ? ids[(size_t)t * K + j] : -1;
-    const uint32_t lt = (1u << lane) - 1u;
-    for (int e = 0; e < E; ++e) {
-      int slot = -1;
 #pragma unroll
-      for (int j = 0; j < K; ++j)
-        if (my[j] == e) slot = j;
-      const uint32_t m = __ballot_sync(0xffffffffu, slot >= 0);
-      if (m == 0) continue;
-      if (slot >= 0) {
-        const int gr = s_pre[e] + __popc(m & lt);
+    for (int j = 0; j < K; ++j)
+      if (live) atomicOr(&s_mask[my[j]], 1u << lane);
+    __syncwarp();
+    const uint32_t lt = (1u << lane) - 1u;
+    if (live) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const int e = my[j];
+        const int gr = s_pre[e] + __popc(s_mask[e] & lt);
         // integer replica split: replica r owns floor(n/R) + [r < n mod R] ranks
-        const int n = s_n[e], Re = s_rbase[e + 1] - s_rbase[e];
-        const int q = n / Re, rem = n % Re;
-        const int r = gr < rem * (q + 1) ? gr / (q + 1) : rem + (gr - rem * (q + 1)) / q;
+        const int Re = s_rbase[e + 1] - s_rbase[e];
+        int r = 0;
+        if (Re > 1) {
+          const int n = s_n[e], q = n / Re, rem = n % Re;
+          r = gr < rem * (q + 1) ? gr / (q + 1) : rem + (gr - rem * (q + 1)) / q;
+        }
         const int f = s_rbase[e] + r;
-        const uint32_t code = static_cast<uint32_t>(s_rrow[f] + gr) | (static_cast<uint32_t>(s_rrem[f]) << kTargetShift);
-        codes[lane * K + slot] = code;
-        if (blockIdx.y == 0) row_code[(size_t)t * K + slot] = code;
+        const uint32_t code =
+            static_cast<uint32_t>(s_rrow[f] + gr) | (static_cast<uint32_t>(s_rrem[f]) << kTargetShift);
+        codes[lane * K + j] = code;
+        if (blockIdx.y == 0) row_code[(size_t)t * K + j] = code;
       }
     }
   }
   __syncthreads();
 
-  // stream rows: each warp copies tokens warp, warp+4, ...; the row's 16-byte
-  // chunks are split over gridDim.y CTAs (small batches: decode keeps every
-  // SM busy; the ranking above is recomputed per split, it is a few ballots)
+  // stream rows: this CTA covers 16-byte chunks [c_begin, c_end) of every
+  // token row of the block (rows split over gridDim.y CTAs for small
+  // batches).  (token, chunk) items are spread over all threads and U loads
+  // are issued before any store, so the copy pays one memory latency per U
+  // items instead of one per token.
   const int chunks_all = d / 8;
   const int per = (chunks_all + gridDim.y - 1) / gridDim.y;
-  const int c_begin = blockIdx.y * per, chunks = min(chunks_all, c_begin + per);
-  for (int i = warp; i < ntok; i += 4) {
-    const __nv_bfloat16* src = x + (size_t)(t_base + i) * d;
-    __nv_bfloat16* dst[K];
+  const int c_begin = blockIdx.y * per, c_end = min(chunks_all, c_begin + per);
+  const int nch = max(0, c_end - c_begin);
+  const int items = ntok * nch;
+  constexpr int U = 4;
+  for (int i0 = threadIdx.x; i0 < items; i0 += blockDim.x * U) {
+    int4 v[U];
+    int tok[U], ch[U];
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      const uint32_t c = codes[i * K + j];
-      dst[j] = s_tgt[c >> kTargetShift] + (size_t)(c & kRowMask) * d;  // local, send buffer or a peer's rows
+    for (int u = 0; u < U; ++u) {
+      const int it = i0 + u * blockDim.x;
+      tok[u] = it / nch;
+      ch[u] = c_begin + (it - tok[u] * nch);
+      if (it < items) v[u] = ld_nc_v4(x + (size_t)(t_base + tok[u]) * d + (size_t)ch[u] * 8);
     }
-    for (int c0 = c_begin + lane; c0 < chunks; c0 += 32 * 4) {
-      int4 v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c0 + 32 * u < chunks) v[u] = ld_nc_v4(src + (size_t)(c0 + 32 * u) * 8);
+    for (int u = 0; u < U; ++u) {
+      if (i0 + u * blockDim.x >= items) break;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c0 + 32 * u < chunks) {
+      for (int j = 0; j < K; ++j) {
+        const uint32_t c = codes[tok[u] * K + j];
+        // local rows, the NCCL send buffer or a peer's received rows
+        st_v4(s_tgt[c >> kTargetShift] + (size_t)(c & kRowMask) * d + (size_t)ch[u] * 8, v[u]);
+      }
+    }
+  }
+  if (sig.G > 0) {
+    // peer memory: every thread's remote stores are performed system-wide
+    // before its CTA counts itself done; the last CTA publishes the epoch
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned total = gridDim.x * gridDim.y;
+      if (atomicAdd(sig.counter, 1u) == total - 1) {
+        *sig.counter = 0u;
+        __threadfence_system();
 #pragma unroll
-          for (int j = 0; j < K; ++j) st_v4(dst[j] + (size_t)(c0 + 32 * u) * 8, v[u]);
-        }
+        for (int g = 0; g < 8; ++g)
+          if (g < sig.G)
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig.flags[g] + sig.kind * 8 + sig.src),
+                         "r"(sig.epoch)
+                         : "memory");
+      }
     }
   }
 }
@@ -162,10 +199,12 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
 // -------------------------------------------------------------- combine
 template <int K>
 __global__ void __launch_bounds__(256)
-combine_kernel(const RowTargets sources, int T, int d, const uint32_t* __restrict__ row_code,
+combine_kernel(const __grid_constant__ RowTargets sources, int T, int d, const uint32_t* __restrict__ row_code,
                const float* __restrict__ wts, __nv_bfloat16* __restrict__ y) {
   __shared__ const __nv_bfloat16* s_src[kMaxTargets];
-  if (threadIdx.x < kMaxTargets) s_src[threadIdx.x] = static_cast<const __nv_bfloat16*>(sources.base[threadIdx.x]);
+#pragma unroll
+  for (int i = 0; i < kMaxTargets; ++i)
+    if (threadIdx.x == i) s_src[i] = static_cast<const __nv_bfloat16*>(sources.base[i]);
   __syncthreads();
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -296,14 +335,14 @@ cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, co
 
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
                             const int32_t* block_pre, const DevPlan* plan, const RowTargets& targets,
-                            uint32_t* row_code, cudaStream_t s) {
+                            uint32_t* row_code, const PeerSignal& sig, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   if (d % 8) return cudaErrorInvalidValue;
   const int nblk = (T + 31) / 32;
   // at least ~2 CTAs per SM: split each row's chunks when there are few blocks
-  const int split = std::max(1, std::min((2 * 148 + nblk - 1) / nblk, d / 8 / 32));
+  const int split = std::max(1, std::min((2 * 148 + nblk - 1) / nblk, d / 8 / 16));
   const dim3 grid(nblk, split);
-  MOE_SWITCH_K(k, (dispatch_kernel<KK><<<grid, 128, 0, s>>>(x, T, d, E, ids, block_pre, plan, targets, row_code)));
+  MOE_SWITCH_K(k, (dispatch_kernel<KK><<<grid, 128, 0, s>>>(x, T, d, E, ids, block_pre, plan, targets, row_code, sig)));
   return cudaGetLastError();
 }
 

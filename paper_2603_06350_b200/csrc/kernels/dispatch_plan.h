@@ -22,6 +22,15 @@ struct RowTargets {
   void* base[kMaxTargets];
 };
 
+// Peer-memory exchange: after its last row store, the dispatch grid publishes
+// `epoch` in flags[g][kind * 8 + src] of every rank g (G == 0: no signal).
+struct PeerSignal {
+  uint32_t* flags[8];
+  uint32_t* counter;  // CTAs finished (self-resetting)
+  int G, src, kind;
+  uint32_t epoch;
+};
+
 // One GEMM segment = the rows of one replica placed on this rank.
 struct GemmSeg {
   int row_start;  // first row in the received (permuted) buffer

@@ -167,11 +167,13 @@ __global__ void swiglu_f32_kernel(const float* __restrict__ C, int rows, int ff,
   }
 }
 
-__global__ void combine_f32_kernel(const RowTargets sources, int T, int d, int k,
+__global__ void combine_f32_kernel(const __grid_constant__ RowTargets sources, int T, int d, int k,
                                    const uint32_t* __restrict__ row_code, const float* __restrict__ wts,
                                    float* __restrict__ y) {
   __shared__ const float* s_src[kMaxTargets];
-  if (threadIdx.x < kMaxTargets) s_src[threadIdx.x] = static_cast<const float*>(sources.base[threadIdx.x]);
+#pragma unroll
+  for (int i = 0; i < kMaxTargets; ++i)
+    if (threadIdx.x == i) s_src[i] = static_cast<const float*>(sources.base[i]);
   __syncthreads();
   const size_t n = (size_t)T * d;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {

@@ -91,17 +91,22 @@ __device__ __forceinline__ void warp_topk(const float* row, int base, int E, int
   }
 }
 
-// top-k, softmax and histograms for one 32-token block whose stacked logits
-// sit in shared memory (row stride LD); warp w handles tokens 4w .. 4w+3.
-template <int LD>
-__device__ __forceinline__ void select_and_count(const float* red, int* hist, int blk, int T, int E, int n_pred,
-                                                 int k, int32_t* __restrict__ ids, float* __restrict__ wts,
-                                                 int32_t* __restrict__ counts, int32_t* __restrict__ block_counts,
+// top-k, softmax and histograms for `ntok` tokens of one 32-token block,
+// starting at token tok0 of the block, whose stacked logits sit in shared
+// memory (row stride LD, row 0 = tok0); warp w handles ntok / kWarps tokens.
+// ACCUM: the block's histogram row is shared with other CTAs (atomic adds
+// into a zeroed row) instead of being written whole.
+template <int LD, bool ACCUM>
+__device__ __forceinline__ void select_and_count(const float* red, int* hist, int blk, int tok0, int ntok, int T,
+                                                 int E, int n_pred, int k, int32_t* __restrict__ ids,
+                                                 float* __restrict__ wts, int32_t* __restrict__ counts,
+                                                 int32_t* __restrict__ block_counts,
                                                  int32_t* __restrict__ pred_counts) {
   const int warp = threadIdx.x >> 5, lane = lane_id();
-  for (int q = 0; q < kBlockTokens / kWarps; ++q) {
-    const int lt = warp * (kBlockTokens / kWarps) + q;
-    const int t = blk * kBlockTokens + lt;
+  const int per = ntok / kWarps;
+  for (int q = 0; q < per; ++q) {
+    const int lt = warp * per + q;
+    const int t = blk * kBlockTokens + tok0 + lt;
     if (t >= T) break;
     const float* row = red + lt * LD;
     for (int gi = 0; gi <= n_pred; ++gi) {
@@ -132,7 +137,11 @@ __device__ __forceinline__ void select_and_count(const float* red, int* hist, in
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     const int h = hist[e];
-    block_counts[(size_t)blk * E + e] = h;
+    if (ACCUM) {
+      if (h) atomicAdd(block_counts + (size_t)blk * E + e, h);
+    } else {
+      block_counts[(size_t)blk * E + e] = h;
+    }
     if (h) atomicAdd(counts + e, h);
   }
 }
@@ -204,13 +213,22 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_b
   if (gridDim.y > 1) {
     float* dst = partial + ((size_t)blockIdx.y * gridDim.x + blk) * kBlockTokens * kCols;
     for (int i = threadIdx.x; i < kBlockTokens * kCols; i += blockDim.x) dst[i] = red[(i / kCols) * kLd + i % kCols];
+    // the finishing CTAs add into the block's histogram row
+    if (blockIdx.y == 0)
+      for (int e = threadIdx.x; e < E; e += blockDim.x) block_counts[(size_t)blk * E + e] = 0;
     return;
   }
-  select_and_count<kLd>(red, hist, blk, T, E, n_pred, k, ids, wts, counts, block_counts, pred_counts);
+  select_and_count<kLd, false>(red, hist, blk, 0, kBlockTokens, T, E, n_pred, k, ids, wts, counts, block_counts,
+                               pred_counts);
 }
 
-// Sums the split-K partial logits of one 32-token block in slice order
-// (deterministic), then top-k / softmax / histograms as in the fused kernel.
+// Sums the split-K partial logits of kFinishTokens tokens of one 32-token
+// block in slice order (deterministic; all slices are loaded before the
+// first add, so the sum costs one memory latency, not `splits`), then top-k /
+// softmax / histograms as in the fused kernel, one token per warp.
+constexpr int kFinishTokens = kWarps;
+constexpr int kMaxSplits = 16;
+
 template <int NT>
 __global__ void __launch_bounds__(kWarps * 32)
 gate_finish_kernel(const float* __restrict__ partial, int splits, int T, int E, int n_pred, int k,
@@ -218,17 +236,26 @@ gate_finish_kernel(const float* __restrict__ partial, int splits, int T, int E, 
                    int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts) {
   constexpr int kCols = 8 * NT;
   constexpr int kLd = kCols + 4;
-  __shared__ float red[kBlockTokens * kLd];
+  __shared__ float red[kFinishTokens * kLd];
   __shared__ int hist[256];
-  const int blk = blockIdx.x;
+  const int blk = blockIdx.x, tok0 = blockIdx.y * kFinishTokens;
+  const int nblk = gridDim.x;
   for (int i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
-  for (int i = threadIdx.x; i < kBlockTokens * kCols; i += blockDim.x) {
-    float v = 0.0f;
-    for (int s = 0; s < splits; ++s) v += partial[((size_t)s * gridDim.x + blk) * kBlockTokens * kCols + i];
-    red[(i / kCols) * kLd + i % kCols] = v;
+  for (int i = threadIdx.x; i < kFinishTokens * kCols; i += blockDim.x) {
+    const float* src = partial + ((size_t)blk * kBlockTokens + tok0) * kCols + i;
+    const size_t slice_stride = (size_t)nblk * kBlockTokens * kCols;
+    float v[kMaxSplits];
+#pragma unroll
+    for (int s = 0; s < kMaxSplits; ++s) v[s] = s < splits ? __ldcg(src + s * slice_stride) : 0.0f;
+    float acc = v[0];
+#pragma unroll
+    for (int s = 1; s < kMaxSplits; ++s)
+      if (s < splits) acc += v[s];
+    red[(i / kCols) * kLd + i % kCols] = acc;
   }
   __syncthreads();
-  select_and_count<kLd>(red, hist, blk, T, E, n_pred, k, ids, wts, counts, block_counts, pred_counts);
+  select_and_count<kLd, true>(red, hist, blk, tok0, kFinishTokens, T, E, n_pred, k, ids, wts, counts, block_counts,
+                              pred_counts);
 }
 
 int gate_num_blocks(int T) { return (T + kBlockTokens - 1) / kBlockTokens; }
@@ -264,7 +291,8 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
     gate_topk_kernel<NT_><<<grid, block, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,       \
                                                       block_counts, pred_counts, partial);                 \
     if (splits > 1)                                                                                         \
-      gate_finish_kernel<NT_><<<nblk, block, 0, stream>>>(partial, splits, T, E, n_pred, k, ids, wts,       \
+      gate_finish_kernel<NT_><<<dim3(nblk, kBlockTokens / kFinishTokens), block, 0, stream>>>(              \
+          partial, splits, T, E, n_pred, k, ids, wts,                                                       \
                                                           counts, block_counts, pred_counts);               \
     return cudaGetLastError();                                                                              \
   }

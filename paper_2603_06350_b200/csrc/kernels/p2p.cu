@@ -81,7 +81,8 @@ __device__ __forceinline__ void wait_all(const uint32_t* my_flags, int G, int ki
   }
 }
 
-__global__ void __launch_bounds__(32) p2p_signal_kernel(PeerSlabs peers, int G, int kind, int src, uint32_t epoch) {
+__global__ void __launch_bounds__(32)
+p2p_signal_kernel(const __grid_constant__ PeerSlabs peers, int G, int kind, int src, uint32_t epoch) {
   signal_all(peers, G, kind, src, epoch);
 }
 
@@ -91,9 +92,9 @@ __global__ void __launch_bounds__(32) p2p_wait_kernel(const uint32_t* my_flags, 
 }
 
 // signal + wait + gather: counts_all[g][:] = rank g's histogram (stride ints)
-__global__ void __launch_bounds__(256) p2p_counts_kernel(PeerSlabs peers, int G, int rank, int stride,
-                                                         uint32_t epoch, uint64_t timeout_ns, int* err,
-                                                         int32_t* __restrict__ counts_all) {
+__global__ void __launch_bounds__(256)
+p2p_counts_kernel(const __grid_constant__ PeerSlabs peers, int G, int rank, int stride, uint32_t epoch,
+                  uint64_t timeout_ns, int* err, int32_t* __restrict__ counts_all) {
   if (threadIdx.x < 32) {
     signal_all(peers, G, kFlagCounts, rank, epoch);
     wait_all(peers.flags[rank], G, kFlagCounts, epoch, timeout_ns, err);
