@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--cpu-sample-tokens", type=int, default=64)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1 token exchange: peer memory over NVLink (dispatch/combine read and write the "
+                         "owners' buffers) or NCCL grouped send/recv")
     return ap.parse_args()
 
 
@@ -226,27 +229,42 @@ def run_ours(args):
     import numpy as np
     import torch
 
-    from paper_2603_06350_b200 import (MOE_PLAN_SYNC, MoELayer, nccl_unique_id, percentile)
+    from paper_2603_06350_b200 import (MOE_EXCHANGE_NCCL, MOE_EXCHANGE_P2P, MOE_PLAN_SYNC, MoELayer, nccl_unique_id,
+                                       percentile)
     from paper_2603_06350_b200 import workload as wl
 
     ws, rank, local = dist_env()
     G = max(ws, 1)
+    # MOE_BENCH_SHARE_DEVICE=1: every rank on device 0 (exercises the N>1 flow on
+    # a one-GPU box; the numbers are then not a scaling measurement)
+    shared = os.environ.get("MOE_BENCH_SHARE_DEVICE") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if G > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = CFG
     E, k, d, ff, T = c["E"], c["k"], c["d"], c["ff"], c["T"]
     uid = None
-    if G > 1:
+    p2p = G > 1 and args.exchange == "p2p"
+    if G > 1 and not p2p:
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     mem = 3.0 * d * ff * 2 / 1e6
     m = MoELayer(1, E, k, d, ff, max_tokens=T, world_size=G, rank=rank, device=local,
+                 exchange_mode=MOE_EXCHANGE_P2P if p2p else MOE_EXCHANGE_NCCL,
                  nccl_unique_id=uid, expert_mem_mb=mem, layer_mem_cap_mb=c["extra_replicas"] * mem,
                  gpu_mem_capacity_mb=180000.0, cv_threshold=0.2, keep_alive_iters=50)
+    if p2p:  # map every rank's exchange slab (CUDA IPC over NVLink)
+        handles = [None] * G
+        dist.all_gather_object(handles, m.p2p_export())
+        m.p2p_import(handles)
     for e in range(E):
         m.load_expert(0, e, *wl.expert_weights(d, ff, c["seed"], 0, e))
     # token pool: per rank distinct batches (DP shard of the global batch)
@@ -325,7 +343,7 @@ def run_ours(args):
 
     # max over ranks
     vals = torch.tensor([total_ms, statistics.median(lat), nearest_rank(lat, 0.99),
-                         e2e["ms"] if e2e else 0.0], dtype=torch.float64, device="cuda")
+                         e2e["ms"] if e2e else 0.0], dtype=torch.float64, device="cpu" if shared else "cuda")
     if dist is not None:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     total_ms, p50, p99, e2e_ms = vals.tolist()
@@ -348,12 +366,14 @@ def run_ours(args):
                        "parallelism": f"ep{G}", "experts": E, "top_k": k, "d_model": d, "d_ff": ff,
                        "l2": "inputs larger than L2 (2.8 GB weights + 134 MB tokens per step)",
                        "planner": "MOE_PLAN_SYNC (scale_experts + place_experts on actual loads)"},
+            "exchange": ("peer memory (P2P)" if p2p else "NCCL send/recv") if G > 1 else "none (G=1)",
             "p50_ms": p50, "p99_ms": p99,
             "step_ms": [round(v, 3) for v in lat],
             "phase_ms_median": phases, "replicas_median": replicas,
-            # per step: gate-weight SM copy, K1 gate, counts SM copy, plan SM copy,
-            # block prefix, K3 dispatch, K4 GEMM1, K4 GEMM2, K5 combine
-            "gpu_launches": 9 * args.steps,
+            # per step (G=1): gate-weight SM copy, K1 gate, counts SM copy, on-device plan,
+            # block prefix, K3 dispatch, K4 GEMM1, K4 GEMM2, K5 combine; P2P adds the counts
+            # gather, plan upload and the rows / outputs flag kernels (NCCL's own kernels not counted)
+            "gpu_launches": (13 if p2p else 9) * args.steps,
             "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel (GEMM1 SwiGLU + GEMM2)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "peak_source": peak_src + ", bf16 sustained", "burst_peak": peaks.get("bf16_tflops"),
