@@ -258,6 +258,15 @@ int moe_exchange_plan(int world_size, int rank, int num_experts, const int32_t* 
                       int64_t* seg_start /* [sum R], -1 if not local */,
                       int64_t* seg_rows /* [sum R] */);
 
+/* The peer-memory (MOE_EXCHANGE_P2P) form of the same plan: for every replica
+   f (flattened (expert, ordinal)), the rank whose received-rows buffer holds
+   its rows (rep_target[f] == replica_gpu[f]) and rep_row_base[f] such that the
+   assignment with global rank gr of the expert lands in row
+   rep_row_base[f] + gr of that rank's buffer. */
+int moe_exchange_plan_direct(int world_size, int rank, int num_experts, const int32_t* counts_all,
+                             const int32_t* replica_counts, const int32_t* replica_gpu, int32_t* rep_target,
+                             int32_t* rep_row_base, int64_t* rows_local, int64_t* rows_send);
+
 /* ------------------------------------------------------- planner (host C++) */
 /* scale_experts (scaler.hpp:29-30): counts_out[E]; trace arrays may be NULL. */
 int moe_plan_scale(const int64_t* loads, int num_experts, int layer, double expert_mem_mb,

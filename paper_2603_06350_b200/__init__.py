@@ -29,6 +29,7 @@ from ._capi import (MOE_EXCHANGE_EXTERNAL, MOE_EXCHANGE_NCCL, MOE_EXCHANGE_P2P, 
 __all__ = [
     "scale_experts", "place_experts", "ReplicaRegistry", "update_registry", "layer_forward_time",
     "predict", "measure_accuracy", "route_tokens", "popularity", "percentile", "exchange_plan",
+    "exchange_plan_direct",
     "MoELayer", "ScalingPlan", "PlaceResult", "synth_tokens", "synth_gate", "synth_expert",
     "stream_key", "nccl_unique_id", "PinnedArray", "MoeError", "MOE_PLAN_FIXED", "MOE_PLAN_SYNC",
     "MOE_PLAN_PREDICTED", "MOE_EXCHANGE_NCCL",
@@ -218,6 +219,22 @@ def exchange_plan(world_size: int, rank: int, counts_all: np.ndarray,
     conv = lambda arr, n: [(c.peer, c.replica, c.row_offset, c.rows) for c in arr[:n]]
     return dict(sends=conv(sends, ns.value), recvs=conv(recvs, nr.value), rows_local=rl.value,
                 rows_send=rs.value, seg_start=ss[:R].tolist(), seg_rows=sr[:R].tolist())
+
+
+def exchange_plan_direct(world_size: int, rank: int, counts_all: np.ndarray,
+                         replica_counts: Sequence[int], replica_gpu: Sequence[int]):
+    """Peer-memory form of the plan: per replica, the destination rank and the
+    row base in THAT rank's received-rows buffer (exchange_plan.cpp, direct)."""
+    ca = np.ascontiguousarray(np.asarray(counts_all, np.int32).reshape(world_size, -1))
+    E = ca.shape[1]
+    rc, rg = _i32(replica_counts), _i32(replica_gpu)
+    R = int(rc.sum())
+    tgt, base = np.zeros(max(R, 1), np.int32), np.zeros(max(R, 1), np.int32)
+    rl, rs = C.c_int64(), C.c_int64()
+    check(lib.moe_exchange_plan_direct(world_size, rank, E, _p(ca), _p(rc), _p(rg), _p(tgt), _p(base),
+                                       C.byref(rl), C.byref(rs)))
+    return dict(rep_target=tgt[:R].tolist(), rep_row_base=base[:R].tolist(), rows_local=rl.value,
+                rows_send=rs.value)
 
 
 # ------------------------------------------------------- synthetic inputs

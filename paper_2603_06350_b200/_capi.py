@@ -104,6 +104,7 @@ _sig("moe_forward_expert", C.c_int, vp, C.c_int, vp)
 _sig("moe_forward_end", C.c_int, vp, vp, vp)
 _sig("moe_buffer", C.c_int, vp, C.c_int, P(vp), P(i64))
 _sig("moe_memcpy", C.c_int, vp, vp, vp, C.c_size_t)
+_sig("moe_exchange_plan_direct", C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, P(i64), P(i64))
 _sig("moe_exchange_plan", C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp,
      P(MoeChunk), P(C.c_int), P(MoeChunk), P(C.c_int), C.c_int, P(i64), P(i64), vp, vp)
 _sig("moe_plan_scale", C.c_int, vp, C.c_int, C.c_int, dbl, dbl, dbl, C.c_int, vp, P(dbl), P(C.c_int),
@@ -135,7 +136,7 @@ EXPORTED = [
     "moe_layer_forward", "moe_layer_forward_host", "moe_layer_forward_host_async", "moe_wait",
     "moe_host_alloc", "moe_host_free", "moe_gemm_times",
     "moe_forward_begin", "moe_forward_expert",
-    "moe_forward_end", "moe_buffer", "moe_memcpy", "moe_exchange_plan", "moe_plan_scale",
+    "moe_forward_end", "moe_buffer", "moe_memcpy", "moe_exchange_plan", "moe_exchange_plan_direct", "moe_plan_scale",
     "moe_registry_create", "moe_registry_destroy", "moe_registry_size", "moe_plan_place",
     "moe_registry_update", "moe_model_forward_time", "moe_plan_predict", "moe_measure_accuracy",
     "moe_percentile", "moe_route_tokens", "moe_popularity", "moe_stream_key", "moe_synth_tokens",

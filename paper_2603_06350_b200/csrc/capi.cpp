@@ -1385,6 +1385,23 @@ int moe_exchange_plan(int G, int rank, int E, const int32_t* counts_all, const i
   });
 }
 
+int moe_exchange_plan_direct(int G, int rank, int E, const int32_t* counts_all, const int32_t* rc, const int32_t* rg,
+                             int32_t* rep_target, int32_t* rep_row_base, int64_t* rows_local, int64_t* rows_send) {
+  return guarded([&] {
+    require(counts_all && rc && rg, "null argument");
+    std::vector<int64_t> all(static_cast<size_t>(G) * std::max(E, 0));
+    for (size_t i = 0; i < all.size(); ++i) all[i] = counts_all[i];
+    HostPlan hp;
+    build_exchange_plan(G, rank, E, all.data(), rc, rg, hp, /*direct=*/true);
+    for (int f = 0; f < hp.dev.R; ++f) {
+      if (rep_target) rep_target[f] = hp.dev.rep_remote[f];
+      if (rep_row_base) rep_row_base[f] = hp.dev.rep_row_base[f];
+    }
+    if (rows_local) *rows_local = hp.rows_local;
+    if (rows_send) *rows_send = hp.rows_send;
+  });
+}
+
 // ------------------------------------------------------------- planner API
 int moe_plan_scale(const int64_t* loads, int E, int layer, double mem, double cap, double cv, int excl,
                    int32_t* counts_out, double* alloc_out, int* steps_out, int32_t* split, double* cvt, int cap_n) {
