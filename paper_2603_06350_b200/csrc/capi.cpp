@@ -55,13 +55,16 @@ struct PeerSlabs {
   uint32_t* flags[kMaxRanks];
   const int32_t* counts[kMaxRanks];
 };
-cudaError_t launch_p2p_signal(const PeerSlabs& peers, int G, int kind, int src, uint32_t epoch, cudaStream_t s);
-cudaError_t launch_p2p_wait(const uint32_t* my_flags, int G, int kind, uint32_t epoch, uint64_t timeout_ns, int* err,
-                            cudaStream_t s);
-cudaError_t launch_p2p_counts(const PeerSlabs& peers, int G, int rank, int stride, uint32_t epoch,
+cudaError_t launch_p2p_signal(const PeerSlabs& peers, int G, int kind, int src, const uint32_t* epoch,
+                              cudaStream_t s);
+cudaError_t launch_p2p_wait(const uint32_t* my_flags, int G, int kind, const uint32_t* epoch, uint64_t timeout_ns,
+                            int* err, cudaStream_t s);
+cudaError_t launch_p2p_counts(const PeerSlabs& peers, int G, int rank, int stride, uint32_t* epoch,
                               uint64_t timeout_ns, int* err, int32_t* counts_all, cudaStream_t s);
 cudaError_t launch_small_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
 cudaError_t launch_plan_local(const int32_t* counts, int E, DevPlan* plan, cudaStream_t s);
+cudaError_t launch_plan_exchange(const int32_t* counts_all, int stride, int G, int rank, const PlacementTable* pt,
+                                 DevPlan* plan, cudaStream_t s);
 // K7 fp32 path
 cudaError_t launch_gate_f32(const float* x, int T, int d, const float* wg, int E, int k, int32_t* ids, float* wts,
                             int32_t* counts, int32_t* block_counts, cudaStream_t s);
@@ -82,6 +85,11 @@ cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUten
 cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                 __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream);
+cudaError_t preload_gate_kernels();
+cudaError_t preload_dispatch_kernels();
+cudaError_t preload_gemm_kernels();
+cudaError_t preload_fp32_kernels();
+cudaError_t preload_p2p_kernels();
 // host
 uint64_t stream_key(uint64_t seed, uint64_t a, uint64_t b, uint64_t tag);
 void synth_tokens(uint64_t key, int64_t first, int64_t tokens, int d, int E, uint16_t* x);
@@ -129,6 +137,7 @@ int guarded(F&& f) {
 
 constexpr size_t pad16(size_t b) { return (b + 15) & ~size_t(15); }
 static_assert(sizeof(DevPlan) % 16 == 0, "DevPlan is copied in 16-byte words");
+static_assert(sizeof(PlacementTable) % 16 == 0, "PlacementTable is copied in 16-byte words");
 
 void require(bool ok, const std::string& msg) {
   if (!ok) throw std::invalid_argument(msg);
@@ -250,6 +259,10 @@ struct Layer {
   int plan_source = 0;                      // 0 fixed, 1 actual, 2 predicted, 3 historical bootstrap
   int warm = 0, cold = 0;
   std::vector<moeless::LoadVector> history;
+  // device copy of the placement for the on-device exchange planner (P2P)
+  DevBuf<PlacementTable> ptab;
+  PlacementTable* h_ptab = nullptr;  // pinned staging
+  cudaEvent_t ev_ptab = nullptr;     // staging buffer free again
 };
 
 struct GraphKey {
@@ -257,8 +270,9 @@ struct GraphKey {
   const void* x;
   const void* y;
   cudaEvent_t x_consumed;
+  bool pred;
   bool operator<(const GraphKey& o) const {
-    return std::tie(layer, T, x, y, x_consumed) < std::tie(o.layer, o.T, o.x, o.y, o.x_consumed);
+    return std::tie(layer, T, x, y, x_consumed, pred) < std::tie(o.layer, o.T, o.x, o.y, o.x_consumed, o.pred);
   }
 };
 
@@ -267,6 +281,7 @@ struct PendingPlan {
   int layer = 0, mode = 0;
   long iteration = 0;
   int stride = 0;
+  int gemm_slot = -1;  // K4 timing-ring slot whose row count the host plan fills in
 };
 
 struct EventSet {
@@ -350,7 +365,7 @@ struct moe_ctx {
   std::vector<void*> ipc_opened;  // peer slabs opened with cudaIpcOpenMemHandle
   PeerSlabs peers{};
   RowTargets xp_targets{}, yp_targets{};  // rank g -> g's xp / yp
-  uint32_t epoch = 0;                      // forwards issued; the flag value of the current one
+  DevBuf<uint32_t> epoch_dev;              // the current forward's epoch (device; counts kernel increments)
   int* p2p_err = nullptr;                  // mapped pinned: first timed-out wait (1 + kind*8 + rank)
   DevBuf<uint32_t> dispatch_counter;       // CTAs of the signalling dispatch grid that finished
   uint64_t p2p_timeout_ns = 10000000000ull;
@@ -370,6 +385,46 @@ void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, 
                             reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, pred_counts ? c->n_pred : 0,
                             c->k, c->ids.p, c->wts.p, c->counts.p, c->block_counts.p,
                             pred_counts ? pred_counts : c->pred_counts.p, c->gate_partial.p, s));
+}
+
+// The placement changed (planner, moe_set_placement or default): refresh the
+// device copy the on-device exchange planner reads (peer-memory contexts).
+void placement_changed(moe_ctx* c, int layer) {
+  Layer& L = c->layers[layer];
+  L.has_placement = true;
+  if (!c->p2p) return;
+  const int R = static_cast<int>(L.rep_gpu.size());
+  if (R > kMaxReplicas) throw std::invalid_argument("too many replicas in one layer");
+  if (!L.ptab.p) {
+    L.ptab.alloc(1);
+    CU_CHECK(cudaHostAlloc(&L.h_ptab, sizeof(PlacementTable), cudaHostAllocMapped));
+    CU_CHECK(cudaEventCreateWithFlags(&L.ev_ptab, cudaEventDisableTiming));
+  } else {
+    CU_CHECK(cudaEventSynchronize(L.ev_ptab));  // the previous upload has left the staging copy
+  }
+  PlacementTable& t = *L.h_ptab;
+  t.E = c->E;
+  t.R = R;
+  int f = 0;
+  for (int e = 0; e < c->E; ++e) {
+    t.rep_base[e] = f;
+    for (int r = 0; r < L.rep_counts[e]; ++r, ++f) t.expert_of[f] = e;
+  }
+  t.rep_base[c->E] = f;
+  for (int i = 0; i < R; ++i) t.gpu_of[i] = L.rep_gpu[i];
+  // SM copy from mapped memory: never queues behind bulk token copies
+  CU_CHECK(launch_small_copy(L.ptab.p, L.h_ptab, sizeof(PlacementTable), c->stream));
+  CU_CHECK(cudaEventRecord(L.ev_ptab, c->stream));
+}
+
+// default: one replica per expert, expert e on GPU e mod G (static_plan, baselines.cpp:32-60)
+void ensure_placement(moe_ctx* c, int layer) {
+  Layer& L = c->layers[layer];
+  if (L.has_placement) return;
+  L.rep_counts.assign(c->E, 1);
+  L.rep_gpu.resize(c->E);
+  for (int e = 0; e < c->E; ++e) L.rep_gpu[e] = e % c->G;
+  placement_changed(c, layer);
 }
 
 // Decide the placement for this forward (host), then build + upload the plan.
@@ -397,7 +452,7 @@ void plan_layer(moe_ctx* c, int layer, const std::vector<int64_t>& loads, long i
   L.rep_counts.assign(sp.replica_counts.begin(), sp.replica_counts.end());
   L.rep_gpu.clear();
   for (auto& v : pr.placement.gpu_for) L.rep_gpu.insert(L.rep_gpu.end(), v.begin(), v.end());
-  L.has_placement = true;
+  placement_changed(c, layer);
 }
 
 // buf: [G][stride] int32 from the gate — per rank, E actual counts followed by
@@ -437,12 +492,8 @@ void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int3
     ++L.bootstraps;
   } else if (plan_mode == MOE_PLAN_PREDICTED) {
     L.plan_source = 2;  // placement made d layers ago from the predictor
-  } else if (!L.has_placement) {
-    // default: one replica per expert, expert e on GPU e mod G (static_plan, baselines.cpp:32-60)
-    L.rep_counts.assign(c->E, 1);
-    L.rep_gpu.resize(c->E);
-    for (int e = 0; e < c->E; ++e) L.rep_gpu[e] = e % c->G;
-    L.has_placement = true;
+  } else {
+    ensure_placement(c, layer);
   }
   // plan layer + d from this layer's predictor histogram (the MoEless
   // layer-aware predictor: plan ahead, evaluate on the actual loads)
@@ -480,7 +531,7 @@ void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool u
       sig.G = c->G;
       sig.src = c->rank;
       sig.kind = kFlagRows;
-      sig.epoch = c->epoch;
+      sig.epoch = c->epoch_dev.p;
     }
   } else {
     t.base[0] = c->xp.p;
@@ -501,8 +552,9 @@ void stage_exchange(moe_ctx* c, bool forward, cudaStream_t s) {
     const int kind = forward ? kFlagRows : kFlagOutputs;
     // the rows signal is fused into the dispatch kernel (a rank without tokens
     // launches no dispatch and signals here)
-    if (!forward || c->cur_T == 0) CU_CHECK(launch_p2p_signal(c->peers, c->G, kind, c->rank, c->epoch, s));
-    CU_CHECK(launch_p2p_wait(c->peers.flags[c->rank], c->G, kind, c->epoch, c->p2p_timeout_ns, c->p2p_err, s));
+    if (!forward || c->cur_T == 0)
+      CU_CHECK(launch_p2p_signal(c->peers, c->G, kind, c->rank, c->epoch_dev.p, s));
+    CU_CHECK(launch_p2p_wait(c->peers.flags[c->rank], c->G, kind, c->epoch_dev.p, c->p2p_timeout_ns, c->p2p_err, s));
     return;
   }
   if (c->desc.exchange_mode != MOE_EXCHANGE_NCCL) return;
@@ -599,7 +651,9 @@ void flush_pending_plan(moe_ctx* c) {
   if (!c->pending.active) return;
   c->pending.active = false;
   CU_CHECK(cudaEventSynchronize(c->ev_counts));
+  check_p2p(c);
   stage_plan(c, c->pending.layer, c->pending.mode, c->pending.iteration, c->h_counts, c->pending.stride);
+  if (c->pending.gemm_slot >= 0) c->gemm_rows[c->pending.gemm_slot] = c->plan.rows_local;
 }
 
 Layer& layer_at(moe_ctx* c, int layer) {
@@ -621,24 +675,81 @@ void ensure_pools(moe_ctx* c, Layer& L) {
   L.expert_loaded.assign(c->E, 0);
 }
 
-// The single-GPU device sequence of one forward (no host synchronisation):
-// gate (+predictor) -> histogram to mapped host memory -> on-device plan ->
-// dispatch -> GEMM1 -> GEMM2 -> combine.  Used for CUDA-graph capture.
-void enqueue_local_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, uint16_t* y, cudaStream_t s,
-                           bool with_pred, int stride, cudaEvent_t x_consumed) {
-  // events recorded inside a capture must be external record nodes, so each
-  // replay signals them for the host (flush_pending_plan, x reuse)
-  const unsigned rec = cudaEventRecordExternal;
+// Enqueue one forward.  Three planning paths:
+//   local : G == 1 — the device builds the dispatch plan from its own
+//           histogram (plan_local_kernel);
+//   ahead : peer-memory exchange (G > 1, bf16) with the placement decided
+//           before the layer (FIXED, or PREDICTED planned d layers ahead) —
+//           the device builds the exchange plan from the gathered histograms
+//           (plan_exchange_kernel);
+//   host  : otherwise (NCCL chunk lists, MOE_PLAN_SYNC or a bootstrap layer
+//           at G > 1) — one host round trip: counts down, plan up.
+// local / ahead never wait for the host: the MoEless planner bookkeeping
+// (scale/place on the actual loads for SYNC, registry, predictor accuracy,
+// planning layer l + d) runs when the next call flushes it, as soon as this
+// forward's histogram is in mapped host memory.  Those two paths are also
+// capturable as one CUDA graph (capturing = true: external event nodes, no
+// per-call timing events).
+template <class Mark>
+void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, uint16_t* y, int plan_mode,
+                     long iteration, cudaStream_t s, bool with_pred, int stride, cudaEvent_t x_consumed, bool ahead,
+                     bool capturing, Mark&& mark) {
+  const unsigned rec = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+  const bool deferred = c->G == 1 || ahead;
+  mark(0);
   stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr);
-  CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * stride), s));
-  CU_CHECK(cudaEventRecordWithFlags(c->ev_counts, s, rec));
-  CU_CHECK(launch_plan_local(c->counts.p, c->E, c->dplan.p, s));
-  stage_dispatch(c, x, T, s, /*upload_plan=*/false);
-  if (x_consumed) CU_CHECK(cudaEventRecordWithFlags(x_consumed, s, rec));
-  const int64_t rows = static_cast<int64_t>(T) * c->k;
+  if (c->G > 1 && c->p2p) {
+    // every rank reads every histogram from its owner's slab
+    CU_CHECK(launch_p2p_counts(c->peers, c->G, c->rank, stride, c->epoch_dev.p, c->p2p_timeout_ns, c->p2p_err,
+                               c->counts_all.p, s));
+    CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
+  } else if (c->G > 1) {
+    require(c->desc.exchange_mode == MOE_EXCHANGE_NCCL, "staged API required for external exchange");
+    g_nccl.check(g_nccl.AllGather(c->counts.p, c->counts_all.p, stride, ncclInt32, c->comm, s), "ncclAllGather");
+    CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
+  } else {
+    CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * stride), s));
+  }
+  if (deferred) {
+    CU_CHECK(cudaEventRecordWithFlags(c->ev_counts, s, rec));
+    mark(1);
+    if (c->G == 1)
+      CU_CHECK(launch_plan_local(c->counts.p, c->E, c->dplan.p, s));
+    else
+      CU_CHECK(launch_plan_exchange(c->counts_all.p, stride, c->G, c->rank, L.ptab.p, c->dplan.p, s));
+    mark(2);
+    stage_dispatch(c, x, T, s, /*upload_plan=*/false);
+  } else {
+    mark(1);
+    CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram
+    check_p2p(c);
+    stage_plan(c, layer, plan_mode, iteration, c->h_counts, stride);
+    mark(2);
+    stage_dispatch(c, x, T, s);  // uploads the plan; P2P rows land in their owners' buffers
+  }
+  if (x_consumed) CU_CHECK(cudaEventRecordWithFlags(x_consumed, s, rec));  // x is not read after dispatch
+  mark(3);
+  stage_exchange(c, true, s);
+  mark(4);
+  // rows only sizes the fp32 SwiGLU pass (bf16 GEMMs read the device plan)
+  const int64_t rows = c->G == 1 ? static_cast<int64_t>(T) * c->k : (ahead ? c->rows_cap : c->plan.rows_local);
+  const int gslot = static_cast<int>(c->gemm_seq % moe_ctx::kGemmRing);
+  if (!capturing) CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][0], s));
   launch_ffn_gemm(c, layer, 0, s, rows);
+  if (!capturing) CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][1], s));
+  mark(5);
   launch_ffn_gemm(c, layer, 1, s, rows);
+  if (!capturing) {
+    CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][2], s));
+    c->gemm_rows[gslot] = ahead ? -1 : rows;  // "ahead": filled in when the plan is flushed
+    ++c->gemm_seq;
+  }
+  mark(6);
+  stage_exchange(c, false, s);
+  mark(7);
   stage_combine(c, y, T, s);
+  mark(8);
+  if (deferred && !capturing) c->pending = PendingPlan{true, layer, plan_mode, iteration, stride, ahead ? gslot : -1};
 }
 
 void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y, int plan_mode, long iteration,
@@ -651,25 +762,30 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
           "unknown plan mode");
   for (int e = 0; e < c->E; ++e)
     if (!L.w13.p || !L.expert_loaded[e]) throw std::invalid_argument("expert weights not loaded for layer");
+  if (c->p2p) {
+    require(c->p2p_ready, "moe_p2p_import must be called before a peer-memory forward");
+    check_p2p(c);
+  }
   EventSet& ev = c->events;
   const bool timed = st != nullptr;
-  auto mark = [&](int i) {
-    if (timed) CU_CHECK(cudaEventRecord(ev.ev[i], s));
-  };
-  flush_pending_plan(c);  // the previous call's deferred planner work (G = 1)
+  flush_pending_plan(c);  // the previous call's deferred planner work
   // the fused predictor (K2) runs when the layer has predictor weights: its
   // histograms follow the gate's in the same counts buffer
   const bool with_pred = c->n_pred > 0 && L.has_pred_weights;
   const int stride = with_pred ? c->count_stride : c->E;
-  if (c->use_graphs && c->G == 1 && !timed) {
-    // Replay the layer's whole device sequence (8-10 kernels) as one CUDA
+  const bool ahead = c->G > 1 && c->p2p && !c->fp32 &&
+                     (plan_mode == MOE_PLAN_FIXED || (plan_mode == MOE_PLAN_PREDICTED && L.plan_for == iteration));
+  if (ahead) ensure_placement(c, layer);
+  if (c->use_graphs && !timed && (c->G == 1 || ahead)) {
+    // Replay the layer's whole device sequence (8-14 kernels) as one CUDA
     // graph: captured once per (layer, tokens, buffers), then launched with a
     // single call — the launch-bound decode regime pays one launch, not ten.
-    const GraphKey key{layer, T, x, y, x_consumed};
+    const GraphKey key{layer, T, x, y, x_consumed, with_pred};
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
       CU_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-      enqueue_local_forward(c, L, layer, x, T, y, s, with_pred, stride, x_consumed);
+      enqueue_forward(c, L, layer, x, T, y, plan_mode, iteration, s, with_pred, stride, x_consumed, ahead, true,
+                      [](int) {});
       cudaGraph_t g = nullptr;
       CU_CHECK(cudaStreamEndCapture(s, &g));
       cudaGraphExec_t ex = nullptr;
@@ -679,71 +795,13 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
       it = c->graphs.emplace(key, ex).first;
     }
     CU_CHECK(cudaGraphLaunch(it->second, s));
-    c->pending = PendingPlan{true, layer, plan_mode, iteration, stride};
+    c->pending = PendingPlan{true, layer, plan_mode, iteration, stride, -1};
     return;
   }
-  mark(0);
-  stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr);
-  if (c->G > 1 && c->p2p) {
-    // peer memory: every rank reads every histogram from its owner; the host
-    // plans as in the NCCL path (one round trip), then dispatch writes rows
-    // directly into the owners' buffers
-    require(c->p2p_ready, "moe_p2p_import must be called before a peer-memory forward");
-    check_p2p(c);
-    const uint32_t ep = ++c->epoch;
-    CU_CHECK(launch_p2p_counts(c->peers, c->G, c->rank, stride, ep, c->p2p_timeout_ns, c->p2p_err,
-                               c->counts_all.p, s));
-    CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
-    mark(1);
-    CU_CHECK(cudaStreamSynchronize(s));
-    check_p2p(c);
-    stage_plan(c, layer, plan_mode, iteration, c->h_counts, stride);
-    mark(2);
-    stage_dispatch(c, x, T, s);  // rows land in their owners' buffers
-  } else if (c->G > 1) {
-    // NCCL needs every chunk size on the host: one round trip per layer.
-    require(c->desc.exchange_mode == MOE_EXCHANGE_NCCL, "staged API required for external exchange");
-    g_nccl.check(g_nccl.AllGather(c->counts.p, c->counts_all.p, stride, ncclInt32, c->comm, s), "ncclAllGather");
-    CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
-    mark(1);
-    CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram
-    stage_plan(c, layer, plan_mode, iteration, c->h_counts, stride);
-    mark(2);
-    stage_dispatch(c, x, T, s);
-  } else {
-    // One GPU: the device builds the dispatch plan from its own histogram and
-    // the layer never waits for the host.  The MoEless planner (scale_experts
-    // / place_experts / registry, MOE_PLAN_SYNC) runs on the histogram as soon
-    // as it lands in mapped host memory — its replica decisions cannot change
-    // single-GPU work (co-located replicas share one GEMM segment), so running
-    // it off the critical path keeps the reference's per-layer semantics.
-    CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * stride), s));
-    CU_CHECK(cudaEventRecord(c->ev_counts, s));
-    mark(1);
-    CU_CHECK(launch_plan_local(c->counts.p, c->E, c->dplan.p, s));
-    c->pending = PendingPlan{true, layer, plan_mode, iteration, stride};
-    mark(2);
-    stage_dispatch(c, x, T, s, /*upload_plan=*/false);
-  }
-  if (x_consumed) CU_CHECK(cudaEventRecord(x_consumed, s));  // x is not read after dispatch
-  mark(3);
-  stage_exchange(c, true, s);
-  mark(4);
-  const int gslot = static_cast<int>(c->gemm_seq % moe_ctx::kGemmRing);
-  const int64_t rows_here = c->G == 1 ? static_cast<int64_t>(T) * c->k : c->plan.rows_local;
-  CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][0], s));
-  launch_ffn_gemm(c, layer, 0, s, rows_here);
-  CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][1], s));
-  mark(5);
-  launch_ffn_gemm(c, layer, 1, s, rows_here);
-  CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][2], s));
-  c->gemm_rows[gslot] = rows_here;
-  ++c->gemm_seq;
-  mark(6);
-  stage_exchange(c, false, s);
-  mark(7);
-  stage_combine(c, y, T, s);
-  mark(8);
+  enqueue_forward(c, L, layer, x, T, y, plan_mode, iteration, s, with_pred, stride, x_consumed, ahead, false,
+                  [&](int i) {
+                    if (timed) CU_CHECK(cudaEventRecord(ev.ev[i], s));
+                  });
   if (timed) {
     CU_CHECK(cudaEventSynchronize(ev.ev[8]));
     flush_pending_plan(c);
@@ -834,6 +892,12 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->elem = c->fp32 ? 2 : 1;
     require(!c->fp32 || c->n_pred == 0, "the fp32 mode has no fused predictor");
     CU_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    // load every kernel now, not lazily at first launch (see preload_*)
+    CU_CHECK(preload_gate_kernels());
+    CU_CHECK(preload_dispatch_kernels());
+    CU_CHECK(preload_gemm_kernels());
+    CU_CHECK(preload_fp32_kernels());
+    CU_CHECK(preload_p2p_kernels());
     const int64_t assign = static_cast<int64_t>(c->Tmax) * c->k;
     c->rows_cap = assign * c->G;  // worst case: every rank routes everything here
     c->send_cap = c->G > 1 ? assign : 1;
@@ -872,6 +936,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
       CU_CHECK(cudaHostAlloc(&c->p2p_err, sizeof(int) * 4, cudaHostAllocMapped));
       c->dispatch_counter.alloc(4);
       CU_CHECK(cudaMemset(c->dispatch_counter.p, 0, 16));
+      c->epoch_dev.alloc(4);
+      CU_CHECK(cudaMemset(c->epoch_dev.p, 0, 16));
       *c->p2p_err = 0;
       if (const char* v = std::getenv("MOE_P2P_TIMEOUT_MS")) c->p2p_timeout_ns = std::strtoull(v, nullptr, 10) * 1000000ull;
     }
@@ -914,6 +980,10 @@ int moe_ctx_destroy(moe_ctx* c) {
     cudaStreamSynchronize(c->stream);
     if (c->comm) g_nccl.CommDestroy(c->comm);
     for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
+    for (Layer& L : c->layers) {
+      if (L.h_ptab) cudaFreeHost(L.h_ptab);
+      if (L.ev_ptab) cudaEventDestroy(L.ev_ptab);
+    }
     if (c->p2p_err) cudaFreeHost(c->p2p_err);
     c->events.destroy();
     if (c->hplan) cudaFreeHost(c->hplan);
@@ -1138,7 +1208,7 @@ int moe_set_placement(moe_ctx* c, int layer, const int32_t* rc, const int32_t* r
               "replica placed on invalid GPU " + std::to_string(rg[i]));
     L.rep_counts.assign(rc, rc + c->E);
     L.rep_gpu.assign(rg, rg + total);
-    L.has_placement = true;
+    placement_changed(c, layer);
   });
 }
 
@@ -1344,6 +1414,8 @@ int moe_buffer(moe_ctx* c, int which, void** ptr, int64_t* rows) {
       case 6: *ptr = c->row_code.p; r = static_cast<int64_t>(c->cur_T) * c->k; break;
       case 7: *ptr = c->counts.p; r = c->E; break;
       case 8: *ptr = c->h.p; r = c->plan.rows_local; break;
+      case 9: *ptr = c->p2p ? c->slab.p + c->off_flags : nullptr; r = kFlagKinds * kMaxRanks; break;  // P2P flags
+      case 10: *ptr = c->epoch_dev.p; r = 1; break;  // P2P device epoch
       default: throw std::invalid_argument("unknown buffer id");
     }
     if (rows) *rows = r;

@@ -189,7 +189,7 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
         for (int g = 0; g < 8; ++g)
           if (g < sig.G)
             asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig.flags[g] + sig.kind * 8 + sig.src),
-                         "r"(sig.epoch)
+                         "r"(*sig.epoch)
                          : "memory");
       }
     }
@@ -296,6 +296,99 @@ cudaError_t launch_plan_local(const int32_t* counts, int E, DevPlan* plan, cudaS
   return cudaGetLastError();
 }
 
+// ---------------------------------------------- on-device exchange plan (G > 1)
+// Peer-memory exchange with a placement decided BEFORE the layer (FIXED, or
+// MOE_PLAN_PREDICTED planned d layers ahead): every rank derives the same
+// direct plan as exchange_plan.cpp (direct mode) from the gathered
+// histograms — integer replica split, per-GPU segment layout in replica
+// order, this rank's merged segments — without a host round trip.
+__global__ void __launch_bounds__(512)
+plan_exchange_kernel(const int32_t* __restrict__ counts_all, int stride, int G, int rank,
+                     const PlacementTable* __restrict__ pt, DevPlan* __restrict__ plan) {
+  __shared__ int s_n[kMaxExperts], s_off[kMaxExperts], s_mine[kMaxExperts];
+  __shared__ int s_lrows[kMaxExperts], s_lfirst[kMaxExperts];
+  __shared__ int s_start[kMaxReplicas], s_size[kMaxReplicas], s_gpu[kMaxReplicas];
+  __shared__ int s_send;
+  const int tid = threadIdx.x;
+  const int E = pt->E, R = pt->R;
+  for (int e = tid; e < E; e += blockDim.x) {
+    int n = 0, off = 0;
+    for (int g = 0; g < G; ++g) {
+      const int c = counts_all[g * stride + e];
+      if (g < rank) off += c;
+      n += c;
+    }
+    s_n[e] = n;
+    s_off[e] = off;
+    s_mine[e] = counts_all[rank * stride + e];
+    s_lrows[e] = 0;
+    s_lfirst[e] = 0x7fffffff;
+    plan->n_e[e] = n;
+    plan->src_off[e] = off;
+    plan->rep_base[e] = pt->rep_base[e];
+  }
+  if (tid == 0) {
+    plan->rep_base[E] = R;
+    s_send = 0;
+  }
+  __syncthreads();
+  for (int f = tid; f < R; f += blockDim.x) {
+    const int e = pt->expert_of[f];
+    const int rb = pt->rep_base[e], Re = pt->rep_base[e + 1] - rb, r = f - rb;
+    const int n = s_n[e], q = n / Re, rem = n % Re;
+    s_size[f] = q + (r < rem ? 1 : 0);
+    s_start[f] = r * q + min(r, rem);
+    s_gpu[f] = pt->gpu_of[f];
+  }
+  __syncthreads();
+  for (int f = tid; f < R; f += blockDim.x) {
+    const int g = s_gpu[f], size = s_size[f], start = s_start[f];
+    int seg = 0;  // rows of earlier replicas on the same GPU (replica-order layout)
+    for (int h = 0; h < f; ++h) seg += s_gpu[h] == g ? s_size[h] : 0;
+    plan->rep_row_base[f] = seg - start;
+    plan->rep_remote[f] = g;
+    const int e = pt->expert_of[f];
+    if (g == rank) {
+      if (size > 0) {
+        atomicAdd(&s_lrows[e], size);
+        atomicMin(&s_lfirst[e], seg);
+      }
+    } else {
+      const int lo = max(start, s_off[e]), hi = min(start + size, s_off[e] + s_mine[e]);
+      if (hi > lo) atomicAdd(&s_send, hi - lo);
+    }
+  }
+  __syncthreads();
+  // this rank's local replicas of one expert are adjacent in its buffer: one
+  // GEMM segment per expert with rows here, in expert order
+  for (int e = tid; e < E; e += blockDim.x) {
+    if (s_lrows[e] == 0) continue;
+    int idx = 0;
+    for (int h = 0; h < e; ++h) idx += s_lrows[h] > 0 ? 1 : 0;
+    plan->segs[idx] = GemmSeg{s_lfirst[e], s_lrows[e], e, 0};
+  }
+  if (tid == 0) {
+    int nseg = 0, rows = 0;
+    for (int e = 0; e < E; ++e) {
+      nseg += s_lrows[e] > 0 ? 1 : 0;
+      rows += s_lrows[e];
+    }
+    plan->E = E;
+    plan->R = R;
+    plan->G = G;
+    plan->rank = rank;
+    plan->nseg = nseg;
+    plan->rows_local = rows;
+    plan->rows_send = s_send;
+  }
+}
+
+cudaError_t launch_plan_exchange(const int32_t* counts_all, int stride, int G, int rank, const PlacementTable* pt,
+                                 DevPlan* plan, cudaStream_t s) {
+  plan_exchange_kernel<<<1, 512, 0, s>>>(counts_all, stride, G, rank, pt, plan);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------- small SM copies
 // Copies a few KB between device memory and MAPPED pinned host memory with
 // the SMs instead of a copy engine, so control data (gate histogram out,
@@ -357,6 +450,26 @@ cudaError_t launch_combine(const RowTargets& sources, int T, int d, int k, const
   const dim3 grid(ctas, split);
   MOE_SWITCH_K(k, (combine_kernel<KK><<<grid, 256, 0, s>>>(sources, T, d, row_code, wts, y)));
   return cudaGetLastError();
+}
+
+// Load every kernel of this file now (CUDA 12 loads kernels lazily on first
+// launch, and a lazy load may wait for the whole context — including a
+// peer-exchange kernel spinning on another rank that shares the context).
+cudaError_t preload_dispatch_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {
+      reinterpret_cast<const void*>(block_prefix_kernel),  reinterpret_cast<const void*>(dispatch_kernel<1>),
+      reinterpret_cast<const void*>(dispatch_kernel<2>),   reinterpret_cast<const void*>(dispatch_kernel<4>),
+      reinterpret_cast<const void*>(dispatch_kernel<6>),   reinterpret_cast<const void*>(dispatch_kernel<8>),
+      reinterpret_cast<const void*>(combine_kernel<1>),    reinterpret_cast<const void*>(combine_kernel<2>),
+      reinterpret_cast<const void*>(combine_kernel<4>),    reinterpret_cast<const void*>(combine_kernel<6>),
+      reinterpret_cast<const void*>(combine_kernel<8>),    reinterpret_cast<const void*>(plan_local_kernel),
+      reinterpret_cast<const void*>(plan_exchange_kernel), reinterpret_cast<const void*>(small_copy_kernel)};
+  for (const void* f : fns) {
+    const cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace moe

@@ -26,9 +26,20 @@ struct RowTargets {
 // `epoch` in flags[g][kind * 8 + src] of every rank g (G == 0: no signal).
 struct PeerSignal {
   uint32_t* flags[8];
-  uint32_t* counter;  // CTAs finished (self-resetting)
-  int G, src, kind;
-  uint32_t epoch;
+  uint32_t* counter;      // CTAs finished (self-resetting)
+  const uint32_t* epoch;  // the forward's epoch (device memory)
+  int G, src, kind, pad;
+};
+
+// A layer's placement as the device planner reads it (ScalingPlan.replica_counts
+// flattened to rep_base, Placement.gpu_for to gpu_of; types.hpp:59,
+// placer.hpp:17).  Uploaded when the host planner decides it — for
+// MOE_PLAN_PREDICTED d layers before the layer runs.
+struct PlacementTable {
+  int E, R, pad0, pad1;
+  int rep_base[kMaxExperts + 4];
+  int gpu_of[kMaxReplicas];
+  int expert_of[kMaxReplicas];
 };
 
 // One GEMM segment = the rows of one replica placed on this rank.

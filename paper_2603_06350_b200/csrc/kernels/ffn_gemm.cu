@@ -662,4 +662,22 @@ cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorM
   return cudaGetLastError();
 }
 
+// Load every kernel of this file now (CUDA 12 loads kernels lazily on first
+// launch, and a lazy load may wait for the whole context — including a
+// peer-exchange kernel spinning on another rank that shares the context).
+cudaError_t preload_gemm_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {reinterpret_cast<const void*>(grouped_gemm_kernel<0>),
+                       reinterpret_cast<const void*>(grouped_gemm_kernel<1>),
+                       reinterpret_cast<const void*>(grouped_gemm_2sm_kernel<0>),
+                       reinterpret_cast<const void*>(grouped_gemm_2sm_kernel<1>),
+                       reinterpret_cast<const void*>(grouped_gemm_m256_kernel<0>),
+                       reinterpret_cast<const void*>(grouped_gemm_m256_kernel<1>)};
+  for (const void* f : fns) {
+    const cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace moe

@@ -219,4 +219,20 @@ cudaError_t launch_combine_f32(const RowTargets& sources, int T, int d, int k, c
   return cudaGetLastError();
 }
 
+// Load every kernel of this file now (CUDA 12 loads kernels lazily on first
+// launch, and a lazy load may wait for the whole context — including a
+// peer-exchange kernel spinning on another rank that shares the context).
+cudaError_t preload_fp32_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {reinterpret_cast<const void*>(gate_f32_kernel),
+                       reinterpret_cast<const void*>(grouped_sgemm_kernel),
+                       reinterpret_cast<const void*>(swiglu_f32_kernel),
+                       reinterpret_cast<const void*>(combine_f32_kernel)};
+  for (const void* f : fns) {
+    const cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace moe

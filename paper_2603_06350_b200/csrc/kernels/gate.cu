@@ -306,4 +306,23 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
   return cudaErrorInvalidValue;
 }
 
+// Load every kernel of this file now (CUDA 12 loads kernels lazily on first
+// launch, and a lazy load may wait for the whole context — including a
+// peer-exchange kernel spinning on another rank that shares the context).
+cudaError_t preload_gate_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {
+      reinterpret_cast<const void*>(gate_topk_kernel<1>),    reinterpret_cast<const void*>(gate_topk_kernel<2>),
+      reinterpret_cast<const void*>(gate_topk_kernel<4>),    reinterpret_cast<const void*>(gate_topk_kernel<8>),
+      reinterpret_cast<const void*>(gate_topk_kernel<16>),   reinterpret_cast<const void*>(gate_topk_kernel<32>),
+      reinterpret_cast<const void*>(gate_finish_kernel<1>),  reinterpret_cast<const void*>(gate_finish_kernel<2>),
+      reinterpret_cast<const void*>(gate_finish_kernel<4>),  reinterpret_cast<const void*>(gate_finish_kernel<8>),
+      reinterpret_cast<const void*>(gate_finish_kernel<16>), reinterpret_cast<const void*>(gate_finish_kernel<32>)};
+  for (const void* f : fns) {
+    const cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace moe

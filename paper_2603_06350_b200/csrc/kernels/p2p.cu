@@ -13,7 +13,10 @@
 //
 // Flags: flags[kind][src] in the RECEIVER's slab, written by rank src with a
 // system-scope release store of the forward's epoch (monotone, never reset);
-// waiters use acquire loads.  Per forward (epoch n):
+// waiters use acquire loads.  The epoch lives in device memory: the counts
+// kernel opens a forward by incrementing it and every later kernel of the
+// forward reads it, so a captured CUDA graph replays with fresh epochs.
+// Per forward (epoch n):
 //   kCounts  src's gate histogram for n is readable       (before the gather)
 //   kRows    src finished storing its rows into my xp     (before GEMM1)
 //   kOutputs src's GEMM2 for n is done, its yp readable    (before combine)
@@ -82,19 +85,23 @@ __device__ __forceinline__ void wait_all(const uint32_t* my_flags, int G, int ki
 }
 
 __global__ void __launch_bounds__(32)
-p2p_signal_kernel(const __grid_constant__ PeerSlabs peers, int G, int kind, int src, uint32_t epoch) {
-  signal_all(peers, G, kind, src, epoch);
+p2p_signal_kernel(const __grid_constant__ PeerSlabs peers, int G, int kind, int src, const uint32_t* epoch) {
+  signal_all(peers, G, kind, src, *epoch);
 }
 
-__global__ void __launch_bounds__(32) p2p_wait_kernel(const uint32_t* my_flags, int G, int kind, uint32_t epoch,
+__global__ void __launch_bounds__(32) p2p_wait_kernel(const uint32_t* my_flags, int G, int kind, const uint32_t* epoch,
                                                       uint64_t timeout_ns, int* err) {
-  wait_all(my_flags, G, kind, epoch, timeout_ns, err);
+  wait_all(my_flags, G, kind, *epoch, timeout_ns, err);
 }
 
-// signal + wait + gather: counts_all[g][:] = rank g's histogram (stride ints)
+// opens the forward (epoch + 1), then signal + wait + gather:
+// counts_all[g][:] = rank g's histogram (stride ints)
 __global__ void __launch_bounds__(256)
-p2p_counts_kernel(const __grid_constant__ PeerSlabs peers, int G, int rank, int stride, uint32_t epoch,
+p2p_counts_kernel(const __grid_constant__ PeerSlabs peers, int G, int rank, int stride, uint32_t* epoch_dev,
                   uint64_t timeout_ns, int* err, int32_t* __restrict__ counts_all) {
+  const uint32_t epoch = *epoch_dev + 1u;
+  __syncthreads();
+  if (threadIdx.x == 0) *epoch_dev = epoch;
   if (threadIdx.x < 32) {
     signal_all(peers, G, kFlagCounts, rank, epoch);
     wait_all(peers.flags[rank], G, kFlagCounts, epoch, timeout_ns, err);
@@ -107,24 +114,40 @@ p2p_counts_kernel(const __grid_constant__ PeerSlabs peers, int G, int rank, int 
   }
 }
 
-cudaError_t launch_p2p_signal(const PeerSlabs& peers, int G, int kind, int src, uint32_t epoch, cudaStream_t s) {
+cudaError_t launch_p2p_signal(const PeerSlabs& peers, int G, int kind, int src, const uint32_t* epoch,
+                              cudaStream_t s) {
   if (G > kMaxRanks) return cudaErrorInvalidValue;
   p2p_signal_kernel<<<1, 32, 0, s>>>(peers, G, kind, src, epoch);
   return cudaGetLastError();
 }
 
-cudaError_t launch_p2p_wait(const uint32_t* my_flags, int G, int kind, uint32_t epoch, uint64_t timeout_ns, int* err,
-                            cudaStream_t s) {
+cudaError_t launch_p2p_wait(const uint32_t* my_flags, int G, int kind, const uint32_t* epoch, uint64_t timeout_ns,
+                            int* err, cudaStream_t s) {
   if (G > kMaxRanks) return cudaErrorInvalidValue;
   p2p_wait_kernel<<<1, 32, 0, s>>>(my_flags, G, kind, epoch, timeout_ns, err);
   return cudaGetLastError();
 }
 
-cudaError_t launch_p2p_counts(const PeerSlabs& peers, int G, int rank, int stride, uint32_t epoch,
+cudaError_t launch_p2p_counts(const PeerSlabs& peers, int G, int rank, int stride, uint32_t* epoch,
                               uint64_t timeout_ns, int* err, int32_t* counts_all, cudaStream_t s) {
   if (G > kMaxRanks) return cudaErrorInvalidValue;
   p2p_counts_kernel<<<1, 256, 0, s>>>(peers, G, rank, stride, epoch, timeout_ns, err, counts_all);
   return cudaGetLastError();
+}
+
+// Load every kernel of this file now (CUDA 12 loads kernels lazily on first
+// launch, and a lazy load may wait for the whole context — including a
+// peer-exchange kernel spinning on another rank that shares the context).
+cudaError_t preload_p2p_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {reinterpret_cast<const void*>(p2p_signal_kernel),
+                       reinterpret_cast<const void*>(p2p_wait_kernel),
+                       reinterpret_cast<const void*>(p2p_counts_kernel)};
+  for (const void* f : fns) {
+    const cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace moe

@@ -21,7 +21,8 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_2603_06350_b200 import (MOE_EXCHANGE_P2P, MOE_PLAN_FIXED, MOE_PLAN_SYNC, MoeError, MoELayer)
+from paper_2603_06350_b200 import (MOE_EXCHANGE_P2P, MOE_PLAN_FIXED, MOE_PLAN_PREDICTED, MOE_PLAN_SYNC, MoeError,
+                                   MoELayer)
 from paper_2603_06350_b200 import workload as wl
 
 pytestmark = pytest.mark.gpu
@@ -126,7 +127,7 @@ def test_p2p_sync_planner_replicas(cuda):
 
 
 def test_p2p_rank_out_of_step_times_out(cuda, monkeypatch):
-    """A rank whose peers never arrive fails the call instead of hanging."""
+    """A rank whose peers never arrive fails instead of hanging the GPU."""
     import torch
     monkeypatch.setenv("MOE_P2P_TIMEOUT_MS", "300")
     E, k, d, ff, T = 8, 2, 256, 256, 64
@@ -137,8 +138,9 @@ def test_p2p_rank_out_of_step_times_out(cuda, monkeypatch):
             m.load_expert(0, e, *wl.expert_weights(d, ff, 1, 0, e))
     x = torch.from_numpy(wl.tokens(T, d, E, 1, 0).view(np.int16)).to(cuda)
     y = torch.zeros((T, d), dtype=torch.int16, device=cuda)
-    with pytest.raises(MoeError, match="timed out"):
+    with pytest.raises(MoeError, match="timed out"):  # device-planned: surfaces at the next sync point
         ms[0].forward(0, x, y, MOE_PLAN_FIXED, 0)
+        ms[0].sync()
     ms[0].close()
     ms[1].close()
 
@@ -161,3 +163,82 @@ def test_p2p_two_processes_ipc(cuda, tmp_path):
     for p, o in zip(procs, outs):
         assert p.returncode == 0, o[-3000:]
         assert "P2P-IPC OK" in o, o[-3000:]
+
+
+def test_p2p_predicted_planning_ahead(cuda):
+    """MOE_PLAN_PREDICTED at G=2 over a 3-layer stack: layer l's fused
+    predictor scores layer l+1, every rank plans layer l+1 from the gathered
+    predicted histogram while layer l finishes, and layer l+1 runs with the
+    ON-DEVICE exchange plan (no host round trip).  Layer 0 bootstraps from
+    history on the host.  Outputs stay bit-identical to G = 1."""
+    import torch
+    G, L, E, k, d, ff, T = 2, 3, 16, 2, 1024, 1408, 160
+    mem = 3.0 * d * ff * 2 / 1e6
+    ms = [MoELayer(L, E, k, d, ff, max_tokens=T, world_size=G, rank=r, exchange_mode=MOE_EXCHANGE_P2P,
+                   num_predictor_targets=1, expert_mem_mb=mem, layer_mem_cap_mb=(E + 4) * mem) for r in range(G)]
+    handles = [m.p2p_export() for m in ms]
+    for m in ms:
+        m.p2p_import(handles)
+    one = MoELayer(L, E, k, d, ff, max_tokens=T, expert_mem_mb=mem, layer_mem_cap_mb=E * mem)
+    gates = [wl.gate_weights(E, d, 1.5, 1, l, 0) for l in range(L)]
+    for m in ms + [one]:
+        for l in range(L):
+            m.set_gate(l, gates[l])
+            for e in range(E):
+                m.load_expert(l, e, *wl.expert_weights(d, ff, 1, l, e))
+    for m in ms:
+        for l in range(L - 1):
+            m.set_predictor(l, 0, gates[l + 1])  # scores layer l+1's routing from layer l's input
+    xd = [torch.from_numpy(wl.tokens(T, d, E, 1, 500 + r).view(np.int16)).to(cuda) for r in range(G)]
+    yd = [[torch.zeros((T, d), dtype=torch.int16, device=cuda) for _ in range(L)] for _ in range(G)]
+    sources = []
+    for it in range(3):
+        def rank_stack(r):
+            out = []
+            for l in range(L):
+                out.append(ms[r].forward(l, xd[r], yd[r][l], MOE_PLAN_PREDICTED, it, stats=True))
+            return out
+        sts = _parallel(ms, rank_stack)
+        torch.cuda.synchronize()
+        sources.append([st.plan_source for st in sts[0]])
+        for r in range(G):
+            assert [st.plan_source for st in sts[r]] == sources[-1]
+            for l in range(L):
+                y1 = torch.zeros((T, d), dtype=torch.int16, device=cuda)
+                one.forward(l, xd[r], y1, MOE_PLAN_FIXED, it)
+                one.sync()
+                assert torch.equal(yd[r][l], y1), (it, r, l)
+        assert sum(st.rows_local for st in [sts[r][1] for r in range(G)]) == k * G * T
+    assert all(src[0] == 3 and src[1] == 2 and src[2] == 2 for src in sources), sources
+    for m in ms + [one]:
+        m.close()
+
+
+def test_p2p_graph_replay(cuda):
+    """A peer-memory layer with a fixed placement replays as one CUDA graph per
+    rank (epochs live in device memory); results equal the eager G = 1 layer."""
+    import torch
+    G, E, k, d, ff, T = 2, 8, 2, 1024, 1408, 96
+    ms = _ranks(G, E, k, d, ff, T, cuda_graphs=True)
+    one = _single(E, k, d, ff, T)
+    for m in ms + [one]:
+        for e in range(E):
+            m.load_expert(0, e, *wl.expert_weights(d, ff, 1, 0, e))
+    for m in ms:
+        m.set_placement(0, [1, 2, 1, 1, 1, 1, 1, 1], [0, 1, 0, 1, 1, 0, 1, 0, 1])
+    xd = [torch.from_numpy(wl.tokens(T, d, E, 1, 600 + r).view(np.int16)).to(cuda) for r in range(G)]
+    yd = [torch.zeros((T, d), dtype=torch.int16, device=cuda) for _ in range(G)]
+    for it in range(5):
+        wg = wl.gate_weights(E, d, 1.3, 1, 0, it)
+        for m in ms + [one]:
+            m.set_gate(0, wg)
+        _parallel(ms, lambda r: ms[r].forward(0, xd[r], yd[r], MOE_PLAN_FIXED, it))
+        for m in ms:
+            m.sync()
+        for r in range(G):
+            y1 = torch.zeros_like(yd[r])
+            one.forward(0, xd[r], y1, MOE_PLAN_FIXED, it)
+            one.sync()
+            assert torch.equal(yd[r], y1), (it, r)
+    for m in ms + [one]:
+        m.close()
