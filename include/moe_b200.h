@@ -214,7 +214,10 @@ int moe_wait(moe_ctx* ctx, int64_t ticket);
 /* K4 device times of the most recent forwards (<= 64), oldest first, measured
    with CUDA events recorded around the two grouped GEMMs of EVERY forward
    (no host synchronisation inside the forward).  Synchronises the ctx
-   stream, then fills up to max_n entries and *n_out. */
+   stream, then fills up to max_n entries and *n_out.  GEMM2 is launched
+   programmatically behind GEMM1 (it streams its weights during GEMM1's
+   tail), so by default gemm1_ms holds the GEMM1+GEMM2 interval and gemm2_ms
+   is 0; env MOE_PDL=0 serialises them and reports them apart. */
 int moe_gemm_times(moe_ctx* ctx, int max_n, float* gemm1_ms, float* gemm2_ms, int64_t* rows, int* n_out);
 
 /* Page-locked host buffers for the pipelined API (portable + mapped). */

@@ -84,7 +84,8 @@ cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUten
                                     __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream);
 cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
-                                __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream);
+                                __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, int* sched,
+                                bool pdl);
 cudaError_t preload_gate_kernels();
 cudaError_t preload_dispatch_kernels();
 cudaError_t preload_gemm_kernels();
@@ -316,6 +317,9 @@ struct moe_ctx {
   DevBuf<float> gu_f32;   // fp32 GEMM1 output [rows_cap][2 ff]
   DevBuf<float> gate_partial;  // split-K gate scratch (small batches)
   bool use_graphs = false;     // replay single-GPU forwards as CUDA graphs
+  bool dyn_sched = false;      // K4 claims tiles from a global counter (MOE_GEMM_SCHED=dynamic; A/B: no gain)
+  bool use_pdl = true;         // K4 launched programmatically behind its producer (MOE_PDL=0: off)
+  DevBuf<int> gemm_sched;      // [GEMM1 next, done, GEMM2 next, done], zero between launches
   std::map<GraphKey, cudaGraphExec_t> graphs;
   // K4 timing ring: events around GEMM1 / GEMM2 of every forward (no sync)
   static constexpr int kGemmRing = 64;
@@ -603,15 +607,27 @@ void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t r
     return;
   }
   const bool two_sm = c->gemm_variant == 2, m256 = c->gemm_variant == 3;
-  auto fn = two_sm ? launch_grouped_gemm_2sm : (m256 ? launch_grouped_gemm_m256 : launch_grouped_gemm);
-  const CUtensorMap* a1 = m256 ? &c->tmA1w : &c->tmA1;
-  const CUtensorMap* a2 = m256 ? &c->tmA2w : &c->tmA2;
+  if (two_sm || m256) {
+    auto fn = two_sm ? launch_grouped_gemm_2sm : launch_grouped_gemm_m256;
+    const CUtensorMap* a1 = m256 ? &c->tmA1w : &c->tmA1;
+    const CUtensorMap* a2 = m256 ? &c->tmA2w : &c->tmA2;
+    if (which == 0)
+      CU_CHECK(fn(0, a1, two_sm ? &L.tmB1h : &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d,
+                  2 * c->ff, reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, c->num_sms, s));
+    else
+      CU_CHECK(fn(1, a2, two_sm ? &L.tmB2h : &L.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
+                  reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s));
+    return;
+  }
+  // 1-SM kernel with the dynamic tile scheduler (counter pair per GEMM)
+  int* sched = c->dyn_sched ? c->gemm_sched.p + 2 * which : nullptr;
   if (which == 0)
-    CU_CHECK(fn(0, a1, two_sm ? &L.tmB1h : &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d, 2 * c->ff,
-                reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, c->num_sms, s));
+    CU_CHECK(launch_grouped_gemm(0, &c->tmA1, &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d,
+                                 2 * c->ff, reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, c->num_sms, s, sched,
+                                 c->use_pdl));
   else
-    CU_CHECK(fn(1, a2, two_sm ? &L.tmB2h : &L.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
-                reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s));
+    CU_CHECK(launch_grouped_gemm(1, &c->tmA2, &L.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
+                                 reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s, sched, c->use_pdl));
 }
 
 void stage_expert(moe_ctx* c, int layer, cudaStream_t s) {
@@ -736,7 +752,9 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   const int gslot = static_cast<int>(c->gemm_seq % moe_ctx::kGemmRing);
   if (!capturing) CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][0], s));
   launch_ffn_gemm(c, layer, 0, s, rows);
-  if (!capturing) CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][1], s));
+  // (with PDL, an event between the GEMMs would serialise them: GEMM1+GEMM2 is
+  // then timed as one interval, reported as GEMM1 with GEMM2 = 0)
+  if (!capturing && !c->use_pdl) CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][1], s));
   mark(5);
   launch_ffn_gemm(c, layer, 1, s, rows);
   if (!capturing) {
@@ -881,6 +899,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->use_graphs = D.use_cuda_graphs != 0;
     if (const char* v = std::getenv("MOE_CUDA_GRAPHS")) c->use_graphs = std::string(v) == "1";
     c->num_sms = prop.multiProcessorCount;
+    if (const char* v = std::getenv("MOE_GEMM_SCHED")) c->dyn_sched = std::string(v) == "dynamic";
+    if (const char* v = std::getenv("MOE_PDL")) c->use_pdl = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_GEMM_VARIANT")) {
       const std::string s(v);
       c->gemm_variant = s == "1sm" ? 1 : (s == "2sm" ? 2 : (s == "m256" ? 3 : 0));
@@ -942,6 +962,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
       if (const char* v = std::getenv("MOE_P2P_TIMEOUT_MS")) c->p2p_timeout_ns = std::strtoull(v, nullptr, 10) * 1000000ull;
     }
     c->dplan.alloc(1);
+    c->gemm_sched.alloc(4);
+    CU_CHECK(cudaMemset(c->gemm_sched.p, 0, 4 * sizeof(int)));
     {  // split-K gate scratch: <= 296 (block, split) CTAs x 32 tokens x padded logits
       int nt = 1;
       while (8 * nt < c->count_stride) nt *= 2;
@@ -1322,8 +1344,12 @@ int moe_gemm_times(moe_ctx* c, int max_n, float* g1, float* g2, int64_t* rows, i
     for (int i = 0; i < n; ++i) {
       const int slot = static_cast<int>((c->gemm_seq - n + i) % moe_ctx::kGemmRing);
       float a = 0.0f, b = 0.0f;
-      CU_CHECK(cudaEventElapsedTime(&a, c->gemm_ev[slot][0], c->gemm_ev[slot][1]));
-      CU_CHECK(cudaEventElapsedTime(&b, c->gemm_ev[slot][1], c->gemm_ev[slot][2]));
+      if (c->use_pdl) {  // GEMM1 and GEMM2 overlap: one interval
+        CU_CHECK(cudaEventElapsedTime(&a, c->gemm_ev[slot][0], c->gemm_ev[slot][2]));
+      } else {
+        CU_CHECK(cudaEventElapsedTime(&a, c->gemm_ev[slot][0], c->gemm_ev[slot][1]));
+        CU_CHECK(cudaEventElapsedTime(&b, c->gemm_ev[slot][1], c->gemm_ev[slot][2]));
+      }
       if (g1) g1[i] = a;
       if (g2) g2[i] = b;
       if (rows) rows[i] = c->gemm_rows[slot];

@@ -175,6 +175,7 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
       }
     }
   }
+  griddep_launch_dependents();  // GEMM1 may launch and stream weights while the last CTAs drain
   if (sig.G > 0) {
     // peer memory: every thread's remote stores are performed system-wide
     // before its CTA counts itself done; the last CTA publishes the epoch

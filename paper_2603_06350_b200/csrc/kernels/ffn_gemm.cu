@@ -47,14 +47,19 @@ constexpr uint32_t kTmemCols = 512;
 
 enum : int { EPI_SWIGLU = 0, EPI_STORE = 1 };
 
+// dynamic tile scheduler: the producer warp claims tiles from a global
+// counter and hands their ids to the MMA and epilogue warps through a ring
+constexpr int kTileRing = 8;
+
 struct SmemLayout {
   // offsets relative to the 1024-aligned base
   static constexpr uint32_t a = 0;
   static constexpr uint32_t b = a + STAGES * kStageBytesA;
   static constexpr uint32_t bars = b + STAGES * kStageBytesB;       // 8-byte mbarriers
-  static constexpr uint32_t n_bars = 2 * STAGES + 4;
+  static constexpr uint32_t n_bars = 2 * STAGES + 4 + 2 * kTileRing;
   static constexpr uint32_t tmem_slot = bars + n_bars * 8;
-  static constexpr uint32_t seg_tiles = tmem_slot + 16;              // int[kMaxSegs + 1]
+  static constexpr uint32_t tile_ring = tmem_slot + 16;              // int[kTileRing]
+  static constexpr uint32_t seg_tiles = tile_ring + kTileRing * 4;   // int[kMaxSegs + 1]
   static constexpr uint32_t segs = seg_tiles + (kMaxSegs + 1) * 4 + 12;  // int4[kMaxSegs]
   static constexpr uint32_t end = ((segs + 15) / 16) * 16 + kMaxSegs * 16;
 };
@@ -89,11 +94,17 @@ __device__ __forceinline__ TileCoord decode_tile(int t, const int* seg_tiles, co
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 
+// Tile order is the same static sequence (decode_tile) either way; with a
+// scheduler counter (sched != nullptr: [0] next tile, [1] CTAs done, zero
+// before the launch, reset by the last CTA) tiles are CLAIMED in that order by
+// whichever CTA's producer is free, so SMs that draw less bandwidth take
+// fewer tiles instead of finishing last.
 template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total,
-                    int k_total, int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld) {
+                    int k_total, int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld,
+                    int* __restrict__ sched) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout::bars);
@@ -101,7 +112,10 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint64_t* ring_full = bars + 2 * STAGES + 4;
+  uint64_t* ring_empty = ring_full + kTileRing;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SmemLayout::tmem_slot);
+  volatile int* ring = reinterpret_cast<volatile int*>(smem + SmemLayout::tile_ring);
   int* seg_tiles = reinterpret_cast<int*>(smem + SmemLayout::seg_tiles);
   int4* segs = reinterpret_cast<int4*>(smem + SmemLayout::segs);
 
@@ -116,6 +130,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    for (int r = 0; r < kTileRing; ++r) { mbar_init(&ring_full[r], 1); mbar_init(&ring_empty[r], 5); }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
@@ -134,18 +149,48 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = nseg > 0 ? seg_tiles[nseg] : 0;
   const int num_kb = k_total / BK;
+  // the next kernel (GEMM2 after GEMM1) may launch now: its CTAs take SMs as
+  // this grid's CTAs retire and stream their own weights during our tail
+  griddep_launch_dependents();
 
   if (warp == 0) {
     // ---------------------------------------------------------- producer
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
+      int rslot = 0;
+      uint32_t rphase = 0;
       const uint64_t pol_b = policy_evict_last();
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      int t = blockIdx.x;
+      bool first = true;
+      while (true) {
+        if (sched) t = atomicAdd(sched, 1);  // claim the next tile in the static order
+        mbar_wait(&ring_empty[rslot], rphase ^ 1);
+        ring[rslot] = t < total_tiles ? t : -1;  // -1: no more tiles
+        mbar_arrive(&ring_full[rslot]);
+        if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
+        if (t >= total_tiles) break;
         const TileCoord c = decode_tile<kGroupM<EPI>>(t, seg_tiles, segs, nseg, n_tiles);
         const int a_row = segs[c.seg].x + c.m * BM;
         const int b_row = segs[c.seg].z * b_rows_per_slot + c.n * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        int kb0 = 0;
+        if (first) {
+          // Launched programmatically behind the kernel that produces A: the
+          // weight tiles of the first stages do not depend on it, so stream
+          // them while that kernel drains, then wait for it before loading A.
+          first = false;
+          kb0 = num_kb < STAGES ? num_kb : STAGES;
+          for (int kb = 0; kb < kb0; ++kb) {
+            mbar_arrive_expect_tx(&full[kb], kStageBytes);  // fresh stages: no empty wait
+            tma_load_2d_hint(smem + SmemLayout::b + kb * kStageBytesB, &tmB, &full[kb], kb * BK, b_row, pol_b);
+          }
+          griddep_wait();
+          for (int kb = 0; kb < kb0; ++kb)
+            tma_load_2d(smem + SmemLayout::a + kb * kStageBytesA, &tmA, &full[kb], kb * BK, a_row);
+          stage = kb0 == STAGES ? 0 : kb0;
+          phase = kb0 == STAGES ? 1u : 0u;
+        }
+        for (int kb = kb0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], kStageBytes);
           tma_load_2d(smem + SmemLayout::a + stage * kStageBytesA, &tmA, &full[stage], kb * BK, a_row);
@@ -153,6 +198,12 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                            pol_b);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        if (!sched) t += gridDim.x;
+      }
+      if (sched && atomicAdd(sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+        // every CTA has made its last claim: reset for the next launch
+        sched[0] = 0;
+        sched[1] = 0;
       }
     }
   } else if (warp == 1) {
@@ -165,7 +216,14 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       uint32_t acc_phase = 0;
       const uint32_t a_base = smem_u32(smem + SmemLayout::a);
       const uint32_t b_base = smem_u32(smem + SmemLayout::b);
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      int rslot = 0;
+      uint32_t rphase = 0;
+      while (true) {
+        mbar_wait(&ring_full[rslot], rphase);
+        const int t = ring[rslot];
+        mbar_arrive(&ring_empty[rslot]);
+        if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
+        if (t < 0) break;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -189,7 +247,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     const int quarter = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    int rslot = 0;
+    uint32_t rphase = 0;
+    while (true) {
+      mbar_wait(&ring_full[rslot], rphase);
+      const int t = ring[rslot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ring_empty[rslot]);
+      if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
+      if (t < 0) break;
       const TileCoord c = decode_tile<kGroupM<EPI>>(t, seg_tiles, segs, nseg, n_tiles);
       const int4 sg = segs[c.seg];
       const int row = c.m * BM + quarter * 32 + lane;
@@ -244,6 +310,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
+  // a CTA without tiles never waited: completing this grid must still imply
+  // that the kernel before it completed (stream order for later kernels)
+  griddep_wait();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -645,7 +714,8 @@ int gemm_smem_bytes() { return static_cast<int>(kSmemBytes); }
 
 cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
-                                __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream) {
+                                __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, int* sched,
+                                bool pdl) {
   if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
   static bool configured = false;
   if (!configured) {
@@ -653,13 +723,23 @@ cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorM
     cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     configured = true;
   }
+  // programmatic dependent launch: the kernel starts while the previous one
+  // drains (it waits in griddepcontrol.wait before reading A)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_ctas);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (epi == EPI_SWIGLU)
-    grouped_gemm_kernel<EPI_SWIGLU><<<num_ctas, kThreads, kSmemBytes, stream>>>(
-        *tmA, *tmB, segs, nseg, n_total, k_total, b_rows_per_slot, out, out_ld);
-  else
-    grouped_gemm_kernel<EPI_STORE><<<num_ctas, kThreads, kSmemBytes, stream>>>(
-        *tmA, *tmB, segs, nseg, n_total, k_total, b_rows_per_slot, out, out_ld);
-  return cudaGetLastError();
+    return cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI_SWIGLU>, *tmA, *tmB, segs, nseg, n_total, k_total,
+                              b_rows_per_slot, out, out_ld, sched);
+  return cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI_STORE>, *tmA, *tmB, segs, nseg, n_total, k_total,
+                            b_rows_per_slot, out, out_ld, sched);
 }
 
 // Load every kernel of this file now (CUDA 12 loads kernels lazily on first

@@ -91,6 +91,8 @@ p2p_signal_kernel(const __grid_constant__ PeerSlabs peers, int G, int kind, int 
 
 __global__ void __launch_bounds__(32) p2p_wait_kernel(const uint32_t* my_flags, int G, int kind, const uint32_t* epoch,
                                                       uint64_t timeout_ns, int* err) {
+  // GEMM1 (launched programmatically) may start streaming weights while we wait
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   wait_all(my_flags, G, kind, *epoch, timeout_ns, err);
 }
 
