@@ -236,7 +236,9 @@ int moe_forward_end(moe_ctx* ctx, uint16_t* y_dev, void* stream);
 /* Device buffers of the staged forward: which = 0 recv/permuted X, 1 send X,
    2 expert output Y (recv layout), 3 return buffer (send layout), 4 ids,
    5 weights, 6 row codes, 7 counts, 8 SwiGLU intermediate H, 9 peer-exchange
-   flags [4][8] u32 (P2P), 10 the P2P device epoch.  rows_out = valid rows. */
+   flags [4][8] u32 (P2P), 10 the P2P device epoch, 11 the row -> token list
+   of a single-GPU forward whose GEMM1 gathers x in place (int32, written
+   instead of buffer 0 there).  rows_out = valid rows. */
 int moe_buffer(moe_ctx* ctx, int which, void** ptr_out, int64_t* rows_out);
 /* cudaMemcpyDefault-style copy between any host/device pointers (UVA), on the
    ctx stream, synchronous on return — the transport hook of the staged API. */

@@ -47,7 +47,7 @@ cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, co
                                 int32_t* block_pre, cudaStream_t s);
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
                             const int32_t* block_pre, const DevPlan* plan, const RowTargets& targets,
-                            uint32_t* row_code, const PeerSignal& sig, cudaStream_t s);
+                            uint32_t* row_code, const PeerSignal& sig, cudaStream_t s, int32_t* perm_src);
 // K6 over peer memory (p2p.cu)
 constexpr int kMaxRanks = 8;
 enum { kFlagCounts = 0, kFlagRows = 1, kFlagOutputs = 2, kFlagKinds = 4 };
@@ -85,7 +85,7 @@ cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUten
 cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                 __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, int* sched,
-                                bool pdl);
+                                bool pdl, const int32_t* a_gather);
 cudaError_t preload_gate_kernels();
 cudaError_t preload_dispatch_kernels();
 cudaError_t preload_gemm_kernels();
@@ -319,6 +319,15 @@ struct moe_ctx {
   bool use_graphs = false;     // replay single-GPU forwards as CUDA graphs
   bool dyn_sched = false;      // K4 claims tiles from a global counter (MOE_GEMM_SCHED=dynamic; A/B: no gain)
   bool use_pdl = true;         // K4 launched programmatically behind its producer (MOE_PDL=0: off)
+  // single GPU: GEMM1 gathers its A rows from x with TMA gather4 and the
+  // dispatch kernel only ranks (MOE_GATHER=1).  Opt-in: bit-identical, but 32
+  // gather4 instructions per 16 KB A stage make GEMM1 2.7x slower than one
+  // tile load (profiles/ab_gather4_r01.md), far more than the copy it saves.
+  bool gather = false;
+  DevBuf<int32_t> perm_src;    // gathered GEMM1: permuted row -> token
+  CUtensorMap tmX;             // gather4 map over the current x ({64, 1} box)
+  const void* tmX_ptr = nullptr;
+  int tmX_T = -1;
   DevBuf<int> gemm_sched;      // [GEMM1 next, done, GEMM2 next, done], zero between launches
   std::map<GraphKey, cudaGraphExec_t> graphs;
   // K4 timing ring: events around GEMM1 / GEMM2 of every forward (no sync)
@@ -519,7 +528,8 @@ void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int3
   *c->hplan = c->plan.dev;
 }
 
-void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool upload_plan = true) {
+void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool upload_plan = true,
+                    bool gather = false) {
   if (upload_plan)
     CU_CHECK(launch_small_copy(c->dplan.p, c->hplan, sizeof(DevPlan), s));  // SM copy from mapped pinned memory
   const int nblk = gate_num_blocks(T);
@@ -542,7 +552,7 @@ void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool u
     t.base[kSendTarget] = c->send.p;
   }
   CU_CHECK(launch_dispatch(reinterpret_cast<const __nv_bfloat16*>(x), T, c->xw, c->E, c->k, c->ids.p, c->block_pre.p,
-                           c->dplan.p, t, c->row_code.p, sig, s));
+                           c->dplan.p, t, c->row_code.p, sig, s, gather ? c->perm_src.p : nullptr));
 }
 
 // The exchange step of one direction.  NCCL: grouped send/recv, forward: my
@@ -589,7 +599,7 @@ void stage_exchange(moe_ctx* c, bool forward, cudaStream_t s) {
 // B200's 1 kW cap it settles ~190 MHz lower and nets ~4% less throughput on
 // the Mixtral layer (profiles/ab_gemm_variants_r01.md), so it is opt-in
 // (MOE_GEMM_VARIANT=2sm) until it is made more energy-efficient.
-void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t rows = 0) {
+void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t rows = 0, bool gather = false) {
   Layer& L = c->layers[layer];
   if (c->fp32) {  // K7: SIMT fp32 grouped GEMMs (+ SwiGLU pass between them)
     const GemmSeg* segs = c->dplan.p->segs;
@@ -622,12 +632,13 @@ void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t r
   // 1-SM kernel with the dynamic tile scheduler (counter pair per GEMM)
   int* sched = c->dyn_sched ? c->gemm_sched.p + 2 * which : nullptr;
   if (which == 0)
-    CU_CHECK(launch_grouped_gemm(0, &c->tmA1, &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d,
-                                 2 * c->ff, reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, c->num_sms, s, sched,
-                                 c->use_pdl));
+    CU_CHECK(launch_grouped_gemm(0, gather ? &c->tmX : &c->tmA1, &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg,
+                                 2 * c->ff, c->d, 2 * c->ff, reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff,
+                                 c->num_sms, s, sched, c->use_pdl, gather ? c->perm_src.p : nullptr));
   else
     CU_CHECK(launch_grouped_gemm(1, &c->tmA2, &L.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
-                                 reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s, sched, c->use_pdl));
+                                 reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s, sched, c->use_pdl,
+                                 nullptr));
 }
 
 void stage_expert(moe_ctx* c, int layer, cudaStream_t s) {
@@ -712,6 +723,14 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
                      bool capturing, Mark&& mark) {
   const unsigned rec = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
   const bool deferred = c->G == 1 || ahead;
+  // single GPU, bf16, 1-SM K4: GEMM1 gathers its A rows from x (TMA gather4)
+  // and the dispatch kernel only ranks — no permuted copy of the tokens
+  const bool gather = c->gather && c->G == 1 && !c->fp32 && (c->gemm_variant == 0 || c->gemm_variant == 1) && T > 0;
+  if (gather && (c->tmX_ptr != x || c->tmX_T != T)) {
+    c->tmX = make_kmajor_map(x, T, c->d, 1);
+    c->tmX_ptr = x;
+    c->tmX_T = T;
+  }
   mark(0);
   stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr);
   if (c->G > 1 && c->p2p) {
@@ -734,7 +753,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
     else
       CU_CHECK(launch_plan_exchange(c->counts_all.p, stride, c->G, c->rank, L.ptab.p, c->dplan.p, s));
     mark(2);
-    stage_dispatch(c, x, T, s, /*upload_plan=*/false);
+    stage_dispatch(c, x, T, s, /*upload_plan=*/false, gather);
   } else {
     mark(1);
     CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram
@@ -743,7 +762,8 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
     mark(2);
     stage_dispatch(c, x, T, s);  // uploads the plan; P2P rows land in their owners' buffers
   }
-  if (x_consumed) CU_CHECK(cudaEventRecordWithFlags(x_consumed, s, rec));  // x is not read after dispatch
+  // x is not read after dispatch (after GEMM1 when GEMM1 gathers from it)
+  if (x_consumed && !gather) CU_CHECK(cudaEventRecordWithFlags(x_consumed, s, rec));
   mark(3);
   stage_exchange(c, true, s);
   mark(4);
@@ -751,12 +771,14 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   const int64_t rows = c->G == 1 ? static_cast<int64_t>(T) * c->k : (ahead ? c->rows_cap : c->plan.rows_local);
   const int gslot = static_cast<int>(c->gemm_seq % moe_ctx::kGemmRing);
   if (!capturing) CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][0], s));
-  launch_ffn_gemm(c, layer, 0, s, rows);
+  launch_ffn_gemm(c, layer, 0, s, rows, gather);
   // (with PDL, an event between the GEMMs would serialise them: GEMM1+GEMM2 is
   // then timed as one interval, reported as GEMM1 with GEMM2 = 0)
   if (!capturing && !c->use_pdl) CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][1], s));
   mark(5);
   launch_ffn_gemm(c, layer, 1, s, rows);
+  // (after GEMM2, not between the GEMMs: an event there would serialise the PDL pair)
+  if (x_consumed && gather) CU_CHECK(cudaEventRecordWithFlags(x_consumed, s, rec));
   if (!capturing) {
     CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][2], s));
     c->gemm_rows[gslot] = ahead ? -1 : rows;  // "ahead": filled in when the plan is flushed
@@ -901,6 +923,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->num_sms = prop.multiProcessorCount;
     if (const char* v = std::getenv("MOE_GEMM_SCHED")) c->dyn_sched = std::string(v) == "dynamic";
     if (const char* v = std::getenv("MOE_PDL")) c->use_pdl = std::string(v) != "0";
+    if (const char* v = std::getenv("MOE_GATHER")) c->gather = std::string(v) == "1";
     if (const char* v = std::getenv("MOE_GEMM_VARIANT")) {
       const std::string s(v);
       c->gemm_variant = s == "1sm" ? 1 : (s == "2sm" ? 2 : (s == "m256" ? 3 : 0));
@@ -934,6 +957,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     // row buffers in 16-bit units: one row = d_model * elem units (elem 2 for fp32)
     c->xw = c->d * c->elem;
     c->xp.alloc(static_cast<size_t>(c->rows_cap) * c->xw);
+    c->perm_src.alloc(static_cast<size_t>(c->rows_cap));
     c->h.alloc(static_cast<size_t>(c->rows_cap) * c->ff * c->elem);
     c->yp.alloc(static_cast<size_t>(c->rows_cap) * c->xw);
     c->send.alloc(static_cast<size_t>(c->send_cap) * c->xw);
@@ -1442,6 +1466,7 @@ int moe_buffer(moe_ctx* c, int which, void** ptr, int64_t* rows) {
       case 8: *ptr = c->h.p; r = c->plan.rows_local; break;
       case 9: *ptr = c->p2p ? c->slab.p + c->off_flags : nullptr; r = kFlagKinds * kMaxRanks; break;  // P2P flags
       case 10: *ptr = c->epoch_dev.p; r = 1; break;  // P2P device epoch
+      case 11: *ptr = c->perm_src.p; r = c->plan.rows_local; break;  // gathered GEMM1: row -> token
       default: throw std::invalid_argument("unknown buffer id");
     }
     if (rows) *rows = r;

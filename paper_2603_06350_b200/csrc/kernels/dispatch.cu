@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(128)
 dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const int32_t* __restrict__ ids,
                 const int32_t* __restrict__ block_pre, const DevPlan* __restrict__ plan,
                 const __grid_constant__ RowTargets targets, uint32_t* __restrict__ row_code,
-                const __grid_constant__ PeerSignal sig) {
+                const __grid_constant__ PeerSignal sig, int32_t* __restrict__ perm_src) {
   __shared__ uint32_t codes[32 * K];
   // the block's prefix row and the plan tables the ranking reads, staged once
   // (coalesced) so the ranking never waits on L2
@@ -138,8 +138,13 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
             static_cast<uint32_t>(s_rrow[f] + gr) | (static_cast<uint32_t>(s_rrem[f]) << kTargetShift);
         codes[lane * K + j] = code;
         if (blockIdx.y == 0) row_code[(size_t)t * K + j] = code;
+        if (perm_src) perm_src[code & kRowMask] = t;  // gathered GEMM1: row -> token
       }
     }
+  }
+  if (perm_src) {  // single GPU, gathered GEMM1: the rows are read from x in place
+    griddep_launch_dependents();
+    return;
   }
   __syncthreads();
 
@@ -429,14 +434,16 @@ cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, co
 
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
                             const int32_t* block_pre, const DevPlan* plan, const RowTargets& targets,
-                            uint32_t* row_code, const PeerSignal& sig, cudaStream_t s) {
+                            uint32_t* row_code, const PeerSignal& sig, cudaStream_t s, int32_t* perm_src) {
   if (T <= 0) return cudaSuccess;
   if (d % 8) return cudaErrorInvalidValue;
   const int nblk = (T + 31) / 32;
   // at least ~2 CTAs per SM: split each row's chunks when there are few blocks
-  const int split = std::max(1, std::min((2 * 148 + nblk - 1) / nblk, d / 8 / 16));
+  // (ranking only when GEMM1 gathers the rows itself)
+  const int split = perm_src ? 1 : std::max(1, std::min((2 * 148 + nblk - 1) / nblk, d / 8 / 16));
   const dim3 grid(nblk, split);
-  MOE_SWITCH_K(k, (dispatch_kernel<KK><<<grid, 128, 0, s>>>(x, T, d, E, ids, block_pre, plan, targets, row_code, sig)));
+  MOE_SWITCH_K(k, (dispatch_kernel<KK><<<grid, 128, 0, s>>>(x, T, d, E, ids, block_pre, plan, targets, row_code, sig,
+                                                            perm_src)));
   return cudaGetLastError();
 }
 

@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total,
                     int k_total, int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld,
-                    int* __restrict__ sched) {
+                    int* __restrict__ sched, const int32_t* __restrict__ a_gather) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout::bars);
@@ -153,7 +153,78 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   // this grid's CTAs retire and stream their own weights during our tail
   griddep_launch_dependents();
 
-  if (warp == 0) {
+  if (warp == 0 && a_gather) {
+    // ------------------------------------------- producer, gathered A rows
+    // GEMM1 straight from the token rows (single GPU): permuted row p of the
+    // A operand is token a_gather[p] of x, so the dispatch kernel only ranks
+    // and never copies rows.  The whole warp produces: lane i gathers rows
+    // 4i .. 4i+3 of every A stage with one TMA gather4; lane 0 also loads B.
+    int stage = 0;
+    uint32_t phase = 0;
+    int rslot = 0;
+    uint32_t rphase = 0;
+    const uint64_t pol_b = policy_evict_last();
+    const int rows_end = nseg > 0 ? segs[nseg - 1].x + segs[nseg - 1].y : 0;
+    int t = blockIdx.x;
+    bool first = true;
+    while (true) {
+      if (sched) {
+        if (lane == 0) t = atomicAdd(sched, 1);
+        t = __shfl_sync(0xffffffffu, t, 0);
+      }
+      mbar_wait(&ring_empty[rslot], rphase ^ 1);
+      if (lane == 0) {
+        ring[rslot] = t < total_tiles ? t : -1;
+        mbar_arrive(&ring_full[rslot]);
+      }
+      if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
+      if (t >= total_tiles) break;
+      const TileCoord c = decode_tile<kGroupM<EPI>>(t, seg_tiles, segs, nseg, n_tiles);
+      const int a_row = segs[c.seg].x + c.m * BM;
+      const int b_row = segs[c.seg].z * b_rows_per_slot + c.n * BN;
+      int kb0 = 0;
+      if (first) {
+        first = false;
+        kb0 = num_kb < STAGES ? num_kb : STAGES;
+        if (lane == 0)
+          for (int kb = 0; kb < kb0; ++kb) {
+            mbar_arrive_expect_tx(&full[kb], kStageBytes);
+            tma_load_2d_hint(smem + SmemLayout::b + kb * kStageBytesB, &tmB, &full[kb], kb * BK, b_row, pol_b);
+          }
+        griddep_wait();  // the row list is the previous kernel's output
+      }
+      int r[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int p = a_row + 4 * lane + v;
+        r[v] = p < rows_end ? a_gather[p] : 0;  // rows past the last segment: any valid row
+      }
+      __syncwarp();
+      for (int kb = 0; kb < kb0; ++kb)
+        tma_gather4(smem + SmemLayout::a + kb * kStageBytesA + lane * 4 * BK * 2, &tmA, &full[kb], kb * BK, r[0],
+                    r[1], r[2], r[3]);
+      if (kb0) {
+        stage = kb0 == STAGES ? 0 : kb0;
+        phase = kb0 == STAGES ? 1u : 0u;
+      }
+      for (int kb = kb0; kb < num_kb; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[stage], kStageBytes);
+          tma_load_2d_hint(smem + SmemLayout::b + stage * kStageBytesB, &tmB, &full[stage], kb * BK, b_row, pol_b);
+        }
+        __syncwarp();
+        tma_gather4(smem + SmemLayout::a + stage * kStageBytesA + lane * 4 * BK * 2, &tmA, &full[stage], kb * BK,
+                    r[0], r[1], r[2], r[3]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (!sched) t += gridDim.x;
+    }
+    if (sched && lane == 0 && atomicAdd(sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+    }
+  } else if (warp == 0) {
     // ---------------------------------------------------------- producer
     if (elect_one()) {
       int stage = 0;
@@ -715,7 +786,7 @@ int gemm_smem_bytes() { return static_cast<int>(kSmemBytes); }
 cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                 __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, int* sched,
-                                bool pdl) {
+                                bool pdl, const int32_t* a_gather) {
   if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
   static bool configured = false;
   if (!configured) {
@@ -737,9 +808,9 @@ cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorM
   cfg.numAttrs = 1;
   if (epi == EPI_SWIGLU)
     return cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI_SWIGLU>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                              b_rows_per_slot, out, out_ld, sched);
+                              b_rows_per_slot, out, out_ld, sched, a_gather);
   return cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI_STORE>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                            b_rows_per_slot, out, out_ld, sched);
+                            b_rows_per_slot, out, out_ld, sched, a_gather);
 }
 
 // Load every kernel of this file now (CUDA 12 loads kernels lazily on first

@@ -84,6 +84,18 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* desc, ui
       : "memory");
 }
 
+// TMA gather4 (sm_100a): 4 arbitrary rows r0..r3 of a 2D K-major tensor whose
+// map has a {64 cols, 1 row} box, columns [c0, c0 + 64), land as 4 consecutive
+// 128-byte rows at smem_dst (swizzled by smem address like a tile load).
+__device__ __forceinline__ void tma_gather4(void* smem_dst, const void* desc, uint64_t* bar, int c0, int r0,
+                                            int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+
 // Same, with an L2 cache-policy hint (createpolicy result).
 __device__ __forceinline__ void tma_load_2d_hint(void* smem_dst, const void* desc, uint64_t* bar,
                                                  int c0, int c1, uint64_t policy) {

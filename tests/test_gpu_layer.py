@@ -128,3 +128,29 @@ def test_layer_forward_matches_torch_fp32(cuda):
     err = float((y - ref).abs().max() / ref.abs().max())
     assert err <= TOL_REL, err
     m.close()
+
+
+@pytest.mark.parametrize("E,k,d,ff,T,rc", [
+    (8, 2, 1024, 3584, 999, [2, 1, 3, 1, 1, 1, 1, 2]),
+    (64, 8, 2048, 1408, 256, [1] * 60 + [2, 3, 1, 2]),
+    (16, 2, 4096, 1408, 1, [1] * 16),
+])
+def test_gathered_gemm1_matches_dispatch_copy(cuda, monkeypatch, E, k, d, ff, T, rc):
+    """Single GPU: GEMM1 gathering its rows from x with TMA gather4 (default)
+    must give bit-identical outputs to GEMM1 over the dispatch kernel's
+    permuted copy (MOE_GATHER=0), and the row -> token list it reads must be
+    the inverse of the row codes."""
+    import torch
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("MOE_GATHER", flag)
+        m, st, y, y_ref, ids_o, counts_o = _layer_case(cuda, E, k, d, ff, T, rc)
+        assert _rel_err(y, y_ref) <= TOL_REL
+        if flag == "1":
+            codes = m.read_buffer(6, np.uint32, (T, k)).reshape(-1).astype(np.int64)
+            perm = m.read_buffer(11, np.int32, (T * k,))
+            assert np.array_equal(np.sort(codes), np.arange(T * k))
+            assert np.array_equal(perm[codes], np.repeat(np.arange(T), k))
+        outs.append(y)
+        m.close()
+    assert np.array_equal(outs[0], outs[1])
