@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
                     help="N>1 token exchange: peer memory over NVLink (dispatch/combine read and write the "
                          "owners' buffers) or NCCL grouped send/recv")
+    ap.add_argument("--residency", choices=["all", "placed"], default="all",
+                    help="N>1 expert weights: every expert resident on every GPU, or only home experts + "
+                         "replica cache slots with cold replicas copied from their home GPU over NVLink")
     return ap.parse_args()
 
 
@@ -260,7 +263,8 @@ def run_ours(args):
     m = MoELayer(1, E, k, d, ff, max_tokens=T, world_size=G, rank=rank, device=local,
                  exchange_mode=MOE_EXCHANGE_P2P if p2p else MOE_EXCHANGE_NCCL,
                  nccl_unique_id=uid, expert_mem_mb=mem, layer_mem_cap_mb=c["extra_replicas"] * mem,
-                 gpu_mem_capacity_mb=180000.0, cv_threshold=0.2, keep_alive_iters=50)
+                 gpu_mem_capacity_mb=180000.0, cv_threshold=0.2, keep_alive_iters=50,
+                 residency=1 if (p2p and args.residency == "placed") else 0)
     if p2p:  # map every rank's exchange slab (CUDA IPC over NVLink)
         handles = [None] * G
         dist.all_gather_object(handles, m.p2p_export())
@@ -285,8 +289,8 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for it in range(args.warmup):
-        step(it, stats=False)
+    placed = p2p and args.residency == "placed"
+    cold = [step(it, stats=placed) for it in range(args.warmup)]  # PLACED: the cold starts happen here
     barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -313,6 +317,19 @@ def run_ours(args):
               for name in ("gate_ms", "plan_ms", "dispatch_ms", "a2a_dispatch_ms", "gemm1_ms", "gemm2_ms",
                            "a2a_combine_ms", "combine_ms")}
     replicas = statistics.median(s.replica_count for s in stats)
+    residency = None
+    if p2p and args.residency == "placed":
+        residency = {"mode": "placed (home experts + replica cache slots, cold copies from the home GPU)",
+                     "copies_per_step": statistics.mean(s.weight_copies for s in stats),
+                     "hits_per_step": statistics.mean(s.weight_hits for s in stats),
+                     "copy_ms_median_when_cold": statistics.median(
+                         [s.weight_copy_ms for s in stats if s.weight_copies] or [0.0]),
+                     "copy_mb_per_step": statistics.mean(s.weight_copy_mb for s in stats),
+                     "warmup_copies": [s.weight_copies for s in cold],
+                     "warmup_copy_ms": [round(s.weight_copy_ms, 3) for s in cold],
+                     "warmup_forward_ms": [round(s.forward_ms, 3) for s in cold],
+                     "note": "copy time measured on the weight stream (peer copy engine); with "
+                             "MOE_BENCH_SHARE_DEVICE the 'peer' is the same GPU (D2D, not NVLink)"}
 
     # e2e through the host-buffer C-ABI entry point
     e2e = None
@@ -385,6 +402,8 @@ def run_ours(args):
                          "traffic_source": (traffic or {}).get("source")},
             "clocks": clk.summary(),
         }
+        if residency is not None:
+            line["residency"] = residency
         if e2e is not None:
             xb = T * d * 2 + E * d * 2
             line["e2e"] = {"value": G * T * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s",

@@ -106,8 +106,32 @@ typedef struct {
   int precision;              /* MOE_PRECISION_BF16 (default) or MOE_PRECISION_FP32 */
   int use_cuda_graphs;        /* 1: single-GPU forwards are captured once per (layer, tokens,
                                  buffers) and replayed as one CUDA graph launch */
-  int reserved[4];
+  int residency;              /* MOE_RESIDENCY_ALL (default) or MOE_RESIDENCY_PLACED */
+  int replica_slots;          /* PLACED: cache slots per layer for replicas of non-home experts
+                                 (0 = min(E - home, gpu_mem_capacity_mb / expert_mem_mb)) */
+  int reserved[2];
 } moe_ctx_desc;
+
+/* Expert weight residency (the reference's ReplicaRegistry
+   keep-alive, proj/src/placer.cpp:11-43,124-130, and cold starts,
+   simulator.cpp:198-199).
+   ALL:    every expert of every layer is resident on every rank (180 GB of HBM
+           holds a 32-layer Mixtral stack), so any placement runs without
+           copies.
+   PLACED: rank g permanently holds only its home experts (e mod G == g, the
+           static_plan placement, baselines.cpp:32-60) plus replica_slots cache
+           slots per layer.  When a placement puts a replica of a non-home
+           expert on g and the expert is not cached, its weights are copied
+           from the home rank's slot over NVLink (peer memory, copy engine, on
+           a side stream ordered after the layer's previous forward) into a
+           free or least-recently-used slot; the layer's GEMMs wait for the
+           copy.  A placement planned d layers ahead (MOE_PLAN_PREDICTED)
+           therefore pre-warms its replicas while the layers between run; a
+           synchronous plan (MOE_PLAN_SYNC) pays the copy on the critical path
+           — the measured cold start.  Requires MOE_EXCHANGE_P2P (G > 1); at
+           G == 1 every expert is home.  moe_load_expert_weights stores home
+           experts only (calls for other experts are accepted and ignored). */
+enum { MOE_RESIDENCY_ALL = 0, MOE_RESIDENCY_PLACED = 1 };
 
 /* precision of activations, weights and outputs.  BF16: bf16 in/out, fp32
    accumulate on tcgen05 (tolerance 2e-2).  FP32: fp32 in/out, fp32 FFMA
@@ -131,6 +155,11 @@ typedef struct {
   int32_t counts[256];          /* this rank's gate histogram (E <= 256) */
   double predictor_accuracy;    /* measure_accuracy(prediction made d layers ago, actual); -1 if none */
   int32_t plan_source;          /* 0 fixed, 1 actual loads, 2 predicted ahead, 3 history bootstrap */
+  /* MOE_RESIDENCY_PLACED: weight movement caused by this layer's latest placement */
+  int32_t weight_copies;        /* experts copied into cache slots (cold) */
+  int32_t weight_hits;          /* non-home experts already cached (warm) */
+  double weight_copy_ms;        /* copy-stream time of those copies (0 if none) */
+  double weight_copy_mb;        /* bytes copied, MB */
 } moe_layer_stats;
 
 const char* moe_last_error(void);
@@ -155,7 +184,9 @@ typedef struct {
   uint64_t bytes;        /* slab size */
   uint64_t off_flags, off_counts, off_xp, off_yp;
   int32_t device, rank, world_size, version;
-  unsigned char reserved[56];
+  uint64_t off_weights;  /* MOE_RESIDENCY_PLACED: weight slots inside the slab */
+  uint64_t weight_bytes;
+  unsigned char reserved[40];
 } moe_p2p_handle;        /* 192 bytes */
 int moe_p2p_export(moe_ctx* ctx, moe_p2p_handle* out);
 int moe_p2p_import(moe_ctx* ctx, const moe_p2p_handle* handles, int n);
@@ -240,6 +271,10 @@ int moe_forward_end(moe_ctx* ctx, uint16_t* y_dev, void* stream);
    of a single-GPU forward whose GEMM1 gathers x in place (int32, written
    instead of buffer 0 there).  rows_out = valid rows. */
 int moe_buffer(moe_ctx* ctx, int which, void** ptr_out, int64_t* rows_out);
+/* Weight residency of one layer on this rank: slot_of[E] = weight slot the
+   GEMMs read for expert e (-1: not resident here; ALL: slot_of[e] == e),
+   n_slots_out = slots in the layer's pool. */
+int moe_residency(moe_ctx* ctx, int layer, int32_t* slot_of, int* n_slots_out);
 /* cudaMemcpyDefault-style copy between any host/device pointers (UVA), on the
    ctx stream, synchronous on return — the transport hook of the staged API. */
 int moe_memcpy(moe_ctx* ctx, void* dst, const void* src, size_t bytes);

@@ -303,7 +303,7 @@ class MoELayer:
                  num_predictor_targets: int = 0, expert_mem_mb: float = 0.0,
                  layer_mem_cap_mb: float = 0.0, gpu_mem_capacity_mb: float = 180000.0,
                  cv_threshold: float = 0.2, keep_alive_iters: int = 50, predictor_distance: int = 1,
-                 precision: int = 0, cuda_graphs: bool = False):
+                 precision: int = 0, cuda_graphs: bool = False, residency: int = 0, replica_slots: int = 0):
         d = MoeCtxDesc()
         d.num_layers, d.num_experts, d.top_k = num_layers, num_experts, top_k
         d.d_model, d.d_ff, d.max_tokens = d_model, d_ff, max_tokens
@@ -317,6 +317,7 @@ class MoELayer:
         d.predictor_distance = predictor_distance
         d.precision = precision
         d.use_cuda_graphs = int(cuda_graphs)
+        d.residency, d.replica_slots = residency, replica_slots
         self.fp32 = precision == 1
         h = C.c_void_p()
         check(lib.moe_ctx_create(C.byref(d), C.byref(h)))
@@ -344,6 +345,13 @@ class MoELayer:
 
     def sync(self) -> None:
         check(lib.moe_ctx_sync(self._h))
+
+    def residency(self, layer: int) -> Tuple[np.ndarray, int]:
+        """(slot of each expert on this rank, -1 = not resident; slots in the layer's pool)."""
+        out = np.empty(self.E, np.int32)
+        n = C.c_int()
+        check(lib.moe_residency(self._h, layer, out.ctypes.data, C.byref(n)))
+        return out, n.value
 
     def p2p_export(self) -> bytes:
         """This rank's peer-memory handle (MOE_EXCHANGE_P2P): 192 opaque bytes

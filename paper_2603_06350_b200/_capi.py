@@ -16,6 +16,7 @@ MOE_OK, MOE_EINVAL, MOE_EINFEASIBLE, MOE_ECUDA, MOE_ENCCL, MOE_ESTATE = range(6)
 MOE_EXCHANGE_NCCL, MOE_EXCHANGE_EXTERNAL, MOE_EXCHANGE_P2P = 0, 1, 2
 MOE_PLAN_FIXED, MOE_PLAN_SYNC, MOE_PLAN_PREDICTED = 0, 1, 2
 MOE_PRECISION_BF16, MOE_PRECISION_FP32 = 0, 1
+MOE_RESIDENCY_ALL, MOE_RESIDENCY_PLACED = 0, 1
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -37,7 +38,8 @@ class MoeCtxDesc(C.Structure):
         ("num_predictor_targets", C.c_int),
         ("expert_mem_mb", dbl), ("layer_mem_cap_mb", dbl), ("gpu_mem_capacity_mb", dbl),
         ("cv_threshold", dbl), ("keep_alive_iters", C.c_int), ("predictor_distance", C.c_int),
-        ("precision", C.c_int), ("use_cuda_graphs", C.c_int), ("reserved", C.c_int * 4),
+        ("precision", C.c_int), ("use_cuda_graphs", C.c_int), ("residency", C.c_int),
+        ("replica_slots", C.c_int), ("reserved", C.c_int * 2),
     ]
 
 
@@ -49,6 +51,7 @@ class MoeLayerStats(C.Structure):
         ("a2a_combine_ms", dbl), ("combine_ms", dbl), ("rows_local", i64), ("rows_sent", i64),
         ("warm_count", C.c_int), ("cold_count", C.c_int), ("counts", i32 * 256),
         ("predictor_accuracy", dbl), ("plan_source", i32),
+        ("weight_copies", i32), ("weight_hits", i32), ("weight_copy_ms", dbl), ("weight_copy_mb", dbl),
     ]
 
 
@@ -57,7 +60,7 @@ class MoeP2PHandle(C.Structure):
         ("ipc", C.c_ubyte * 64), ("pid", u64), ("base", u64), ("bytes", u64),
         ("off_flags", u64), ("off_counts", u64), ("off_xp", u64), ("off_yp", u64),
         ("device", i32), ("rank", i32), ("world_size", i32), ("version", i32),
-        ("reserved", C.c_ubyte * 56),
+        ("off_weights", u64), ("weight_bytes", u64), ("reserved", C.c_ubyte * 40),
     ]
 
 
@@ -98,6 +101,7 @@ _sig("moe_layer_forward_host_async", C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_
 _sig("moe_wait", C.c_int, vp, i64)
 _sig("moe_host_alloc", C.c_int, C.c_size_t, P(vp))
 _sig("moe_gemm_times", C.c_int, vp, C.c_int, vp, vp, vp, P(C.c_int))
+_sig("moe_residency", C.c_int, vp, C.c_int, vp, P(C.c_int))
 _sig("moe_host_free", C.c_int, vp)
 _sig("moe_forward_begin", C.c_int, vp, C.c_int, vp, C.c_int, vp, vp)
 _sig("moe_forward_expert", C.c_int, vp, C.c_int, vp)
@@ -134,7 +138,7 @@ EXPORTED = [
     "moe_load_expert_weights_f32", "moe_set_gate_weights_f32",
     "moe_set_predictor_weights", "moe_set_placement", "moe_gate_topk", "moe_predict_loads",
     "moe_layer_forward", "moe_layer_forward_host", "moe_layer_forward_host_async", "moe_wait",
-    "moe_host_alloc", "moe_host_free", "moe_gemm_times",
+    "moe_host_alloc", "moe_host_free", "moe_gemm_times", "moe_residency",
     "moe_forward_begin", "moe_forward_expert",
     "moe_forward_end", "moe_buffer", "moe_memcpy", "moe_exchange_plan", "moe_exchange_plan_direct", "moe_plan_scale",
     "moe_registry_create", "moe_registry_destroy", "moe_registry_size", "moe_plan_place",

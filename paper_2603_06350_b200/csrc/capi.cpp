@@ -264,6 +264,16 @@ struct Layer {
   DevBuf<PlacementTable> ptab;
   PlacementTable* h_ptab = nullptr;  // pinned staging
   cudaEvent_t ev_ptab = nullptr;     // staging buffer free again
+  // MOE_RESIDENCY_PLACED: which weight slot holds each expert on this rank
+  std::vector<int> slot_of;           // [E], -1 = not resident
+  std::vector<int> cache_expert;      // [cache slots] expert cached there, -1 free
+  std::vector<long> cache_stamp;      // [cache slots] last placement that needed it (LRU)
+  long placements = 0;
+  std::vector<std::pair<int, int>> pending_copies;  // (slot, expert) not yet issued
+  cudaEvent_t ev_used = nullptr;      // after the layer's last enqueued GEMM2 (slots free to overwrite)
+  cudaEvent_t ev_wstart = nullptr, ev_wready = nullptr;  // the latest copy batch on the weight stream
+  bool used_recorded = false, wready_valid = false, wready_timed = false;
+  int copies_last = 0, hits_last = 0;
 };
 
 struct GraphKey {
@@ -382,6 +392,15 @@ struct moe_ctx {
   int* p2p_err = nullptr;                  // mapped pinned: first timed-out wait (1 + kind*8 + rank)
   DevBuf<uint32_t> dispatch_counter;       // CTAs of the signalling dispatch grid that finished
   uint64_t p2p_timeout_ns = 10000000000ull;
+  // expert weight residency (MOE_RESIDENCY_PLACED): per layer [home slots | cache
+  // slots] of W13 then W2 inside the slab, so peers can copy home experts out
+  bool placed = false;
+  int home_slots = 0, cache_slots = 0, slots = 0;
+  size_t off_weights = 0, layer_wbytes = 0, w13_slot_bytes = 0, w2_slot_bytes = 0;
+  uint8_t* peer_base[kMaxRanks] = {};
+  cudaStream_t wstream = nullptr;        // weight copies (copy engines, off the compute stream)
+  cudaEvent_t ev_peers_ready = nullptr;  // after the first forward's cross-rank handshake
+  bool peers_ready = false;
 };
 
 namespace {
@@ -400,12 +419,92 @@ void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, 
                             pred_counts ? pred_counts : c->pred_counts.p, c->gate_partial.p, s));
 }
 
-// The placement changed (planner, moe_set_placement or default): refresh the
-// device copy the on-device exchange planner reads (peer-memory contexts).
+void ensure_pools(moe_ctx* c, Layer& L);
+
+// MOE_RESIDENCY_PLACED: issue the layer's pending weight copies on the weight
+// stream — each cold expert's W13/W2 from its home rank's slot (peer memory
+// over NVLink, copy engines) into the cache slot chosen for it.  The stream
+// first waits for the layer's last enqueued GEMMs (the slot may hold an
+// evicted expert they still read); the layer's next GEMM1 waits for ev_wready.
+// Before the first forward's cross-rank handshake a peer may not have loaded
+// its home experts yet, so copies wait for it (issued from enqueue_forward).
+void issue_weight_copies(moe_ctx* c, int layer) {
+  Layer& L = c->layers[layer];
+  if (L.pending_copies.empty() || !c->peers_ready) return;
+  if (L.used_recorded) CU_CHECK(cudaStreamWaitEvent(c->wstream, L.ev_used, 0));
+  CU_CHECK(cudaEventRecord(L.ev_wstart, c->wstream));
+  const size_t lo = static_cast<size_t>(layer) * c->layer_wbytes;
+  const size_t w2_base = static_cast<size_t>(c->slots) * c->w13_slot_bytes;
+  uint8_t* dst = c->slab.p + c->off_weights + lo;
+  for (const auto& sc : L.pending_copies) {
+    const int slot = sc.first, e = sc.second;
+    const uint8_t* src = c->peer_base[e % c->G] + c->off_weights + lo;
+    const size_t hs = static_cast<size_t>(e / c->G);
+    CU_CHECK(cudaMemcpyAsync(dst + slot * c->w13_slot_bytes, src + hs * c->w13_slot_bytes, c->w13_slot_bytes,
+                             cudaMemcpyDefault, c->wstream));
+    CU_CHECK(cudaMemcpyAsync(dst + w2_base + slot * c->w2_slot_bytes, src + w2_base + hs * c->w2_slot_bytes,
+                             c->w2_slot_bytes, cudaMemcpyDefault, c->wstream));
+  }
+  CU_CHECK(cudaEventRecord(L.ev_wready, c->wstream));
+  L.wready_valid = true;
+  L.wready_timed = true;
+  L.pending_copies.clear();
+}
+
+// MOE_RESIDENCY_PLACED: make every expert that has a replica on this rank
+// resident — its home slot, the cache slot it already occupies (warm: the
+// ReplicaRegistry keep-alive made physical, placer.cpp:84-92), or a free /
+// least-recently-used cache slot it is copied into (cold).  Co-located
+// replicas of one expert share one slot (they are one GEMM segment).
+void apply_residency(moe_ctx* c, int layer) {
+  Layer& L = c->layers[layer];
+  if (!c->placed) return;
+  ensure_pools(c, L);
+  ++L.placements;
+  std::vector<char> need(c->E, 0);
+  size_t f = 0;
+  for (int e = 0; e < c->E; ++e)
+    for (int r = 0; r < L.rep_counts[e]; ++r, ++f)
+      if (L.rep_gpu[f] == c->rank) need[e] = 1;
+  int copies = 0, hits = 0;
+  for (int e = 0; e < c->E; ++e)
+    if (need[e] && e % c->G != c->rank && L.slot_of[e] >= 0) {
+      L.cache_stamp[L.slot_of[e] - c->home_slots] = L.placements;
+      ++hits;
+    }
+  for (int e = 0; e < c->E; ++e) {
+    if (!need[e] || e % c->G == c->rank || L.slot_of[e] >= 0) continue;
+    int best = -1;  // a free slot (stamp -1) or the least recently needed one this placement does not use
+    for (int i = 0; i < c->cache_slots; ++i) {
+      const int ce = L.cache_expert[i];
+      if (ce >= 0 && need[ce]) continue;
+      if (best < 0 || L.cache_stamp[i] < L.cache_stamp[best]) best = i;
+    }
+    if (best < 0)
+      throw Status(MOE_EINFEASIBLE, "no replica slot free for expert " + std::to_string(e) + " of layer " +
+                                        std::to_string(layer) + " on GPU " + std::to_string(c->rank) + " (" +
+                                        std::to_string(c->cache_slots) + " cache slots)");
+    if (L.cache_expert[best] >= 0) L.slot_of[L.cache_expert[best]] = -1;  // evicted
+    L.cache_expert[best] = e;
+    L.cache_stamp[best] = L.placements;
+    L.slot_of[e] = c->home_slots + best;
+    L.pending_copies.emplace_back(c->home_slots + best, e);
+    ++copies;
+  }
+  L.copies_last = copies;
+  L.hits_last = hits;
+  if (copies == 0) L.wready_timed = false;
+  issue_weight_copies(c, layer);
+}
+
+// The placement changed (planner, moe_set_placement or default): make its
+// replicas resident (PLACED) and refresh the device copy the on-device
+// exchange planner reads (peer-memory contexts).
 void placement_changed(moe_ctx* c, int layer) {
   Layer& L = c->layers[layer];
   L.has_placement = true;
   if (!c->p2p) return;
+  apply_residency(c, layer);
   const int R = static_cast<int>(L.rep_gpu.size());
   if (R > kMaxReplicas) throw std::invalid_argument("too many replicas in one layer");
   if (!L.ptab.p) {
@@ -425,6 +524,7 @@ void placement_changed(moe_ctx* c, int layer) {
   }
   t.rep_base[c->E] = f;
   for (int i = 0; i < R; ++i) t.gpu_of[i] = L.rep_gpu[i];
+  for (int e = 0; e < c->E; ++e) t.slot_of[e] = c->placed ? std::max(0, L.slot_of[e]) : e;
   // SM copy from mapped memory: never queues behind bulk token copies
   CU_CHECK(launch_small_copy(L.ptab.p, L.h_ptab, sizeof(PlacementTable), c->stream));
   CU_CHECK(cudaEventRecord(L.ev_ptab, c->stream));
@@ -523,6 +623,12 @@ void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int3
   L.history.push_back({layer, total});
   if (L.history.size() > 16) L.history.erase(L.history.begin());
   build_exchange_plan(c->G, c->rank, c->E, all.data(), L.rep_counts.data(), L.rep_gpu.data(), c->plan, c->p2p);
+  if (c->placed)  // GEMM segments read the expert's resident slot, not the expert index
+    for (int i = 0; i < c->plan.dev.nseg; ++i) {
+      GemmSeg& g = c->plan.dev.segs[i];
+      require(L.slot_of[g.slot] >= 0, "expert " + std::to_string(g.slot) + " has rows here but is not resident");
+      g.slot = L.slot_of[g.slot];
+    }
   if (c->plan.rows_local > c->rows_cap || (!c->p2p && c->plan.rows_send > c->send_cap))
     throw Status(MOE_EINFEASIBLE, "received rows exceed workspace capacity");
   *c->hplan = c->plan.dev;
@@ -691,14 +797,30 @@ Layer& layer_at(moe_ctx* c, int layer) {
 
 void ensure_pools(moe_ctx* c, Layer& L) {
   if (L.w13.p) return;
-  L.w13.alloc(static_cast<size_t>(c->E) * 2 * c->ff * c->d * c->elem);
-  L.w2.alloc(static_cast<size_t>(c->E) * c->d * c->ff * c->elem);
+  // weight slots: one per expert (ALL), or home + cache slots inside the slab (PLACED)
+  const int nslots = c->placed ? c->slots : c->E;
+  if (c->placed) {
+    const size_t li = static_cast<size_t>(&L - c->layers.data());
+    uint8_t* base = c->slab.p + c->off_weights + li * c->layer_wbytes;
+    L.w13.view(base, static_cast<size_t>(nslots) * 2 * c->ff * c->d);
+    L.w2.view(base + static_cast<size_t>(nslots) * c->w13_slot_bytes, static_cast<size_t>(nslots) * c->d * c->ff);
+    L.slot_of.assign(c->E, -1);
+    for (int e = c->rank; e < c->E; e += c->G) L.slot_of[e] = e / c->G;  // home experts
+    L.cache_expert.assign(c->cache_slots, -1);
+    L.cache_stamp.assign(c->cache_slots, -1);
+    CU_CHECK(cudaEventCreateWithFlags(&L.ev_used, cudaEventDisableTiming));
+    CU_CHECK(cudaEventCreate(&L.ev_wstart));
+    CU_CHECK(cudaEventCreate(&L.ev_wready));
+  } else {
+    L.w13.alloc(static_cast<size_t>(nslots) * 2 * c->ff * c->d * c->elem);
+    L.w2.alloc(static_cast<size_t>(nslots) * c->d * c->ff * c->elem);
+  }
   L.expert_loaded.assign(c->E, 0);
   if (c->fp32) return;  // SIMT fp32 path: no tensor maps
-  L.tmB1 = make_kmajor_map(L.w13.p, static_cast<uint64_t>(c->E) * 2 * c->ff, c->d, 256);
-  L.tmB2 = make_kmajor_map(L.w2.p, static_cast<uint64_t>(c->E) * c->d, c->ff, 256);
-  L.tmB1h = make_kmajor_map(L.w13.p, static_cast<uint64_t>(c->E) * 2 * c->ff, c->d, 128);
-  L.tmB2h = make_kmajor_map(L.w2.p, static_cast<uint64_t>(c->E) * c->d, c->ff, 128);
+  L.tmB1 = make_kmajor_map(L.w13.p, static_cast<uint64_t>(nslots) * 2 * c->ff, c->d, 256);
+  L.tmB2 = make_kmajor_map(L.w2.p, static_cast<uint64_t>(nslots) * c->d, c->ff, 256);
+  L.tmB1h = make_kmajor_map(L.w13.p, static_cast<uint64_t>(nslots) * 2 * c->ff, c->d, 128);
+  L.tmB2h = make_kmajor_map(L.w2.p, static_cast<uint64_t>(nslots) * c->d, c->ff, 128);
   L.expert_loaded.assign(c->E, 0);
 }
 
@@ -737,6 +859,14 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
     // every rank reads every histogram from its owner's slab
     CU_CHECK(launch_p2p_counts(c->peers, c->G, c->rank, stride, c->epoch_dev.p, c->p2p_timeout_ns, c->p2p_err,
                                c->counts_all.p, s));
+    if (c->placed && !c->peers_ready) {
+      // every rank has entered its first forward, so every home expert is
+      // loaded: weight copies from peers may start from here on
+      CU_CHECK(cudaEventRecord(c->ev_peers_ready, s));
+      CU_CHECK(cudaStreamWaitEvent(c->wstream, c->ev_peers_ready, 0));
+      c->peers_ready = true;
+      for (size_t l = 0; l < c->layers.size(); ++l) issue_weight_copies(c, static_cast<int>(l));
+    }
     CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
   } else if (c->G > 1) {
     require(c->desc.exchange_mode == MOE_EXCHANGE_NCCL, "staged API required for external exchange");
@@ -770,6 +900,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   // rows only sizes the fp32 SwiGLU pass (bf16 GEMMs read the device plan)
   const int64_t rows = c->G == 1 ? static_cast<int64_t>(T) * c->k : (ahead ? c->rows_cap : c->plan.rows_local);
   const int gslot = static_cast<int>(c->gemm_seq % moe_ctx::kGemmRing);
+  if (c->placed && L.wready_valid) CU_CHECK(cudaStreamWaitEvent(s, L.ev_wready, 0));  // cold replicas copied in
   if (!capturing) CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][0], s));
   launch_ffn_gemm(c, layer, 0, s, rows, gather);
   // (with PDL, an event between the GEMMs would serialise them: GEMM1+GEMM2 is
@@ -779,6 +910,10 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   launch_ffn_gemm(c, layer, 1, s, rows);
   // (after GEMM2, not between the GEMMs: an event there would serialise the PDL pair)
   if (x_consumed && gather) CU_CHECK(cudaEventRecordWithFlags(x_consumed, s, rec));
+  if (c->placed) {  // the layer's slots may be overwritten once these GEMMs are done
+    CU_CHECK(cudaEventRecord(L.ev_used, s));
+    L.used_recorded = true;
+  }
   if (!capturing) {
     CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][2], s));
     c->gemm_rows[gslot] = ahead ? -1 : rows;  // "ahead": filled in when the plan is flushed
@@ -816,7 +951,7 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   const bool ahead = c->G > 1 && c->p2p && !c->fp32 &&
                      (plan_mode == MOE_PLAN_FIXED || (plan_mode == MOE_PLAN_PREDICTED && L.plan_for == iteration));
   if (ahead) ensure_placement(c, layer);
-  if (c->use_graphs && !timed && (c->G == 1 || ahead)) {
+  if (c->use_graphs && !timed && (c->G == 1 || ahead) && !c->placed) {
     // Replay the layer's whole device sequence (8-14 kernels) as one CUDA
     // graph: captured once per (layer, tokens, buffers), then launched with a
     // single call — the launch-bound decode regime pays one launch, not ten.
@@ -864,6 +999,16 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
     st->cold_count = L.cold;
     st->predictor_accuracy = L.last_accuracy;
     st->plan_source = L.plan_source;
+    st->weight_copies = L.copies_last;
+    st->weight_hits = L.hits_last;
+    st->weight_copy_mb = L.copies_last * static_cast<double>(c->w13_slot_bytes + c->w2_slot_bytes) / 1e6;
+    st->weight_copy_ms = 0.0;
+    if (L.wready_timed && L.wready_valid) {
+      float ms = 0.0f;
+      CU_CHECK(cudaEventSynchronize(L.ev_wready));
+      CU_CHECK(cudaEventElapsedTime(&ms, L.ev_wstart, L.ev_wready));
+      st->weight_copy_ms = ms;
+    }
     for (int e = 0; e < c->E && e < 256; ++e) st->counts[e] = c->h_counts[static_cast<size_t>(c->rank) * c->E + e];
   }
 }
@@ -934,6 +1079,26 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->fp32 = D.precision == MOE_PRECISION_FP32;
     c->elem = c->fp32 ? 2 : 1;
     require(!c->fp32 || c->n_pred == 0, "the fp32 mode has no fused predictor");
+    require(D.residency == MOE_RESIDENCY_ALL || D.residency == MOE_RESIDENCY_PLACED, "unknown residency");
+    c->placed = D.residency == MOE_RESIDENCY_PLACED && c->G > 1;  // G == 1: every expert is home
+    if (c->placed) {
+      require(D.exchange_mode == MOE_EXCHANGE_P2P,
+              "MOE_RESIDENCY_PLACED needs the peer-memory exchange (MOE_EXCHANGE_P2P): replicas are copied "
+              "from their home rank over NVLink");
+      require(!c->fp32, "MOE_RESIDENCY_PLACED supports the bf16 path only");
+      c->home_slots = (c->E + c->G - 1) / c->G;
+      // the same layout on every rank (peers address each other's slots)
+      const int max_cache = c->E - c->E / c->G;
+      const double mem = D.expert_mem_mb > 0 ? D.expert_mem_mb : 3.0 * c->d * c->ff * 2 / 1e6;
+      int cache = D.replica_slots > 0 ? D.replica_slots
+                                      : static_cast<int>(std::min<double>(max_cache, std::floor(
+                                            (D.gpu_mem_capacity_mb > 0 ? D.gpu_mem_capacity_mb : 180000.0) / mem)));
+      c->cache_slots = std::max(1, std::min(cache, max_cache));
+      c->slots = c->home_slots + c->cache_slots;
+      c->w13_slot_bytes = static_cast<size_t>(2) * c->ff * c->d * 2;
+      c->w2_slot_bytes = static_cast<size_t>(c->d) * c->ff * 2;
+      c->layer_wbytes = static_cast<size_t>(c->slots) * (c->w13_slot_bytes + c->w2_slot_bytes);
+    }
     CU_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     // load every kernel now, not lazily at first launch (see preload_*)
     CU_CHECK(preload_gate_kernels());
@@ -972,7 +1137,9 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
       c->off_counts = up(sizeof(uint32_t) * kFlagKinds * kMaxRanks);
       c->off_xp = c->off_counts + up(sizeof(int32_t) * c->count_stride);
       c->off_yp = c->off_xp + up(rows_bytes);
-      c->slab.alloc(c->off_yp + up(rows_bytes));
+      c->off_weights = c->off_yp + up(rows_bytes);
+      // MOE_RESIDENCY_PLACED: every layer's weight slots live in the slab too
+      c->slab.alloc(c->off_weights + (c->placed ? c->layer_wbytes * c->layers.size() : 0));
       CU_CHECK(cudaMemset(c->slab.p, 0, c->off_xp));  // flags start at epoch 0
       c->counts.view(c->slab.p + c->off_counts, pad16(sizeof(int32_t) * c->count_stride) / 4);
       c->xp.view(c->slab.p + c->off_xp, static_cast<size_t>(c->rows_cap) * c->xw);
@@ -983,6 +1150,10 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
       c->epoch_dev.alloc(4);
       CU_CHECK(cudaMemset(c->epoch_dev.p, 0, 16));
       *c->p2p_err = 0;
+      if (c->placed) {
+        CU_CHECK(cudaStreamCreateWithFlags(&c->wstream, cudaStreamNonBlocking));
+        CU_CHECK(cudaEventCreateWithFlags(&c->ev_peers_ready, cudaEventDisableTiming));
+      }
       if (const char* v = std::getenv("MOE_P2P_TIMEOUT_MS")) c->p2p_timeout_ns = std::strtoull(v, nullptr, 10) * 1000000ull;
     }
     c->dplan.alloc(1);
@@ -1026,10 +1197,14 @@ int moe_ctx_destroy(moe_ctx* c) {
     cudaStreamSynchronize(c->stream);
     if (c->comm) g_nccl.CommDestroy(c->comm);
     for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
+    if (c->wstream) cudaStreamSynchronize(c->wstream);
     for (Layer& L : c->layers) {
       if (L.h_ptab) cudaFreeHost(L.h_ptab);
-      if (L.ev_ptab) cudaEventDestroy(L.ev_ptab);
+      for (cudaEvent_t e : {L.ev_ptab, L.ev_used, L.ev_wstart, L.ev_wready})
+        if (e) cudaEventDestroy(e);
     }
+    if (c->ev_peers_ready) cudaEventDestroy(c->ev_peers_ready);
+    if (c->wstream) cudaStreamDestroy(c->wstream);
     if (c->p2p_err) cudaFreeHost(c->p2p_err);
     c->events.destroy();
     if (c->hplan) cudaFreeHost(c->hplan);
@@ -1093,6 +1268,8 @@ int moe_p2p_export(moe_ctx* c, moe_p2p_handle* out) {
     h.rank = c->rank;
     h.world_size = c->G;
     h.version = 1;
+    h.off_weights = c->off_weights;
+    h.weight_bytes = c->placed ? c->layer_wbytes * c->layers.size() : 0;
     *out = h;
   });
 }
@@ -1110,7 +1287,8 @@ int moe_p2p_import(moe_ctx* c, const moe_p2p_handle* hs, int n) {
                                                                           " is not rank " + std::to_string(g) +
                                                                           " of this world");
       require(h.bytes == c->slab.n && h.off_xp == c->off_xp && h.off_yp == c->off_yp &&
-                  h.off_counts == c->off_counts,
+                  h.off_counts == c->off_counts && h.off_weights == c->off_weights &&
+                  h.weight_bytes == (c->placed ? c->layer_wbytes * c->layers.size() : 0),
               "rank " + std::to_string(g) + " was created with a different shape");
       uint8_t* base = nullptr;
       if (g == c->rank) {
@@ -1139,6 +1317,7 @@ int moe_p2p_import(moe_ctx* c, const moe_p2p_handle* hs, int n) {
       c->peers.flags[g] = reinterpret_cast<uint32_t*>(base + h.off_flags);
       c->peers.counts[g] = reinterpret_cast<const int32_t*>(base + h.off_counts);
       c->xp_targets.base[g] = base + h.off_xp;
+      c->peer_base[g] = base;
       c->yp_targets.base[g] = base + h.off_yp;
     }
     c->p2p_ready = true;
@@ -1155,19 +1334,27 @@ void load_expert_impl(moe_ctx* c, int layer, int expert, const void* w1v, const 
   require(expert >= 0 && expert < c->E, "expert out of range");
   require(w1v && w3v && w2v, "null weight pointer");
   ensure_pools(c, L);
+  int slot = expert;
+  if (c->placed) {
+    if (expert % c->G != c->rank) {  // not home here: replicas are copied from the home rank
+      L.expert_loaded[expert] = 1;
+      return;
+    }
+    slot = expert / c->G;
+  }
   const uint16_t* w1 = static_cast<const uint16_t*>(w1v);
   const uint16_t* w3 = static_cast<const uint16_t*>(w3v);
   const uint16_t* w2 = static_cast<const uint16_t*>(w2v);
   // W13 pool: per 128-row block b of the expert, rows [W1[b*128..], W3[b*128..]]
   const size_t row = static_cast<size_t>(c->d) * elem;  // one weight row in 16-bit units
-  uint16_t* base = L.w13.p + static_cast<size_t>(expert) * 2 * c->ff * row;
+  uint16_t* base = L.w13.p + static_cast<size_t>(slot) * 2 * c->ff * row;
   for (int b = 0; b < c->ff / 128; ++b) {
     CU_CHECK(cudaMemcpyAsync(base + static_cast<size_t>(b) * 256 * row, w1 + static_cast<size_t>(b) * 128 * row,
                              128 * row * 2, cudaMemcpyHostToDevice, c->stream));
     CU_CHECK(cudaMemcpyAsync(base + (static_cast<size_t>(b) * 256 + 128) * row, w3 + static_cast<size_t>(b) * 128 * row,
                              128 * row * 2, cudaMemcpyHostToDevice, c->stream));
   }
-  CU_CHECK(cudaMemcpyAsync(L.w2.p + static_cast<size_t>(expert) * c->d * c->ff * elem, w2,
+  CU_CHECK(cudaMemcpyAsync(L.w2.p + static_cast<size_t>(slot) * c->d * c->ff * elem, w2,
                            static_cast<size_t>(c->d) * c->ff * 2 * elem, cudaMemcpyHostToDevice, c->stream));
   CU_CHECK(cudaStreamSynchronize(c->stream));
   L.expert_loaded[expert] = 1;
@@ -1356,6 +1543,20 @@ int moe_layer_forward_host_async(moe_ctx* c, int layer, const uint16_t* x_host, 
     CU_CHECK(cudaEventRecord(c->ev_done[slot], c->d2h));
     CU_CHECK(cudaEventRecord(c->ev_ticket[tk % moe_ctx::kTicketRing], c->d2h));
     if (ticket) *ticket = tk;
+  });
+}
+
+int moe_residency(moe_ctx* c, int layer, int32_t* slot_of, int* n_slots) {
+  return guarded([&] {
+    Layer& L = layer_at(c, layer);
+    require(slot_of != nullptr, "null argument");
+    if (c->placed) {
+      ensure_pools(c, L);
+      for (int e = 0; e < c->E; ++e) slot_of[e] = L.slot_of[e];
+    } else {
+      for (int e = 0; e < c->E; ++e) slot_of[e] = e;
+    }
+    if (n_slots) *n_slots = c->placed ? c->slots : c->E;
   });
 }
 

@@ -371,7 +371,7 @@ plan_exchange_kernel(const int32_t* __restrict__ counts_all, int stride, int G, 
     if (s_lrows[e] == 0) continue;
     int idx = 0;
     for (int h = 0; h < e; ++h) idx += s_lrows[h] > 0 ? 1 : 0;
-    plan->segs[idx] = GemmSeg{s_lfirst[e], s_lrows[e], e, 0};
+    plan->segs[idx] = GemmSeg{s_lfirst[e], s_lrows[e], pt->slot_of[e], 0};
   }
   if (tid == 0) {
     int nseg = 0, rows = 0;

@@ -40,6 +40,7 @@ struct PlacementTable {
   int rep_base[kMaxExperts + 4];
   int gpu_of[kMaxReplicas];
   int expert_of[kMaxReplicas];
+  int slot_of[kMaxExperts];  // this rank's weight slot of expert e (MOE_RESIDENCY_PLACED; else e)
 };
 
 // One GEMM segment = the rows of one replica placed on this rank.
