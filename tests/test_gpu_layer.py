@@ -31,7 +31,9 @@ def _build(E, k, d, ff, T, seed=1, layer=0, iteration=0, s=1.2):
 
 
 @pytest.mark.parametrize("E,k,d,T", [(8, 2, 1024, 2048), (16, 2, 4096, 1024), (64, 8, 2048, 256),
-                                     (8, 2, 4096, 999), (64, 8, 2048, 1)])
+                                     (8, 2, 4096, 999), (64, 8, 2048, 1),
+                                     # >= 4736 tokens: the TMA-staged gate kernel (ragged last block)
+                                     (8, 2, 4096, 5001), (16, 2, 1024, 8192), (32, 4, 2048, 4800)])
 def test_gate_ids_counts_bitexact(cuda, E, k, d, T):
     import torch
     x, wg, _ = _build(E, k, d, 128, T)

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("E,k,d,T,npred", [(8, 2, 4096, 2048, 1), (8, 2, 1024, 777, 3), (16, 2, 2048, 512, 2),
-                                           (64, 8, 2048, 256, 1)])
+                                           (64, 8, 2048, 256, 1), (8, 2, 4096, 6000, 1), (8, 2, 1024, 5000, 3)])
 def test_predictor_counts_bitexact(cuda, E, k, d, T, npred):
     import torch
     m = MoELayer(1, E, k, d, 128, max_tokens=T, num_predictor_targets=npred)
