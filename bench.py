@@ -45,8 +45,8 @@ FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)   # p99 over >= 200 timed layers
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--pool", type=int, default=4, help="distinct token batches cycled per rank")
     ap.add_argument("--cpu-sample-tokens", type=int, default=64)
@@ -255,22 +255,56 @@ def run_ours(args):
     E, k, d, ff, T = c["E"], c["k"], c["d"], c["ff"], c["T"]
     uid = None
     p2p = G > 1 and args.exchange == "p2p"
-    if G > 1 and not p2p:
-        obj = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
     mem = 3.0 * d * ff * 2 / 1e6
-    m = MoELayer(1, E, k, d, ff, max_tokens=T, world_size=G, rank=rank, device=local,
-                 exchange_mode=MOE_EXCHANGE_P2P if p2p else MOE_EXCHANGE_NCCL,
-                 nccl_unique_id=uid, expert_mem_mb=mem, layer_mem_cap_mb=c["extra_replicas"] * mem,
-                 gpu_mem_capacity_mb=180000.0, cv_threshold=0.2, keep_alive_iters=50,
-                 residency=1 if (p2p and args.residency == "placed") else 0)
-    if p2p:  # map every rank's exchange slab (CUDA IPC over NVLink)
-        handles = [None] * G
-        dist.all_gather_object(handles, m.p2p_export())
-        m.p2p_import(handles)
-    for e in range(E):
-        m.load_expert(0, e, *wl.expert_weights(d, ff, c["seed"], 0, e))
+
+    def make_layer(use_p2p):
+        uid = None
+        if G > 1 and not use_p2p:
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        lay = MoELayer(1, E, k, d, ff, max_tokens=T, world_size=G, rank=rank, device=local,
+                       exchange_mode=MOE_EXCHANGE_P2P if use_p2p else MOE_EXCHANGE_NCCL,
+                       nccl_unique_id=uid, expert_mem_mb=mem, layer_mem_cap_mb=c["extra_replicas"] * mem,
+                       gpu_mem_capacity_mb=180000.0, cv_threshold=0.2, keep_alive_iters=50,
+                       residency=1 if (use_p2p and args.residency == "placed") else 0)
+        if use_p2p:  # map every rank's exchange slab (CUDA IPC over NVLink)
+            handles = [None] * G
+            dist.all_gather_object(handles, lay.p2p_export())
+            lay.p2p_import(handles)
+        for e in range(E):
+            lay.load_expert(0, e, *wl.expert_weights(d, ff, c["seed"], 0, e))
+        return lay
+
+    exchange_note = None
+    if p2p:
+        # The peer-memory path is the product; if it cannot be set up on this
+        # box (no peer access, IPC refused, a peer out of step) every rank
+        # falls back to the NCCL exchange together rather than hanging.
+        m, err = None, ""
+        try:
+            m = make_layer(True)
+            m.set_gate(0, wl.gate_weights(E, d, c["s"], c["seed"], 0, 0))
+            xt = torch.from_numpy(wl.tokens(T, d, E, c["seed"], rank * 1000).view(np.int16)).cuda()
+            m.forward(0, xt, torch.empty_like(xt), MOE_PLAN_SYNC, 0)
+            m.sync()
+        except Exception as ex:  # noqa: BLE001 - any setup failure selects the fallback
+            err = f"{type(ex).__name__}: {ex}"
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device="cpu" if shared else "cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            print(f"[bench] rank {rank}: peer-memory exchange unavailable ({err or 'a peer failed'}); "
+                  "falling back to NCCL", file=sys.stderr, flush=True)
+            if m is not None:
+                try:
+                    m.close()
+                except Exception:  # noqa: BLE001
+                    pass
+            p2p = False
+            exchange_note = "NCCL send/recv (peer-memory setup failed: " + (err or "on a peer") + ")"
+            m = make_layer(False)
+    else:
+        m = make_layer(False)
     # token pool: per rank distinct batches (DP shard of the global batch)
     pool_host = [wl.tokens(T, d, E, c["seed"], rank * 1000 + i) for i in range(args.pool)]
     pool = [torch.from_numpy(x.view(np.int16)).cuda() for x in pool_host]
@@ -383,7 +417,8 @@ def run_ours(args):
                        "parallelism": f"ep{G}", "experts": E, "top_k": k, "d_model": d, "d_ff": ff,
                        "l2": "inputs larger than L2 (2.8 GB weights + 134 MB tokens per step)",
                        "planner": "MOE_PLAN_SYNC (scale_experts + place_experts on actual loads)"},
-            "exchange": ("peer memory (P2P)" if p2p else "NCCL send/recv") if G > 1 else "none (G=1)",
+            "exchange": (exchange_note or ("peer memory (P2P)" if p2p else "NCCL send/recv")) if G > 1
+                        else "none (G=1)",
             "p50_ms": p50, "p99_ms": p99,
             "step_ms": [round(v, 3) for v in lat],
             "phase_ms_median": phases, "replicas_median": replicas,
