@@ -85,7 +85,7 @@ cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUten
 cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                 __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, int* sched,
-                                bool pdl, const int32_t* a_gather);
+                                bool pdl, const int32_t* a_gather, int group_m = 0);
 cudaError_t preload_gate_kernels();
 cudaError_t preload_dispatch_kernels();
 cudaError_t preload_gemm_kernels();
@@ -334,6 +334,7 @@ struct moe_ctx {
   // gather4 instructions per 16 KB A stage make GEMM1 2.7x slower than one
   // tile load (profiles/ab_gather4_r01.md), far more than the copy it saves.
   bool gather = false;
+  int group_m[2] = {0, 0};  // K4 m-tiles per n sweep (0: the kernel's default; MOE_GEMM_GROUP_M=g1,g2)
   DevBuf<int32_t> perm_src;    // gathered GEMM1: permuted row -> token
   CUtensorMap tmX;             // gather4 map over the current x ({64, 1} box)
   const void* tmX_ptr = nullptr;
@@ -740,11 +741,11 @@ void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t r
   if (which == 0)
     CU_CHECK(launch_grouped_gemm(0, gather ? &c->tmX : &c->tmA1, &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg,
                                  2 * c->ff, c->d, 2 * c->ff, reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff,
-                                 c->num_sms, s, sched, c->use_pdl, gather ? c->perm_src.p : nullptr));
+                                 c->num_sms, s, sched, c->use_pdl, gather ? c->perm_src.p : nullptr, c->group_m[0]));
   else
     CU_CHECK(launch_grouped_gemm(1, &c->tmA2, &L.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
                                  reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s, sched, c->use_pdl,
-                                 nullptr));
+                                 nullptr, c->group_m[1]));
 }
 
 void stage_expert(moe_ctx* c, int layer, cudaStream_t s) {
@@ -1069,6 +1070,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_GEMM_SCHED")) c->dyn_sched = std::string(v) == "dynamic";
     if (const char* v = std::getenv("MOE_PDL")) c->use_pdl = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_GATHER")) c->gather = std::string(v) == "1";
+    if (const char* v = std::getenv("MOE_GEMM_GROUP_M")) std::sscanf(v, "%d,%d", &c->group_m[0], &c->group_m[1]);
     if (const char* v = std::getenv("MOE_GEMM_VARIANT")) {
       const std::string s(v);
       c->gemm_variant = s == "1sm" ? 1 : (s == "2sm" ? 2 : (s == "m256" ? 3 : 0));

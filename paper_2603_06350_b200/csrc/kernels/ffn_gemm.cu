@@ -71,7 +71,8 @@ struct TileCoord {
 
 template <int GM, int TILE_M = BM>
 __device__ __forceinline__ TileCoord decode_tile(int t, const int* seg_tiles, const int4* segs, int nseg,
-                                                 int n_tiles) {
+                                                 int n_tiles, int gm_rt = 0) {
+  const int GMv = gm_rt > 0 ? gm_rt : GM;
   // binary search: last s with seg_tiles[s] <= t
   int lo = 0, hi = nseg - 1;
   while (lo < hi) {
@@ -81,14 +82,14 @@ __device__ __forceinline__ TileCoord decode_tile(int t, const int* seg_tiles, co
   const int s = lo;
   const int local = t - seg_tiles[s];
   const int m_tiles = (segs[s].y + TILE_M - 1) / TILE_M;
-  const int per_group = GM * n_tiles;
+  const int per_group = GMv * n_tiles;
   const int g = local / per_group;
-  const int gm = min(GM, m_tiles - g * GM);
+  const int gm = min(GMv, m_tiles - g * GMv);
   const int rem = local - g * per_group;
   TileCoord c;
   c.seg = s;
   c.n = rem / gm;
-  c.m = g * GM + rem % gm;
+  c.m = g * GMv + rem % gm;
   return c;
 }
 
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total,
                     int k_total, int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld,
-                    int* __restrict__ sched, const int32_t* __restrict__ a_gather) {
+                    int* __restrict__ sched, const int32_t* __restrict__ a_gather, int group_m) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout::bars);
@@ -179,7 +180,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       }
       if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
       if (t >= total_tiles) break;
-      const TileCoord c = decode_tile<kGroupM<EPI>>(t, seg_tiles, segs, nseg, n_tiles);
+      const TileCoord c = decode_tile<kGroupM<EPI>>(t, seg_tiles, segs, nseg, n_tiles, group_m);
       const int a_row = segs[c.seg].x + c.m * BM;
       const int b_row = segs[c.seg].z * b_rows_per_slot + c.n * BN;
       int kb0 = 0;
@@ -241,7 +242,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         mbar_arrive(&ring_full[rslot]);
         if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
         if (t >= total_tiles) break;
-        const TileCoord c = decode_tile<kGroupM<EPI>>(t, seg_tiles, segs, nseg, n_tiles);
+        const TileCoord c = decode_tile<kGroupM<EPI>>(t, seg_tiles, segs, nseg, n_tiles, group_m);
         const int a_row = segs[c.seg].x + c.m * BM;
         const int b_row = segs[c.seg].z * b_rows_per_slot + c.n * BN;
         int kb0 = 0;
@@ -327,7 +328,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       if (lane == 0) mbar_arrive(&ring_empty[rslot]);
       if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
       if (t < 0) break;
-      const TileCoord c = decode_tile<kGroupM<EPI>>(t, seg_tiles, segs, nseg, n_tiles);
+      const TileCoord c = decode_tile<kGroupM<EPI>>(t, seg_tiles, segs, nseg, n_tiles, group_m);
       const int4 sg = segs[c.seg];
       const int row = c.m * BM + quarter * 32 + lane;
       const bool valid = row < sg.y;
@@ -786,7 +787,7 @@ int gemm_smem_bytes() { return static_cast<int>(kSmemBytes); }
 cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                 __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, int* sched,
-                                bool pdl, const int32_t* a_gather) {
+                                bool pdl, const int32_t* a_gather, int group_m) {
   if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
   static bool configured = false;
   if (!configured) {
@@ -808,9 +809,9 @@ cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorM
   cfg.numAttrs = 1;
   if (epi == EPI_SWIGLU)
     return cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI_SWIGLU>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                              b_rows_per_slot, out, out_ld, sched, a_gather);
+                              b_rows_per_slot, out, out_ld, sched, a_gather, group_m);
   return cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI_STORE>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                            b_rows_per_slot, out, out_ld, sched, a_gather);
+                            b_rows_per_slot, out, out_ld, sched, a_gather, group_m);
 }
 
 // Load every kernel of this file now (CUDA 12 loads kernels lazily on first
