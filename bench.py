@@ -351,6 +351,20 @@ def run_ours(args):
               for name in ("gate_ms", "plan_ms", "dispatch_ms", "a2a_dispatch_ms", "gemm1_ms", "gemm2_ms",
                            "a2a_combine_ms", "combine_ms")}
     replicas = statistics.median(s.replica_count for s in stats)
+    a2a = None
+    if G > 1:
+        # bytes this rank ships to other ranks per direction; with the peer-memory
+        # exchange they move inside dispatch (remote stores) and combine (remote
+        # loads), so the bus rate is bounded below by bytes / kernel time
+        sent = statistics.median(s.rows_sent for s in stats) * d * 2
+        disp = phases["dispatch_ms"] + phases["a2a_dispatch_ms"]
+        comb = phases["combine_ms"] + phases["a2a_combine_ms"]
+        a2a = {"remote_bytes_per_direction": sent, "dispatch_ms": disp, "combine_ms": comb,
+               "bus_gbs_dispatch": sent / (disp * 1e-3) / 1e9 if disp > 0 else None,
+               "bus_gbs_combine": sent / (comb * 1e-3) / 1e9 if comb > 0 else None,
+               "peak_gbs_per_direction": 900.0,
+               "note": "rank 0; dispatch/combine include local rows and the flag handshakes"
+                       + ("; ranks share one GPU (not NVLink)" if shared else "")}
     residency = None
     if p2p and args.residency == "placed":
         residency = {"mode": "placed (home experts + replica cache slots, cold copies from the home GPU)",
@@ -439,6 +453,8 @@ def run_ours(args):
         }
         if residency is not None:
             line["residency"] = residency
+        if a2a is not None:
+            line["all_to_all"] = a2a
         if e2e is not None:
             xb = T * d * 2 + E * d * 2
             line["e2e"] = {"value": G * T * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s",
