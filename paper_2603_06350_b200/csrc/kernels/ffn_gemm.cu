@@ -520,7 +520,9 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+      // A tiles are reused by every n tile of the group: evict_first here made
+      // GEMM1 re-read them from HBM (21 GB per launch instead of 3 GB)
+      const uint64_t pol_a = policy_evict_normal(), pol_b = policy_evict_last();
       for (int t = cluster; t < total_tiles; t += num_clusters) {
         const TileCoord c = decode_tile<kGroupM2<EPI>, BM2>(t, seg_tiles, segs, nseg, n_tiles);
         const int a_row = segs[c.seg].x + c.m * BM2 + static_cast<int>(rank) * 128;
