@@ -102,6 +102,7 @@ class ClockSampler:
     def __init__(self, gpu_index, period_s=0.01):
         self.gpu, self.period = gpu_index, period_s
         self.rows, self.err = [], None
+        self.e0 = self.energy_j = self.limit_w = None
 
     def _loop(self):
         import pynvml as N
@@ -109,11 +110,18 @@ class ClockSampler:
             N.nvmlInit()
             h = N.nvmlDeviceGetHandleByIndex(self.gpu)
             smax = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            try:
+                self.limit_w = N.nvmlDeviceGetEnforcedPowerLimit(h) / 1000.0
+                self.e0 = N.nvmlDeviceGetTotalEnergyConsumption(h)  # mJ since driver load
+            except Exception:  # noqa: BLE001 - energy counters are optional
+                self.e0 = None
             while not self.stop.is_set():
                 reasons = N.nvmlDeviceGetCurrentClocksEventReasons(h)
                 self.rows.append(dict(sm=N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM), smax=smax,
                                       power=N.nvmlDeviceGetPowerUsage(h) / 1000.0, reasons=reasons))
                 self.stop.wait(self.period)
+            if self.e0 is not None:
+                self.energy_j = (N.nvmlDeviceGetTotalEnergyConsumption(h) - self.e0) / 1000.0
         except Exception as e:  # no NVML: report unsampled
             self.err = repr(e)
 
@@ -142,7 +150,8 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(r["sm"] for r in loaded), "sm_max_mhz": max(r["smax"] for r in self.rows),
                 "reasons": sorted(reasons), "samples": len(loaded),
-                "power_w_median": statistics.median(r["power"] for r in loaded), "source": "NVML, 10 ms period"}
+                "power_w_median": statistics.median(r["power"] for r in loaded), "power_limit_w": self.limit_w,
+                "energy_j": self.energy_j, "source": "NVML, 10 ms period; energy = total-energy counter delta"}
 
 
 def nearest_rank(values, q):
@@ -177,6 +186,34 @@ def cpu_reference_step(sample_tokens, it, cache):
                                c["extra_replicas"] * mem, 1, oracle.P(loads))
     y, ids, w, counts = oracle.layer_forward(x, wg, cache["experts"], [1] * c["E"], c["k"])
     return time.perf_counter() - t0, ("reference" if ref is not None else "port")
+
+
+def cpu_cfg1_full_layer():
+    """The reference's own CPU-runnable configuration (BASELINE.json configs[0],
+    cfg1: E8 k2 d1024 ff3584, 2048 tokens, fixed placement) as ONE full layer on
+    the host: the reference planner path (oracle/_ref) + the oracle port of the
+    data path on all host threads.  Compare with bench_configs.py cfg1."""
+    import numpy as np
+
+    import oracle
+    from paper_2603_06350_b200 import workload as wl
+    c = dict(wl.CONFIGS["cfg1"])
+    E, k, d, ff, T = c["E"], c["k"], c["d"], c["ff"], c["T"]
+    experts = [wl.expert_weights(d, ff, 1, 0, e) for e in range(E)]
+    x = wl.tokens(T, d, E, 1, 0)
+    wg = wl.gate_weights(E, d, c["s"], 1, 0, 0)
+    ref = oracle.ref()
+    mem = 3.0 * d * ff * 2 / 1e6
+    oracle.layer_forward(x[:16], wg, experts, [1] * E, k)  # page in
+    t0 = time.perf_counter()
+    loads = np.zeros(E, np.int64)
+    if ref is not None:
+        ref.ref_cpu_layer_path(T, E, k, c["s"], 1, 1, mem, mem * E, 1, oracle.P(loads))
+    oracle.layer_forward(x, wg, experts, [1] * E, k)
+    dt = time.perf_counter() - t0
+    return {"value": T / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port", "ms_per_layer": 1e3 * dt,
+            "sample": "cfg1 in full: one 2048-token layer (E8 k2 d1024 ff3584), reference planner path + oracle "
+                      "data path"}
 
 
 def run_cpu_baseline(sample_tokens, steps=2):
@@ -451,6 +488,15 @@ def run_ours(args):
                          "traffic_source": (traffic or {}).get("source")},
             "clocks": clk.summary(),
         }
+        clk_sum = line["clocks"]
+        if clk_sum.get("energy_j"):
+            # the K4 clock is set by the board power cap: energy per step is the
+            # figure a faster kernel has to lower
+            jps = clk_sum["energy_j"] / args.steps
+            line["energy"] = {"joules_per_step": jps, "avg_power_w": clk_sum["energy_j"] / (total_ms * 1e-3),
+                              "power_limit_w": clk_sum.get("power_limit_w"),
+                              "k4_tflop_per_joule": statistics.median(gflop) / jps / 1e12,
+                              "note": "whole board, timed region (includes the counter's sampling slack)"}
         if residency is not None:
             line["residency"] = residency
         if a2a is not None:
@@ -465,6 +511,7 @@ def run_ours(args):
                                   "until the last result is in host memory"}
         if G == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = run_cpu_baseline(args.cpu_sample_tokens)
+            line["cpu_baseline_cfg1_full"] = cpu_cfg1_full_layer()
         print(json.dumps(line), flush=True)
     m.close()
     if dist is not None:
