@@ -96,6 +96,20 @@ __device__ __forceinline__ void tma_gather4(void* smem_dst, const void* desc, ui
       : "memory");
 }
 
+// 1D bulk copy global -> shared of `bytes` contiguous bytes (multiple of 16,
+// both addresses 16-byte aligned), completing on an mbarrier.
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Barrier over the first `threads` threads of the CTA (id 1; 0 is __syncthreads).
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
 // Same, with an L2 cache-policy hint (createpolicy result).
 __device__ __forceinline__ void tma_load_2d_hint(void* smem_dst, const void* desc, uint64_t* bar,
                                                  int c0, int c1, uint64_t policy) {
