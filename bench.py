@@ -39,6 +39,18 @@ METRIC = "MoE-layer tokens/s + p99 layer latency, Mixtral-8x7B shape, 1/2/4/8 B2
 WORKLOAD = ("cfg2: Mixtral-8x7B MoE layer (E=8, top-2, d_model=4096, d_ff=14336), "
             "16384 tokens per GPU, Zipf s=1.2 routing, straggler replicas (MoEless planner, "
             "cap 4 extra replicas), expert parallel over the GPUs")
+# --workload: the other BASELINE.json layer shapes through the same flow (the
+# headline metric is cfg2's; these lines are labelled with their own shape)
+OTHER_WORKLOADS = {
+    "cfg1": (dict(E=8, k=2, d=1024, ff=3584, T=2048, s=1.2, extra_replicas=0, seed=1),
+             "cfg1: E=8 top-2 d_model=1024 d_ff=3584, 2048 tokens per GPU, Zipf s=1.2"),
+    "cfg3": (dict(E=16, k=2, d=4096, ff=6400, T=16384, s=1.2, extra_replicas=8, seed=1),
+             "cfg3: Phi-3.5-MoE layer (E=16, top-2, d_model=4096, d_ff=6400), 16384 tokens per GPU, Zipf s=1.2, "
+             "expert parallel with straggler replicas"),
+    "cfg5": (dict(E=64, k=8, d=2048, ff=1408, T=256, s=2.0, extra_replicas=16, seed=1),
+             "cfg5: fine-grained decode (E=64, top-8, d_model=2048, d_ff=1408), 256 tokens per GPU, heavy skew "
+             "Zipf s=2.0"),
+}
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -55,6 +67,8 @@ def parse():
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
                     help="N>1 token exchange: peer memory over NVLink (dispatch/combine read and write the "
                          "owners' buffers) or NCCL grouped send/recv")
+    ap.add_argument("--workload", choices=["cfg2", "cfg1", "cfg3", "cfg5"], default="cfg2",
+                    help="layer shape (cfg2 = the headline Mixtral layer)")
     ap.add_argument("--residency", choices=["all", "placed"], default="all",
                     help="N>1 expert weights: every expert resident on every GPU, or only home experts + "
                          "replica cache slots with cold replicas copied from their home GPU over NVLink")
@@ -466,7 +480,8 @@ def run_ours(args):
             "dtype": "bf16", "data": "synthetic (keyed Zipf-skewed gate inputs, random-init expert weights)",
             "config": {"workload": WORKLOAD, "global_batch": G * T, "tokens_per_gpu": T, "seq_len": None,
                        "parallelism": f"ep{G}", "experts": E, "top_k": k, "d_model": d, "d_ff": ff,
-                       "l2": "inputs larger than L2 (2.8 GB weights + 134 MB tokens per step)",
+                       "l2": f"inputs larger than L2 ({E * 3 * d * ff * 2 / 1e9:.2f} GB of expert weights + "
+                             f"{T * d * 2 / 1e6:.0f} MB of tokens per step vs 126 MB of L2)",
                        "planner": "MOE_PLAN_SYNC (scale_experts + place_experts on actual loads)"},
             "exchange": (exchange_note or ("peer memory (P2P)" if p2p else "NCCL send/recv")) if G > 1
                         else "none (G=1)",
@@ -521,7 +536,10 @@ def run_ours(args):
 
 
 def main():
+    global CFG, WORKLOAD
     args = parse()
+    if args.workload != "cfg2":
+        CFG, WORKLOAD = OTHER_WORKLOADS[args.workload]
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
