@@ -461,37 +461,47 @@ void apply_residency(moe_ctx* c, int layer) {
   Layer& L = c->layers[layer];
   if (!c->placed) return;
   ensure_pools(c, L);
-  ++L.placements;
+  const long stamp = L.placements + 1;
   std::vector<char> need(c->E, 0);
   size_t f = 0;
   for (int e = 0; e < c->E; ++e)
     for (int r = 0; r < L.rep_counts[e]; ++r, ++f)
       if (L.rep_gpu[f] == c->rank) need[e] = 1;
-  int copies = 0, hits = 0;
+  // decide on copies of the slot state; the layer keeps its residency if the
+  // placement does not fit
+  std::vector<int> slot_of = L.slot_of, cache_expert = L.cache_expert;
+  std::vector<long> cache_stamp = L.cache_stamp;
+  std::vector<std::pair<int, int>> fills;
+  int hits = 0;
   for (int e = 0; e < c->E; ++e)
-    if (need[e] && e % c->G != c->rank && L.slot_of[e] >= 0) {
-      L.cache_stamp[L.slot_of[e] - c->home_slots] = L.placements;
+    if (need[e] && e % c->G != c->rank && slot_of[e] >= 0) {
+      cache_stamp[slot_of[e] - c->home_slots] = stamp;
       ++hits;
     }
   for (int e = 0; e < c->E; ++e) {
-    if (!need[e] || e % c->G == c->rank || L.slot_of[e] >= 0) continue;
+    if (!need[e] || e % c->G == c->rank || slot_of[e] >= 0) continue;
     int best = -1;  // a free slot (stamp -1) or the least recently needed one this placement does not use
     for (int i = 0; i < c->cache_slots; ++i) {
-      const int ce = L.cache_expert[i];
+      const int ce = cache_expert[i];
       if (ce >= 0 && need[ce]) continue;
-      if (best < 0 || L.cache_stamp[i] < L.cache_stamp[best]) best = i;
+      if (best < 0 || cache_stamp[i] < cache_stamp[best]) best = i;
     }
     if (best < 0)
       throw Status(MOE_EINFEASIBLE, "no replica slot free for expert " + std::to_string(e) + " of layer " +
                                         std::to_string(layer) + " on GPU " + std::to_string(c->rank) + " (" +
                                         std::to_string(c->cache_slots) + " cache slots)");
-    if (L.cache_expert[best] >= 0) L.slot_of[L.cache_expert[best]] = -1;  // evicted
-    L.cache_expert[best] = e;
-    L.cache_stamp[best] = L.placements;
-    L.slot_of[e] = c->home_slots + best;
-    L.pending_copies.emplace_back(c->home_slots + best, e);
-    ++copies;
+    if (cache_expert[best] >= 0) slot_of[cache_expert[best]] = -1;  // evicted
+    cache_expert[best] = e;
+    cache_stamp[best] = stamp;
+    slot_of[e] = c->home_slots + best;
+    fills.emplace_back(c->home_slots + best, e);
   }
+  const int copies = static_cast<int>(fills.size());
+  L.placements = stamp;
+  L.slot_of.swap(slot_of);
+  L.cache_expert.swap(cache_expert);
+  L.cache_stamp.swap(cache_stamp);
+  L.pending_copies.insert(L.pending_copies.end(), fills.begin(), fills.end());
   L.copies_last = copies;
   L.hits_last = hits;
   if (copies == 0) L.wready_timed = false;
@@ -1441,9 +1451,18 @@ int moe_set_placement(moe_ctx* c, int layer, const int32_t* rc, const int32_t* r
     for (int i = 0; i < total; ++i)
       require(rg[i] >= 0 && rg[i] < c->G,
               "replica placed on invalid GPU " + std::to_string(rg[i]));
+    std::vector<int32_t> old_counts = L.rep_counts, old_gpu = L.rep_gpu;
+    const bool had = L.has_placement;
     L.rep_counts.assign(rc, rc + c->E);
     L.rep_gpu.assign(rg, rg + total);
-    placement_changed(c, layer);
+    try {
+      placement_changed(c, layer);
+    } catch (...) {  // an infeasible placement leaves the previous one in force
+      L.rep_counts.swap(old_counts);
+      L.rep_gpu.swap(old_gpu);
+      L.has_placement = had;
+      throw;
+    }
   });
 }
 

@@ -128,8 +128,10 @@ def test_placed_eviction_with_small_cache(cuda):
             assert torch.equal(yd[r], y1), (it, r)
     # a placement that needs more non-home experts on rank 0 than it has slots
     rg = [0] * E
+    before = ms[0].residency(0)[0].copy()
     with pytest.raises(MoeError, match="no replica slot free"):
         ms[0].set_placement(0, [1] * E, rg)
+    assert np.array_equal(ms[0].residency(0)[0], before)  # the previous residency stays in force
     for m in ms + [one]:
         m.close()
 
