@@ -416,6 +416,24 @@ def run_ours(args):
                "peak_gbs_per_direction": 900.0,
                "note": "rank 0; dispatch/combine include local rows and the flag handshakes"
                        + ("; ranks share one GPU (not NVLink)" if shared else "")}
+    balance = None
+    if G > 1:
+        # straggler balance of the planner's placement on the same steps: rows
+        # each rank's GEMMs ran vs the rows static EP (expert e on GPU e mod G,
+        # no replicas; baselines.cpp:32-60) would have put on each rank
+        dev = "cpu" if shared else "cuda"
+        mine = torch.tensor([[float(s.rows_local) for s in stats]], dtype=torch.float64, device=dev)
+        allr = [torch.zeros_like(mine) for _ in range(G)]
+        dist.all_gather(allr, mine)
+        per_rank = torch.cat(allr).cpu().numpy()                       # [G, steps]
+        cnt = torch.tensor([[float(v) for v in s.counts[:E]] for s in stats], dtype=torch.float64, device=dev)
+        dist.all_reduce(cnt)                                            # global histogram per step
+        cnt = cnt.cpu().numpy()
+        static = np.stack([cnt[:, [e for e in range(E) if e % G == g]].sum(axis=1) for g in range(G)])
+        ratio = lambda a: float(np.median(a.max(axis=0) / np.maximum(a.mean(axis=0), 1.0)))
+        balance = {"rows_per_rank_median": [float(v) for v in np.median(per_rank, axis=1)],
+                   "max_over_mean": ratio(per_rank), "static_ep_max_over_mean": ratio(static),
+                   "note": "median over the stats steps; 1.0 = perfectly balanced ranks"}
     residency = None
     if p2p and args.residency == "placed":
         residency = {"mode": "placed (home experts + replica cache slots, cold copies from the home GPU)",
@@ -516,6 +534,8 @@ def run_ours(args):
             line["residency"] = residency
         if a2a is not None:
             line["all_to_all"] = a2a
+        if balance is not None:
+            line["straggler_balance"] = balance
         if e2e is not None:
             xb = T * d * 2 + E * d * 2
             line["e2e"] = {"value": G * T * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s",
