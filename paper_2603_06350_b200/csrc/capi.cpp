@@ -47,7 +47,8 @@ cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, co
                                 int32_t* block_pre, cudaStream_t s);
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
                             const int32_t* block_pre, const DevPlan* plan, const RowTargets& targets,
-                            uint32_t* row_code, const PeerSignal& sig, cudaStream_t s, int32_t* perm_src);
+                            uint32_t* row_code, const PeerSignal& sig, cudaStream_t s, int32_t* perm_src,
+                            int32_t* row_owner);
 // K6 over peer memory (p2p.cu)
 constexpr int kMaxRanks = 8;
 enum { kFlagCounts = 0, kFlagRows = 1, kFlagOutputs = 2, kFlagKinds = 4 };
@@ -85,7 +86,7 @@ cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUten
 cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                 __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, int* sched,
-                                bool pdl, const int32_t* a_gather, int group_m = 0);
+                                bool pdl, const int32_t* a_gather, int group_m, const FusedCombine& fc);
 cudaError_t preload_gate_kernels();
 cudaError_t preload_dispatch_kernels();
 cudaError_t preload_gemm_kernels();
@@ -334,6 +335,13 @@ struct moe_ctx {
   // gather4 instructions per 16 KB A stage make GEMM1 2.7x slower than one
   // tile load (profiles/ab_gather4_r01.md), far more than the copy it saves.
   bool gather = false;
+  // single GPU: the combine runs in GEMM2's epilogue (MOE_FUSED_COMBINE=1).  Opt-in:
+  // bit-identical, but no faster under the power cap at cfg2 and slower for
+  // short-K shapes (the late rows' sums serialise on 4 epilogue warps),
+  // profiles/ab_fused_combine_r01.md
+  bool fuse_combine = false;
+  DevBuf<int32_t> row_owner;  // [rows_cap] row -> t * k + j
+  DevBuf<int32_t> comb_cnt;   // [Tmax * d / 256] arrivals per (token, GEMM2 n tile)
   int group_m[2] = {0, 0};  // K4 m-tiles per n sweep (0: the kernel's default; MOE_GEMM_GROUP_M=g1,g2)
   DevBuf<int32_t> perm_src;    // gathered GEMM1: permuted row -> token
   CUtensorMap tmX;             // gather4 map over the current x ({64, 1} box)
@@ -646,7 +654,7 @@ void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int3
 }
 
 void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool upload_plan = true,
-                    bool gather = false) {
+                    bool gather = false, bool fused = false) {
   if (upload_plan)
     CU_CHECK(launch_small_copy(c->dplan.p, c->hplan, sizeof(DevPlan), s));  // SM copy from mapped pinned memory
   const int nblk = gate_num_blocks(T);
@@ -669,7 +677,8 @@ void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool u
     t.base[kSendTarget] = c->send.p;
   }
   CU_CHECK(launch_dispatch(reinterpret_cast<const __nv_bfloat16*>(x), T, c->xw, c->E, c->k, c->ids.p, c->block_pre.p,
-                           c->dplan.p, t, c->row_code.p, sig, s, gather ? c->perm_src.p : nullptr));
+                           c->dplan.p, t, c->row_code.p, sig, s, gather ? c->perm_src.p : nullptr,
+                           fused ? c->row_owner.p : nullptr));
 }
 
 // The exchange step of one direction.  NCCL: grouped send/recv, forward: my
@@ -716,7 +725,8 @@ void stage_exchange(moe_ctx* c, bool forward, cudaStream_t s) {
 // B200's 1 kW cap it settles ~190 MHz lower and nets ~4% less throughput on
 // the Mixtral layer (profiles/ab_gemm_variants_r01.md), so it is opt-in
 // (MOE_GEMM_VARIANT=2sm) until it is made more energy-efficient.
-void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t rows = 0, bool gather = false) {
+void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t rows = 0, bool gather = false,
+                     uint16_t* fused_y = nullptr) {
   Layer& L = c->layers[layer];
   if (c->fp32) {  // K7: SIMT fp32 grouped GEMMs (+ SwiGLU pass between them)
     const GemmSeg* segs = c->dplan.p->segs;
@@ -751,11 +761,22 @@ void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t r
   if (which == 0)
     CU_CHECK(launch_grouped_gemm(0, gather ? &c->tmX : &c->tmA1, &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg,
                                  2 * c->ff, c->d, 2 * c->ff, reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff,
-                                 c->num_sms, s, sched, c->use_pdl, gather ? c->perm_src.p : nullptr, c->group_m[0]));
-  else
+                                 c->num_sms, s, sched, c->use_pdl, gather ? c->perm_src.p : nullptr, c->group_m[0],
+                                 FusedCombine{}));
+  else {
+    FusedCombine fc{};
+    if (fused_y) {
+      fc.row_owner = c->row_owner.p;
+      fc.row_code = c->row_code.p;
+      fc.wts = c->wts.p;
+      fc.counters = c->comb_cnt.p;
+      fc.y = fused_y;
+      fc.k = c->k;
+    }
     CU_CHECK(launch_grouped_gemm(1, &c->tmA2, &L.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
                                  reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s, sched, c->use_pdl,
-                                 nullptr, c->group_m[1]));
+                                 nullptr, c->group_m[1], fc));
+  }
 }
 
 void stage_expert(moe_ctx* c, int layer, cudaStream_t s) {
@@ -859,6 +880,8 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   // single GPU, bf16, 1-SM K4: GEMM1 gathers its A rows from x (TMA gather4)
   // and the dispatch kernel only ranks — no permuted copy of the tokens
   const bool gather = c->gather && c->G == 1 && !c->fp32 && (c->gemm_variant == 0 || c->gemm_variant == 1) && T > 0;
+  // single GPU, bf16, 1-SM K4: the combine runs inside GEMM2's epilogue
+  const bool fused = c->fuse_combine && c->G == 1 && !c->fp32 && (c->gemm_variant == 0 || c->gemm_variant == 1);
   if (gather && (c->tmX_ptr != x || c->tmX_T != T)) {
     c->tmX = make_kmajor_map(x, T, c->d, 1);
     c->tmX_ptr = x;
@@ -894,7 +917,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
     else
       CU_CHECK(launch_plan_exchange(c->counts_all.p, stride, c->G, c->rank, L.ptab.p, c->dplan.p, s));
     mark(2);
-    stage_dispatch(c, x, T, s, /*upload_plan=*/false, gather);
+    stage_dispatch(c, x, T, s, /*upload_plan=*/false, gather, fused);
   } else {
     mark(1);
     CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram
@@ -918,7 +941,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   // then timed as one interval, reported as GEMM1 with GEMM2 = 0)
   if (!capturing && !c->use_pdl) CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][1], s));
   mark(5);
-  launch_ffn_gemm(c, layer, 1, s, rows);
+  launch_ffn_gemm(c, layer, 1, s, rows, false, fused ? y : nullptr);
   // (after GEMM2, not between the GEMMs: an event there would serialise the PDL pair)
   if (x_consumed && gather) CU_CHECK(cudaEventRecordWithFlags(x_consumed, s, rec));
   if (c->placed) {  // the layer's slots may be overwritten once these GEMMs are done
@@ -933,7 +956,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   mark(6);
   stage_exchange(c, false, s);
   mark(7);
-  stage_combine(c, y, T, s);
+  if (!fused) stage_combine(c, y, T, s);
   mark(8);
   if (deferred && !capturing) c->pending = PendingPlan{true, layer, plan_mode, iteration, stride, ahead ? gslot : -1};
 }
@@ -1080,6 +1103,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_GEMM_SCHED")) c->dyn_sched = std::string(v) == "dynamic";
     if (const char* v = std::getenv("MOE_PDL")) c->use_pdl = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_GATHER")) c->gather = std::string(v) == "1";
+    if (const char* v = std::getenv("MOE_FUSED_COMBINE")) c->fuse_combine = std::string(v) == "1";
     if (const char* v = std::getenv("MOE_GEMM_GROUP_M")) std::sscanf(v, "%d,%d", &c->group_m[0], &c->group_m[1]);
     if (const char* v = std::getenv("MOE_GEMM_VARIANT")) {
       const std::string s(v);
@@ -1135,6 +1159,9 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->xw = c->d * c->elem;
     c->xp.alloc(static_cast<size_t>(c->rows_cap) * c->xw);
     c->perm_src.alloc(static_cast<size_t>(c->rows_cap));
+    c->row_owner.alloc(static_cast<size_t>(c->rows_cap));
+    c->comb_cnt.alloc(static_cast<size_t>(c->Tmax) * std::max(1, c->d / 256));
+    CU_CHECK(cudaMemset(c->comb_cnt.p, 0, c->comb_cnt.n * sizeof(int32_t)));
     c->h.alloc(static_cast<size_t>(c->rows_cap) * c->ff * c->elem);
     c->yp.alloc(static_cast<size_t>(c->rows_cap) * c->xw);
     c->send.alloc(static_cast<size_t>(c->send_cap) * c->xw);

@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(128)
 dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const int32_t* __restrict__ ids,
                 const int32_t* __restrict__ block_pre, const DevPlan* __restrict__ plan,
                 const __grid_constant__ RowTargets targets, uint32_t* __restrict__ row_code,
-                const __grid_constant__ PeerSignal sig, int32_t* __restrict__ perm_src) {
+                const __grid_constant__ PeerSignal sig, int32_t* __restrict__ perm_src,
+                int32_t* __restrict__ row_owner) {
   __shared__ uint32_t codes[32 * K];
   // the block's prefix row and the plan tables the ranking reads, staged once
   // (coalesced) so the ranking never waits on L2
@@ -139,6 +140,7 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
         codes[lane * K + j] = code;
         if (blockIdx.y == 0) row_code[(size_t)t * K + j] = code;
         if (perm_src) perm_src[code & kRowMask] = t;  // gathered GEMM1: row -> token
+        if (row_owner) row_owner[code & kRowMask] = t * K + j;  // fused combine: row -> (token, slot)
       }
     }
   }
@@ -434,7 +436,8 @@ cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, co
 
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
                             const int32_t* block_pre, const DevPlan* plan, const RowTargets& targets,
-                            uint32_t* row_code, const PeerSignal& sig, cudaStream_t s, int32_t* perm_src) {
+                            uint32_t* row_code, const PeerSignal& sig, cudaStream_t s, int32_t* perm_src,
+                            int32_t* row_owner) {
   if (T <= 0) return cudaSuccess;
   if (d % 8) return cudaErrorInvalidValue;
   const int nblk = (T + 31) / 32;
@@ -443,7 +446,7 @@ cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, 
   const int split = perm_src ? 1 : std::max(1, std::min((2 * 148 + nblk - 1) / nblk, d / 8 / 16));
   const dim3 grid(nblk, split);
   MOE_SWITCH_K(k, (dispatch_kernel<KK><<<grid, 128, 0, s>>>(x, T, d, E, ids, block_pre, plan, targets, row_code, sig,
-                                                            perm_src)));
+                                                            perm_src, row_owner)));
   return cudaGetLastError();
 }
 

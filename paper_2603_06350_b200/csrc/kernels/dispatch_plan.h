@@ -51,6 +51,19 @@ struct GemmSeg {
   int pad;
 };
 
+// Single GPU: the combine fused into GEMM2's epilogue.  Every expert-output
+// row knows its (token, slot) (row_owner, written by the dispatch kernel); the
+// last of a token's k rows to finish an n tile sums the k rows of that tile in
+// slot order — the combine kernel's arithmetic — and writes y.
+struct FusedCombine {
+  const int32_t* row_owner;  // [rows] t * k + j; nullptr: no fusion (separate combine kernel)
+  const uint32_t* row_code;  // [T * k] (token, slot) -> row
+  const float* wts;          // [T * k]
+  int32_t* counters;         // [T * n_tiles] arrivals per (token, n tile); zero between forwards
+  void* y;                   // [T, d] bf16
+  int k, pad;
+};
+
 struct DevPlan {
   int E, R, G, rank;
   int nseg;        // GEMM segments on this rank (replicas here with rows > 0)

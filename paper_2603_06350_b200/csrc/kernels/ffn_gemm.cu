@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total,
                     int k_total, int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld,
-                    int* __restrict__ sched, const int32_t* __restrict__ a_gather, int group_m) {
+                    int* __restrict__ sched, const int32_t* __restrict__ a_gather, int group_m,
+                    const __grid_constant__ FusedCombine fc) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout::bars);
@@ -317,6 +318,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   } else {
     // --------------------------------------------------------- epilogue
     const int quarter = warp & 3;
+    if (EPI == EPI_STORE && fc.row_owner) griddep_wait();  // row_owner / weights come from earlier kernels
     int acc = 0;
     uint32_t acc_phase = 0;
     int rslot = 0;
@@ -378,8 +380,52 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) mbar_arrive(&tempty[acc]);  // the accumulator is free before the combine below
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if constexpr (EPI == EPI_STORE) {
+        if (fc.row_owner && valid) {
+          // fused combine: this row's 256 columns are in Yp; the last of the
+          // token's k rows to get here sums all k in slot order (as
+          // combine_kernel: acc = fma(w_j, y_j, acc) from 0) and writes y
+          const int own = fc.row_owner[grow];
+          const int tok = own / fc.k;
+          int32_t* ctr = fc.counters + (size_t)tok * n_tiles + c.n;
+          __threadfence();
+          if (atomicAdd(ctr, 1) == fc.k - 1) {
+            *ctr = 0;  // ready for the next forward
+            __threadfence();
+            const __nv_bfloat16* src[8];
+            float w[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (j < fc.k) {
+                src[j] = out + (size_t)(fc.row_code[(size_t)tok * fc.k + j] & kRowMask) * out_ld + c.n * BN;
+                w[j] = fc.wts[(size_t)tok * fc.k + j];
+              }
+            __nv_bfloat16* yrow = static_cast<__nv_bfloat16*>(fc.y) + (size_t)tok * out_ld + c.n * BN;
+#pragma unroll 1
+            for (int c8 = 0; c8 < BN / 8; ++c8) {
+              float a8[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) a8[i] = 0.0f;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                if (j >= fc.k) break;
+                const int4 v = __ldcg(reinterpret_cast<const int4*>(src[j] + c8 * 8));
+                const uint32_t* u = reinterpret_cast<const uint32_t*>(&v);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  a8[2 * i] = fmaf(w[j], bf16lo(u[i]), a8[2 * i]);
+                  a8[2 * i + 1] = fmaf(w[j], bf16hi(u[i]), a8[2 * i + 1]);
+                }
+              }
+              *reinterpret_cast<int4*>(yrow + c8 * 8) =
+                  make_int4(pack_bf16(a8[0], a8[1]), pack_bf16(a8[2], a8[3]), pack_bf16(a8[4], a8[5]),
+                            pack_bf16(a8[6], a8[7]));
+            }
+          }
+        }
+      }
     }
   }
   // a CTA without tiles never waited: completing this grid must still imply
@@ -789,7 +835,7 @@ int gemm_smem_bytes() { return static_cast<int>(kSmemBytes); }
 cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                 __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, int* sched,
-                                bool pdl, const int32_t* a_gather, int group_m) {
+                                bool pdl, const int32_t* a_gather, int group_m, const FusedCombine& fc) {
   if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
   static bool configured = false;
   if (!configured) {
@@ -811,9 +857,9 @@ cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorM
   cfg.numAttrs = 1;
   if (epi == EPI_SWIGLU)
     return cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI_SWIGLU>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                              b_rows_per_slot, out, out_ld, sched, a_gather, group_m);
+                              b_rows_per_slot, out, out_ld, sched, a_gather, group_m, fc);
   return cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<EPI_STORE>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                            b_rows_per_slot, out, out_ld, sched, a_gather, group_m);
+                            b_rows_per_slot, out, out_ld, sched, a_gather, group_m, fc);
 }
 
 // Load every kernel of this file now (CUDA 12 loads kernels lazily on first

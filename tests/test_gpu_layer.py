@@ -156,3 +156,24 @@ def test_gathered_gemm1_matches_dispatch_copy(cuda, monkeypatch, E, k, d, ff, T,
         outs.append(y)
         m.close()
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("E,k,d,ff,T,rc", [
+    (8, 2, 1024, 3584, 999, [2, 1, 3, 1, 1, 1, 1, 2]),
+    (64, 8, 2048, 1408, 256, [1] * 60 + [2, 3, 1, 2]),
+    (16, 2, 4096, 1408, 1, [1] * 16),
+    (8, 1, 1024, 1408, 300, [1] * 8),
+])
+def test_fused_combine_matches_combine_kernel(cuda, monkeypatch, E, k, d, ff, T, rc):
+    """Single GPU: the combine fused into GEMM2's epilogue (MOE_FUSED_COMBINE=1; the last of a
+    token's k rows per n tile sums them in slot order) must be bit-identical to
+    the separate combine kernel (MOE_FUSED_COMBINE=0), on repeated forwards
+    (the arrival counters reset themselves)."""
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("MOE_FUSED_COMBINE", flag)
+        m, st, y, y_ref, ids_o, counts_o = _layer_case(cuda, E, k, d, ff, T, rc)
+        assert _rel_err(y, y_ref) <= TOL_REL
+        outs.append(y)
+        m.close()
+    assert np.array_equal(outs[0], outs[1])
