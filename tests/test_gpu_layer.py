@@ -177,3 +177,56 @@ def test_fused_combine_matches_combine_kernel(cuda, monkeypatch, E, k, d, ff, T,
         outs.append(y)
         m.close()
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_empty_batch_forward(cuda):
+    """T = 0 (a rank or a step with no tokens): every kernel is skipped or
+    degenerate, the call succeeds, nothing is routed, and the next non-empty
+    forward is unaffected."""
+    import torch
+    E, k, d, ff = 8, 2, 1024, 1408
+    x, wg, experts = _build(E, k, d, ff, 64, seed=5)
+    m = MoELayer(1, E, k, d, ff, max_tokens=64)
+    m.set_gate(0, wg)
+    for e, (w1, w3, w2) in enumerate(experts):
+        m.load_expert(0, e, w1, w3, w2)
+    empty = torch.zeros((0, d), dtype=torch.int16, device=cuda)
+    st = m.forward(0, empty, torch.zeros((0, d), dtype=torch.int16, device=cuda), MOE_PLAN_FIXED, 0, stats=True)
+    assert st.rows_local == 0 and sum(st.counts[:E]) == 0
+    xd = _to_dev(x, torch)
+    yd = torch.zeros((64, d), dtype=torch.int16, device=cuda)
+    m.forward(0, xd, yd, MOE_PLAN_FIXED, 1)
+    torch.cuda.synchronize()
+    y = oracle.bf16_to_f32(yd.cpu().numpy().view(np.uint16))
+    y_ref = oracle.layer_forward(x, wg, experts, [1] * E, k, round_h=True)[0]
+    assert _rel_err(y, y_ref) <= TOL_REL
+    m.close()
+
+
+def test_gate_exact_ties_pick_lower_expert(cuda):
+    """Experts 2 and 5 (and 6, 7) get identical gate rows: their logits tie
+    exactly for every token, and the top-k takes the LOWER index first, as the
+    oracle does (route_tokens has no ties; this is the Mixtral-convention rule
+    of DESIGN.md §K1)."""
+    import torch
+    E, k, d, T = 8, 2, 1024, 512
+    x, wg, _ = _build(E, k, d, 128, T, seed=9)
+    wg = wg.copy()
+    wg[5] = wg[2]
+    wg[7] = wg[6]
+    ids_o, w_o, counts_o = oracle.gate(x, wg, k)
+    m = MoELayer(1, E, k, d, 128, max_tokens=T)
+    m.set_gate(0, wg)
+    ids = torch.zeros((T, k), dtype=torch.int32, device=cuda)
+    w = torch.zeros((T, k), dtype=torch.float32, device=cuda)
+    counts = torch.zeros(E, dtype=torch.int32, device=cuda)
+    m.gate(0, _to_dev(x, torch), ids, w, counts)
+    torch.cuda.synchronize()
+    ids = ids.cpu().numpy()
+    assert np.array_equal(ids, ids_o)
+    # an upper twin is only ever chosen right after its lower twin (equal logit)
+    for lo, hi in ((2, 5), (6, 7)):
+        rows, slot = np.nonzero(ids == hi)
+        assert np.all(slot == 1) and np.all(ids[rows, 0] == lo)
+        assert np.all(ids[ids[:, 0] == lo, 1] == hi)  # when the lower twin leads, the upper one follows
+    m.close()
