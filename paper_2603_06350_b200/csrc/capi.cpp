@@ -1,17 +1,17 @@
 // capi.cpp — the C-ABI drop-in boundary (include/moe_b200.h).
 //
-// Owns one device's share of the MoE layer: weights pool, workspace, TMA
-// descriptors, streams and (for G > 1) the NCCL communicator, and sequences a
-// layer forward:
+// Owns one device's share of the MoE layer: weight pools (and, with
+// MOE_RESIDENCY_PLACED, the replica weight slots), workspace, TMA descriptors,
+// streams, the peer-memory slab or NCCL communicator, and sequences a layer
+// forward (enqueue_forward):
 //
-//   K1 gate+topk+hist (+K2 predictor)      gate.cu
-//   [counts all-gather, NCCL]              G > 1
-//   host: plan (scale/place if MOE_PLAN_SYNC) + exchange plan, one H2D upload
-//   block prefix + K3 dispatch             dispatch.cu
-//   [row all-to-all, NCCL grouped p2p]     G > 1
-//   K4 GEMM1 (SwiGLU) + GEMM2              ffn_gemm.cu  (tcgen05/TMEM/TMA)
-//   [row all-to-all back]                  G > 1
-//   K5 combine                             dispatch.cu
+//   K1 gate + top-k + histogram (+K2 predictor)        gate.cu
+//   G > 1: counts exchange (peer slabs, or NCCL all-gather)
+//   plan: on the device (G = 1, or placement planned ahead) or on the host
+//         (scale_experts / place_experts on the actual loads, exchange plan)
+//   block prefix + K3 dispatch (peer stores at G > 1)  dispatch.cu
+//   K4 GEMM1 (SwiGLU) + GEMM2                          ffn_gemm.cu  (tcgen05/TMEM/TMA)
+//   K5 combine (peer loads at G > 1)                   dispatch.cu
 //
 // Replaces layer_forward_time (proj/src/cost_model.cpp:91-122) for callers
 // that want the real layer instead of the analytic model.
