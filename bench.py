@@ -431,9 +431,16 @@ def run_ours(args):
         cnt = cnt.cpu().numpy()
         static = np.stack([cnt[:, [e for e in range(E) if e % G == g]].sum(axis=1) for g in range(G)])
         ratio = lambda a: float(np.median(a.max(axis=0) / np.maximum(a.mean(axis=0), 1.0)))
+        # oracle_balance_time (baselines.cpp:141-154): the GEMM time every rank
+        # would need with the rows spread perfectly, from rank 0's per-row rate
+        rows0 = statistics.median(s.rows_local for s in stats)
+        gemm0 = statistics.median(s.gemm1_ms + s.gemm2_ms for s in stats)
         balance = {"rows_per_rank_median": [float(v) for v in np.median(per_rank, axis=1)],
                    "max_over_mean": ratio(per_rank), "static_ep_max_over_mean": ratio(static),
-                   "note": "median over the stats steps; 1.0 = perfectly balanced ranks"}
+                   "gemm_ms_perfect_balance": gemm0 / max(rows0, 1) * float(np.median(per_rank.mean(axis=0))),
+                   "gemm_ms_slowest_rank_est": gemm0 / max(rows0, 1) * float(np.median(per_rank.max(axis=0))),
+                   "note": "median over the stats steps; 1.0 = perfectly balanced ranks; GEMM ms from rank 0's "
+                           "per-row rate (the oracle_balance_time line)"}
     residency = None
     if p2p and args.residency == "placed":
         residency = {"mode": "placed (home experts + replica cache slots, cold copies from the home GPU)",
