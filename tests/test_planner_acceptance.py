@@ -74,3 +74,13 @@ def test_cold_placement_within_greedy_bound_1000_instances():  # acceptance.cpp:
         worst = max(worst, max(sums) / bound)
         assert max(sums) <= bound * (1 + 1e-12), (i, max(sums), bound)
     assert worst <= 1.0
+
+
+def test_noisy_predictor_hits_configured_accuracy():  # acceptance.cpp:379-404
+    from paper_2603_06350_b200 import measure_accuracy, predict
+    actual = [15000] * 8 + [0] * 8
+    popularity = [0.0] * 8 + [0.125] * 8  # misplaced tokens never overlap the actual mass
+    for a in (0.7, 0.8, 0.9):
+        pred, _ = predict(1, actual, layer=0, accuracy=[a], distance=1, iteration=5, seed=99,
+                          popularity=popularity)
+        assert abs(measure_accuracy(pred, actual) - a) <= 0.02, a
