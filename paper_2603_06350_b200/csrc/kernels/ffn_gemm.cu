@@ -93,7 +93,10 @@ __device__ __forceinline__ TileCoord decode_tile(int t, const int* seg_tiles, co
   return c;
 }
 
-__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+// silu(g) = g * sigmoid(g) with the fast reciprocal: the product is rounded to
+// bf16 right after, and the exact IEEE division made the SwiGLU epilogue the
+// longest part of a decode tile (cfg5)
+__device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 // Tile order is the same static sequence (decode_tile) either way; with a
 // scheduler counter (sched != nullptr: [0] next tile, [1] CTAs done, zero
@@ -334,11 +337,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const int4 sg = segs[c.seg];
       const int row = c.m * BM + quarter * 32 + lane;
       const bool valid = row < sg.y;
+      // a 32-row band past the segment's end (most of a decode tile) has
+      // nothing to store: skip its TMEM loads and math (warp-uniform)
+      const bool band_live = c.m * BM + quarter * 32 < sg.y;
       const size_t grow = static_cast<size_t>(sg.x + row);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
-      if constexpr (EPI == EPI_SWIGLU) {
+      if (!band_live) {
+      } else if constexpr (EPI == EPI_SWIGLU) {
         __nv_bfloat16* dst = out + grow * out_ld + c.n * (BN / 2);
 #pragma unroll 1
         for (int ch = 0; ch < BN / 2 / 32; ++ch) {
