@@ -34,12 +34,13 @@ def run_config(name, steps, warmup, graphs=False):
         m.load_expert(0, e, *wl.expert_weights(d, ff, 1, 0, e))
     pool = [torch.from_numpy(wl.tokens(T, d, E, 1, i).view(np.int16)).cuda() for i in range(4)]
     n_it = warmup + steps + 10
-    gates = [wl.gate_weights(E, d, s, 1, 0, it) for it in range(n_it)]
+    gates = torch.from_numpy(np.stack([wl.gate_weights(E, d, s, 1, 0, it)
+                                       for it in range(n_it)]).view(np.int16)).cuda()
     y = torch.empty((T, d), dtype=torch.int16, device="cuda")
     stream = torch.cuda.ExternalStream(m.stream_ptr)
 
     def step(it, stats=False):
-        m.set_gate(0, gates[it])
+        m.set_gate_device(0, gates[it])  # device-resident per-iteration gates
         return m.forward(0, pool[it % 4], y, MOE_PLAN_SYNC, it, stats=stats)
 
     for it in range(warmup):

@@ -203,6 +203,10 @@ int moe_set_gate_weights(moe_ctx* ctx, int layer, const uint16_t* wg);
 int moe_load_expert_weights_f32(moe_ctx* ctx, int layer, int expert, const float* w1, const float* w3,
                                 const float* w2);
 int moe_set_gate_weights_f32(moe_ctx* ctx, int layer, const float* wg);
+/* Gate weights already in device memory ([E, d_model], the context's
+   precision): a stream-ordered device-to-device copy (stream NULL = the
+   context's), so per-call gate updates cost no host staging. */
+int moe_set_gate_weights_device(moe_ctx* ctx, int layer, const void* wg_dev, void* stream);
 /* predictor weights for target `slot` (< num_predictor_targets), scored from
    layer `layer`'s hidden states: [E, d_model] */
 int moe_set_predictor_weights(moe_ctx* ctx, int layer, int slot, const uint16_t* wp);

@@ -383,6 +383,13 @@ class MoELayer:
         fn = lib.moe_set_gate_weights_f32 if self.fp32 else lib.moe_set_gate_weights
         check(fn(self._h, layer, _p(wg)))
 
+    def set_gate_device(self, layer: int, wg) -> None:
+        """Gate weights from a device tensor ([E, d_model], the context's precision),
+        stream-ordered on the context's stream."""
+        if tuple(wg.shape) != (self.E, self.d) or not wg.is_contiguous():
+            raise ValueError("gate weight must be a contiguous [E, d_model] device tensor")
+        check(lib.moe_set_gate_weights_device(self._h, layer, C.c_void_p(wg.data_ptr()), None))
+
     def set_predictor(self, layer: int, slot: int, wp: np.ndarray) -> None:
         check(lib.moe_set_predictor_weights(self._h, layer, slot, _p(np.ascontiguousarray(wp))))
 

@@ -600,6 +600,22 @@ void set_gate_impl(moe_ctx* c, int layer, const void* wg, int elem) {
 }
 }  // namespace
 
+int moe_set_gate_weights_device(moe_ctx* c, int layer, const void* wg_dev, void* stream) {
+  return guarded([&] {
+    Layer& L = layer_at(c, layer);
+    require(wg_dev != nullptr, "null gate weights");
+    if (!L.wg.p) {
+      L.wg.alloc(static_cast<size_t>(c->E) * c->d * (1 + c->n_pred) * c->elem);
+      CU_CHECK(cudaMemsetAsync(L.wg.p, 0, L.wg.n * 2, c->stream));
+    }
+    // stream-ordered device -> device copy: no staging, no host wait
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    CU_CHECK(cudaMemcpyAsync(L.wg.p, wg_dev, static_cast<size_t>(c->E) * c->d * 2 * c->elem,
+                             cudaMemcpyDeviceToDevice, s));
+    L.has_gate = true;
+  });
+}
+
 int moe_set_gate_weights_f32(moe_ctx* c, int layer, const float* wg) {
   return guarded([&] { set_gate_impl(c, layer, wg, 2); });
 }

@@ -230,3 +230,33 @@ def test_gate_exact_ties_pick_lower_expert(cuda):
         assert np.all(slot == 1) and np.all(ids[rows, 0] == lo)
         assert np.all(ids[ids[:, 0] == lo, 1] == hi)  # when the lower twin leads, the upper one follows
     m.close()
+
+
+def test_device_gate_update_matches_host_upload(cuda):
+    """moe_set_gate_weights_device (stream-ordered D2D copy of a resident gate)
+    routes exactly like the host upload, call after call."""
+    import torch
+    E, k, d, ff, T = 8, 2, 1024, 1408, 256
+    x, _, experts = _build(E, k, d, ff, T, seed=21)
+    gates = [wl.gate_weights(E, d, 1.3, 1, 0, it) for it in range(3)]
+    outs = []
+    for dev in (False, True):
+        m = MoELayer(1, E, k, d, ff, max_tokens=T)
+        for e, (w1, w3, w2) in enumerate(experts):
+            m.load_expert(0, e, w1, w3, w2)
+        xd = _to_dev(x, torch)
+        gd = torch.from_numpy(np.stack(gates).view(np.int16)).to(cuda)
+        ys = []
+        for it in range(3):
+            if dev:
+                m.set_gate_device(0, gd[it])
+            else:
+                m.set_gate(0, gates[it])
+            yd = torch.zeros((T, d), dtype=torch.int16, device=cuda)
+            m.forward(0, xd, yd, MOE_PLAN_FIXED, it)
+            ys.append(yd)
+        m.sync()
+        outs.append([y.cpu().numpy() for y in ys])
+        m.close()
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
