@@ -26,7 +26,10 @@
 namespace moe {
 thread_local std::string g_last_error;
 
-void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, int32_t* pred_counts) {
+// mirror: the gate's last CTA also copies the histograms (gate + predictor,
+// `stride` ints) into mapped host memory for the host planner (single GPU)
+void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, int32_t* pred_counts,
+                bool mirror = false, int stride = 0) {
   require(L.has_gate, "gate weights not set for layer");
   CU_CHECK(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * c->count_stride, s));
   if (c->fp32) {
@@ -37,7 +40,8 @@ void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, 
   CU_CHECK(launch_gate_topk(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
                             reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, pred_counts ? c->n_pred : 0,
                             c->k, c->ids.p, c->wts.p, c->counts.p, c->block_counts.p,
-                            pred_counts ? pred_counts : c->pred_counts.p, c->gate_partial.p, s));
+                            pred_counts ? pred_counts : c->pred_counts.p, c->gate_partial.p, s,
+                            mirror ? c->h_counts : nullptr, stride, c->gate_ticket.p));
 }
 
 // buf: [G][stride] int32 from the gate — per rank, E actual counts followed by
@@ -106,12 +110,15 @@ void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int3
   *c->hplan = c->plan.dev;
 }
 
+// local_plan (single GPU): the scan launch also builds the dispatch plan from
+// the gate histogram on the device (one extra CTA)
 void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool upload_plan = true,
-                    bool gather = false, bool fused = false) {
+                    bool gather = false, bool fused = false, bool local_plan = false) {
   if (upload_plan)
     CU_CHECK(launch_small_copy(c->dplan.p, c->hplan, sizeof(DevPlan), s));  // SM copy from mapped pinned memory
   const int nblk = gate_num_blocks(T);
-  CU_CHECK(launch_block_prefix(c->block_counts.p, nblk, c->E, c->dplan.p, c->block_pre.p, s));
+  CU_CHECK(launch_block_prefix(c->block_counts.p, nblk, c->E, c->dplan.p, c->block_pre.p, s,
+                               local_plan ? c->counts.p : nullptr));
   // rows move as opaque 16-byte chunks: the row width in 16-bit units covers fp32 rows too
   RowTargets t{};
   PeerSignal sig{};
@@ -306,7 +313,8 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
     c->tmX_T = T;
   }
   mark(0);
-  stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr);
+  const bool mirrored = c->G == 1 && !c->fp32 && T > 0;  // the gate publishes the histograms itself
+  stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr, mirrored, stride);
   if (c->G > 1 && c->p2p) {
     // every rank reads every histogram from its owner's slab
     CU_CHECK(launch_p2p_counts(c->peers, c->G, c->rank, stride, c->epoch_dev.p, c->p2p_timeout_ns, c->p2p_err,
@@ -324,18 +332,15 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
     require(c->desc.exchange_mode == MOE_EXCHANGE_NCCL, "staged API required for external exchange");
     g_nccl.check(g_nccl.AllGather(c->counts.p, c->counts_all.p, stride, ncclInt32, c->comm, s), "ncclAllGather");
     CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
-  } else {
+  } else if (!mirrored) {
     CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * stride), s));
   }
   if (deferred) {
     CU_CHECK(cudaEventRecordWithFlags(c->ev_counts, s, rec));
     mark(1);
-    if (c->G == 1)
-      CU_CHECK(launch_plan_local(c->counts.p, c->E, c->dplan.p, s));
-    else
-      CU_CHECK(launch_plan_exchange(c->counts_all.p, stride, c->G, c->rank, L.ptab.p, c->dplan.p, s));
+    if (c->G > 1) CU_CHECK(launch_plan_exchange(c->counts_all.p, stride, c->G, c->rank, L.ptab.p, c->dplan.p, s));
     mark(2);
-    stage_dispatch(c, x, T, s, /*upload_plan=*/false, gather, fused);
+    stage_dispatch(c, x, T, s, /*upload_plan=*/false, gather, fused, /*local_plan=*/c->G == 1);
   } else {
     mark(1);
     CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram

@@ -319,6 +319,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->xp.alloc(static_cast<size_t>(c->rows_cap) * c->xw);
     c->perm_src.alloc(static_cast<size_t>(c->rows_cap));
     c->row_owner.alloc(static_cast<size_t>(c->rows_cap));
+    c->gate_ticket.alloc(4);
+    CU_CHECK(cudaMemset(c->gate_ticket.p, 0, 4 * sizeof(unsigned)));
     c->comb_cnt.alloc(static_cast<size_t>(c->Tmax) * std::max(1, c->d / 256));
     CU_CHECK(cudaMemset(c->comb_cnt.p, 0, c->comb_cnt.n * sizeof(int32_t)));
     c->h.alloc(static_cast<size_t>(c->rows_cap) * c->ff * c->elem);

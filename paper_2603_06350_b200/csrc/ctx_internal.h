@@ -32,9 +32,10 @@ namespace moe {
 int gate_num_blocks(int T);
 cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bfloat16* w_all, int E, int n_pred,
                              int k, int32_t* ids, float* wts, int32_t* counts, int32_t* block_counts,
-                             int32_t* pred_counts, float* partial, cudaStream_t stream);
+                             int32_t* pred_counts, float* partial, cudaStream_t stream,
+                             int32_t* host_counts = nullptr, int host_n = 0, unsigned* ticket = nullptr);
 cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, const DevPlan* plan,
-                                int32_t* block_pre, cudaStream_t s);
+                                int32_t* block_pre, cudaStream_t s, const int32_t* local_counts = nullptr);
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
                             const int32_t* block_pre, const DevPlan* plan, const RowTargets& targets,
                             uint32_t* row_code, const PeerSignal& sig, cudaStream_t s, int32_t* perm_src,
@@ -299,6 +300,7 @@ struct moe_ctx {
   // short-K shapes (the late rows' sums serialise on 4 epilogue warps),
   // profiles/ab_fused_combine_r01.md
   bool fuse_combine = false;
+  DevBuf<unsigned> gate_ticket;  // CTAs of the gate grid done (histogram mirror, self-resetting)
   DevBuf<int32_t> row_owner;  // [rows_cap] row -> t * k + j
   DevBuf<int32_t> comb_cnt;   // [Tmax * d / 256] arrivals per (token, GEMM2 n tile)
   int group_m[2] = {0, 0};  // K4 m-tiles per n sweep (0: the kernel's default; MOE_GEMM_GROUP_M=g1,g2)

@@ -35,10 +35,20 @@ namespace moe {
 // ------------------------------------------------------- block prefix scan
 // block_pre[b][e] = src_off[e] + sum_{b' < b} block_counts[b'][e].  One CTA per
 // expert column; each thread scans a contiguous chunk of blocks.
+__device__ void plan_local_body(const int32_t* __restrict__ counts, int E, DevPlan* __restrict__ plan);
+
+// local_counts != nullptr (single GPU): the dispatch plan is built by one extra
+// CTA (index E) from the gate histogram, and every source offset is 0 — the
+// plan kernel and the scan share one launch.
 __global__ void __launch_bounds__(512)
 block_prefix_kernel(const int32_t* __restrict__ block_counts, int nblk, int E,
-                    const DevPlan* __restrict__ plan, int32_t* __restrict__ block_pre) {
+                    const DevPlan* __restrict__ plan, int32_t* __restrict__ block_pre,
+                    const int32_t* __restrict__ local_counts, DevPlan* __restrict__ local_plan) {
   const int e = blockIdx.x;
+  if (e == E) {
+    plan_local_body(local_counts, E, local_plan);
+    return;
+  }
   const int tid = threadIdx.x;
   const int per = (nblk + blockDim.x - 1) / blockDim.x;
   const int b0 = tid * per, b1 = min(nblk, b0 + per);
@@ -65,7 +75,7 @@ block_prefix_kernel(const int32_t* __restrict__ block_counts, int nblk, int E,
     if (lane < (int)(blockDim.x >> 5)) warp_sums[lane] = w;  // inclusive warp prefix
   }
   __syncthreads();
-  int run = plan->src_off[e] + (warp > 0 ? warp_sums[warp - 1] : 0) + incl - local;
+  int run = (local_counts ? 0 : plan->src_off[e]) + (warp > 0 ? warp_sums[warp - 1] : 0) + incl - local;
   for (int b = b0; b < b1; ++b) {
     block_pre[(size_t)b * E + e] = run;
     run += block_counts[(size_t)b * E + e];
@@ -262,8 +272,7 @@ combine_kernel(const __grid_constant__ RowTargets sources, int T, int d, const u
 // one GEMM segment, so the dispatch plan is an exclusive scan of the gate
 // histogram — built on the device, no host round trip.  Row placement is
 // identical to the host plan's (expert e's rows start at sum_{e'<e} n_e').
-__global__ void __launch_bounds__(256) plan_local_kernel(const int32_t* __restrict__ counts, int E,
-                                                         DevPlan* __restrict__ plan) {
+__device__ void plan_local_body(const int32_t* __restrict__ counts, int E, DevPlan* __restrict__ plan) {
   __shared__ int base[kMaxExperts + 1];
   __shared__ int seg_idx[kMaxExperts + 1];
   const int tid = threadIdx.x;
@@ -297,6 +306,11 @@ __global__ void __launch_bounds__(256) plan_local_kernel(const int32_t* __restri
     plan->rep_remote[e] = 0;
     if (n > 0) plan->segs[seg_idx[e]] = GemmSeg{base[e], n, e, 0};
   }
+}
+
+__global__ void __launch_bounds__(256) plan_local_kernel(const int32_t* __restrict__ counts, int E,
+                                                         DevPlan* __restrict__ plan) {
+  plan_local_body(counts, E, plan);
 }
 
 cudaError_t launch_plan_local(const int32_t* counts, int E, DevPlan* plan, cudaStream_t s) {
@@ -418,9 +432,11 @@ cudaError_t launch_small_copy(void* dst, const void* src, size_t bytes, cudaStre
 
 // ------------------------------------------------------------- launchers
 cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, const DevPlan* plan,
-                                int32_t* block_pre, cudaStream_t s) {
-  if (nblk <= 0) return cudaSuccess;
-  block_prefix_kernel<<<E, 512, 0, s>>>(block_counts, nblk, E, plan, block_pre);
+                                int32_t* block_pre, cudaStream_t s, const int32_t* local_counts) {
+  if (nblk <= 0 && !local_counts) return cudaSuccess;
+  // with local_counts: + one CTA that builds the single-GPU plan into *plan
+  block_prefix_kernel<<<E + (local_counts ? 1 : 0), 512, 0, s>>>(block_counts, nblk, E, plan, block_pre,
+                                                                   local_counts, const_cast<DevPlan*>(plan));
   return cudaGetLastError();
 }
 

@@ -146,6 +146,29 @@ __device__ __forceinline__ void select_and_count(const float* red, int* hist, in
   }
 }
 
+// Host mirror of the histograms (single GPU): the last CTA of the grid to
+// finish copies counts[0, n) — gate then predictor histograms — into mapped
+// pinned memory for the host planner, instead of a separate copy kernel.
+struct CountsMirror {
+  int32_t* host;      // mapped pinned [n]; nullptr = no mirror
+  unsigned* ticket;   // CTAs done (self-resetting)
+  int n;
+};
+
+__device__ __forceinline__ void publish_counts(const int32_t* counts, const CountsMirror& m) {
+  if (!m.host) return;
+  __shared__ bool last;
+  __threadfence();  // this CTA's histogram atomics are visible device-wide
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(m.ticket, 1u) == gridDim.x * gridDim.y - 1;
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    for (int i = threadIdx.x; i < m.n; i += blockDim.x) m.host[i] = __ldcg(counts + i);
+    if (threadIdx.x == 0) *m.ticket = 0u;
+  }
+}
+
 }  // namespace
 
 // x [T, d] bf16; w_all [(1 + n_pred) * E, d] bf16 (rows 0..E-1 = gate).
@@ -158,7 +181,8 @@ template <int NT>
 __global__ void __launch_bounds__(kWarps * 32)
 gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_bfloat16* __restrict__ w_all, int E,
                  int n_pred, int k, int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
-                 int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts, float* __restrict__ partial) {
+                 int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts, float* __restrict__ partial,
+                 const __grid_constant__ CountsMirror mirror) {
   constexpr int kCols = 8 * NT;
   constexpr int kLd = kCols + 4;  // padded row of the reduction buffer
   __shared__ float red[kBlockTokens * kLd];
@@ -220,6 +244,7 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_b
   }
   select_and_count<kLd, false>(red, hist, blk, 0, kBlockTokens, T, E, n_pred, k, ids, wts, counts, block_counts,
                                pred_counts);
+  publish_counts(counts, mirror);
 }
 
 // Sums the split-K partial logits of kFinishTokens tokens of one 32-token
@@ -233,7 +258,8 @@ template <int NT>
 __global__ void __launch_bounds__(kWarps * 32)
 gate_finish_kernel(const float* __restrict__ partial, int splits, int T, int E, int n_pred, int k,
                    int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
-                   int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts) {
+                   int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts,
+                   const __grid_constant__ CountsMirror mirror) {
   constexpr int kCols = 8 * NT;
   constexpr int kLd = kCols + 4;
   __shared__ float red[kFinishTokens * kLd];
@@ -256,6 +282,7 @@ gate_finish_kernel(const float* __restrict__ partial, int splits, int T, int E, 
   __syncthreads();
   select_and_count<kLd, true>(red, hist, blk, tok0, kFinishTokens, T, E, n_pred, k, ids, wts, counts, block_counts,
                               pred_counts);
+  publish_counts(counts, mirror);
 }
 
 int gate_num_blocks(int T) { return (T + kBlockTokens - 1) / kBlockTokens; }
@@ -279,8 +306,10 @@ size_t gate_partial_floats(int T, int d, int Etot) {
 
 cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bfloat16* w_all, int E,
                              int n_pred, int k, int32_t* ids, float* wts, int32_t* counts,
-                             int32_t* block_counts, int32_t* pred_counts, float* partial, cudaStream_t stream) {
+                             int32_t* block_counts, int32_t* pred_counts, float* partial, cudaStream_t stream,
+                             int32_t* host_counts, int host_n, unsigned* ticket) {
   if (T <= 0) return cudaSuccess;
+  const CountsMirror mirror{host_counts, ticket, host_n};
   const int Etot = E * (1 + n_pred);
   if (Etot > 32 * kPerLane || k > 8 || (d % 256) != 0) return cudaErrorInvalidValue;
   const int nblk = gate_num_blocks(T);
@@ -289,11 +318,11 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
 #define MOE_GATE_CASE(NT_)                                                                                  \
   if (Etot <= 8 * NT_) {                                                                                    \
     gate_topk_kernel<NT_><<<grid, block, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,       \
-                                                      block_counts, pred_counts, partial);                 \
+                                                      block_counts, pred_counts, partial,                  \
+                                                      splits > 1 ? CountsMirror{} : mirror);               \
     if (splits > 1)                                                                                         \
       gate_finish_kernel<NT_><<<dim3(nblk, kBlockTokens / kFinishTokens), block, 0, stream>>>(              \
-          partial, splits, T, E, n_pred, k, ids, wts,                                                       \
-                                                          counts, block_counts, pred_counts);               \
+          partial, splits, T, E, n_pred, k, ids, wts, counts, block_counts, pred_counts, mirror);           \
     return cudaGetLastError();                                                                              \
   }
   MOE_GATE_CASE(1)
