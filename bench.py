@@ -517,10 +517,14 @@ def run_ours(args):
             "p50_ms": p50, "p99_ms": p99,
             "step_ms": [round(v, 3) for v in lat],
             "phase_ms_median": phases, "replicas_median": replicas,
-            # per step (G=1): gate-weight SM copy, K1 gate, counts SM copy, on-device plan,
-            # block prefix, K3 dispatch, K4 GEMM1, K4 GEMM2, K5 combine; P2P adds the counts
-            # gather, plan upload and the rows / outputs flag kernels (NCCL's own kernels not counted)
-            "gpu_launches": (13 if p2p else 9) * args.steps,
+            # our kernels per step.  G=1: K1 gate (+ its split-K finish for small
+            # batches; it also mirrors the histograms to the host), block prefix + on-device
+            # plan (one launch), K3 dispatch, K4 GEMM1, K4 GEMM2, K5 combine.  P2P (host-planned
+            # SYNC steps): gate, counts gather, counts SM copy, plan upload, prefix, dispatch,
+            # rows wait, GEMM1, GEMM2, outputs signal + wait, combine.  NCCL: gate, counts copy,
+            # plan upload, prefix, dispatch, GEMM1, GEMM2, combine (NCCL's own kernels and the
+            # gate-weight memcpy not counted)
+            "gpu_launches": (12 if p2p else (8 if G > 1 else 6 + (1 if T <= 32 * 148 else 0))) * args.steps,
             "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel (GEMM1 SwiGLU + GEMM2)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "peak_source": peak_src + ", bf16 sustained", "burst_peak": peaks.get("bf16_tflops"),
