@@ -54,7 +54,6 @@ cudaError_t launch_p2p_wait(const uint32_t* my_flags, int G, int kind, const uin
 cudaError_t launch_p2p_counts(const PeerSlabs& peers, int G, int rank, int stride, uint32_t* epoch,
                               uint64_t timeout_ns, int* err, int32_t* counts_all, cudaStream_t s);
 cudaError_t launch_small_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
-cudaError_t launch_plan_local(const int32_t* counts, int E, DevPlan* plan, cudaStream_t s);
 cudaError_t launch_plan_exchange(const int32_t* counts_all, int stride, int G, int rank, const PlacementTable* pt,
                                  DevPlan* plan, cudaStream_t s);
 // K7 fp32 path

@@ -272,6 +272,7 @@ combine_kernel(const __grid_constant__ RowTargets sources, int T, int d, const u
 // one GEMM segment, so the dispatch plan is an exclusive scan of the gate
 // histogram — built on the device, no host round trip.  Row placement is
 // identical to the host plan's (expert e's rows start at sum_{e'<e} n_e').
+// Runs as the extra CTA of the block-prefix launch (block_prefix_kernel).
 __device__ void plan_local_body(const int32_t* __restrict__ counts, int E, DevPlan* __restrict__ plan) {
   __shared__ int base[kMaxExperts + 1];
   __shared__ int seg_idx[kMaxExperts + 1];
@@ -308,15 +309,6 @@ __device__ void plan_local_body(const int32_t* __restrict__ counts, int E, DevPl
   }
 }
 
-__global__ void __launch_bounds__(256) plan_local_kernel(const int32_t* __restrict__ counts, int E,
-                                                         DevPlan* __restrict__ plan) {
-  plan_local_body(counts, E, plan);
-}
-
-cudaError_t launch_plan_local(const int32_t* counts, int E, DevPlan* plan, cudaStream_t s) {
-  plan_local_kernel<<<1, 256, 0, s>>>(counts, E, plan);
-  return cudaGetLastError();
-}
 
 // ---------------------------------------------- on-device exchange plan (G > 1)
 // Peer-memory exchange with a placement decided BEFORE the layer (FIXED, or
@@ -490,7 +482,7 @@ cudaError_t preload_dispatch_kernels() {
       reinterpret_cast<const void*>(dispatch_kernel<6>),   reinterpret_cast<const void*>(dispatch_kernel<8>),
       reinterpret_cast<const void*>(combine_kernel<1>),    reinterpret_cast<const void*>(combine_kernel<2>),
       reinterpret_cast<const void*>(combine_kernel<4>),    reinterpret_cast<const void*>(combine_kernel<6>),
-      reinterpret_cast<const void*>(combine_kernel<8>),    reinterpret_cast<const void*>(plan_local_kernel),
+      reinterpret_cast<const void*>(combine_kernel<8>),
       reinterpret_cast<const void*>(plan_exchange_kernel), reinterpret_cast<const void*>(small_copy_kernel)};
   for (const void* f : fns) {
     const cudaError_t e = cudaFuncGetAttributes(&a, f);
