@@ -242,3 +242,44 @@ def test_p2p_graph_replay(cuda):
             assert torch.equal(yd[r], y1), (it, r)
     for m in ms + [one]:
         m.close()
+
+
+def test_p2p_predicted_planning_distance_two(cuda):
+    """As test_p2p_predicted_planning_ahead with predictor distance 2 over 4
+    layers at G=2: layers 2-3 run the on-device exchange plan from placements
+    decided two layers earlier; outputs bit-identical to G = 1."""
+    import torch
+    G, L, E, k, d, ff, T, dist = 2, 4, 16, 2, 1024, 1408, 128, 2
+    mem = 3.0 * d * ff * 2 / 1e6
+    ms = [MoELayer(L, E, k, d, ff, max_tokens=T, world_size=G, rank=r, exchange_mode=MOE_EXCHANGE_P2P,
+                   num_predictor_targets=1, predictor_distance=dist, expert_mem_mb=mem,
+                   layer_mem_cap_mb=(E + 4) * mem) for r in range(G)]
+    handles = [m.p2p_export() for m in ms]
+    for m in ms:
+        m.p2p_import(handles)
+    one = MoELayer(L, E, k, d, ff, max_tokens=T, expert_mem_mb=mem, layer_mem_cap_mb=E * mem)
+    gates = [wl.gate_weights(E, d, 1.5, 1, l, 0) for l in range(L)]
+    for m in ms + [one]:
+        for l in range(L):
+            m.set_gate(l, gates[l])
+            for e in range(E):
+                m.load_expert(l, e, *wl.expert_weights(d, ff, 1, l, e))
+    for m in ms:
+        for l in range(L - dist):
+            m.set_predictor(l, 0, gates[l + dist])
+    xd = [torch.from_numpy(wl.tokens(T, d, E, 1, 800 + r).view(np.int16)).to(cuda) for r in range(G)]
+    yd = [[torch.zeros((T, d), dtype=torch.int16, device=cuda) for _ in range(L)] for _ in range(G)]
+    for it in range(3):
+        def rank_stack(r):
+            return [ms[r].forward(l, xd[r], yd[r][l], MOE_PLAN_PREDICTED, it, stats=True) for l in range(L)]
+        sts = _parallel(ms, rank_stack)
+        torch.cuda.synchronize()
+        for r in range(G):
+            assert [st.plan_source for st in sts[r]] == [3, 3, 2, 2]
+            for l in range(L):
+                y1 = torch.zeros((T, d), dtype=torch.int16, device=cuda)
+                one.forward(l, xd[r], y1, MOE_PLAN_FIXED, it)
+                one.sync()
+                assert torch.equal(yd[r][l], y1), (it, r, l)
+    for m in ms + [one]:
+        m.close()

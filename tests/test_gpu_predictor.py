@@ -70,3 +70,41 @@ def test_sync_planner_inside_forward_matches_host_planner(cuda):
         y_ref = oracle.layer_forward(x[idx], wg, experts, [1] * E, k)[0]
         assert float(np.max(np.abs(y[idx] - y_ref)) / np.max(np.abs(y_ref))) <= 2e-2
     m.close()
+
+
+def test_predicted_planning_distance_two(cuda):
+    """MOE_PLAN_PREDICTED with predictor distance d = 2 over a 5-layer stack:
+    layer l's fused predictor scores layer l + 2, layers 0-1 bootstrap from
+    history (simulator.cpp:146-151), layers 2-4 run on placements planned two
+    layers ahead; outputs equal the fixed-placement layer."""
+    import torch
+    from paper_2603_06350_b200 import MOE_PLAN_FIXED, MOE_PLAN_PREDICTED, MoELayer
+    from paper_2603_06350_b200 import workload as wl
+    L, E, k, d, ff, T, dist = 5, 8, 2, 1024, 1408, 256, 2
+    mem = 3.0 * d * ff * 2 / 1e6
+    m = MoELayer(L, E, k, d, ff, max_tokens=T, num_predictor_targets=1, predictor_distance=dist,
+                 expert_mem_mb=mem, layer_mem_cap_mb=(E + 3) * mem)
+    ref = MoELayer(L, E, k, d, ff, max_tokens=T, expert_mem_mb=mem, layer_mem_cap_mb=E * mem)
+    gates = [wl.gate_weights(E, d, 1.5, 1, l, 0) for l in range(L)]
+    for mm in (m, ref):
+        for l in range(L):
+            mm.set_gate(l, gates[l])
+            for e in range(E):
+                mm.load_expert(l, e, *wl.expert_weights(d, ff, 1, l, e))
+    for l in range(L - dist):
+        m.set_predictor(l, 0, gates[l + dist])
+    xs = [torch.from_numpy(wl.tokens(T, d, E, 1, 40 + l).view(np.int16)).to(cuda) for l in range(L)]
+    for it in range(3):
+        sts = []
+        for l in range(L):
+            y = torch.zeros((T, d), dtype=torch.int16, device=cuda)
+            sts.append(m.forward(l, xs[l], y, MOE_PLAN_PREDICTED, it, stats=True))
+            y1 = torch.zeros_like(y)
+            ref.forward(l, xs[l], y1, MOE_PLAN_FIXED, it)
+            ref.sync()
+            assert torch.equal(y, y1), (it, l)
+        assert [st.plan_source for st in sts] == [3, 3, 2, 2, 2], [st.plan_source for st in sts]
+        for st in sts[dist:]:
+            assert 0.9 <= st.predictor_accuracy <= 1.0  # the predictor is layer l+2's own gate
+    m.close()
+    ref.close()
