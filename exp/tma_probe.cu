@@ -11,14 +11,15 @@ using namespace moe;
 constexpr int STAGES = 4, BK = 64, BN = 256;
 constexpr uint32_t kB = BN * BK * 2;
 
-__global__ void __launch_bounds__(64, 1) stream_b(const __grid_constant__ CUtensorMap tmB,
+__global__ void __launch_bounds__(192, 1) stream_b(const __grid_constant__ CUtensorMap tmB,
                                                    const __grid_constant__ CUtensorMap tmA, int a_rows, int tiles,
-                                                   int n_tiles, int rows_per_slot, int num_kb, int stages, int* sink) {
+                                                   int n_tiles, int rows_per_slot, int num_kb, int stages, int* sink, int spin) {
   extern __shared__ uint8_t raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[8], empty[8];
+  __shared__ uint64_t full[8], empty[8], done;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&done, 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -45,6 +46,9 @@ __global__ void __launch_bounds__(64, 1) stream_b(const __grid_constant__ CUtens
         if (++stage == stages) { stage = 0; phase ^= 1; }
       }
     if (acc == 0x7fffffff) *sink = acc;
+    mbar_arrive(&done);
+  } else if (threadIdx.x >= 64 && spin) {  // idle warps waiting like K4's epilogue warps
+    mbar_wait(&done, 0);
   }
 }
 
@@ -73,19 +77,19 @@ int main() {
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   enc(&ma128, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xa, adims, strides, abox128, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  for (int a_rows : {0, 32, 128})
+  for (int spin : {0, 1}) for (int a_rows : {128})
   for (int stages : {4}) {
     const size_t smem = stages * (kB + 16384) + 1024;
     cudaFuncSetAttribute(stream_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     for (int grid : {148}) {
       cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-      for (int i = 0; i < 3; ++i) stream_b<<<grid, 64, smem>>>(m, a_rows == 32 ? ma32 : ma128, a_rows, tiles, n_tiles, rows, d / BK, stages, sink);
+      for (int i = 0; i < 3; ++i) stream_b<<<grid, spin ? 192 : 64, smem>>>(m, a_rows == 32 ? ma32 : ma128, a_rows, tiles, n_tiles, rows, d / BK, stages, sink, spin);
       cudaEventRecord(a);
-      for (int i = 0; i < 10; ++i) stream_b<<<grid, 64, smem>>>(m, a_rows == 32 ? ma32 : ma128, a_rows, tiles, n_tiles, rows, d / BK, stages, sink);
+      for (int i = 0; i < 10; ++i) stream_b<<<grid, spin ? 192 : 64, smem>>>(m, a_rows == 32 ? ma32 : ma128, a_rows, tiles, n_tiles, rows, d / BK, stages, sink, spin);
       cudaEventRecord(b); cudaEventSynchronize(b);
       float ms; cudaEventElapsedTime(&ms, a, b); ms /= 10;
       const double gb = (double)tiles * BN * d * 2 / 1e9;
-      printf("a_rows %d stages %d grid %d: %.1f us  %.2f TB/s  (%s)\n", a_rows, stages, grid, ms * 1e3, gb / (ms * 1e-3) / 1e3,
+      printf("spin %d a_rows %d stages %d grid %d: %.1f us  %.2f TB/s  (%s)\n", spin, a_rows, stages, grid, ms * 1e3, gb / (ms * 1e-3) / 1e3,
              cudaGetErrorString(cudaGetLastError()));
     }
   }
