@@ -145,12 +145,15 @@ def test_p2p_rank_out_of_step_times_out(cuda, monkeypatch):
     ms[1].close()
 
 
-def test_p2p_two_processes_ipc(cuda, tmp_path):
+@pytest.mark.parametrize("residency", [0, 1])
+def test_p2p_two_processes_ipc(cuda, tmp_path, residency):
     """Two processes on the same device, slabs shared with CUDA IPC handles
     exchanged over gloo (tests/p2p_worker.py); each checks itself against a
-    single-GPU forward."""
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29731", PYTHONPATH=ROOT)
-    procs = [subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "p2p_worker.py"), str(r), "2"],
+    single-GPU forward.  residency=1: MOE_RESIDENCY_PLACED, so cold replicas are
+    copied out of the peer process's IPC-mapped weight slots."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29731 + residency), PYTHONPATH=ROOT)
+    procs = [subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "p2p_worker.py"), str(r), "2",
+                               str(residency)],
                               env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT) for r in range(2)]
     outs = []
     for p in procs:
@@ -163,6 +166,9 @@ def test_p2p_two_processes_ipc(cuda, tmp_path):
     for p, o in zip(procs, outs):
         assert p.returncode == 0, o[-3000:]
         assert "P2P-IPC OK" in o, o[-3000:]
+    if residency:  # some replica was copied across the process boundary
+        copies = [int(o.split("weight copies")[-1].split()[0]) for o in outs]
+        assert sum(copies) > 0, copies
 
 
 def test_p2p_predicted_planning_ahead(cuda):
