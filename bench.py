@@ -61,7 +61,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--pool", type=int, default=4, help="distinct token batches cycled per rank")
-    ap.add_argument("--cpu-sample-tokens", type=int, default=64)
+    ap.add_argument("--cpu-sample-tokens", type=int, default=256,
+                    help="tokens of the workload per reference-arm step (~0.5 s of host work each)")
+    ap.add_argument("--cpu-baseline-tokens", type=int, default=1024,
+                    help="tokens per sample of our arm's cpu_baseline leg (two samples)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
@@ -560,7 +563,7 @@ def run_ours(args):
                                   "H2D/D2H of neighbouring steps overlap the layer), wall clock over all steps "
                                   "until the last result is in host memory"}
         if G == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = run_cpu_baseline(args.cpu_sample_tokens)
+            line["cpu_baseline"] = run_cpu_baseline(args.cpu_baseline_tokens)
             line["cpu_baseline_cfg1_full"] = cpu_cfg1_full_layer()
         print(json.dumps(line), flush=True)
     m.close()
