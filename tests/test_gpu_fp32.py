@@ -54,3 +54,43 @@ def test_fp32_mode_within_1e4(cuda, E, k, d, ff, T, rc):
     err = float((torch.from_numpy(y).double() - ref).abs().max() / ref.abs().max())
     assert err <= TOL_FP32, err
     m.close()
+
+
+def test_fp32_mode_two_ranks_peer_memory(cuda):
+    """fp32 mode with two ranks sharing the GPU over the peer-memory exchange
+    (SYNC planning: host-planned exchange, fp32 rows moved as opaque 16-byte
+    chunks): each rank's output equals the single-GPU fp32 layer bit for bit."""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2603_06350_b200 import MOE_EXCHANGE_P2P, MOE_PLAN_SYNC
+    G, E, k, d, ff, T = 2, 8, 2, 256, 256, 96
+    rng = np.random.default_rng(5)
+    wg = oracle.bf16_to_f32(wl.gate_weights(E, d, 1.4, 1, 0, 0))
+    experts = [((rng.standard_normal((ff, d)) / np.sqrt(d)).astype(np.float32),
+                (rng.standard_normal((ff, d)) / np.sqrt(d)).astype(np.float32),
+                (rng.standard_normal((d, ff)) / np.sqrt(ff)).astype(np.float32)) for _ in range(E)]
+    mem = 3.0 * d * ff * 4 / 1e6
+    ms = [MoELayer(1, E, k, d, ff, max_tokens=T, world_size=G, rank=r, exchange_mode=MOE_EXCHANGE_P2P, precision=1,
+                   expert_mem_mb=mem, layer_mem_cap_mb=(E + 2) * mem) for r in range(G)]
+    handles = [m.p2p_export() for m in ms]
+    for m in ms:
+        m.p2p_import(handles)
+    one = MoELayer(1, E, k, d, ff, max_tokens=T, precision=1, expert_mem_mb=mem, layer_mem_cap_mb=E * mem)
+    for m in ms + [one]:
+        m.set_gate(0, np.ascontiguousarray(wg))
+        for e, w in enumerate(experts):
+            m.load_expert(0, e, *w)
+    xs = [torch.from_numpy(np.ascontiguousarray(oracle.bf16_to_f32(wl.tokens(T, d, E, 1, 70 + r)))).to(cuda)
+          for r in range(G)]
+    ys = [torch.zeros((T, d), dtype=torch.float32, device=cuda) for _ in range(G)]
+    with ThreadPoolExecutor(G) as ex:
+        list(ex.map(lambda r: ms[r].forward(0, xs[r], ys[r], MOE_PLAN_SYNC, 0), range(G)))
+    for m in ms:
+        m.sync()
+    for r in range(G):
+        y1 = torch.zeros_like(ys[r])
+        one.forward(0, xs[r], y1, MOE_PLAN_FIXED, 0)
+        one.sync()
+        assert torch.equal(ys[r], y1), r
+    for m in ms + [one]:
+        m.close()
