@@ -210,6 +210,15 @@ int moe_set_gate_weights_device(moe_ctx* ctx, int layer, const void* wg_dev, voi
 /* predictor weights for target `slot` (< num_predictor_targets), scored from
    layer `layer`'s hidden states: [E, d_model] */
 int moe_set_predictor_weights(moe_ctx* ctx, int layer, int slot, const uint16_t* wp);
+/* The batched predictor MLP for target `slot`: hidden = relu(x W1^T) with
+   E hidden units (W1 [E, d_model] bf16, computed in the gate's read of x),
+   out[e] = sum_j W2[e][j] hidden[j] (W2 [E, E] fp32, accumulated in j order
+   with fused multiply-adds), histogram of top-k(out).  w1 NULL keeps the
+   slot's current rows; w2 NULL returns the slot to the linear predictor.
+   Replaces the reference's LayerAwarePredictor::predict scoring
+   (predictor.cpp:38-62) with a learned model, as moe_set_predictor_weights
+   does with a linear one. */
+int moe_set_predictor_mlp(moe_ctx* ctx, int layer, int slot, const uint16_t* w1, const float* w2);
 
 /* ------------------------------------------------------------- placement */
 /* replica_counts[E] >= 1; replica_gpu[sum R] flattened (expert, ordinal).   */

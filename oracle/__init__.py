@@ -54,6 +54,7 @@ def orc():
             "orc_synth_gate": (None, [u64, C.c_int, C.c_int, vp, vp, vp]),
             "orc_synth_expert": (None, [u64, C.c_int, C.c_int, vp, vp, vp]),
             "orc_gate": (None, [vp, i64, C.c_int, vp, C.c_int, C.c_int, vp, vp, vp, vp]),
+            "orc_predict_mlp": (None, [vp, i64, C.c_int, vp, C.c_int, vp, C.c_int, vp]),
             "orc_dispatch": (C.c_int, [C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp]),
             "orc_expert_ffn": (None, [vp, i64, C.c_int, C.c_int, vp, vp, vp, C.c_int, C.c_int, vp]),
             "orc_combine": (None, [vp, C.c_int, vp, vp, i64, C.c_int, vp]),
@@ -168,6 +169,16 @@ def gate(x, wg, top_k, want_logits=False):
     orc().orc_gate(P(np.ascontiguousarray(x)), T, d, P(np.ascontiguousarray(wg)), E, top_k, P(ids), P(w),
                    P(counts), P(logits) if want_logits else None)
     return (ids, w, counts, logits) if want_logits else (ids, w, counts)
+
+
+def predict_mlp(x, w1, w2, top_k):
+    """Histogram of top-k(W2 relu(W1 x)) per token (the MLP predictor)."""
+    T, d = x.shape
+    E = w1.shape[0]
+    counts = np.zeros(E, np.int32)
+    orc().orc_predict_mlp(P(np.ascontiguousarray(x)), T, d, P(np.ascontiguousarray(w1)), E,
+                          P(np.ascontiguousarray(w2, np.float32)), top_k, P(counts))
+    return counts
 
 
 def dispatch(ids_per_rank, top_k, experts, replica_counts, replica_gpu):

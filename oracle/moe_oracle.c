@@ -284,6 +284,44 @@ void orc_gate(const uint16_t* x, int64_t tokens, int d, const uint16_t* wg, int 
   free(used);
 }
 
+/* The batched predictor MLP (moe_set_predictor_mlp; the learned stand-in
+ * for LayerAwarePredictor::predict's scoring, predictor.cpp:38-62):
+ * hidden_j = relu(x . W1_j) (E units, fp32 dot products as in orc_gate),
+ * out_e = fmaf chain over j ascending of W2[e][j] * hidden_j from 0, then
+ * top-k of out with the same lowest-index tie rule; counts = histogram. */
+void orc_predict_mlp(const uint16_t* x, int64_t tokens, int d, const uint16_t* w1, int experts,
+                     const float* w2, int top_k, int32_t* counts) {
+  float* h = (float*)malloc(sizeof(float) * experts);
+  float* out = (float*)malloc(sizeof(float) * experts);
+  int* used = (int*)malloc(sizeof(int) * experts);
+  memset(counts, 0, sizeof(int32_t) * experts);
+  for (int64_t t = 0; t < tokens; ++t) {
+    const uint16_t* xr = x + t * d;
+    for (int j = 0; j < experts; ++j) {
+      const uint16_t* wr = w1 + (int64_t)j * d;
+      float acc = 0.0f;
+      for (int c = 0; c < d; ++c) acc += bf2f(xr[c]) * bf2f(wr[c]);
+      h[j] = acc > 0.0f ? acc : 0.0f;
+    }
+    for (int e = 0; e < experts; ++e) {
+      float acc = 0.0f;
+      for (int j = 0; j < experts; ++j) acc = fmaf(w2[(int64_t)e * experts + j], h[j], acc);
+      out[e] = acc;
+      used[e] = 0;
+    }
+    for (int j = 0; j < top_k; ++j) {
+      int best = -1;
+      for (int e = 0; e < experts; ++e)
+        if (!used[e] && (best < 0 || out[e] > out[best])) best = e;
+      used[best] = 1;
+      counts[best]++;
+    }
+  }
+  free(h);
+  free(out);
+  free(used);
+}
+
 /* ----------------------------------------------------- dispatch (K3/K6) */
 /* Integer replica split (cost_model.cpp:98-106 made integer):
  * expert e's n_e assignments, ordered by (source rank, token index), are cut

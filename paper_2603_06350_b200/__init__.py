@@ -393,6 +393,14 @@ class MoELayer:
     def set_predictor(self, layer: int, slot: int, wp: np.ndarray) -> None:
         check(lib.moe_set_predictor_weights(self._h, layer, slot, _p(np.ascontiguousarray(wp))))
 
+    def set_predictor_mlp(self, layer: int, slot: int, w1, w2) -> None:
+        """MLP predictor for `slot`: w1 [E, d] bf16 bits (None keeps the rows),
+        w2 [E, E] fp32 (None: back to linear)."""
+        a1 = None if w1 is None else np.ascontiguousarray(w1)
+        a2 = None if w2 is None else np.ascontiguousarray(w2, dtype=np.float32)
+        check(lib.moe_set_predictor_mlp(self._h, layer, slot, _p(a1) if a1 is not None else None,
+                                        _p(a2) if a2 is not None else None))
+
     def set_placement(self, layer: int, replica_counts, replica_gpu) -> None:
         rc, rg = _i32(replica_counts), _i32(replica_gpu)
         check(lib.moe_set_placement(self._h, layer, _p(rc), _p(rg)))

@@ -93,6 +93,7 @@ _sig("moe_load_expert_weights_f32", C.c_int, vp, C.c_int, C.c_int, vp, vp, vp)
 _sig("moe_set_gate_weights_f32", C.c_int, vp, C.c_int, vp)
 _sig("moe_set_gate_weights_device", C.c_int, vp, C.c_int, vp, vp)
 _sig("moe_set_predictor_weights", C.c_int, vp, C.c_int, C.c_int, vp)
+_sig("moe_set_predictor_mlp", C.c_int, vp, C.c_int, C.c_int, vp, vp)
 _sig("moe_set_placement", C.c_int, vp, C.c_int, vp, vp)
 _sig("moe_gate_topk", C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp)
 _sig("moe_predict_loads", C.c_int, vp, C.c_int, vp, C.c_int, vp, vp)
@@ -137,7 +138,7 @@ EXPORTED = [
     "moe_last_error", "moe_version", "moe_nccl_unique_id", "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_stream",
     "moe_ctx_sync", "moe_p2p_export", "moe_p2p_import", "moe_load_expert_weights", "moe_set_gate_weights",
     "moe_load_expert_weights_f32", "moe_set_gate_weights_f32", "moe_set_gate_weights_device",
-    "moe_set_predictor_weights", "moe_set_placement", "moe_gate_topk", "moe_predict_loads",
+    "moe_set_predictor_weights", "moe_set_predictor_mlp", "moe_set_placement", "moe_gate_topk", "moe_predict_loads",
     "moe_layer_forward", "moe_layer_forward_host", "moe_layer_forward_host_async", "moe_wait",
     "moe_host_alloc", "moe_host_free", "moe_gemm_times", "moe_residency",
     "moe_forward_begin", "moe_forward_expert",

@@ -41,7 +41,7 @@ void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, 
                             reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, pred_counts ? c->n_pred : 0,
                             c->k, c->ids.p, c->wts.p, c->counts.p, c->block_counts.p,
                             pred_counts ? pred_counts : c->pred_counts.p, c->gate_partial.p, s,
-                            mirror ? c->h_counts : nullptr, stride, c->gate_ticket.p));
+                            mirror ? c->h_counts : nullptr, stride, c->gate_ticket.p, L.pred_w2.p, L.mlp_mask));
 }
 
 // buf: [G][stride] int32 from the gate — per rank, E actual counts followed by
@@ -412,7 +412,7 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
     // Replay the layer's whole device sequence (8-14 kernels) as one CUDA
     // graph: captured once per (layer, tokens, buffers), then launched with a
     // single call — the launch-bound decode regime pays one launch, not ten.
-    const GraphKey key{layer, T, x, y, x_consumed, with_pred};
+    const GraphKey key{layer, T, x, y, x_consumed, with_pred, L.mlp_mask};
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
       CU_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -491,7 +491,7 @@ int moe_gate_topk(moe_ctx* c, int layer, const uint16_t* x, int T, int32_t* ids,
     CU_CHECK(launch_gate_topk(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
                               reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, pred_counts ? c->n_pred : 0, c->k,
                               ids, w, counts, c->block_counts.p, pred_counts ? pred_counts : c->pred_counts.p,
-                              c->gate_partial.p, s));
+                              c->gate_partial.p, s, nullptr, 0, nullptr, L.pred_w2.p, L.mlp_mask));
   });
 }
 
@@ -509,7 +509,8 @@ int moe_predict_loads(moe_ctx* c, int layer, const uint16_t* x, int T, int32_t* 
     CU_CHECK(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * c->E, s));
     CU_CHECK(launch_gate_topk(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
                               reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, c->n_pred, c->k, c->ids.p,
-                              c->wts.p, c->counts.p, c->block_counts.p, pred_counts, c->gate_partial.p, s));
+                              c->wts.p, c->counts.p, c->block_counts.p, pred_counts, c->gate_partial.p, s, nullptr,
+                              0, nullptr, L.pred_w2.p, L.mlp_mask));
   });
 }
 

@@ -642,6 +642,30 @@ int moe_set_predictor_weights(moe_ctx* c, int layer, int slot, const uint16_t* w
   });
 }
 
+int moe_set_predictor_mlp(moe_ctx* c, int layer, int slot, const uint16_t* w1, const float* w2) {
+  return guarded([&] {
+    Layer& L = layer_at(c, layer);
+    require(slot >= 0 && slot < c->n_pred, "predictor slot out of range");
+    require(slot < 32, "MLP predictor slots are limited to 32");
+    if (w1) {
+      const int rc = moe_set_predictor_weights(c, layer, slot, w1);
+      if (rc != MOE_OK) throw Status{rc, g_last_error};
+    }
+    CU_CHECK(cudaStreamSynchronize(c->stream));
+    if (!w2) {  // back to the linear predictor
+      L.mlp_mask &= ~(1u << slot);
+      return;
+    }
+    const size_t EE = static_cast<size_t>(c->E) * c->E;
+    if (!L.pred_w2.p) {
+      L.pred_w2.alloc(EE * c->n_pred);
+      CU_CHECK(cudaMemset(L.pred_w2.p, 0, L.pred_w2.n * sizeof(float)));
+    }
+    CU_CHECK(cudaMemcpy(L.pred_w2.p + slot * EE, w2, EE * sizeof(float), cudaMemcpyHostToDevice));
+    L.mlp_mask |= 1u << slot;
+  });
+}
+
 int moe_set_placement(moe_ctx* c, int layer, const int32_t* rc, const int32_t* rg) {
   return guarded([&] {
     Layer& L = layer_at(c, layer);

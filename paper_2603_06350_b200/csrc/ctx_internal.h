@@ -33,7 +33,8 @@ int gate_num_blocks(int T);
 cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bfloat16* w_all, int E, int n_pred,
                              int k, int32_t* ids, float* wts, int32_t* counts, int32_t* block_counts,
                              int32_t* pred_counts, float* partial, cudaStream_t stream,
-                             int32_t* host_counts = nullptr, int host_n = 0, unsigned* ticket = nullptr);
+                             int32_t* host_counts = nullptr, int host_n = 0, unsigned* ticket = nullptr,
+                             const float* pred_w2 = nullptr, unsigned mlp_mask = 0);
 cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, const DevPlan* plan,
                                 int32_t* block_pre, cudaStream_t s, const int32_t* local_counts = nullptr);
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
@@ -211,6 +212,8 @@ struct Layer {
   std::vector<int32_t> rep_counts, rep_gpu;  // placement (host)
   bool has_placement = false;
   bool has_pred_weights = false;
+  DevBuf<float> pred_w2;   // [n_pred][E][E] output layers of MLP predictor slots
+  unsigned mlp_mask = 0;   // bit p: predictor slot p is an MLP (W2 set)
   // layer-aware predictor state (MOE_PLAN_PREDICTED)
   std::vector<int64_t> pred_loads;          // predicted loads for this layer (made d layers earlier)
   bool pred_valid = false;
@@ -242,8 +245,10 @@ struct GraphKey {
   const void* y;
   cudaEvent_t x_consumed;
   bool pred;
+  unsigned mlp;  // kernel arguments captured by value: a new predictor mask is a new graph
   bool operator<(const GraphKey& o) const {
-    return std::tie(layer, T, x, y, x_consumed, pred) < std::tie(o.layer, o.T, o.x, o.y, o.x_consumed, o.pred);
+    return std::tie(layer, T, x, y, x_consumed, pred, mlp) <
+           std::tie(o.layer, o.T, o.x, o.y, o.x_consumed, o.pred, o.mlp);
   }
 };
 

@@ -58,15 +58,10 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
 
 // Top-k over logits [base, base+E) of one token's stacked row in shared
 // memory; lane l looks at l, l+32, ...  Every lane returns the same result.
-__device__ __forceinline__ void warp_topk(const float* row, int base, int E, int k, int (&ids_out)[8],
-                                          float (&logit_out)[8]) {
+// Top-k over per-lane values own[s] = value of expert lane + 32 s.
+__device__ __forceinline__ void warp_topk_vals(const float (&own)[kPerLane], int E, int k, int (&ids_out)[8],
+                                               float (&logit_out)[8]) {
   const int lane = lane_id();
-  float own[kPerLane];
-#pragma unroll
-  for (int s = 0; s < kPerLane; ++s) {
-    const int e = lane + 32 * s;
-    own[s] = e < E ? row[base + e] : -FLT_MAX;
-  }
   uint32_t taken = 0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -91,17 +86,63 @@ __device__ __forceinline__ void warp_topk(const float* row, int base, int E, int
   }
 }
 
+__device__ __forceinline__ void warp_topk(const float* row, int base, int E, int k, int (&ids_out)[8],
+                                          float (&logit_out)[8]) {
+  const int lane = lane_id();
+  float own[kPerLane];
+#pragma unroll
+  for (int s = 0; s < kPerLane; ++s) {
+    const int e = lane + 32 * s;
+    own[s] = e < E ? row[base + e] : -FLT_MAX;
+  }
+  warp_topk_vals(own, E, k, ids_out, logit_out);
+}
+
+// The batched predictor MLP (K2 with a hidden layer): its E hidden units are
+// the slot's stacked rows (computed in the same read of x as the gate), so
+// per token the warp turns them in place into out[e] = sum_j W2[e][j]
+// relu(hidden_j) — an fmaf chain in j order, reproducible bit for bit on the
+// CPU — and the usual top-k runs on out.  W2 [E][E] fp32 per slot.  A
+// separate instantiation (MLP = true): the linear path keeps its registers.
+struct PredictorMlp {
+  const float* w2;  // [n_pred][E][E]; nullptr: every slot linear
+  uint32_t mask;    // bit p: slot p is an MLP
+};
+
+__device__ __forceinline__ void mlp_scores_inplace(float* seg, int E, const float* __restrict__ w2) {
+  const int lane = lane_id();
+  float own[kPerLane];
+#pragma unroll
+  for (int s = 0; s < kPerLane; ++s) {
+    const int e = lane + 32 * s;
+    float acc = 0.0f;
+    if (e < E) {
+      const float* w = w2 + (size_t)e * E;
+      for (int j = 0; j < E; ++j) {
+        const float h = seg[j];
+        acc = fmaf(__ldg(w + j), h > 0.0f ? h : 0.0f, acc);
+      }
+    }
+    own[s] = acc;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < kPerLane; ++s)
+    if (lane + 32 * s < E) seg[lane + 32 * s] = own[s];
+  __syncwarp();
+}
+
 // top-k, softmax and histograms for `ntok` tokens of one 32-token block,
 // starting at token tok0 of the block, whose stacked logits sit in shared
 // memory (row stride LD, row 0 = tok0); warp w handles ntok / kWarps tokens.
 // ACCUM: the block's histogram row is shared with other CTAs (atomic adds
 // into a zeroed row) instead of being written whole.
-template <int LD, bool ACCUM>
+template <int LD, bool ACCUM, bool MLP>
 __device__ __forceinline__ void select_and_count(const float* red, int* hist, int blk, int tok0, int ntok, int T,
                                                  int E, int n_pred, int k, int32_t* __restrict__ ids,
                                                  float* __restrict__ wts, int32_t* __restrict__ counts,
                                                  int32_t* __restrict__ block_counts,
-                                                 int32_t* __restrict__ pred_counts) {
+                                                 int32_t* __restrict__ pred_counts, const PredictorMlp& mlp) {
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int per = ntok / kWarps;
   for (int q = 0; q < per; ++q) {
@@ -112,6 +153,8 @@ __device__ __forceinline__ void select_and_count(const float* red, int* hist, in
     for (int gi = 0; gi <= n_pred; ++gi) {
       int sel[8];
       float lg[8];
+      if (MLP && gi > 0 && ((mlp.mask >> (gi - 1)) & 1u))
+        mlp_scores_inplace(const_cast<float*>(row) + gi * E, E, mlp.w2 + (size_t)(gi - 1) * E * E);
       warp_topk(row, gi * E, E, k, sel, lg);
       if (lane == 0) {
         if (gi == 0) {
@@ -177,12 +220,12 @@ __device__ __forceinline__ void publish_counts(const int32_t* counts, const Coun
 // NT = n-tiles of 8 stacked logits (E * (1 + n_pred) <= 8 * NT).  With
 // gridDim.y > 1 the CTA covers a 1/gridDim.y share of d and writes its
 // partial logits to `partial` instead of selecting.
-template <int NT>
+template <int NT, bool MLP>
 __global__ void __launch_bounds__(kWarps * 32)
 gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_bfloat16* __restrict__ w_all, int E,
                  int n_pred, int k, int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
                  int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts, float* __restrict__ partial,
-                 const __grid_constant__ CountsMirror mirror) {
+                 const __grid_constant__ CountsMirror mirror, const __grid_constant__ PredictorMlp mlp) {
   constexpr int kCols = 8 * NT;
   constexpr int kLd = kCols + 4;  // padded row of the reduction buffer
   __shared__ float red[kBlockTokens * kLd];
@@ -242,8 +285,8 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_b
       for (int e = threadIdx.x; e < E; e += blockDim.x) block_counts[(size_t)blk * E + e] = 0;
     return;
   }
-  select_and_count<kLd, false>(red, hist, blk, 0, kBlockTokens, T, E, n_pred, k, ids, wts, counts, block_counts,
-                               pred_counts);
+  select_and_count<kLd, false, MLP>(red, hist, blk, 0, kBlockTokens, T, E, n_pred, k, ids, wts, counts, block_counts,
+                               pred_counts, mlp);
   publish_counts(counts, mirror);
 }
 
@@ -254,12 +297,12 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_b
 constexpr int kFinishTokens = kWarps;
 constexpr int kMaxSplits = 16;
 
-template <int NT>
+template <int NT, bool MLP>
 __global__ void __launch_bounds__(kWarps * 32)
 gate_finish_kernel(const float* __restrict__ partial, int splits, int T, int E, int n_pred, int k,
                    int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
                    int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts,
-                   const __grid_constant__ CountsMirror mirror) {
+                   const __grid_constant__ CountsMirror mirror, const __grid_constant__ PredictorMlp mlp) {
   constexpr int kCols = 8 * NT;
   constexpr int kLd = kCols + 4;
   __shared__ float red[kFinishTokens * kLd];
@@ -280,8 +323,8 @@ gate_finish_kernel(const float* __restrict__ partial, int splits, int T, int E, 
     red[(i / kCols) * kLd + i % kCols] = acc;
   }
   __syncthreads();
-  select_and_count<kLd, true>(red, hist, blk, tok0, kFinishTokens, T, E, n_pred, k, ids, wts, counts, block_counts,
-                              pred_counts);
+  select_and_count<kLd, true, MLP>(red, hist, blk, tok0, kFinishTokens, T, E, n_pred, k, ids, wts, counts, block_counts,
+                              pred_counts, mlp);
   publish_counts(counts, mirror);
 }
 
@@ -307,23 +350,31 @@ size_t gate_partial_floats(int T, int d, int Etot) {
 cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bfloat16* w_all, int E,
                              int n_pred, int k, int32_t* ids, float* wts, int32_t* counts,
                              int32_t* block_counts, int32_t* pred_counts, float* partial, cudaStream_t stream,
-                             int32_t* host_counts, int host_n, unsigned* ticket) {
+                             int32_t* host_counts, int host_n, unsigned* ticket, const float* pred_w2,
+                             unsigned mlp_mask) {
   if (T <= 0) return cudaSuccess;
   const CountsMirror mirror{host_counts, ticket, host_n};
+  const PredictorMlp mlp{pred_w2, mlp_mask};
   const int Etot = E * (1 + n_pred);
   if (Etot > 32 * kPerLane || k > 8 || (d % 256) != 0) return cudaErrorInvalidValue;
   const int nblk = gate_num_blocks(T);
   const int splits = partial ? gate_splits(T, d) : 1;
   const dim3 grid(nblk, splits), block(kWarps * 32);
+  const bool with_mlp = pred_w2 != nullptr && (mlp_mask & ((n_pred >= 32 ? 0u : (1u << n_pred)) - 1u)) != 0;
+#define MOE_GATE_LAUNCH(NT_, MLP_)                                                                          \
+  {                                                                                                         \
+    gate_topk_kernel<NT_, MLP_><<<grid, block, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts, \
+                                                            block_counts, pred_counts, partial,            \
+                                                            splits > 1 ? CountsMirror{} : mirror, mlp);    \
+    if (splits > 1)                                                                                         \
+      gate_finish_kernel<NT_, MLP_><<<dim3(nblk, kBlockTokens / kFinishTokens), block, 0, stream>>>(        \
+          partial, splits, T, E, n_pred, k, ids, wts, counts, block_counts, pred_counts, mirror, mlp);      \
+    return cudaGetLastError();                                                                              \
+  }
 #define MOE_GATE_CASE(NT_)                                                                                  \
   if (Etot <= 8 * NT_) {                                                                                    \
-    gate_topk_kernel<NT_><<<grid, block, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,       \
-                                                      block_counts, pred_counts, partial,                  \
-                                                      splits > 1 ? CountsMirror{} : mirror);               \
-    if (splits > 1)                                                                                         \
-      gate_finish_kernel<NT_><<<dim3(nblk, kBlockTokens / kFinishTokens), block, 0, stream>>>(              \
-          partial, splits, T, E, n_pred, k, ids, wts, counts, block_counts, pred_counts, mirror);           \
-    return cudaGetLastError();                                                                              \
+    if (with_mlp) MOE_GATE_LAUNCH(NT_, true)                                                                \
+    MOE_GATE_LAUNCH(NT_, false)                                                                             \
   }
   MOE_GATE_CASE(1)
   MOE_GATE_CASE(2)
@@ -331,6 +382,7 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
   MOE_GATE_CASE(8)
   MOE_GATE_CASE(16)
   MOE_GATE_CASE(32)
+#undef MOE_GATE_LAUNCH
 #undef MOE_GATE_CASE
   return cudaErrorInvalidValue;
 }
@@ -341,12 +393,13 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
 cudaError_t preload_gate_kernels() {
   cudaFuncAttributes a;
   const void* fns[] = {
-      reinterpret_cast<const void*>(gate_topk_kernel<1>),    reinterpret_cast<const void*>(gate_topk_kernel<2>),
-      reinterpret_cast<const void*>(gate_topk_kernel<4>),    reinterpret_cast<const void*>(gate_topk_kernel<8>),
-      reinterpret_cast<const void*>(gate_topk_kernel<16>),   reinterpret_cast<const void*>(gate_topk_kernel<32>),
-      reinterpret_cast<const void*>(gate_finish_kernel<1>),  reinterpret_cast<const void*>(gate_finish_kernel<2>),
-      reinterpret_cast<const void*>(gate_finish_kernel<4>),  reinterpret_cast<const void*>(gate_finish_kernel<8>),
-      reinterpret_cast<const void*>(gate_finish_kernel<16>), reinterpret_cast<const void*>(gate_finish_kernel<32>)};
+#define MOE_GATE_FNS(NT_)                                                                               \
+  reinterpret_cast<const void*>(gate_topk_kernel<NT_, false>),                                          \
+      reinterpret_cast<const void*>(gate_topk_kernel<NT_, true>),                                       \
+      reinterpret_cast<const void*>(gate_finish_kernel<NT_, false>),                                    \
+      reinterpret_cast<const void*>(gate_finish_kernel<NT_, true>)
+      MOE_GATE_FNS(1), MOE_GATE_FNS(2), MOE_GATE_FNS(4), MOE_GATE_FNS(8), MOE_GATE_FNS(16), MOE_GATE_FNS(32)};
+#undef MOE_GATE_FNS
   for (const void* f : fns) {
     const cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;

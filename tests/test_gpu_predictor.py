@@ -108,3 +108,82 @@ def test_predicted_planning_distance_two(cuda):
             assert 0.9 <= st.predictor_accuracy <= 1.0  # the predictor is layer l+2's own gate
     m.close()
     ref.close()
+
+
+@pytest.mark.parametrize("E,k,d,T,npred,mlp_slots", [(8, 2, 4096, 2048, 1, (0,)), (16, 2, 1024, 777, 3, (0, 2)),
+                                                     (64, 8, 2048, 300, 2, (1,)), (8, 2, 1024, 5000, 2, (0, 1))])
+def test_predictor_mlp_counts_bitexact(cuda, E, k, d, T, npred, mlp_slots):
+    """The batched predictor MLP (moe_set_predictor_mlp): hidden = relu of the
+    slot's stacked rows, W2 (arbitrary fp32) applied per token in the gate
+    kernel; histograms bit-identical to the oracle's fmaf chain, linear slots
+    unchanged beside MLP slots, w2=None returns a slot to linear."""
+    import torch
+    rng = np.random.default_rng(E * 1000 + T)
+    m = MoELayer(1, E, k, d, 128, max_tokens=T, num_predictor_targets=npred)
+    wg = wl.gate_weights(E, d, 1.2, 1, 0, 0)
+    wps = [wl.gate_weights(E, d, 1.2, 1, 1 + p, 0) for p in range(npred)]
+    w2s = {p: rng.standard_normal((E, E)).astype(np.float32) for p in mlp_slots}
+    m.set_gate(0, wg)
+    for p, wp in enumerate(wps):
+        if p in w2s:
+            m.set_predictor_mlp(0, p, wp, w2s[p])
+        else:
+            m.set_predictor(0, p, wp)
+    x = wl.tokens(T, d, E, 1, 9)
+    xd = torch.from_numpy(x.view(np.int16)).to(cuda)
+    ids = torch.zeros((T, k), dtype=torch.int32, device=cuda)
+    w = torch.zeros((T, k), dtype=torch.float32, device=cuda)
+    counts = torch.zeros(E, dtype=torch.int32, device=cuda)
+    pred = torch.zeros((npred, E), dtype=torch.int32, device=cuda)
+    m.gate(0, xd, ids, w, counts, pred)
+    torch.cuda.synchronize()
+    assert np.array_equal(ids.cpu().numpy(), oracle.gate(x, wg, k)[0])
+    for p, wp in enumerate(wps):
+        want = oracle.predict_mlp(x, wp, w2s[p], k) if p in w2s else oracle.gate(x, wp, k)[2]
+        assert np.array_equal(pred[p].cpu().numpy(), want), p
+    pred2 = torch.zeros_like(pred)
+    m.predict_loads(0, xd, pred2)
+    torch.cuda.synchronize()
+    assert torch.equal(pred, pred2)
+    p0 = mlp_slots[0]
+    m.set_predictor_mlp(0, p0, None, None)  # back to linear, rows kept
+    m.predict_loads(0, xd, pred2)
+    torch.cuda.synchronize()
+    assert np.array_equal(pred2[p0].cpu().numpy(), oracle.gate(x, wps[p0], k)[2])
+    m.close()
+
+
+def test_predictor_mlp_predicted_planning(cuda):
+    """MOE_PLAN_PREDICTED driven by an MLP predictor (W2 = identity, so the
+    scores are relu of layer l+1's gate logits): every layer after the first
+    runs on the predicted placement and its output equals the fixed-placement
+    layer's.  (The synthetic gate logits are mostly negative, so relu ties
+    many scores at 0 and the accuracy is well below the linear predictor's.)"""
+    import torch
+    from paper_2603_06350_b200 import MOE_PLAN_FIXED, MOE_PLAN_PREDICTED
+    L, E, k, d, ff, T = 3, 8, 2, 1024, 1408, 256
+    mem = 3.0 * d * ff * 2 / 1e6
+    m = MoELayer(L, E, k, d, ff, max_tokens=T, num_predictor_targets=1, predictor_distance=1,
+                 expert_mem_mb=mem, layer_mem_cap_mb=(E + 3) * mem)
+    ref = MoELayer(L, E, k, d, ff, max_tokens=T, expert_mem_mb=mem, layer_mem_cap_mb=E * mem)
+    gates = [wl.gate_weights(E, d, 1.5, 1, l, 0) for l in range(L)]
+    for mm in (m, ref):
+        for l in range(L):
+            mm.set_gate(l, gates[l])
+            for e in range(E):
+                mm.load_expert(l, e, *wl.expert_weights(d, ff, 1, l, e))
+    for l in range(L - 1):
+        m.set_predictor_mlp(l, 0, gates[l + 1], np.eye(E, dtype=np.float32))
+    xs = [torch.from_numpy(wl.tokens(T, d, E, 1, 60 + l).view(np.int16)).to(cuda) for l in range(L)]
+    for it in range(2):
+        for l in range(L):
+            y = torch.zeros((T, d), dtype=torch.int16, device=cuda)
+            st = m.forward(l, xs[l], y, MOE_PLAN_PREDICTED, it, stats=True)
+            y1 = torch.zeros_like(y)
+            ref.forward(l, xs[l], y1, MOE_PLAN_FIXED, it)
+            ref.sync()
+            assert torch.equal(y, y1), (it, l)
+            if l >= 1:
+                assert st.plan_source == 2 and 0.0 <= st.predictor_accuracy <= 1.0
+    m.close()
+    ref.close()

@@ -174,3 +174,24 @@ def test_layer_golden():
             e = ids[t, j]
             ref[t] += w[t, j] * oracle.expert_ffn(g["x"][t:t + 1], *experts[e])[0]
     np.testing.assert_allclose(y, ref, rtol=1e-5, atol=1e-6)
+def test_predict_mlp_oracle_against_numpy():
+    """orc_predict_mlp vs numpy on grid weights (every product and partial sum
+    exact in fp32, so summation order cannot matter)."""
+    from paper_2603_06350_b200 import workload as wl
+    E, k, d, T = 16, 2, 256, 200
+    rng = np.random.default_rng(3)
+    x = wl.tokens(T, d, E, 1, 2)
+    w1 = wl.gate_weights(E, d, 1.2, 1, 1, 0)
+    w2 = (rng.integers(-8, 9, (E, E)) / 8.0).astype(np.float32)
+    h = np.maximum(oracle.bf16_to_f32(x).astype(np.float64) @ oracle.bf16_to_f32(w1).T.astype(np.float64), 0.0)
+    out = h @ w2.T.astype(np.float64)
+    want = np.zeros(E, np.int32)
+    for t in range(T):
+        o = out[t].copy()
+        for _ in range(k):
+            b = int(np.argmax(o))  # first maximum = lowest index on ties
+            want[b] += 1
+            o[b] = -np.inf
+    assert np.array_equal(oracle.predict_mlp(x, w1, w2, k), want)
+    # W2 = identity with all-positive hidden units reduces to the linear predictor
+    assert oracle.predict_mlp(x, w1, np.eye(E, dtype=np.float32), k).sum() == T * k
