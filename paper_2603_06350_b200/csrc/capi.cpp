@@ -185,9 +185,29 @@ void stage_exchange(moe_ctx* c, bool forward, cudaStream_t s) {
 // B200's 1 kW cap it settles ~190 MHz lower and nets ~4% less throughput on
 // the Mixtral layer (profiles/ab_gemm_variants_r01.md), so it is opt-in
 // (MOE_GEMM_VARIANT=2sm) until it is made more energy-efficient.
+// Swap-AB decode tiles (weights as the M operand, up to 64 tokens as N) when
+// the batch leaves a few dozen rows per expert: the 128-row tiles would be
+// mostly padding (profiles/ab_swap_r01.md).
+bool use_swap(const moe_ctx* c, int T) {
+  if (c->fp32 || c->gemm_variant == 1 || c->gemm_variant == 2 || c->gemm_variant == 3) return false;
+  if (c->gemm_variant == 4) return true;
+  const int64_t mean_rows = static_cast<int64_t>(T) * c->k * c->G / std::max(1, c->E);  // balanced EP
+  return T > 0 && mean_rows <= c->swap_rows;
+}
+
 void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t rows = 0, bool gather = false,
                      uint16_t* fused_y = nullptr) {
   Layer& L = c->layers[layer];
+  if (!gather && !fused_y && use_swap(c, c->gemm_T)) {
+    if (which == 0)
+      CU_CHECK(launch_grouped_gemm_swap(0, &c->tmA1s, &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d,
+                                        2 * c->ff, reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, c->num_sms, s,
+                                        c->use_pdl));
+    else
+      CU_CHECK(launch_grouped_gemm_swap(1, &c->tmA2s, &L.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
+                                        reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s, c->use_pdl));
+    return;
+  }
   if (c->fp32) {  // K7: SIMT fp32 grouped GEMMs (+ SwiGLU pass between them)
     const GemmSeg* segs = c->dplan.p->segs;
     const int* nseg = &c->dplan.p->nseg;
@@ -304,9 +324,13 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   const bool deferred = c->G == 1 || ahead;
   // single GPU, bf16, 1-SM K4: GEMM1 gathers its A rows from x (TMA gather4)
   // and the dispatch kernel only ranks — no permuted copy of the tokens
-  const bool gather = c->gather && c->G == 1 && !c->fp32 && (c->gemm_variant == 0 || c->gemm_variant == 1) && T > 0;
+  c->gemm_T = T;
+  const bool swap = use_swap(c, T);
+  const bool gather = c->gather && c->G == 1 && !c->fp32 && (c->gemm_variant == 0 || c->gemm_variant == 1) && T > 0 &&
+                      !swap;
   // single GPU, bf16, 1-SM K4: the combine runs inside GEMM2's epilogue
-  const bool fused = c->fuse_combine && c->G == 1 && !c->fp32 && (c->gemm_variant == 0 || c->gemm_variant == 1);
+  const bool fused =
+      c->fuse_combine && c->G == 1 && !c->fp32 && (c->gemm_variant == 0 || c->gemm_variant == 1) && !swap;
   if (gather && (c->tmX_ptr != x || c->tmX_T != T)) {
     c->tmX = make_kmajor_map(x, T, c->d, 1);
     c->tmX_ptr = x;
@@ -634,6 +658,7 @@ int moe_forward_begin(moe_ctx* c, int layer, const uint16_t* x, int T, const int
     require(c->cur_layer == layer && c->cur_x == x && c->cur_T == T, "forward_begin stage 2 without stage 1");
     stage_plan(c, layer, MOE_PLAN_FIXED, 0, counts_all, c->E);
     stage_dispatch(c, x, T, s);
+    c->gemm_T = T;
     CU_CHECK(cudaStreamSynchronize(s));
   });
 }

@@ -266,8 +266,9 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_GEMM_GROUP_M")) std::sscanf(v, "%d,%d", &c->group_m[0], &c->group_m[1]);
     if (const char* v = std::getenv("MOE_GEMM_VARIANT")) {
       const std::string s(v);
-      c->gemm_variant = s == "1sm" ? 1 : (s == "2sm" ? 2 : (s == "m256" ? 3 : 0));
+      c->gemm_variant = s == "1sm" ? 1 : (s == "2sm" ? 2 : (s == "m256" ? 3 : (s == "swap" ? 4 : 0)));
     }
+    if (const char* v = std::getenv("MOE_GEMM_SWAP_ROWS")) c->swap_rows = std::atoi(v);
     c->registry = moeless::ReplicaRegistry(std::max(0, D.keep_alive_iters));
     c->layers.resize(D.num_layers);
     require(D.precision == MOE_PRECISION_BF16 || D.precision == MOE_PRECISION_FP32, "unknown precision");
@@ -371,6 +372,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
       c->tmA2 = make_kmajor_map(c->h.p, c->rows_cap, c->ff, 128);
       c->tmA1w = make_kmajor_map(c->xp.p, c->rows_cap, c->d, 256);
       c->tmA2w = make_kmajor_map(c->h.p, c->rows_cap, c->ff, 256);
+      c->tmA1s = make_kmajor_map(c->xp.p, c->rows_cap, c->d, 32);
+      c->tmA2s = make_kmajor_map(c->h.p, c->rows_cap, c->ff, 32);
     }
     // mapped pinned control buffers, read/written by small SM copies (UVA pointers)
     CU_CHECK(cudaHostAlloc(&c->hplan, sizeof(DevPlan), cudaHostAllocMapped));

@@ -78,6 +78,9 @@ cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorM
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                 __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, int* sched,
                                 bool pdl, const int32_t* a_gather, int group_m, const FusedCombine& fc);
+cudaError_t launch_grouped_gemm_swap(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
+                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
+                                     __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl);
 cudaError_t preload_gate_kernels();
 cudaError_t preload_dispatch_kernels();
 cudaError_t preload_gemm_kernels();
@@ -283,7 +286,9 @@ struct EventSet {
 struct moe_ctx {
   moe_ctx_desc desc{};
   int E = 0, k = 0, d = 0, ff = 0, G = 1, rank = 0, Tmax = 0, n_pred = 0, num_sms = 148;
-  int gemm_variant = 0;  // 0 auto, 1 force 1-SM, 2 force 2-SM (env MOE_GEMM_VARIANT=1sm|2sm)
+  int gemm_variant = 0;  // 0 auto, 1 force 1-SM, 2 force 2-SM, 3 m256, 4 force swap-AB (env MOE_GEMM_VARIANT)
+  int swap_rows = 64;    // auto: swap-AB decode tiles when the mean rows per expert <= this (MOE_GEMM_SWAP_ROWS)
+  int gemm_T = 0;        // tokens of the forward whose GEMMs are being enqueued
   int pred_distance = 1;  // predictor slot 0 scores layer + pred_distance
   int count_stride = 0;   // ints per rank in the counts buffer: E * (1 + n_pred)
   bool fp32 = false;      // MOE_PRECISION_FP32: SIMT fp32 path (K7)
@@ -338,6 +343,7 @@ struct moe_ctx {
   int64_t rows_cap = 0, send_cap = 0;
   CUtensorMap tmA1, tmA2;    // 128-row boxes
   CUtensorMap tmA1w, tmA2w;  // 256-row boxes (256-row single-CTA K4 variant)
+  CUtensorMap tmA1s, tmA2s;  // 32-row boxes (swap-AB decode variant: tokens are the N operand)
   // host staging (pinned)
   DevPlan* hplan = nullptr;
   int32_t* h_counts = nullptr;  // [G][E]

@@ -814,6 +814,257 @@ cudaError_t launch_grouped_gemm_m256(int epi, const CUtensorMap* tmA, const CUte
   return cudaGetLastError();
 }
 
+// ===================================================================
+// Swap-AB decode variant: in the decode regime (a few to a few dozen rows per
+// replica) the 128-row token tile of the kernels above is mostly padding, so
+// the tensor pipe multiplies every weight byte by 128 rows while the kernel is
+// bound by the weight stream.  Here the WEIGHTS are the M operand (two M=128
+// halves of the 256-row weight tile, K-major, the same TMA boxes) and the
+// tokens are N: one tile = up to SN = 64 rows of one segment, the MMA's N set
+// per tile to the rows rounded up to 16 (runtime instruction descriptor).
+// D[feature][token] lands in TMEM with features on the lanes; the epilogue
+// pairs neighbouring lanes (shfl) so each thread stores two adjacent bf16
+// features of one token.  Per weight byte the tensor work drops from 128 rows
+// to the rows actually present, and the smem stage is 32 KB of weights + 4-8
+// KB of tokens (5 stages).
+constexpr int SN = 64, SBOX = 32, STAGES_S = 5;
+constexpr uint32_t kStageTokS = SN * BK * 2, kStageWS = BN * BK * 2, kBoxBytesS = SBOX * BK * 2;
+constexpr uint32_t kTmemColsS = 256;  // 2 accumulators x 2 weight halves x SN token columns
+template <int EPI> constexpr int kGroupMS = EPI == 0 ? 64 : 32;  // 64-row tiles per n sweep
+
+struct SmemLayoutS {
+  static constexpr uint32_t a = 0;  // token tiles
+  static constexpr uint32_t b = a + STAGES_S * kStageTokS;
+  static constexpr uint32_t bars = b + STAGES_S * kStageWS;
+  static constexpr uint32_t n_bars = 2 * STAGES_S + 4;
+  static constexpr uint32_t tmem_slot = bars + n_bars * 8;
+  static constexpr uint32_t seg_tiles = tmem_slot + 16;
+  static constexpr uint32_t segs = seg_tiles + (kMaxSegs + 1) * 4 + 12;
+  static constexpr uint32_t end = ((segs + 15) / 16) * 16 + kMaxSegs * 16;
+};
+constexpr uint32_t kSmemBytesS = SmemLayoutS::end + 1024;
+static_assert(kSmemBytesS <= 232448, "smem budget (swap-AB variant)");
+
+// 32 token columns of one accumulator half -> bf16 pairs of features:
+// lane pairs (2i, 2i+1) swap one value so the even lane stores token j's
+// features (f, f+1) and the odd lane token j+1's.
+__device__ __forceinline__ void store_token_pairs(const float (&v)[32], int lane, int j0, int rows,
+                                                  __nv_bfloat16* __restrict__ base, size_t row0, int out_ld,
+                                                  int col_even) {
+  const bool odd = lane & 1;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float a = v[2 * i], b = v[2 * i + 1];  // tokens j0+2i, j0+2i+1 of this lane's feature
+    const float other = __shfl_xor_sync(0xffffffffu, odd ? a : b, 1);
+    const int row = j0 + 2 * i + (odd ? 1 : 0);
+    const uint32_t packed = odd ? pack_bf16(other, b) : pack_bf16(a, other);
+    if (row < rows) *reinterpret_cast<uint32_t*>(base + (row0 + row) * out_ld + col_even) = packed;
+  }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total, int k_total,
+                         int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayoutS::bars);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES_S;
+  uint64_t* tfull = bars + 2 * STAGES_S;
+  uint64_t* tempty = bars + 2 * STAGES_S + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SmemLayoutS::tmem_slot);
+  int* seg_tiles = reinterpret_cast<int*>(smem + SmemLayoutS::seg_tiles);
+  int4* segs = reinterpret_cast<int4*>(smem + SmemLayoutS::segs);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  const int nseg = min(*nseg_g, kMaxSegs);
+  const int n_tiles = n_total / BN;
+
+  for (int i = threadIdx.x; i < nseg; i += kThreads) segs[i] = reinterpret_cast<const int4*>(segs_g)[i];
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES_S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemColsS>(tmem_slot);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int s = 0; s < nseg; ++s) {
+      seg_tiles[s] = acc;
+      acc += ((segs[s].y + SN - 1) / SN) * n_tiles;
+    }
+    seg_tiles[nseg] = acc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_tiles = nseg > 0 ? seg_tiles[nseg] : 0;
+  const int num_kb = k_total / BK;
+  griddep_launch_dependents();
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint64_t pol_b = policy_evict_last();
+      bool first = true;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const TileCoord c = decode_tile<kGroupMS<EPI>, SN>(t, seg_tiles, segs, nseg, n_tiles);
+        const int a_row = segs[c.seg].x + c.m * SN;
+        const int rows = min(SN, segs[c.seg].y - c.m * SN);
+        const int nbox = rows > SBOX ? 2 : 1;
+        const uint32_t bytes = kStageWS + nbox * kBoxBytesS;
+        const int b_row = segs[c.seg].z * b_rows_per_slot + c.n * BN;
+        int kb0 = 0;
+        if (first) {  // weights of the first stages stream while the producer kernel drains (PDL)
+          first = false;
+          kb0 = num_kb < STAGES_S ? num_kb : STAGES_S;
+          for (int kb = 0; kb < kb0; ++kb) {
+            mbar_arrive_expect_tx(&full[kb], bytes);
+            tma_load_2d_hint(smem + SmemLayoutS::b + kb * kStageWS, &tmB, &full[kb], kb * BK, b_row, pol_b);
+          }
+          griddep_wait();
+          for (int kb = 0; kb < kb0; ++kb)
+            for (int bx = 0; bx < nbox; ++bx)
+              tma_load_2d(smem + SmemLayoutS::a + kb * kStageTokS + bx * kBoxBytesS, &tmA, &full[kb], kb * BK,
+                          a_row + bx * SBOX);
+          stage = kb0 == STAGES_S ? 0 : kb0;
+          phase = kb0 == STAGES_S ? 1u : 0u;
+        }
+        for (int kb = kb0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          tma_load_2d_hint(smem + SmemLayoutS::b + stage * kStageWS, &tmB, &full[stage], kb * BK, b_row, pol_b);
+          for (int bx = 0; bx < nbox; ++bx)
+            tma_load_2d(smem + SmemLayoutS::a + stage * kStageTokS + bx * kBoxBytesS, &tmA, &full[stage], kb * BK,
+                        a_row + bx * SBOX);
+          if (++stage == STAGES_S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      const uint32_t a_base = smem_u32(smem + SmemLayoutS::a);
+      const uint32_t b_base = smem_u32(smem + SmemLayoutS::b);
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const TileCoord c = decode_tile<kGroupMS<EPI>, SN>(t, seg_tiles, segs, nseg, n_tiles);
+        const int rows = min(SN, segs[c.seg].y - c.m * SN);
+        const uint32_t idesc = umma_idesc_bf16(128, static_cast<uint32_t>((rows + 15) & ~15));
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + acc * 2 * SN, d1 = d0 + SN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t w_st = b_base + stage * kStageWS;
+          const uint64_t w_top = umma_desc_sw128(w_st);
+          const uint64_t w_bot = umma_desc_sw128(w_st + 128 * 128);  // weight rows 128..255: +16 KB
+          const uint64_t tdesc = umma_desc_sw128(a_base + stage * kStageTokS);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint32_t accf = (kb | k) != 0 ? 1u : 0u;
+            tc_mma_bf16(d0, w_top + 2 * k, tdesc + 2 * k, idesc, accf);
+            tc_mma_bf16(d1, w_bot + 2 * k, tdesc + 2 * k, idesc, accf);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES_S) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // --------------------------------------------------------- epilogue
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const TileCoord c = decode_tile<kGroupMS<EPI>, SN>(t, seg_tiles, segs, nseg, n_tiles);
+      const int4 sg = segs[c.seg];
+      const int rows = min(SN, sg.y - c.m * SN);
+      const size_t row0 = static_cast<size_t>(sg.x) + c.m * SN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * 2 * SN;
+      const int f = quarter * 32 + lane;  // this thread's feature within a 128-row weight half
+#pragma unroll 1
+      for (int j0 = 0; j0 < rows; j0 += 32) {
+        float v[32];
+        if constexpr (EPI == EPI_SWIGLU) {
+          uint32_t g[32], u[32];
+          tmem_ld_32x32b_x32(taddr + j0, g);       // W1 half: gate projections
+          tmem_ld_32x32b_x32(taddr + SN + j0, u);  // W3 half: up projections
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = silu(__uint_as_float(g[i])) * __uint_as_float(u[i]);
+          store_token_pairs(v, lane, j0, rows, out, row0, out_ld, c.n * (BN / 2) + (f & ~1));
+        } else {
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(taddr + h * SN + j0, r);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+            store_token_pairs(v, lane, j0, rows, out, row0, out_ld, c.n * BN + h * 128 + (f & ~1));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  griddep_wait();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemColsS>(tmem_base);
+  }
+}
+
+cudaError_t launch_grouped_gemm_swap(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
+                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
+                                     __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl) {
+  if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(grouped_gemm_swap_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesS);
+    cudaFuncSetAttribute(grouped_gemm_swap_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesS);
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_ctas);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytesS;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (epi == EPI_SWIGLU)
+    return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<EPI_SWIGLU>, *tmA, *tmB, segs, nseg, n_total, k_total,
+                              b_rows_per_slot, out, out_ld);
+  return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<EPI_STORE>, *tmA, *tmB, segs, nseg, n_total, k_total,
+                            b_rows_per_slot, out, out_ld);
+}
+
 // --------------------------------------------------------------- host side
 static_assert(kSmemBytes <= 232448, "smem budget");
 
@@ -879,7 +1130,9 @@ cudaError_t preload_gemm_kernels() {
                        reinterpret_cast<const void*>(grouped_gemm_2sm_kernel<0>),
                        reinterpret_cast<const void*>(grouped_gemm_2sm_kernel<1>),
                        reinterpret_cast<const void*>(grouped_gemm_m256_kernel<0>),
-                       reinterpret_cast<const void*>(grouped_gemm_m256_kernel<1>)};
+                       reinterpret_cast<const void*>(grouped_gemm_m256_kernel<1>),
+                       reinterpret_cast<const void*>(grouped_gemm_swap_kernel<0>),
+                       reinterpret_cast<const void*>(grouped_gemm_swap_kernel<1>)};
   for (const void* f : fns) {
     const cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;

@@ -1,5 +1,6 @@
 """The K4 kernels — 1-SM (M=128 tiles), 2-SM cta_group::2 (M=256 tiles across
-an SM pair) and single-CTA M=256 (two MMAs sharing B) — against the oracle and against each other, on ragged
+an SM pair), single-CTA M=256 (two MMAs sharing B) and swap-AB decode tiles
+(weights as M, up to 64 tokens as N) — against the oracle and against each other, on ragged
 segments (partial tiles, single-row segments, replicas co-located)."""
 import os
 
@@ -40,14 +41,19 @@ def _run(cuda, variant, E, k, d, ff, T, rc, seed=21):
     (8, 2, 2048, 3584, 700, [1] * 8),
     (16, 2, 1024, 1408, 1500, [2] * 16),
     (4, 1, 256, 128, 5, [1] * 4),
+    (64, 8, 2048, 1408, 256, [2] + [1] * 62 + [3]),   # cfg5 decode shape
+    (8, 2, 1024, 1408, 200, [1, 1, 2, 1, 1, 1, 1, 1]),  # 33-64-row and >64-row segments
 ])
 def test_variants_agree_and_match_oracle(cuda, E, k, d, ff, T, rc):
     x, wg, experts, y1 = _run(cuda, "1sm", E, k, d, ff, T, rc)
     _, _, _, y2 = _run(cuda, "2sm", E, k, d, ff, T, rc)
     _, _, _, y3 = _run(cuda, "m256", E, k, d, ff, T, rc)
+    _, _, _, y4 = _run(cuda, "swap", E, k, d, ff, T, rc)
     y_ref = oracle.layer_forward(x, wg, experts, rc, k)[0]
-    for y in (y1, y2, y3):
+    for y in (y1, y2, y3, y4):
         err = float(np.max(np.abs(y - y_ref)) / np.max(np.abs(y_ref)))
         assert err <= 2e-2, err
     # same K order per output element, same fp32 accumulation: bit-identical outputs
     assert np.array_equal(y1, y2) and np.array_equal(y1, y3)
+    # swap-AB (weights as M, tokens as N): the same products in the same K order
+    assert np.array_equal(y1, y4), float(np.max(np.abs(y1 - y4)))
