@@ -199,13 +199,13 @@ void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t r
                      uint16_t* fused_y = nullptr) {
   Layer& L = c->layers[layer];
   if (!gather && !fused_y && use_swap(c, c->gemm_T)) {
-    if (which == 0)
-      CU_CHECK(launch_grouped_gemm_swap(0, &c->tmA1s, &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d,
-                                        2 * c->ff, reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, c->num_sms, s,
-                                        c->use_pdl));
-    else
-      CU_CHECK(launch_grouped_gemm_swap(1, &c->tmA2s, &L.tmB2, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
-                                        reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s, c->use_pdl));
+    // fused: the GEMM1 call launches both GEMMs, the GEMM2 call adds nothing
+    if (c->swap_fuse && which == 1) return;
+    CU_CHECK(launch_grouped_gemm_swap(c->swap_fuse ? 2 : which, &c->tmA1s, &L.tmB1, &c->tmA2s, &L.tmB2,
+                                      c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, 2 * c->ff, c->d,
+                                      reinterpret_cast<__nv_bfloat16*>(c->h.p),
+                                      reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->swap_ready.p,
+                                      static_cast<int>(c->swap_ready.n), c->num_sms, s, c->use_pdl));
     return;
   }
   if (c->fp32) {  // K7: SIMT fp32 grouped GEMMs (+ SwiGLU pass between them)

@@ -269,6 +269,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
       c->gemm_variant = s == "1sm" ? 1 : (s == "2sm" ? 2 : (s == "m256" ? 3 : (s == "swap" ? 4 : 0)));
     }
     if (const char* v = std::getenv("MOE_GEMM_SWAP_ROWS")) c->swap_rows = std::atoi(v);
+    if (const char* v = std::getenv("MOE_SWAP_FUSE")) c->swap_fuse = std::string(v) != "0";
     c->registry = moeless::ReplicaRegistry(std::max(0, D.keep_alive_iters));
     c->layers.resize(D.num_layers);
     require(D.precision == MOE_PRECISION_BF16 || D.precision == MOE_PRECISION_FP32, "unknown precision");
@@ -374,6 +375,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
       c->tmA2w = make_kmajor_map(c->h.p, c->rows_cap, c->ff, 256);
       c->tmA1s = make_kmajor_map(c->xp.p, c->rows_cap, c->d, 32);
       c->tmA2s = make_kmajor_map(c->h.p, c->rows_cap, c->ff, 32);
+      c->swap_ready.alloc(static_cast<size_t>(c->rows_cap) / 64 + kMaxReplicas + 2);
+      CU_CHECK(cudaMemset(c->swap_ready.p, 0, c->swap_ready.n * sizeof(int)));
     }
     // mapped pinned control buffers, read/written by small SM copies (UVA pointers)
     CU_CHECK(cudaHostAlloc(&c->hplan, sizeof(DevPlan), cudaHostAllocMapped));

@@ -78,9 +78,11 @@ cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorM
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                 __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, int* sched,
                                 bool pdl, const int32_t* a_gather, int group_m, const FusedCombine& fc);
-cudaError_t launch_grouped_gemm_swap(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
-                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
-                                     __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl);
+cudaError_t launch_grouped_gemm_swap(int which, const CUtensorMap* tmA1, const CUtensorMap* tmB1,
+                                     const CUtensorMap* tmA2, const CUtensorMap* tmB2, const GemmSeg* segs,
+                                     const int* nseg, int d, int ff, int b_rows1, int b_rows2, __nv_bfloat16* h,
+                                     __nv_bfloat16* yp, int* ready, int ready_n, int num_ctas, cudaStream_t stream,
+                                     bool pdl);
 cudaError_t preload_gate_kernels();
 cudaError_t preload_dispatch_kernels();
 cudaError_t preload_gemm_kernels();
@@ -289,6 +291,8 @@ struct moe_ctx {
   int gemm_variant = 0;  // 0 auto, 1 force 1-SM, 2 force 2-SM, 3 m256, 4 force swap-AB (env MOE_GEMM_VARIANT)
   int swap_rows = 64;    // auto: swap-AB decode tiles when the mean rows per expert <= this (MOE_GEMM_SWAP_ROWS)
   int gemm_T = 0;        // tokens of the forward whose GEMMs are being enqueued
+  bool swap_fuse = true;  // swap-AB: GEMM1 and GEMM2 in one launch (MOE_SWAP_FUSE=0: two)
+  DevBuf<int> swap_ready; // its per-(segment, m-tile) GEMM1-done counters (+ CTA counter)
   int pred_distance = 1;  // predictor slot 0 scores layer + pred_distance
   int count_stride = 0;   // ints per rank in the counts buffer: E * (1 + n_pred)
   bool fp32 = false;      // MOE_PRECISION_FP32: SIMT fp32 path (K7)

@@ -830,7 +830,7 @@ cudaError_t launch_grouped_gemm_m256(int epi, const CUtensorMap* tmA, const CUte
 constexpr int SN = 64, SBOX = 32, STAGES_S = 5;
 constexpr uint32_t kStageTokS = SN * BK * 2, kStageWS = BN * BK * 2, kBoxBytesS = SBOX * BK * 2;
 constexpr uint32_t kTmemColsS = 256;  // 2 accumulators x 2 weight halves x SN token columns
-template <int EPI> constexpr int kGroupMS = EPI == 0 ? 64 : 32;  // 64-row tiles per n sweep
+__host__ __device__ constexpr int group_ms(int epi) { return epi == 0 ? 64 : 32; }  // 64-row tiles per n sweep
 
 struct SmemLayoutS {
   static constexpr uint32_t a = 0;  // token tiles
@@ -838,8 +838,8 @@ struct SmemLayoutS {
   static constexpr uint32_t bars = b + STAGES_S * kStageWS;
   static constexpr uint32_t n_bars = 2 * STAGES_S + 4;
   static constexpr uint32_t tmem_slot = bars + n_bars * 8;
-  static constexpr uint32_t seg_tiles = tmem_slot + 16;
-  static constexpr uint32_t segs = seg_tiles + (kMaxSegs + 1) * 4 + 12;
+  static constexpr uint32_t mt_prefix = tmem_slot + 16;  // int[kMaxSegs + 1]: m-tiles before segment s
+  static constexpr uint32_t segs = mt_prefix + (kMaxSegs + 1) * 4 + 12;
   static constexpr uint32_t end = ((segs + 15) / 16) * 16 + kMaxSegs * 16;
 };
 constexpr uint32_t kSmemBytesS = SmemLayoutS::end + 1024;
@@ -862,11 +862,63 @@ __device__ __forceinline__ void store_token_pairs(const float (&v)[32], int lane
   }
 }
 
-template <int EPI>
+// One GEMM of the swap kernel: GEMM1 (SwiGLU into H) or GEMM2 (store Yp).
+struct SwapPass {
+  __nv_bfloat16* out;
+  int n_tiles, num_kb, b_rows_per_slot, out_ld, epi;
+};
+
+struct SwapTile {
+  int pass, seg, m, n;
+};
+
+// tile t of the launch -> (pass, segment, m-tile, n-tile); the tiles of pass 0
+// come first, each pass in decode_tile's grouped order
+__device__ __forceinline__ SwapTile swap_tile(int t, const int* mt_prefix, int nseg, int mt_total,
+                                              const SwapPass& p0, const SwapPass& p1) {
+  SwapTile r;
+  r.pass = t >= mt_total * p0.n_tiles ? 1 : 0;
+  const SwapPass& p = r.pass ? p1 : p0;
+  if (r.pass) t -= mt_total * p0.n_tiles;
+  int lo = 0, hi = nseg - 1;  // last s with mt_prefix[s] * n_tiles <= t
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (mt_prefix[mid] * p.n_tiles <= t) lo = mid; else hi = mid - 1;
+  }
+  r.seg = lo;
+  const int local = t - mt_prefix[lo] * p.n_tiles;
+  const int m_tiles = mt_prefix[lo + 1] - mt_prefix[lo];
+  const int GM = group_ms(p.epi);
+  const int per_group = GM * p.n_tiles;
+  const int g = local / per_group;
+  const int gm = min(GM, m_tiles - g * GM);
+  const int rem = local - g * per_group;
+  r.n = rem / gm;
+  r.m = g * GM + rem % gm;
+  return r;
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// FUSED: one launch runs GEMM1 then GEMM2 (pass 0 / pass 1).  A GEMM2 tile of
+// (segment, m-tile) waits, before loading its H rows, until every GEMM1 tile
+// of those rows has been stored: ready[(segment, m-tile)] counts epilogue
+// warps done (4 per GEMM1 n-tile).  Every CTA takes its tiles in increasing
+// order and the whole grid is resident (one CTA per SM), so the GEMM1 tiles a
+// wait depends on are always ahead of it; the last CTA to finish zeroes the
+// counters for the next launch.  GEMM2's weights start streaming while GEMM1's
+// last wave drains, and there is no tail between the two GEMMs.
+template <bool FUSED>
 __global__ void __launch_bounds__(kThreads, 1)
-grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                         const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total, int k_total,
-                         int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld) {
+grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
+                         const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
+                         const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, const SwapPass p0,
+                         const SwapPass p1, int* __restrict__ ready, int ready_n) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayoutS::bars);
@@ -875,18 +927,21 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
   uint64_t* tfull = bars + 2 * STAGES_S;
   uint64_t* tempty = bars + 2 * STAGES_S + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SmemLayoutS::tmem_slot);
-  int* seg_tiles = reinterpret_cast<int*>(smem + SmemLayoutS::seg_tiles);
+  int* mt_prefix = reinterpret_cast<int*>(smem + SmemLayoutS::mt_prefix);
   int4* segs = reinterpret_cast<int4*>(smem + SmemLayoutS::segs);
 
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
   const int nseg = min(*nseg_g, kMaxSegs);
-  const int n_tiles = n_total / BN;
 
   for (int i = threadIdx.x; i < nseg; i += kThreads) segs[i] = reinterpret_cast<const int4*>(segs_g)[i];
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmA0);
+    tma_prefetch_desc(&tmB0);
+    if (FUSED) {
+      tma_prefetch_desc(&tmA1);
+      tma_prefetch_desc(&tmB1);
+    }
     for (int s = 0; s < STAGES_S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
     fence_barrier_init();
@@ -896,17 +951,18 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int s = 0; s < nseg; ++s) {
-      seg_tiles[s] = acc;
-      acc += ((segs[s].y + SN - 1) / SN) * n_tiles;
+      mt_prefix[s] = acc;
+      acc += (segs[s].y + SN - 1) / SN;
     }
-    seg_tiles[nseg] = acc;
+    mt_prefix[nseg] = acc;
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int total_tiles = nseg > 0 ? seg_tiles[nseg] : 0;
-  const int num_kb = k_total / BK;
+  const int mt_total = nseg > 0 ? mt_prefix[nseg] : 0;
+  const int total_tiles = mt_total * (p0.n_tiles + (FUSED ? p1.n_tiles : 0));
+  const int ready_target = 4 * p0.n_tiles;
   griddep_launch_dependents();
 
   if (warp == 0) {
@@ -917,34 +973,49 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
       const uint64_t pol_b = policy_evict_last();
       bool first = true;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const TileCoord c = decode_tile<kGroupMS<EPI>, SN>(t, seg_tiles, segs, nseg, n_tiles);
+        const SwapTile c = swap_tile(t, mt_prefix, nseg, mt_total, p0, p1);
+        const SwapPass& p = c.pass ? p1 : p0;
+        const CUtensorMap* tA = c.pass ? &tmA1 : &tmA0;
+        const CUtensorMap* tB = c.pass ? &tmB1 : &tmB0;
         const int a_row = segs[c.seg].x + c.m * SN;
         const int rows = min(SN, segs[c.seg].y - c.m * SN);
         const int nbox = rows > SBOX ? 2 : 1;
         const uint32_t bytes = kStageWS + nbox * kBoxBytesS;
-        const int b_row = segs[c.seg].z * b_rows_per_slot + c.n * BN;
+        const int b_row = segs[c.seg].z * p.b_rows_per_slot + c.n * BN;
+        const int num_kb = p.num_kb;
         int kb0 = 0;
-        if (first) {  // weights of the first stages stream while the producer kernel drains (PDL)
-          first = false;
+        if (first || (FUSED && c.pass == 1)) {
+          // Weights of the first stages go first: they depend neither on the
+          // producer kernel (PDL) nor on the GEMM1 tiles of these rows.
           kb0 = num_kb < STAGES_S ? num_kb : STAGES_S;
+          const int st0 = stage;
           for (int kb = 0; kb < kb0; ++kb) {
-            mbar_arrive_expect_tx(&full[kb], bytes);
-            tma_load_2d_hint(smem + SmemLayoutS::b + kb * kStageWS, &tmB, &full[kb], kb * BK, b_row, pol_b);
+            if (!first) mbar_wait(&empty[stage], phase ^ 1);  // fresh stages need no wait
+            mbar_arrive_expect_tx(&full[stage], bytes);
+            tma_load_2d_hint(smem + SmemLayoutS::b + stage * kStageWS, tB, &full[stage], kb * BK, b_row, pol_b);
+            if (++stage == STAGES_S) { stage = 0; phase ^= 1; }
           }
-          griddep_wait();
-          for (int kb = 0; kb < kb0; ++kb)
+          if (first) griddep_wait();
+          first = false;
+          if (FUSED && c.pass == 1) {
+            const int* r = ready + mt_prefix[c.seg] + c.m;
+            while (ld_acquire_gpu(r) < ready_target) __nanosleep(100);
+            fence_proxy_async_global();  // H was written by generic stores of other SMs
+          }
+          int st = st0;
+          for (int kb = 0; kb < kb0; ++kb) {
             for (int bx = 0; bx < nbox; ++bx)
-              tma_load_2d(smem + SmemLayoutS::a + kb * kStageTokS + bx * kBoxBytesS, &tmA, &full[kb], kb * BK,
+              tma_load_2d(smem + SmemLayoutS::a + st * kStageTokS + bx * kBoxBytesS, tA, &full[st], kb * BK,
                           a_row + bx * SBOX);
-          stage = kb0 == STAGES_S ? 0 : kb0;
-          phase = kb0 == STAGES_S ? 1u : 0u;
+            if (++st == STAGES_S) st = 0;
+          }
         }
         for (int kb = kb0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], bytes);
-          tma_load_2d_hint(smem + SmemLayoutS::b + stage * kStageWS, &tmB, &full[stage], kb * BK, b_row, pol_b);
+          tma_load_2d_hint(smem + SmemLayoutS::b + stage * kStageWS, tB, &full[stage], kb * BK, b_row, pol_b);
           for (int bx = 0; bx < nbox; ++bx)
-            tma_load_2d(smem + SmemLayoutS::a + stage * kStageTokS + bx * kBoxBytesS, &tmA, &full[stage], kb * BK,
+            tma_load_2d(smem + SmemLayoutS::a + stage * kStageTokS + bx * kBoxBytesS, tA, &full[stage], kb * BK,
                         a_row + bx * SBOX);
           if (++stage == STAGES_S) { stage = 0; phase ^= 1; }
         }
@@ -960,7 +1031,8 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
       const uint32_t a_base = smem_u32(smem + SmemLayoutS::a);
       const uint32_t b_base = smem_u32(smem + SmemLayoutS::b);
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const TileCoord c = decode_tile<kGroupMS<EPI>, SN>(t, seg_tiles, segs, nseg, n_tiles);
+        const SwapTile c = swap_tile(t, mt_prefix, nseg, mt_total, p0, p1);
+        const int num_kb = (c.pass ? p1 : p0).num_kb;
         const int rows = min(SN, segs[c.seg].y - c.m * SN);
         const uint32_t idesc = umma_idesc_bf16(128, static_cast<uint32_t>((rows + 15) & ~15));
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -992,7 +1064,8 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      const TileCoord c = decode_tile<kGroupMS<EPI>, SN>(t, seg_tiles, segs, nseg, n_tiles);
+      const SwapTile c = swap_tile(t, mt_prefix, nseg, mt_total, p0, p1);
+      const SwapPass& p = c.pass ? p1 : p0;
       const int4 sg = segs[c.seg];
       const int rows = min(SN, sg.y - c.m * SN);
       const size_t row0 = static_cast<size_t>(sg.x) + c.m * SN;
@@ -1003,14 +1076,14 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
 #pragma unroll 1
       for (int j0 = 0; j0 < rows; j0 += 32) {
         float v[32];
-        if constexpr (EPI == EPI_SWIGLU) {
+        if (p.epi == EPI_SWIGLU) {
           uint32_t g[32], u[32];
           tmem_ld_32x32b_x32(taddr + j0, g);       // W1 half: gate projections
           tmem_ld_32x32b_x32(taddr + SN + j0, u);  // W3 half: up projections
           tc_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = silu(__uint_as_float(g[i])) * __uint_as_float(u[i]);
-          store_token_pairs(v, lane, j0, rows, out, row0, out_ld, c.n * (BN / 2) + (f & ~1));
+          store_token_pairs(v, lane, j0, rows, p.out, row0, p.out_ld, c.n * (BN / 2) + (f & ~1));
         } else {
 #pragma unroll 1
           for (int h = 0; h < 2; ++h) {
@@ -1019,7 +1092,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
             tc_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-            store_token_pairs(v, lane, j0, rows, out, row0, out_ld, c.n * BN + h * 128 + (f & ~1));
+            store_token_pairs(v, lane, j0, rows, p.out, row0, p.out_ld, c.n * BN + h * 128 + (f & ~1));
           }
         }
       }
@@ -1027,27 +1100,48 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_c
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (FUSED && c.pass == 0) {
+        // this warp's share of the tile's H rows is stored: publish it
+        fence_proxy_async_global();
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(ready + mt_prefix[c.seg] + c.m, 1);
+      }
     }
   }
   griddep_wait();
   tc_fence_before();
   __syncthreads();
+  if (FUSED && threadIdx.x == 0) {
+    // every tile of this CTA is done; the last CTA resets the counters
+    __threadfence();
+    if (atomicAdd(ready + ready_n - 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      for (int i = 0; i < mt_total; ++i) ready[i] = 0;
+      ready[ready_n - 1] = 0;
+      __threadfence();
+    }
+  }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<kTmemColsS>(tmem_base);
   }
 }
 
-cudaError_t launch_grouped_gemm_swap(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
-                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
-                                     __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl) {
-  if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
+// which: 0 = GEMM1 alone, 1 = GEMM2 alone, 2 = GEMM1 then GEMM2 in one launch.
+cudaError_t launch_grouped_gemm_swap(int which, const CUtensorMap* tmA1, const CUtensorMap* tmB1,
+                                     const CUtensorMap* tmA2, const CUtensorMap* tmB2, const GemmSeg* segs,
+                                     const int* nseg, int d, int ff, int b_rows1, int b_rows2, __nv_bfloat16* h,
+                                     __nv_bfloat16* yp, int* ready, int ready_n, int num_ctas, cudaStream_t stream,
+                                     bool pdl) {
+  if ((2 * ff) % BN || d % BN || d % BK || ff % BK) return cudaErrorInvalidValue;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(grouped_gemm_swap_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesS);
-    cudaFuncSetAttribute(grouped_gemm_swap_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesS);
+    cudaFuncSetAttribute(grouped_gemm_swap_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesS);
+    cudaFuncSetAttribute(grouped_gemm_swap_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesS);
     configured = true;
   }
+  const SwapPass g1{h, 2 * ff / BN, d / BK, b_rows1, ff, EPI_SWIGLU};
+  const SwapPass g2{yp, d / BN, ff / BK, b_rows2, d, EPI_STORE};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_ctas);
   cfg.blockDim = dim3(kThreads);
@@ -1058,11 +1152,14 @@ cudaError_t launch_grouped_gemm_swap(int epi, const CUtensorMap* tmA, const CUte
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (epi == EPI_SWIGLU)
-    return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<EPI_SWIGLU>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                              b_rows_per_slot, out, out_ld);
-  return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<EPI_STORE>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                            b_rows_per_slot, out, out_ld);
+  if (which == 2)
+    return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<true>, *tmA1, *tmB1, *tmA2, *tmB2, segs, nseg, g1, g2,
+                              ready, ready_n);
+  if (which == 0)
+    return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<false>, *tmA1, *tmB1, *tmA1, *tmB1, segs, nseg, g1, g1,
+                              ready, ready_n);
+  return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<false>, *tmA2, *tmB2, *tmA2, *tmB2, segs, nseg, g2, g2,
+                            ready, ready_n);
 }
 
 // --------------------------------------------------------------- host side
@@ -1131,8 +1228,8 @@ cudaError_t preload_gemm_kernels() {
                        reinterpret_cast<const void*>(grouped_gemm_2sm_kernel<1>),
                        reinterpret_cast<const void*>(grouped_gemm_m256_kernel<0>),
                        reinterpret_cast<const void*>(grouped_gemm_m256_kernel<1>),
-                       reinterpret_cast<const void*>(grouped_gemm_swap_kernel<0>),
-                       reinterpret_cast<const void*>(grouped_gemm_swap_kernel<1>)};
+                       reinterpret_cast<const void*>(grouped_gemm_swap_kernel<false>),
+                       reinterpret_cast<const void*>(grouped_gemm_swap_kernel<true>)};
   for (const void* f : fns) {
     const cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;

@@ -14,13 +14,15 @@ from paper_2603_06350_b200 import workload as wl
 pytestmark = pytest.mark.gpu
 
 
-def _run(cuda, variant, E, k, d, ff, T, rc, seed=21):
+def _run(cuda, variant, E, k, d, ff, T, rc, seed=21, env=None):
     import torch
-    os.environ["MOE_GEMM_VARIANT"] = variant
+    env = dict(env or {}, MOE_GEMM_VARIANT=variant)
+    os.environ.update(env)
     try:
         m = MoELayer(1, E, k, d, ff, max_tokens=T)
     finally:
-        del os.environ["MOE_GEMM_VARIANT"]
+        for key in env:
+            del os.environ[key]
     x = wl.tokens(T, d, E, seed, 0)
     wg = wl.gate_weights(E, d, 1.2, seed, 0, 0)
     experts = [wl.expert_weights(d, ff, seed, 0, e) for e in range(E)]
@@ -48,12 +50,35 @@ def test_variants_agree_and_match_oracle(cuda, E, k, d, ff, T, rc):
     x, wg, experts, y1 = _run(cuda, "1sm", E, k, d, ff, T, rc)
     _, _, _, y2 = _run(cuda, "2sm", E, k, d, ff, T, rc)
     _, _, _, y3 = _run(cuda, "m256", E, k, d, ff, T, rc)
-    _, _, _, y4 = _run(cuda, "swap", E, k, d, ff, T, rc)
+    _, _, _, y4 = _run(cuda, "swap", E, k, d, ff, T, rc)  # GEMM1 + GEMM2 in one launch
+    _, _, _, y5 = _run(cuda, "swap", E, k, d, ff, T, rc, env={"MOE_SWAP_FUSE": "0"})
     y_ref = oracle.layer_forward(x, wg, experts, rc, k)[0]
-    for y in (y1, y2, y3, y4):
+    for y in (y1, y2, y3, y4, y5):
         err = float(np.max(np.abs(y - y_ref)) / np.max(np.abs(y_ref)))
         assert err <= 2e-2, err
     # same K order per output element, same fp32 accumulation: bit-identical outputs
     assert np.array_equal(y1, y2) and np.array_equal(y1, y3)
     # swap-AB (weights as M, tokens as N): the same products in the same K order
     assert np.array_equal(y1, y4), float(np.max(np.abs(y1 - y4)))
+    assert np.array_equal(y1, y5), float(np.max(np.abs(y1 - y5)))
+
+
+def test_swap_fused_repeated_forwards(cuda):
+    """The fused swap-AB launch resets its readiness counters itself: many
+    forwards in a row (eager and CUDA-graph replay) stay equal to the 1-SM
+    kernel's output."""
+    import torch
+    E, k, d, ff, T = 64, 8, 1024, 1408, 128
+    x, wg, experts, y1 = _run(cuda, "1sm", E, k, d, ff, T, [1] * E)
+    for graphs in (False, True):
+        m = MoELayer(1, E, k, d, ff, max_tokens=T, cuda_graphs=graphs)
+        m.set_gate(0, wg)
+        for e, w in enumerate(experts):
+            m.load_expert(0, e, *w)
+        xd = torch.from_numpy(x.view(np.int16)).to(cuda)
+        for it in range(20):
+            yd = torch.zeros((T, d), dtype=torch.int16, device=cuda)
+            m.forward(0, xd, yd, MOE_PLAN_FIXED, it)
+            m.sync()
+            assert np.array_equal(oracle.bf16_to_f32(yd.cpu().numpy().view(np.uint16)), y1), (graphs, it)
+        m.close()
