@@ -144,6 +144,7 @@ def test_gathered_gemm1_matches_dispatch_copy(cuda, monkeypatch, E, k, d, ff, T,
     the inverse of the row codes."""
     import torch
     outs = []
+    monkeypatch.setenv("MOE_GEMM_VARIANT", "1sm")  # gather is a 128-row-tile feature (decode shapes pick swap-AB)
     for flag in ("1", "0"):
         monkeypatch.setenv("MOE_GATHER", flag)
         m, st, y, y_ref, ids_o, counts_o = _layer_case(cuda, E, k, d, ff, T, rc)
