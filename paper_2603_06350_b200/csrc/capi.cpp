@@ -185,23 +185,30 @@ void stage_exchange(moe_ctx* c, bool forward, cudaStream_t s) {
 // B200's 1 kW cap it settles ~190 MHz lower and nets ~4% less throughput on
 // the Mixtral layer (profiles/ab_gemm_variants_r01.md), so it is opt-in
 // (MOE_GEMM_VARIANT=2sm) until it is made more energy-efficient.
-// Swap-AB decode tiles (weights as the M operand, up to 64 tokens as N) when
-// the batch leaves a few dozen rows per expert: the 128-row tiles would be
-// mostly padding (profiles/ab_swap_r01.md).
-bool use_swap(const moe_ctx* c, int T) {
-  if (c->fp32 || c->gemm_variant == 1 || c->gemm_variant == 2 || c->gemm_variant == 3) return false;
-  if (c->gemm_variant == 4) return true;
+// Swap-AB tiles (weights as the M operand, tokens as N; GEMM1 and GEMM2 in one
+// launch): 64-token tiles when the batch leaves a few dozen rows per expert
+// (decode: 128-row tiles would be mostly padding), 128-token tiles for
+// mid-size batches (same MMA work per stage as the 1-SM kernel, no tail
+// between the GEMMs).  Returns the tile's token rows, 0 = the 1-SM kernel
+// (profiles/ab_swap_r01.md).
+int use_swap(const moe_ctx* c, int T) {
+  if (c->fp32 || T <= 0 || c->gemm_variant == 1 || c->gemm_variant == 2 || c->gemm_variant == 3) return 0;
   const int64_t mean_rows = static_cast<int64_t>(T) * c->k * c->G / std::max(1, c->E);  // balanced EP
-  return T > 0 && mean_rows <= c->swap_rows;
+  if (c->gemm_variant == 5) return 64;
+  if (c->gemm_variant == 6) return 128;
+  if (c->gemm_variant == 4) return mean_rows <= 64 ? 64 : 128;
+  if (mean_rows <= c->swap_rows) return 64;
+  return mean_rows <= c->swap128_rows ? 128 : 0;
 }
 
 void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t rows = 0, bool gather = false,
                      uint16_t* fused_y = nullptr) {
   Layer& L = c->layers[layer];
-  if (!gather && !fused_y && use_swap(c, c->gemm_T)) {
+  const int sn = gather || fused_y ? 0 : use_swap(c, c->gemm_T);
+  if (sn) {
     // fused: the GEMM1 call launches both GEMMs, the GEMM2 call adds nothing
     if (c->swap_fuse && which == 1) return;
-    CU_CHECK(launch_grouped_gemm_swap(c->swap_fuse ? 2 : which, &c->tmA1s, &L.tmB1, &c->tmA2s, &L.tmB2,
+    CU_CHECK(launch_grouped_gemm_swap(c->swap_fuse ? 2 : which, sn, &c->tmA1s, &L.tmB1, &c->tmA2s, &L.tmB2,
                                       c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, 2 * c->ff, c->d,
                                       reinterpret_cast<__nv_bfloat16*>(c->h.p),
                                       reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->swap_ready.p,
@@ -325,7 +332,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   // single GPU, bf16, 1-SM K4: GEMM1 gathers its A rows from x (TMA gather4)
   // and the dispatch kernel only ranks — no permuted copy of the tokens
   c->gemm_T = T;
-  const bool swap = use_swap(c, T);
+  const bool swap = use_swap(c, T) != 0;
   const bool gather = c->gather && c->G == 1 && !c->fp32 && (c->gemm_variant == 0 || c->gemm_variant == 1) && T > 0 &&
                       !swap;
   // single GPU, bf16, 1-SM K4: the combine runs inside GEMM2's epilogue

@@ -266,9 +266,16 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_GEMM_GROUP_M")) std::sscanf(v, "%d,%d", &c->group_m[0], &c->group_m[1]);
     if (const char* v = std::getenv("MOE_GEMM_VARIANT")) {
       const std::string s(v);
-      c->gemm_variant = s == "1sm" ? 1 : (s == "2sm" ? 2 : (s == "m256" ? 3 : (s == "swap" ? 4 : 0)));
+      c->gemm_variant = s == "1sm"      ? 1
+                        : s == "2sm"    ? 2
+                        : s == "m256"   ? 3
+                        : s == "swap"   ? 4
+                        : s == "swap64" ? 5
+                        : s == "swap128" ? 6
+                                         : 0;
     }
     if (const char* v = std::getenv("MOE_GEMM_SWAP_ROWS")) c->swap_rows = std::atoi(v);
+    if (const char* v = std::getenv("MOE_GEMM_SWAP128_ROWS")) c->swap128_rows = std::atoi(v);
     if (const char* v = std::getenv("MOE_SWAP_FUSE")) c->swap_fuse = std::string(v) != "0";
     c->registry = moeless::ReplicaRegistry(std::max(0, D.keep_alive_iters));
     c->layers.resize(D.num_layers);

@@ -78,7 +78,7 @@ cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorM
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                 __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, int* sched,
                                 bool pdl, const int32_t* a_gather, int group_m, const FusedCombine& fc);
-cudaError_t launch_grouped_gemm_swap(int which, const CUtensorMap* tmA1, const CUtensorMap* tmB1,
+cudaError_t launch_grouped_gemm_swap(int which, int sn, const CUtensorMap* tmA1, const CUtensorMap* tmB1,
                                      const CUtensorMap* tmA2, const CUtensorMap* tmB2, const GemmSeg* segs,
                                      const int* nseg, int d, int ff, int b_rows1, int b_rows2, __nv_bfloat16* h,
                                      __nv_bfloat16* yp, int* ready, int ready_n, int num_ctas, cudaStream_t stream,
@@ -288,8 +288,9 @@ struct EventSet {
 struct moe_ctx {
   moe_ctx_desc desc{};
   int E = 0, k = 0, d = 0, ff = 0, G = 1, rank = 0, Tmax = 0, n_pred = 0, num_sms = 148;
-  int gemm_variant = 0;  // 0 auto, 1 force 1-SM, 2 force 2-SM, 3 m256, 4 force swap-AB (env MOE_GEMM_VARIANT)
-  int swap_rows = 64;    // auto: swap-AB decode tiles when the mean rows per expert <= this (MOE_GEMM_SWAP_ROWS)
+  int gemm_variant = 0;  // 0 auto, 1 force 1-SM, 2 force 2-SM, 3 m256, 4 swap-AB, 5 swap64, 6 swap128 (MOE_GEMM_VARIANT)
+  int swap_rows = 64;    // auto: 64-token swap-AB tiles when the mean rows per expert <= this (MOE_GEMM_SWAP_ROWS)
+  int swap128_rows = 1024;  // auto: 128-token swap-AB tiles (fused GEMMs) up to this mean (MOE_GEMM_SWAP128_ROWS)
   int gemm_T = 0;        // tokens of the forward whose GEMMs are being enqueued
   bool swap_fuse = true;  // swap-AB: GEMM1 and GEMM2 in one launch (MOE_SWAP_FUSE=0: two)
   DevBuf<int> swap_ready; // its per-(segment, m-tile) GEMM1-done counters (+ CTA counter)

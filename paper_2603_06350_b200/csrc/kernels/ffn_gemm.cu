@@ -827,23 +827,31 @@ cudaError_t launch_grouped_gemm_m256(int epi, const CUtensorMap* tmA, const CUte
 // features of one token.  Per weight byte the tensor work drops from 128 rows
 // to the rows actually present, and the smem stage is 32 KB of weights + 4-8
 // KB of tokens (5 stages).
-constexpr int SN = 64, SBOX = 32, STAGES_S = 5;
-constexpr uint32_t kStageTokS = SN * BK * 2, kStageWS = BN * BK * 2, kBoxBytesS = SBOX * BK * 2;
-constexpr uint32_t kTmemColsS = 256;  // 2 accumulators x 2 weight halves x SN token columns
-__host__ __device__ constexpr int group_ms(int epi) { return epi == 0 ? 64 : 32; }  // 64-row tiles per n sweep
-
-struct SmemLayoutS {
+// SN = 64 (decode: 5 stages of 32 KB weights + 8 KB tokens) or 128 (mid-size
+// batches: the 1-SM kernel's MMA work per stage, 4 stages of 48 KB, plus the
+// fused GEMM1 -> GEMM2 schedule).
+constexpr int SBOX = 32;
+constexpr uint32_t kStageWS = BN * BK * 2, kBoxBytesS = SBOX * BK * 2;
+template <int SN_>
+struct SwapCfg {
+  static constexpr int SN = SN_;
+  static constexpr int STAGES = SN_ == 64 ? 5 : 4;
+  static constexpr uint32_t kStageTok = SN_ * BK * 2;
+  static constexpr uint32_t kTmemCols = 4 * SN_;  // 2 accumulators x 2 weight halves x SN token columns
+  // smem layout, offsets relative to the 1024-aligned base
   static constexpr uint32_t a = 0;  // token tiles
-  static constexpr uint32_t b = a + STAGES_S * kStageTokS;
-  static constexpr uint32_t bars = b + STAGES_S * kStageWS;
-  static constexpr uint32_t n_bars = 2 * STAGES_S + 4;
+  static constexpr uint32_t b = a + STAGES * kStageTok;
+  static constexpr uint32_t bars = b + STAGES * kStageWS;
+  static constexpr uint32_t n_bars = 2 * STAGES + 4;
   static constexpr uint32_t tmem_slot = bars + n_bars * 8;
   static constexpr uint32_t mt_prefix = tmem_slot + 16;  // int[kMaxSegs + 1]: m-tiles before segment s
   static constexpr uint32_t segs = mt_prefix + (kMaxSegs + 1) * 4 + 12;
   static constexpr uint32_t end = ((segs + 15) / 16) * 16 + kMaxSegs * 16;
+  static constexpr uint32_t kSmemBytes = end + 1024;
+  static_assert(kSmemBytes <= 232448, "smem budget (swap-AB variant)");
 };
-constexpr uint32_t kSmemBytesS = SmemLayoutS::end + 1024;
-static_assert(kSmemBytesS <= 232448, "smem budget (swap-AB variant)");
+// SN-row m-tiles swept per n column
+__host__ __device__ constexpr int group_ms(int epi, int sn) { return (epi == 0 ? 64 : 32) * 64 / sn; }
 
 // 32 token columns of one accumulator half -> bf16 pairs of features:
 // lane pairs (2i, 2i+1) swap one value so the even lane stores token j's
@@ -874,6 +882,7 @@ struct SwapTile {
 
 // tile t of the launch -> (pass, segment, m-tile, n-tile); the tiles of pass 0
 // come first, each pass in decode_tile's grouped order
+template <int SN>
 __device__ __forceinline__ SwapTile swap_tile(int t, const int* mt_prefix, int nseg, int mt_total,
                                               const SwapPass& p0, const SwapPass& p1) {
   SwapTile r;
@@ -888,7 +897,7 @@ __device__ __forceinline__ SwapTile swap_tile(int t, const int* mt_prefix, int n
   r.seg = lo;
   const int local = t - mt_prefix[lo] * p.n_tiles;
   const int m_tiles = mt_prefix[lo + 1] - mt_prefix[lo];
-  const int GM = group_ms(p.epi);
+  const int GM = group_ms(p.epi, SN);
   const int per_group = GM * p.n_tiles;
   const int g = local / per_group;
   const int gm = min(GM, m_tiles - g * GM);
@@ -913,22 +922,25 @@ __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence
 // wait depends on are always ahead of it; the last CTA to finish zeroes the
 // counters for the next launch.  GEMM2's weights start streaming while GEMM1's
 // last wave drains, and there is no tail between the two GEMMs.
-template <bool FUSED>
+template <bool FUSED, int SNv>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
                          const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                          const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, const SwapPass p0,
                          const SwapPass p1, int* __restrict__ ready, int ready_n) {
+  using C = SwapCfg<SNv>;
+  constexpr int SN = C::SN, STAGES_S = C::STAGES;
+  constexpr uint32_t kStageTokS = C::kStageTok;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayoutS::bars);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::bars);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES_S;
   uint64_t* tfull = bars + 2 * STAGES_S;
   uint64_t* tempty = bars + 2 * STAGES_S + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SmemLayoutS::tmem_slot);
-  int* mt_prefix = reinterpret_cast<int*>(smem + SmemLayoutS::mt_prefix);
-  int4* segs = reinterpret_cast<int4*>(smem + SmemLayoutS::segs);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::tmem_slot);
+  int* mt_prefix = reinterpret_cast<int*>(smem + C::mt_prefix);
+  int4* segs = reinterpret_cast<int4*>(smem + C::segs);
 
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
@@ -946,7 +958,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<kTmemColsS>(tmem_slot);
+  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
   __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0;
@@ -973,13 +985,13 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
       const uint64_t pol_b = policy_evict_last();
       bool first = true;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const SwapTile c = swap_tile(t, mt_prefix, nseg, mt_total, p0, p1);
+        const SwapTile c = swap_tile<SN>(t, mt_prefix, nseg, mt_total, p0, p1);
         const SwapPass& p = c.pass ? p1 : p0;
         const CUtensorMap* tA = c.pass ? &tmA1 : &tmA0;
         const CUtensorMap* tB = c.pass ? &tmB1 : &tmB0;
         const int a_row = segs[c.seg].x + c.m * SN;
         const int rows = min(SN, segs[c.seg].y - c.m * SN);
-        const int nbox = rows > SBOX ? 2 : 1;
+        const int nbox = (rows + SBOX - 1) / SBOX;
         const uint32_t bytes = kStageWS + nbox * kBoxBytesS;
         const int b_row = segs[c.seg].z * p.b_rows_per_slot + c.n * BN;
         const int num_kb = p.num_kb;
@@ -992,7 +1004,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
           for (int kb = 0; kb < kb0; ++kb) {
             if (!first) mbar_wait(&empty[stage], phase ^ 1);  // fresh stages need no wait
             mbar_arrive_expect_tx(&full[stage], bytes);
-            tma_load_2d_hint(smem + SmemLayoutS::b + stage * kStageWS, tB, &full[stage], kb * BK, b_row, pol_b);
+            tma_load_2d_hint(smem + C::b + stage * kStageWS, tB, &full[stage], kb * BK, b_row, pol_b);
             if (++stage == STAGES_S) { stage = 0; phase ^= 1; }
           }
           if (first) griddep_wait();
@@ -1005,7 +1017,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
           int st = st0;
           for (int kb = 0; kb < kb0; ++kb) {
             for (int bx = 0; bx < nbox; ++bx)
-              tma_load_2d(smem + SmemLayoutS::a + st * kStageTokS + bx * kBoxBytesS, tA, &full[st], kb * BK,
+              tma_load_2d(smem + C::a + st * kStageTokS + bx * kBoxBytesS, tA, &full[st], kb * BK,
                           a_row + bx * SBOX);
             if (++st == STAGES_S) st = 0;
           }
@@ -1013,9 +1025,9 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
         for (int kb = kb0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], bytes);
-          tma_load_2d_hint(smem + SmemLayoutS::b + stage * kStageWS, tB, &full[stage], kb * BK, b_row, pol_b);
+          tma_load_2d_hint(smem + C::b + stage * kStageWS, tB, &full[stage], kb * BK, b_row, pol_b);
           for (int bx = 0; bx < nbox; ++bx)
-            tma_load_2d(smem + SmemLayoutS::a + stage * kStageTokS + bx * kBoxBytesS, tA, &full[stage], kb * BK,
+            tma_load_2d(smem + C::a + stage * kStageTokS + bx * kBoxBytesS, tA, &full[stage], kb * BK,
                         a_row + bx * SBOX);
           if (++stage == STAGES_S) { stage = 0; phase ^= 1; }
         }
@@ -1028,10 +1040,10 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      const uint32_t a_base = smem_u32(smem + SmemLayoutS::a);
-      const uint32_t b_base = smem_u32(smem + SmemLayoutS::b);
+      const uint32_t a_base = smem_u32(smem + C::a);
+      const uint32_t b_base = smem_u32(smem + C::b);
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const SwapTile c = swap_tile(t, mt_prefix, nseg, mt_total, p0, p1);
+        const SwapTile c = swap_tile<SN>(t, mt_prefix, nseg, mt_total, p0, p1);
         const int num_kb = (c.pass ? p1 : p0).num_kb;
         const int rows = min(SN, segs[c.seg].y - c.m * SN);
         const uint32_t idesc = umma_idesc_bf16(128, static_cast<uint32_t>((rows + 15) & ~15));
@@ -1064,7 +1076,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      const SwapTile c = swap_tile(t, mt_prefix, nseg, mt_total, p0, p1);
+      const SwapTile c = swap_tile<SN>(t, mt_prefix, nseg, mt_total, p0, p1);
       const SwapPass& p = c.pass ? p1 : p0;
       const int4 sg = segs[c.seg];
       const int rows = min(SN, sg.y - c.m * SN);
@@ -1123,29 +1135,27 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
   }
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<kTmemColsS>(tmem_base);
+    tmem_dealloc<C::kTmemCols>(tmem_base);
   }
 }
 
-// which: 0 = GEMM1 alone, 1 = GEMM2 alone, 2 = GEMM1 then GEMM2 in one launch.
-cudaError_t launch_grouped_gemm_swap(int which, const CUtensorMap* tmA1, const CUtensorMap* tmB1,
-                                     const CUtensorMap* tmA2, const CUtensorMap* tmB2, const GemmSeg* segs,
-                                     const int* nseg, int d, int ff, int b_rows1, int b_rows2, __nv_bfloat16* h,
-                                     __nv_bfloat16* yp, int* ready, int ready_n, int num_ctas, cudaStream_t stream,
-                                     bool pdl) {
-  if ((2 * ff) % BN || d % BN || d % BK || ff % BK) return cudaErrorInvalidValue;
+template <int SNv>
+cudaError_t launch_swap(int which, const CUtensorMap* tmA1, const CUtensorMap* tmB1, const CUtensorMap* tmA2,
+                        const CUtensorMap* tmB2, const GemmSeg* segs, const int* nseg, const SwapPass& g1,
+                        const SwapPass& g2, int* ready, int ready_n, int num_ctas, cudaStream_t stream, bool pdl) {
+  using C = SwapCfg<SNv>;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(grouped_gemm_swap_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesS);
-    cudaFuncSetAttribute(grouped_gemm_swap_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytesS);
+    cudaFuncSetAttribute(grouped_gemm_swap_kernel<false, SNv>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::kSmemBytes);
+    cudaFuncSetAttribute(grouped_gemm_swap_kernel<true, SNv>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::kSmemBytes);
     configured = true;
   }
-  const SwapPass g1{h, 2 * ff / BN, d / BK, b_rows1, ff, EPI_SWIGLU};
-  const SwapPass g2{yp, d / BN, ff / BK, b_rows2, d, EPI_STORE};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_ctas);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmemBytesS;
+  cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1153,13 +1163,29 @@ cudaError_t launch_grouped_gemm_swap(int which, const CUtensorMap* tmA1, const C
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (which == 2)
-    return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<true>, *tmA1, *tmB1, *tmA2, *tmB2, segs, nseg, g1, g2,
-                              ready, ready_n);
+    return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<true, SNv>, *tmA1, *tmB1, *tmA2, *tmB2, segs, nseg, g1,
+                              g2, ready, ready_n);
   if (which == 0)
-    return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<false>, *tmA1, *tmB1, *tmA1, *tmB1, segs, nseg, g1, g1,
-                              ready, ready_n);
-  return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<false>, *tmA2, *tmB2, *tmA2, *tmB2, segs, nseg, g2, g2,
-                            ready, ready_n);
+    return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<false, SNv>, *tmA1, *tmB1, *tmA1, *tmB1, segs, nseg,
+                              g1, g1, ready, ready_n);
+  return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<false, SNv>, *tmA2, *tmB2, *tmA2, *tmB2, segs, nseg, g2,
+                            g2, ready, ready_n);
+}
+
+// which: 0 = GEMM1 alone, 1 = GEMM2 alone, 2 = GEMM1 then GEMM2 in one launch;
+// sn = token rows per tile (64 or 128).
+cudaError_t launch_grouped_gemm_swap(int which, int sn, const CUtensorMap* tmA1, const CUtensorMap* tmB1,
+                                     const CUtensorMap* tmA2, const CUtensorMap* tmB2, const GemmSeg* segs,
+                                     const int* nseg, int d, int ff, int b_rows1, int b_rows2, __nv_bfloat16* h,
+                                     __nv_bfloat16* yp, int* ready, int ready_n, int num_ctas, cudaStream_t stream,
+                                     bool pdl) {
+  if ((2 * ff) % BN || d % BN || d % BK || ff % BK || (sn != 64 && sn != 128)) return cudaErrorInvalidValue;
+  const SwapPass g1{h, 2 * ff / BN, d / BK, b_rows1, ff, EPI_SWIGLU};
+  const SwapPass g2{yp, d / BN, ff / BK, b_rows2, d, EPI_STORE};
+  return sn == 64 ? launch_swap<64>(which, tmA1, tmB1, tmA2, tmB2, segs, nseg, g1, g2, ready, ready_n, num_ctas,
+                                    stream, pdl)
+                  : launch_swap<128>(which, tmA1, tmB1, tmA2, tmB2, segs, nseg, g1, g2, ready, ready_n, num_ctas,
+                                     stream, pdl);
 }
 
 // --------------------------------------------------------------- host side
@@ -1228,8 +1254,10 @@ cudaError_t preload_gemm_kernels() {
                        reinterpret_cast<const void*>(grouped_gemm_2sm_kernel<1>),
                        reinterpret_cast<const void*>(grouped_gemm_m256_kernel<0>),
                        reinterpret_cast<const void*>(grouped_gemm_m256_kernel<1>),
-                       reinterpret_cast<const void*>(grouped_gemm_swap_kernel<false>),
-                       reinterpret_cast<const void*>(grouped_gemm_swap_kernel<true>)};
+                       reinterpret_cast<const void*>(grouped_gemm_swap_kernel<false, 64>),
+                       reinterpret_cast<const void*>(grouped_gemm_swap_kernel<true, 64>),
+                       reinterpret_cast<const void*>(grouped_gemm_swap_kernel<false, 128>),
+                       reinterpret_cast<const void*>(grouped_gemm_swap_kernel<true, 128>)};
   for (const void* f : fns) {
     const cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;

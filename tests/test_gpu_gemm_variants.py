@@ -52,8 +52,10 @@ def test_variants_agree_and_match_oracle(cuda, E, k, d, ff, T, rc):
     _, _, _, y3 = _run(cuda, "m256", E, k, d, ff, T, rc)
     _, _, _, y4 = _run(cuda, "swap", E, k, d, ff, T, rc)  # GEMM1 + GEMM2 in one launch
     _, _, _, y5 = _run(cuda, "swap", E, k, d, ff, T, rc, env={"MOE_SWAP_FUSE": "0"})
+    _, _, _, y6 = _run(cuda, "swap64", E, k, d, ff, T, rc)
+    _, _, _, y7 = _run(cuda, "swap128", E, k, d, ff, T, rc)
     y_ref = oracle.layer_forward(x, wg, experts, rc, k)[0]
-    for y in (y1, y2, y3, y4, y5):
+    for y in (y1, y2, y3, y4, y5, y6, y7):
         err = float(np.max(np.abs(y - y_ref)) / np.max(np.abs(y_ref)))
         assert err <= 2e-2, err
     # same K order per output element, same fp32 accumulation: bit-identical outputs
@@ -61,6 +63,7 @@ def test_variants_agree_and_match_oracle(cuda, E, k, d, ff, T, rc):
     # swap-AB (weights as M, tokens as N): the same products in the same K order
     assert np.array_equal(y1, y4), float(np.max(np.abs(y1 - y4)))
     assert np.array_equal(y1, y5), float(np.max(np.abs(y1 - y5)))
+    assert np.array_equal(y1, y6) and np.array_equal(y1, y7)
 
 
 def test_swap_fused_repeated_forwards(cuda):
