@@ -118,7 +118,7 @@ void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool u
     CU_CHECK(launch_small_copy(c->dplan.p, c->hplan, sizeof(DevPlan), s));  // SM copy from mapped pinned memory
   const int nblk = gate_num_blocks(T);
   CU_CHECK(launch_block_prefix(c->block_counts.p, nblk, c->E, c->dplan.p, c->block_pre.p, s,
-                               local_plan ? c->counts.p : nullptr));
+                               local_plan ? c->counts.p : nullptr, c->pdl_prefix()));
   // rows move as opaque 16-byte chunks: the row width in 16-bit units covers fp32 rows too
   RowTargets t{};
   PeerSignal sig{};
@@ -138,7 +138,7 @@ void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool u
   }
   CU_CHECK(launch_dispatch(reinterpret_cast<const __nv_bfloat16*>(x), T, c->xw, c->E, c->k, c->ids.p, c->block_pre.p,
                            c->dplan.p, t, c->row_code.p, sig, s, gather ? c->perm_src.p : nullptr,
-                           fused ? c->row_owner.p : nullptr));
+                           fused ? c->row_owner.p : nullptr, c->pdl_prefix()));
 }
 
 // The exchange step of one direction.  NCCL: grouped send/recv, forward: my
@@ -284,7 +284,7 @@ void stage_combine(moe_ctx* c, uint16_t* y, int T, cudaStream_t s) {
     return;
   }
   CU_CHECK(launch_combine(t, T, c->d, c->k, c->row_code.p, c->wts.p, reinterpret_cast<__nv_bfloat16*>(y),
-                          c->num_sms, s));
+                          c->num_sms, s, c->pdl_combine()));
 }
 
 void check_p2p(moe_ctx* c) {
@@ -447,8 +447,18 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
       CU_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-      enqueue_forward(c, L, layer, x, T, y, plan_mode, iteration, s, with_pred, stride, x_consumed, ahead, true,
-                      [](int) {});
+      c->capturing = true;
+      try {
+        enqueue_forward(c, L, layer, x, T, y, plan_mode, iteration, s, with_pred, stride, x_consumed, ahead, true,
+                        [](int) {});
+      } catch (...) {
+        c->capturing = false;
+        cudaGraph_t dead = nullptr;
+        cudaStreamEndCapture(s, &dead);
+        if (dead) cudaGraphDestroy(dead);
+        throw;
+      }
+      c->capturing = false;
       cudaGraph_t g = nullptr;
       CU_CHECK(cudaStreamEndCapture(s, &g));
       cudaGraphExec_t ex = nullptr;

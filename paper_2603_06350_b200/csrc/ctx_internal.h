@@ -36,11 +36,12 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
                              int32_t* host_counts = nullptr, int host_n = 0, unsigned* ticket = nullptr,
                              const float* pred_w2 = nullptr, unsigned mlp_mask = 0);
 cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, const DevPlan* plan,
-                                int32_t* block_pre, cudaStream_t s, const int32_t* local_counts = nullptr);
+                                int32_t* block_pre, cudaStream_t s, const int32_t* local_counts = nullptr,
+                                bool pdl = false);
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
                             const int32_t* block_pre, const DevPlan* plan, const RowTargets& targets,
                             uint32_t* row_code, const PeerSignal& sig, cudaStream_t s, int32_t* perm_src,
-                            int32_t* row_owner);
+                            int32_t* row_owner, bool pdl = false);
 // K6 over peer memory (p2p.cu)
 constexpr int kMaxRanks = 8;
 enum { kFlagCounts = 0, kFlagRows = 1, kFlagOutputs = 2, kFlagKinds = 4 };
@@ -67,7 +68,7 @@ cudaError_t launch_swiglu_f32(const float* C, int rows, int ff, float* H, cudaSt
 cudaError_t launch_combine_f32(const RowTargets& sources, int T, int d, int k, const uint32_t* row_code,
                                const float* wts, float* y, cudaStream_t s);
 cudaError_t launch_combine(const RowTargets& sources, int T, int d, int k, const uint32_t* row_code,
-                           const float* wts, __nv_bfloat16* y, int num_sms, cudaStream_t s);
+                           const float* wts, __nv_bfloat16* y, int num_sms, cudaStream_t s, bool pdl = false);
 cudaError_t launch_grouped_gemm_m256(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                      const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                      __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream);
@@ -292,6 +293,12 @@ struct moe_ctx {
   int swap_rows = 64;    // auto: 64-token swap-AB tiles when the mean rows per expert <= this (MOE_GEMM_SWAP_ROWS)
   int swap128_rows = 1024;  // auto: 128-token swap-AB tiles (fused GEMMs) up to this mean (MOE_GEMM_SWAP128_ROWS)
   int gemm_T = 0;        // tokens of the forward whose GEMMs are being enqueued
+  // programmatic dependent launch of the small kernels (MOE_PDL_FRONT bit mask):
+  // 1 block prefix + dispatch (eager), 2 combine (eager), 4 / 8 the same in CUDA graphs
+  int pdl_front = 1;
+  bool capturing = false;  // enqueue_forward is recording a CUDA graph
+  bool pdl_prefix() const { return (pdl_front & (capturing ? 4 : 1)) != 0; }
+  bool pdl_combine() const { return (pdl_front & (capturing ? 8 : 2)) != 0; }
   bool swap_fuse = true;  // swap-AB: GEMM1 and GEMM2 in one launch (MOE_SWAP_FUSE=0: two)
   DevBuf<int> swap_ready; // its per-(segment, m-tile) GEMM1-done counters (+ CTA counter)
   int pred_distance = 1;  // predictor slot 0 scores layer + pred_distance

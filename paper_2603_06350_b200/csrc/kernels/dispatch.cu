@@ -26,6 +26,7 @@
 //                        slot order, bf16 out; one warp per token.
 #include <algorithm>
 #include <cstdint>
+#include <utility>
 
 #include "dispatch_plan.h"
 #include "sm100_ptx.cuh"
@@ -44,6 +45,8 @@ __global__ void __launch_bounds__(512)
 block_prefix_kernel(const int32_t* __restrict__ block_counts, int nblk, int E,
                     const DevPlan* __restrict__ plan, int32_t* __restrict__ block_pre,
                     const int32_t* __restrict__ local_counts, DevPlan* __restrict__ local_plan) {
+  griddep_wait();               // launched programmatically behind the gate
+  griddep_launch_dependents();  // dispatch CTAs may be scheduled now (they wait for this grid)
   const int e = blockIdx.x;
   if (e == E) {
     plan_local_body(local_counts, E, local_plan);
@@ -98,6 +101,7 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
   __shared__ int s_rrow[kMaxReplicas];
   __shared__ unsigned char s_rrem[kMaxReplicas];
   __shared__ __nv_bfloat16* s_tgt[kMaxTargets];
+  griddep_wait();  // launched programmatically behind the block prefix
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int t_base = b * 32;
@@ -220,6 +224,7 @@ __global__ void __launch_bounds__(256)
 combine_kernel(const __grid_constant__ RowTargets sources, int T, int d, const uint32_t* __restrict__ row_code,
                const float* __restrict__ wts, __nv_bfloat16* __restrict__ y) {
   __shared__ const __nv_bfloat16* s_src[kMaxTargets];
+  griddep_wait();  // launched programmatically behind K4
 #pragma unroll
   for (int i = 0; i < kMaxTargets; ++i)
     if (threadIdx.x == i) s_src[i] = static_cast<const __nv_bfloat16*>(sources.base[i]);
@@ -423,13 +428,31 @@ cudaError_t launch_small_copy(void* dst, const void* src, size_t bytes, cudaStre
 }
 
 // ------------------------------------------------------------- launchers
+// Programmatic dependent launch: the kernel may be scheduled while its
+// predecessor drains and waits in griddepcontrol.wait before touching its
+// inputs, which hides the launch gap between the small per-layer kernels.
+template <class... KArgs, class... Args>
+static cudaError_t launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, const DevPlan* plan,
-                                int32_t* block_pre, cudaStream_t s, const int32_t* local_counts) {
+                                int32_t* block_pre, cudaStream_t s, const int32_t* local_counts, bool pdl) {
   if (nblk <= 0 && !local_counts) return cudaSuccess;
   // with local_counts: + one CTA that builds the single-GPU plan into *plan
-  block_prefix_kernel<<<E + (local_counts ? 1 : 0), 512, 0, s>>>(block_counts, nblk, E, plan, block_pre,
-                                                                   local_counts, const_cast<DevPlan*>(plan));
-  return cudaGetLastError();
+  return launch_pdl(pdl, block_prefix_kernel, dim3(E + (local_counts ? 1 : 0)), dim3(512), s, block_counts, nblk, E, plan,
+                    block_pre, local_counts, const_cast<DevPlan*>(plan));
 }
 
 #define MOE_SWITCH_K(k, ...)                         \
@@ -445,7 +468,7 @@ cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, co
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
                             const int32_t* block_pre, const DevPlan* plan, const RowTargets& targets,
                             uint32_t* row_code, const PeerSignal& sig, cudaStream_t s, int32_t* perm_src,
-                            int32_t* row_owner) {
+                            int32_t* row_owner, bool pdl) {
   if (T <= 0) return cudaSuccess;
   if (d % 8) return cudaErrorInvalidValue;
   const int nblk = (T + 31) / 32;
@@ -453,13 +476,13 @@ cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, 
   // (ranking only when GEMM1 gathers the rows itself)
   const int split = perm_src ? 1 : std::max(1, std::min((2 * 148 + nblk - 1) / nblk, d / 8 / 16));
   const dim3 grid(nblk, split);
-  MOE_SWITCH_K(k, (dispatch_kernel<KK><<<grid, 128, 0, s>>>(x, T, d, E, ids, block_pre, plan, targets, row_code, sig,
-                                                            perm_src, row_owner)));
-  return cudaGetLastError();
+  MOE_SWITCH_K(k, return launch_pdl(pdl, dispatch_kernel<KK>, grid, dim3(128), s, x, T, d, E, ids, block_pre, plan,
+                                    targets, row_code, sig, perm_src, row_owner));
+  return cudaSuccess;
 }
 
 cudaError_t launch_combine(const RowTargets& sources, int T, int d, int k, const uint32_t* row_code,
-                           const float* wts, __nv_bfloat16* y, int num_sms, cudaStream_t s) {
+                           const float* wts, __nv_bfloat16* y, int num_sms, cudaStream_t s, bool pdl) {
   if (T <= 0) return cudaSuccess;
   if (d % 8) return cudaErrorInvalidValue;
   const int warps_needed = T;
@@ -467,8 +490,8 @@ cudaError_t launch_combine(const RowTargets& sources, int T, int d, int k, const
   ctas = ctas < num_sms * 8 ? ctas : num_sms * 8;
   const int split = std::max(1, std::min((2 * num_sms + ctas - 1) / ctas, d / 8 / 32));
   const dim3 grid(ctas, split);
-  MOE_SWITCH_K(k, (combine_kernel<KK><<<grid, 256, 0, s>>>(sources, T, d, row_code, wts, y)));
-  return cudaGetLastError();
+  MOE_SWITCH_K(k, return launch_pdl(pdl, combine_kernel<KK>, grid, dim3(256), s, sources, T, d, row_code, wts, y));
+  return cudaSuccess;
 }
 
 // Load every kernel of this file now (CUDA 12 loads kernels lazily on first

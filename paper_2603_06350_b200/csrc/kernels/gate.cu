@@ -285,6 +285,7 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_b
       for (int e = threadIdx.x; e < E; e += blockDim.x) block_counts[(size_t)blk * E + e] = 0;
     return;
   }
+  griddep_launch_dependents();  // the block-prefix launch may be scheduled (it waits for this grid)
   select_and_count<kLd, false, MLP>(red, hist, blk, 0, kBlockTokens, T, E, n_pred, k, ids, wts, counts, block_counts,
                                pred_counts, mlp);
   publish_counts(counts, mirror);
@@ -323,6 +324,7 @@ gate_finish_kernel(const float* __restrict__ partial, int splits, int T, int E, 
     red[(i / kCols) * kLd + i % kCols] = acc;
   }
   __syncthreads();
+  griddep_launch_dependents();
   select_and_count<kLd, true, MLP>(red, hist, blk, tok0, kFinishTokens, T, E, n_pred, k, ids, wts, counts, block_counts,
                               pred_counts, mlp);
   publish_counts(counts, mirror);
