@@ -842,9 +842,10 @@ struct SwapCfg {
   static constexpr uint32_t a = 0;  // token tiles
   static constexpr uint32_t b = a + STAGES * kStageTok;
   static constexpr uint32_t bars = b + STAGES * kStageWS;
-  static constexpr uint32_t n_bars = 2 * STAGES + 4;
+  static constexpr uint32_t n_bars = 2 * STAGES + 4 + 2 * kTileRing;
   static constexpr uint32_t tmem_slot = bars + n_bars * 8;
-  static constexpr uint32_t mt_prefix = tmem_slot + 16;  // int[kMaxSegs + 1]: m-tiles before segment s
+  static constexpr uint32_t tile_ring = tmem_slot + 16;              // int[kTileRing] (FUSED: claimed tiles)
+  static constexpr uint32_t mt_prefix = tile_ring + kTileRing * 4;   // int[kMaxSegs + 1]: m-tiles before segment s
   static constexpr uint32_t segs = mt_prefix + (kMaxSegs + 1) * 4 + 12;
   static constexpr uint32_t end = ((segs + 15) / 16) * 16 + kMaxSegs * 16;
   static constexpr uint32_t kSmemBytes = end + 1024;
@@ -917,10 +918,12 @@ __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence
 // FUSED: one launch runs GEMM1 then GEMM2 (pass 0 / pass 1).  A GEMM2 tile of
 // (segment, m-tile) waits, before loading its H rows, until every GEMM1 tile
 // of those rows has been stored: ready[(segment, m-tile)] counts epilogue
-// warps done (4 per GEMM1 n-tile).  Every CTA takes its tiles in increasing
-// order and the whole grid is resident (one CTA per SM), so the GEMM1 tiles a
-// wait depends on are always ahead of it; the last CTA to finish zeroes the
-// counters for the next launch.  GEMM2's weights start streaming while GEMM1's
+// warps done (4 per GEMM1 n-tile).  Tiles are CLAIMED in order from a global
+// counter (the producer hands each claim to the MMA and epilogue warps through
+// a shared-memory ring), so when a GEMM2 tile is claimed every GEMM1 tile has
+// already been claimed by a running CTA that finishes it without waiting on
+// anything: no deadlock even when the grid is not fully resident (other
+// kernels on the GPU).  The last CTA to finish zeroes the counters.  GEMM2's weights start streaming while GEMM1's
 // last wave drains, and there is no tail between the two GEMMs.
 template <bool FUSED, int SNv>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -938,8 +941,12 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
   uint64_t* empty = bars + STAGES_S;
   uint64_t* tfull = bars + 2 * STAGES_S;
   uint64_t* tempty = bars + 2 * STAGES_S + 2;
+  uint64_t* ring_full = bars + 2 * STAGES_S + 4;
+  uint64_t* ring_empty = ring_full + kTileRing;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::tmem_slot);
+  volatile int* ring = reinterpret_cast<volatile int*>(smem + C::tile_ring);
   int* mt_prefix = reinterpret_cast<int*>(smem + C::mt_prefix);
+  int* claim = ready + ready_n - 2;  // FUSED: next tile to claim
   int4* segs = reinterpret_cast<int4*>(smem + C::segs);
 
   const int warp = threadIdx.x >> 5;
@@ -956,6 +963,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
     }
     for (int s = 0; s < STAGES_S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    for (int r = 0; r < kTileRing; ++r) { mbar_init(&ring_full[r], 1); mbar_init(&ring_empty[r], 5); }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -984,7 +992,17 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
       uint32_t phase = 0;
       const uint64_t pol_b = policy_evict_last();
       bool first = true;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      int rslot = 0;
+      uint32_t rphase = 0;
+      for (int t = blockIdx.x;; t += gridDim.x) {
+        if (FUSED) {
+          t = atomicAdd(claim, 1);
+          mbar_wait(&ring_empty[rslot], rphase ^ 1);
+          ring[rslot] = t < total_tiles ? t : -1;
+          mbar_arrive(&ring_full[rslot]);
+          if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
+        }
+        if (t >= total_tiles) break;
         const SwapTile c = swap_tile<SN>(t, mt_prefix, nseg, mt_total, p0, p1);
         const SwapPass& p = c.pass ? p1 : p0;
         const CUtensorMap* tA = c.pass ? &tmA1 : &tmA0;
@@ -1042,7 +1060,18 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
       uint32_t acc_phase = 0;
       const uint32_t a_base = smem_u32(smem + C::a);
       const uint32_t b_base = smem_u32(smem + C::b);
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      int rslot = 0;
+      uint32_t rphase = 0;
+      for (int t = blockIdx.x;; t += gridDim.x) {
+        if (FUSED) {
+          mbar_wait(&ring_full[rslot], rphase);
+          t = ring[rslot];
+          mbar_arrive(&ring_empty[rslot]);
+          if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
+          if (t < 0) break;
+        } else if (t >= total_tiles) {
+          break;
+        }
         const SwapTile c = swap_tile<SN>(t, mt_prefix, nseg, mt_total, p0, p1);
         const int num_kb = (c.pass ? p1 : p0).num_kb;
         const int rows = min(SN, segs[c.seg].y - c.m * SN);
@@ -1075,7 +1104,19 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
     const int quarter = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    int rslot = 0;
+    uint32_t rphase = 0;
+    for (int t = blockIdx.x;; t += gridDim.x) {
+      if (FUSED) {
+        mbar_wait(&ring_full[rslot], rphase);
+        t = ring[rslot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ring_empty[rslot]);
+        if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
+        if (t < 0) break;
+      } else if (t >= total_tiles) {
+        break;
+      }
       const SwapTile c = swap_tile<SN>(t, mt_prefix, nseg, mt_total, p0, p1);
       const SwapPass& p = c.pass ? p1 : p0;
       const int4 sg = segs[c.seg];
@@ -1129,6 +1170,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
     __threadfence();
     if (atomicAdd(ready + ready_n - 1, 1) == static_cast<int>(gridDim.x) - 1) {
       for (int i = 0; i < mt_total; ++i) ready[i] = 0;
+      *claim = 0;
       ready[ready_n - 1] = 0;
       __threadfence();
     }
