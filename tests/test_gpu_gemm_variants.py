@@ -85,3 +85,48 @@ def test_swap_fused_repeated_forwards(cuda):
             m.sync()
             assert np.array_equal(oracle.bf16_to_f32(yd.cpu().numpy().view(np.uint16)), y1), (graphs, it)
         m.close()
+
+
+@pytest.mark.timeout(300)
+def test_swap_fused_concurrent_contexts(cuda):
+    """Two contexts on one GPU running fused swap-AB forwards at the same time
+    from two host threads (their persistent grids compete for the SMs): the
+    claimed-tile schedule must neither deadlock nor change a bit."""
+    import threading
+
+    import torch
+    E, k, d, ff, T = 64, 8, 1024, 1408, 256
+    x, wg, experts, y1 = _run(cuda, "1sm", E, k, d, ff, T, [1] * E)
+    layers = []
+    for _ in range(2):
+        m = MoELayer(1, E, k, d, ff, max_tokens=T)
+        m.set_gate(0, wg)
+        for e, w in enumerate(experts):
+            m.load_expert(0, e, *w)
+        layers.append(m)
+    xd = torch.from_numpy(x.view(np.int16)).to(cuda)
+    outs = [[None] * 30 for _ in layers]
+    errors = []
+
+    def worker(i):
+        try:
+            torch.cuda.set_device(cuda)
+            for it in range(30):
+                yd = torch.zeros((T, d), dtype=torch.int16, device=cuda)
+                layers[i].forward(0, xd, yd, MOE_PLAN_FIXED, it)
+                layers[i].sync()
+                outs[i][it] = yd.cpu().numpy()
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for i in range(2):
+        for it in range(30):
+            assert np.array_equal(oracle.bf16_to_f32(outs[i][it].view(np.uint16)), y1), (i, it)
+    for m in layers:
+        m.close()
