@@ -334,10 +334,12 @@ int gate_num_blocks(int T) { return (T + kBlockTokens - 1) / kBlockTokens; }
 
 // K-splits for a batch: enough CTAs to cover the SMs twice, d/(4 S) a
 // multiple of 32, at most 16.
+int g_gate_max_splits = 16;  // env MOE_GATE_MAX_SPLITS (A/B)
+
 int gate_splits(int T, int d) {
   const int nblk = gate_num_blocks(T);
   int s = 1;
-  while (s < 16 && nblk * s * 2 <= 2 * 148 && d % (kSlices * 32 * s * 2) == 0) s *= 2;
+  while (s < g_gate_max_splits && nblk * s * 2 <= 2 * 148 && d % (kSlices * 32 * s * 2) == 0) s *= 2;
   return s;
 }
 
