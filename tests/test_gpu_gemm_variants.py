@@ -130,3 +130,28 @@ def test_swap_fused_concurrent_contexts(cuda):
             assert np.array_equal(oracle.bf16_to_f32(outs[i][it].view(np.uint16)), y1), (i, it)
     for m in layers:
         m.close()
+
+
+@pytest.mark.parametrize("mask", ["0", "15"])
+@pytest.mark.parametrize("graphs", [False, True])
+def test_pdl_front_masks_bit_identical(cuda, mask, graphs):
+    """Programmatic launches of the block prefix / dispatch / combine
+    (MOE_PDL_FRONT) change only scheduling: outputs equal the default's."""
+    import torch
+    E, k, d, ff, T = 16, 2, 1024, 1408, 700
+    x, wg, experts, y_ref = _run(cuda, "1sm", E, k, d, ff, T, [1] * E)
+    os.environ["MOE_PDL_FRONT"] = mask
+    try:
+        m = MoELayer(1, E, k, d, ff, max_tokens=T, cuda_graphs=graphs)
+    finally:
+        del os.environ["MOE_PDL_FRONT"]
+    m.set_gate(0, wg)
+    for e, w in enumerate(experts):
+        m.load_expert(0, e, *w)
+    xd = torch.from_numpy(x.view(np.int16)).to(cuda)
+    for it in range(3):
+        yd = torch.zeros((T, d), dtype=torch.int16, device=cuda)
+        m.forward(0, xd, yd, MOE_PLAN_FIXED, it)
+        m.sync()
+        assert np.array_equal(oracle.bf16_to_f32(yd.cpu().numpy().view(np.uint16)), y_ref), (mask, graphs, it)
+    m.close()
