@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -84,7 +85,7 @@ cudaError_t launch_grouped_gemm_swap(int which, int sn, const CUtensorMap* tmA1,
                                      const int* nseg, int d, int ff, int b_rows1, int b_rows2, __nv_bfloat16* h,
                                      __nv_bfloat16* yp, int* ready, int ready_n, int num_ctas, cudaStream_t stream,
                                      bool pdl);
-extern int g_gate_max_splits;  // K1 split-K bound (env MOE_GATE_MAX_SPLITS)
+extern std::atomic<int> g_gate_max_splits;  // K1 split-K bound (env MOE_GATE_MAX_SPLITS)
 cudaError_t preload_gate_kernels();
 cudaError_t preload_dispatch_kernels();
 cudaError_t preload_gemm_kernels();

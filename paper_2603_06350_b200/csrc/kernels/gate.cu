@@ -34,6 +34,7 @@
 // multiple of 2^-16 below 2^6, so any fp32 summation order — the MMA's
 // included — yields the exact logit, and ids match the CPU oracle bit for bit.
 #include <cfloat>
+#include <atomic>
 #include <cstdint>
 
 #include "sm100_ptx.cuh"
@@ -334,12 +335,13 @@ int gate_num_blocks(int T) { return (T + kBlockTokens - 1) / kBlockTokens; }
 
 // K-splits for a batch: enough CTAs to cover the SMs twice, d/(4 S) a
 // multiple of 32, at most 16.
-int g_gate_max_splits = 16;  // env MOE_GATE_MAX_SPLITS (A/B)
+std::atomic<int> g_gate_max_splits{16};  // env MOE_GATE_MAX_SPLITS (A/B); set at ctx creation
 
 int gate_splits(int T, int d) {
   const int nblk = gate_num_blocks(T);
   int s = 1;
-  while (s < g_gate_max_splits && nblk * s * 2 <= 2 * 148 && d % (kSlices * 32 * s * 2) == 0) s *= 2;
+  const int max_s = g_gate_max_splits.load(std::memory_order_relaxed);
+  while (s < max_s && nblk * s * 2 <= 2 * 148 && d % (kSlices * 32 * s * 2) == 0) s *= 2;
   return s;
 }
 
