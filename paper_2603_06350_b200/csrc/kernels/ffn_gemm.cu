@@ -930,7 +930,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
                          const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                          const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, const SwapPass p0,
-                         const SwapPass p1, int* __restrict__ ready, int ready_n) {
+                         const SwapPass p1, int* __restrict__ ready, int ready_n, int wpol) {
   using C = SwapCfg<SNv>;
   constexpr int SN = C::SN, STAGES_S = C::STAGES;
   constexpr uint32_t kStageTokS = C::kStageTok;
@@ -990,7 +990,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      const uint64_t pol_b = policy_evict_last();
+      const uint64_t pol_b = wpol == 1 ? policy_evict_first() : (wpol == 2 ? policy_evict_normal() : policy_evict_last());
       bool first = true;
       int rslot = 0;
       uint32_t rphase = 0;
@@ -1181,6 +1181,8 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
   }
 }
 
+int g_swap_wpol = 1;  // L2 policy of the swap kernel's weight stream: 1 evict_first (default), 0 evict_last, 2 normal (env MOE_SWAP_WPOL)
+
 template <int SNv>
 cudaError_t launch_swap(int which, const CUtensorMap* tmA1, const CUtensorMap* tmB1, const CUtensorMap* tmA2,
                         const CUtensorMap* tmB2, const GemmSeg* segs, const int* nseg, const SwapPass& g1,
@@ -1206,12 +1208,12 @@ cudaError_t launch_swap(int which, const CUtensorMap* tmA1, const CUtensorMap* t
   cfg.numAttrs = 1;
   if (which == 2)
     return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<true, SNv>, *tmA1, *tmB1, *tmA2, *tmB2, segs, nseg, g1,
-                              g2, ready, ready_n);
+                              g2, ready, ready_n, g_swap_wpol);
   if (which == 0)
     return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<false, SNv>, *tmA1, *tmB1, *tmA1, *tmB1, segs, nseg,
-                              g1, g1, ready, ready_n);
+                              g1, g1, ready, ready_n, g_swap_wpol);
   return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<false, SNv>, *tmA2, *tmB2, *tmA2, *tmB2, segs, nseg, g2,
-                            g2, ready, ready_n);
+                            g2, ready, ready_n, g_swap_wpol);
 }
 
 // which: 0 = GEMM1 alone, 1 = GEMM2 alone, 2 = GEMM1 then GEMM2 in one launch;
