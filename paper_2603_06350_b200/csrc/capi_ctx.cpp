@@ -278,7 +278,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_GEMM_SWAP128_ROWS")) c->swap128_rows = std::atoi(v);
     if (const char* v = std::getenv("MOE_SWAP_FUSE")) c->swap_fuse = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_PDL_FRONT")) c->pdl_front = std::atoi(v);
-    if (const char* v = std::getenv("MOE_SWAP_WPOL")) g_swap_wpol = std::atoi(v);
+    if (const char* v = std::getenv("MOE_SWAP_WPOL")) g_swap_wpol.store(std::atoi(v));
     if (const char* v = std::getenv("MOE_GATE_MAX_SPLITS")) g_gate_max_splits.store(std::max(1, std::atoi(v)));
     c->registry = moeless::ReplicaRegistry(std::max(0, D.keep_alive_iters));
     c->layers.resize(D.num_layers);

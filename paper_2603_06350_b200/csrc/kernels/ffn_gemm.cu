@@ -27,6 +27,7 @@
 // Tile order: segments in (expert, ordinal) order; inside a segment, groups of
 // up to 16 m-tiles sweep all n-tiles so concurrently running CTAs share A
 // rows and B columns through L2.
+#include <atomic>
 #include <cstdint>
 #include <cuda.h>
 
@@ -1181,7 +1182,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
   }
 }
 
-int g_swap_wpol = 1;  // L2 policy of the swap kernel's weight stream: 1 evict_first (default), 0 evict_last, 2 normal (env MOE_SWAP_WPOL)
+std::atomic<int> g_swap_wpol{1};  // L2 policy of the swap kernel's weight stream: 1 evict_first (default), 0 evict_last, 2 normal (env MOE_SWAP_WPOL)
 
 template <int SNv>
 cudaError_t launch_swap(int which, const CUtensorMap* tmA1, const CUtensorMap* tmB1, const CUtensorMap* tmA2,
@@ -1208,12 +1209,12 @@ cudaError_t launch_swap(int which, const CUtensorMap* tmA1, const CUtensorMap* t
   cfg.numAttrs = 1;
   if (which == 2)
     return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<true, SNv>, *tmA1, *tmB1, *tmA2, *tmB2, segs, nseg, g1,
-                              g2, ready, ready_n, g_swap_wpol);
+                              g2, ready, ready_n, g_swap_wpol.load(std::memory_order_relaxed));
   if (which == 0)
     return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<false, SNv>, *tmA1, *tmB1, *tmA1, *tmB1, segs, nseg,
-                              g1, g1, ready, ready_n, g_swap_wpol);
+                              g1, g1, ready, ready_n, g_swap_wpol.load(std::memory_order_relaxed));
   return cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<false, SNv>, *tmA2, *tmB2, *tmA2, *tmB2, segs, nseg, g2,
-                            g2, ready, ready_n, g_swap_wpol);
+                            g2, ready, ready_n, g_swap_wpol.load(std::memory_order_relaxed));
 }
 
 // which: 0 = GEMM1 alone, 1 = GEMM2 alone, 2 = GEMM1 then GEMM2 in one launch;
