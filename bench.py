@@ -50,6 +50,9 @@ OTHER_WORKLOADS = {
     "cfg5": (dict(E=64, k=8, d=2048, ff=1408, T=256, s=2.0, extra_replicas=16, seed=1),
              "cfg5: fine-grained decode (E=64, top-8, d_model=2048, d_ff=1408), 256 tokens per GPU, heavy skew "
              "Zipf s=2.0"),
+    "cfg5s12": (dict(E=64, k=8, d=2048, ff=1408, T=256, s=1.2, extra_replicas=16, seed=1),
+                "cfg5 at the milder skew: fine-grained decode (E=64, top-8, d_model=2048, d_ff=1408), 256 tokens "
+                "per GPU, Zipf s=1.2"),
 }
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
@@ -70,7 +73,7 @@ def parse():
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
                     help="N>1 token exchange: peer memory over NVLink (dispatch/combine read and write the "
                          "owners' buffers) or NCCL grouped send/recv")
-    ap.add_argument("--workload", choices=["cfg2", "cfg1", "cfg3", "cfg5"], default="cfg2",
+    ap.add_argument("--workload", choices=["cfg2", "cfg1", "cfg3", "cfg5", "cfg5s12"], default="cfg2",
                     help="layer shape (cfg2 = the headline Mixtral layer)")
     ap.add_argument("--residency", choices=["all", "placed"], default="all",
                     help="N>1 expert weights: every expert resident on every GPU, or only home experts + "
