@@ -64,8 +64,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--pool", type=int, default=4, help="distinct token batches cycled per rank")
-    ap.add_argument("--cpu-sample-tokens", type=int, default=256,
-                    help="tokens of the workload per reference-arm step (~0.5 s of host work each)")
+    ap.add_argument("--cpu-sample-tokens", type=int, default=2048,
+                    help="tokens of the step's batch the reference arm runs per step (~2-3 s of host work)")
+    ap.add_argument("--cpu-full-layer", type=int, default=1,
+                    help="reference arm: also time one full-batch layer after the steps (0: skip)")
     ap.add_argument("--cpu-baseline-tokens", type=int, default=1024,
                     help="tokens per sample of our arm's cpu_baseline leg (two samples)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -179,109 +181,146 @@ def nearest_rank(values, q):
     return percentile(values, q)
 
 
-# --------------------------------------------------------------- reference arm
-def cpu_reference_step(sample_tokens, it, cache):
-    """One bounded step of the reference CPU path for this metric: the
-    reference's own planner path (oracle/_ref: route_tokens -> predict ->
-    scale_experts -> place_experts -> layer_forward_time, simulator.cpp:116-201)
-    plus the oracle port of the data path the reference only models
-    analytically (gate -> dispatch -> SwiGLU FFN -> combine, all host threads),
-    on `sample_tokens` tokens of the cfg2 workload."""
-    import ctypes as C
-    import numpy as np
+def config_dict(G, c):
+    """The `config` of both arms' lines (identical for the same workload and N)."""
+    E, k, d, ff, T = c["E"], c["k"], c["d"], c["ff"], c["T"]
+    return {"workload": WORKLOAD, "global_batch": G * T, "tokens_per_gpu": T, "seq_len": None,
+            "parallelism": f"ep{G}", "experts": E, "top_k": k, "d_model": d, "d_ff": ff,
+            "l2": f"inputs larger than L2 ({E * 3 * d * ff * 2 / 1e9:.2f} GB of expert weights + "
+                  f"{T * d * 2 / 1e6:.0f} MB of tokens per step vs 126 MB of L2)",
+            "planner": "MOE_PLAN_SYNC (scale_experts + place_experts on actual loads)"}
 
-    import oracle
-    from paper_2603_06350_b200 import workload as wl
-    c = CFG
-    if "experts" not in cache:
-        cache["experts"] = [wl.expert_weights(c["d"], c["ff"], c["seed"], 0, e) for e in range(c["E"])]
-    x = wl.tokens(sample_tokens, c["d"], c["E"], c["seed"], 1000 + it % 4)
-    wg = wl.gate_weights(c["E"], c["d"], c["s"], c["seed"], 0, it)
-    ref = oracle.ref()
-    t0 = time.perf_counter()
-    loads = np.zeros(c["E"], np.int64)
-    mem = 3.0 * c["d"] * c["ff"] * 2 / 1e6
-    if ref is not None:
-        ref.ref_cpu_layer_path(sample_tokens, c["E"], c["k"], c["s"], c["seed"], 1, mem,
-                               c["extra_replicas"] * mem, 1, oracle.P(loads))
-    y, ids, w, counts = oracle.layer_forward(x, wg, cache["experts"], [1] * c["E"], c["k"])
-    return time.perf_counter() - t0, ("reference" if ref is not None else "port")
+
+def host_cpu():
+    """nproc, the threads the CPU path uses, and the CPU model."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model,
+            "threads": int(os.environ.get("OMP_NUM_THREADS", "0")) or os.cpu_count()}
+
+
+# ------------------------------------------------------------ CPU reference path
+# Everything below runs the oracle (oracle/_ref = the UNMODIFIED reference's
+# planner path, oracle/*.c|py = the restated data path) and never imports the
+# product package: the reference arm's process maps only oracle libraries.
+def cpu_layer(c, experts=None):
+    from oracle import workload as owl
+    from oracle.cpu_path import CpuLayer
+    E, k, d, ff = c["E"], c["k"], c["d"], c["ff"]
+    if experts is None:
+        experts = [owl.expert_weights(d, ff, c["seed"], 0, e) for e in range(E)]
+    return CpuLayer(E, k, d, ff, experts, s=c["s"], seed=c["seed"], extra_replicas=c["extra_replicas"])
+
+
+def cpu_sample(c, layer, tokens, it, rank=0):
+    """One step of the CPU path on `tokens` tokens of this step's batch (the
+    keyed generator makes them a prefix of the full batch) under its gate."""
+    from oracle import workload as owl
+    x = owl.tokens(tokens, c["d"], c["E"], c["seed"], rank * 1000 + it % 4)
+    wg = owl.gate_weights(c["E"], c["d"], c["s"], c["seed"], 0, it)
+    _, dt = layer.forward(x, wg)
+    return dt
+
+
+def run_cpu_baseline(c, sample_tokens, experts=None, steps=2):
+    layer = cpu_layer(c, experts)
+    cpu_sample(c, layer, 64, 0)  # page in
+    times = [cpu_sample(c, layer, sample_tokens, i) for i in range(steps)]
+    hc = host_cpu()
+    return {"value": sample_tokens / statistics.median(times), "unit": "tokens/s", "cores": hc["threads"],
+            "kind": "port", "cpu": hc,
+            "sample": (f"{sample_tokens} tokens of the {c['T']}-token layer per sample, median of {steps}: the "
+                       f"reference's per-layer planner path (oracle/_ref) + the oracle data path (gate, stable "
+                       f"dispatch, fp32 SwiGLU FFN on OpenBLAS sgemm, combine) on {hc['threads']} threads "
+                       f"({hc['model']})"),
+            "ms_per_sample": 1e3 * statistics.median(times)}
 
 
 def cpu_cfg1_full_layer():
     """The reference's own CPU-runnable configuration (BASELINE.json configs[0],
-    cfg1: E8 k2 d1024 ff3584, 2048 tokens, fixed placement) as ONE full layer on
-    the host: the reference planner path (oracle/_ref) + the oracle port of the
-    data path on all host threads.  Compare with bench_configs.py cfg1."""
-    import numpy as np
-
-    import oracle
-    from paper_2603_06350_b200 import workload as wl
-    c = dict(wl.CONFIGS["cfg1"])
-    E, k, d, ff, T = c["E"], c["k"], c["d"], c["ff"], c["T"]
-    experts = [wl.expert_weights(d, ff, 1, 0, e) for e in range(E)]
-    x = wl.tokens(T, d, E, 1, 0)
-    wg = wl.gate_weights(E, d, c["s"], 1, 0, 0)
-    ref = oracle.ref()
-    mem = 3.0 * d * ff * 2 / 1e6
-    oracle.layer_forward(x[:16], wg, experts, [1] * E, k)  # page in
-    t0 = time.perf_counter()
-    loads = np.zeros(E, np.int64)
-    if ref is not None:
-        ref.ref_cpu_layer_path(T, E, k, c["s"], 1, 1, mem, mem * E, 1, oracle.P(loads))
-    oracle.layer_forward(x, wg, experts, [1] * E, k)
-    dt = time.perf_counter() - t0
-    return {"value": T / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port", "ms_per_layer": 1e3 * dt,
+    cfg1: E8 k2 d1024 ff3584, 2048 tokens) as ONE full layer on the host."""
+    c = dict(OTHER_WORKLOADS["cfg1"][0])
+    layer = cpu_layer(c)
+    cpu_sample(c, layer, 64, 0)
+    dt = cpu_sample(c, layer, c["T"], 0)
+    hc = host_cpu()
+    return {"value": c["T"] / dt, "unit": "tokens/s", "cores": hc["threads"], "kind": "port", "ms_per_layer": 1e3 * dt,
             "sample": "cfg1 in full: one 2048-token layer (E8 k2 d1024 ff3584), reference planner path + oracle "
                       "data path"}
 
 
-def run_cpu_baseline(sample_tokens, steps=2):
-    cache = {}
-    cpu_reference_step(8, 0, cache)  # warm caches / page in weights
-    times = []
-    kind = "port"
-    for i in range(steps):
-        dt, _ = cpu_reference_step(sample_tokens, i, cache)
-        times.append(dt)
-    value = sample_tokens / statistics.median(times)
-    return {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": kind,
-            "sample": (f"{sample_tokens} tokens of cfg2 per step (of 16384): reference planner path "
-                       f"(oracle/_ref route_tokens/predict/scale/place/forward-model) + oracle port of "
-                       f"gate/dispatch/SwiGLU FFN/combine on {os.cpu_count()} OpenMP threads; median of {steps}"),
-            "ms_per_sample": 1e3 * statistics.median(times)}
-
-
 def run_reference(args):
+    """--impl reference: the CPU path of this metric on the host's cores, rank 0
+    only.  Each step runs a bounded sample of the step's batch (default 2048 of
+    16384 tokens: every token's routing and FFN rows are independent, so the
+    cost is linear in tokens); one full 16384-token layer is also timed once
+    after the steps and reported beside the per-step rate."""
     ws, rank, local = dist_env()
     if rank != 0:
         return 0
-    cache = {}
-    cpu_reference_step(8, 0, cache)
+    import oracle
+    c = CFG
+    G = max(ws, 1)
+    sample = min(args.cpu_sample_tokens, c["T"])
+    layer = cpu_layer(c)
+    cpu_sample(c, layer, 64, 0)  # page in the resident fp32 weights
     for i in range(args.warmup):
-        cpu_reference_step(args.cpu_sample_tokens, i, cache)
-    times = []
-    for i in range(args.steps):
-        dt, kind = cpu_reference_step(args.cpu_sample_tokens, args.warmup + i, cache)
-        times.append(dt)
+        cpu_sample(c, layer, sample, i)
+    times = [cpu_sample(c, layer, sample, args.warmup + i) for i in range(args.steps)]
+    full_s = cpu_sample(c, layer, c["T"], args.warmup + args.steps) if args.cpu_full_layer else None
     total = sum(times)
-    value = args.cpu_sample_tokens * args.steps / total
+    value = sample * args.steps / total
+    ref = oracle.ref()
+    pct = (lambda v, q: ref.ref_percentile((oracle.C.c_double * len(v))(*v), len(v), q)) if ref else None
+    ms = [1e3 * t * c["T"] / sample for t in times]  # per-layer latency at the full batch (linear in tokens)
+    hc = host_cpu()
+    desc = (f"{sample} of the {c['T']} tokens of each step's batch: the UNMODIFIED reference's per-layer "
+            f"planner path (oracle/_ref: route_tokens -> predict -> scale_experts -> place_experts -> "
+            f"layer_forward_time -> update_registry) + the oracle data path the reference only models "
+            f"(gate, stable integer dispatch, fp32 SwiGLU FFN on OpenBLAS sgemm, weighted combine), "
+            f"{hc['threads']} threads on {hc['nproc']} x {hc['model']}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 0,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": WORKLOAD, "sample_tokens_per_step": args.cpu_sample_tokens,
-                   "parallelism": f"{os.cpu_count()} host threads"},
-        "p50_ms": 1e3 * statistics.median(times), "p99_ms": 1e3 * nearest_rank(times, 0.99),
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-                         "sample": f"{args.cpu_sample_tokens} tokens of cfg2 per step; reference planner "
-                                   "path (oracle/_ref) + oracle port of the data path (the reference has "
-                                   "no FFN/dispatch code, only the analytic model)"},
+        "data": "synthetic (the same keyed inputs as the GPU arm, from the oracle's generator)",
+        "config": config_dict(G, c),
+        "p50_ms": statistics.median(ms), "p99_ms": pct(ms, 0.99) if pct else max(ms),
+        "latency_note": "per-layer latency scaled from the sample to the full batch",
+        "sample": {"tokens_per_step": sample, "tokens_per_layer": c["T"],
+                   "full_layer_s": full_s, "full_layer_tokens_per_s": c["T"] / full_s if full_s else None,
+                   "sample_tokens_per_s": value,
+                   "extrapolation": "tokens/s of the sample == tokens/s of the layer when the cost is linear "
+                                    "in tokens; full_layer_tokens_per_s is the measured check"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": hc["threads"], "kind": "reference",
+                         "cpu": hc, "sample": desc},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "repo_libs_loaded": repo_libs_loaded(),
     }
+    assert not any("libmoe_b200" in p for p in line["repo_libs_loaded"]), "reference arm loaded the product"
     print(json.dumps(line), flush=True)
     return 0
+
+
+def repo_libs_loaded():
+    """Shared objects under this repo mapped into the process (/proc/self/maps)."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for line in f:
+                path = line.split()[-1] if len(line.split()) >= 6 else ""
+                if path.startswith(ROOT) and ".so" in path:
+                    out.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(out)
 
 
 # ---------------------------------------------------------------- our arm
@@ -513,11 +552,7 @@ def run_ours(args):
             "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (keyed Zipf-skewed gate inputs, random-init expert weights)",
-            "config": {"workload": WORKLOAD, "global_batch": G * T, "tokens_per_gpu": T, "seq_len": None,
-                       "parallelism": f"ep{G}", "experts": E, "top_k": k, "d_model": d, "d_ff": ff,
-                       "l2": f"inputs larger than L2 ({E * 3 * d * ff * 2 / 1e9:.2f} GB of expert weights + "
-                             f"{T * d * 2 / 1e6:.0f} MB of tokens per step vs 126 MB of L2)",
-                       "planner": "MOE_PLAN_SYNC (scale_experts + place_experts on actual loads)"},
+            "config": config_dict(G, c),
             "exchange": (exchange_note or ("peer memory (P2P)" if p2p else "NCCL send/recv")) if G > 1
                         else "none (G=1)",
             "p50_ms": p50, "p99_ms": p99,
@@ -566,7 +601,8 @@ def run_ours(args):
                                   "H2D/D2H of neighbouring steps overlap the layer), wall clock over all steps "
                                   "until the last result is in host memory"}
         if G == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = run_cpu_baseline(args.cpu_baseline_tokens)
+            line["cpu_baseline"] = run_cpu_baseline(c, args.cpu_baseline_tokens,
+                                                    [wl.expert_weights(d, ff, c["seed"], 0, e) for e in range(E)])
             line["cpu_baseline_cfg1_full"] = cpu_cfg1_full_layer()
         print(json.dumps(line), flush=True)
     m.close()

@@ -215,15 +215,24 @@ int moe_set_predictor_weights(moe_ctx* ctx, int layer, int slot, const uint16_t*
    out[e] = sum_j W2[e][j] hidden[j] (W2 [E, E] fp32, accumulated in j order
    with fused multiply-adds), histogram of top-k(out).  w1 NULL keeps the
    slot's current rows; w2 NULL returns the slot to the linear predictor.
-   Replaces the reference's LayerAwarePredictor::predict scoring
-   (predictor.cpp:38-62) with a learned model, as moe_set_predictor_weights
-   does with a linear one. */
+   The paper's predictor is a gate-shaped linear on layer-l hidden states
+   (PAPER.md:469,696,1069); this slot type adds one hidden layer.  It serves
+   the reference's predict() interface (predictor.hpp:40-43, dispatch at
+   predictor.cpp:146-166), whose stand-ins predict_noisy / predict_historical
+   (predictor.cpp:54-142) only perturb the answer key. */
 int moe_set_predictor_mlp(moe_ctx* ctx, int layer, int slot, const uint16_t* w1, const float* w2);
 
 /* ------------------------------------------------------------- placement */
 /* replica_counts[E] >= 1; replica_gpu[sum R] flattened (expert, ordinal).   */
 int moe_set_placement(moe_ctx* ctx, int layer, const int32_t* replica_counts,
                       const int32_t* replica_gpu);
+
+/* The placement in force for `layer` (after the last forward's planning):
+   replica_counts[E] and replica_gpu[*n_replicas] flattened (expert, ordinal),
+   i.e. ScalingPlan.replica_counts / Placement.gpu_for (types.hpp:59,
+   placer.hpp:17).  replica_gpu may be NULL to query the size. */
+int moe_get_placement(moe_ctx* ctx, int layer, int32_t* replica_counts, int32_t* replica_gpu, int max_replicas,
+                      int* n_replicas);
 
 /* ---------------------------------------------------------- device kernels */
 /* K1 (+K2): x_dev [T, d] -> ids [T, k], weights [T, k], counts [E] (zeroed
@@ -238,6 +247,26 @@ int moe_predict_loads(moe_ctx* ctx, int layer, const uint16_t* x_dev, int tokens
 /* Full layer: y_dev [T, d] = sum_j w_tj FFN_{e_tj}(x_t).  stats may be NULL. */
 int moe_layer_forward(moe_ctx* ctx, int layer, const uint16_t* x_dev, int tokens, uint16_t* y_dev,
                       int plan_mode, long iteration, moe_layer_stats* stats, void* stream);
+
+/* The layer on caller-given routing (the SURVEY §8 c3 bridge): ids_dev [T, k]
+   int32 expert ids and weights_dev [T, k] fp32 (NULL: 1/k each) replace K1, so
+   routing produced outside the gate — e.g. the reference's route_tokens stream
+   (proj/src/workload.cpp:188-230) replayed per token — drives K3 -> K4 -> K5
+   unchanged and the load counts the planner sees are exactly the histogram of
+   those ids.  A token must name k distinct experts in [0, E): otherwise
+   MOE_EINVAL (returned by this call when stats != NULL, else by the next call
+   that synchronises the context), that token's output being 0.  No predictor
+   runs on this path. */
+int moe_layer_forward_ids(moe_ctx* ctx, int layer, const uint16_t* x_dev, const int32_t* ids_dev,
+                          const float* weights_dev, int tokens, uint16_t* y_dev, int plan_mode, long iteration,
+                          moe_layer_stats* stats, void* stream);
+
+/* The dispatch plan the device used for the most recent forward (synchronises
+   the context): n_e[E] = assignments of expert e over all ranks; segs[3 * i ..]
+   = (first row, rows, weight slot) of GEMM segment i on this rank (one per
+   replica here with rows > 0; co-located replicas of an expert form one
+   segment on a single GPU); *nseg segments; *rows_local their total. */
+int moe_last_plan(moe_ctx* ctx, int32_t* n_e, int32_t* segs, int max_segs, int* nseg, int64_t* rows_local);
 
 /* Same with HOST buffers: H2D of x and D2H of y happen inside (the e2e path). */
 int moe_layer_forward_host(moe_ctx* ctx, int layer, const uint16_t* x_host, int tokens,

@@ -423,6 +423,34 @@ class MoELayer:
                                     iteration, C.byref(st) if st is not None else None, stream or None))
         return st
 
+    def forward_ids(self, layer: int, x, ids, y, weights=None, plan_mode: int = MOE_PLAN_FIXED,
+                    iteration: int = 0, stats: bool = False, stream: int = 0) -> Optional[MoeLayerStats]:
+        """The layer on caller-given routing: ids [T, k] int32 (and optional
+        weights [T, k] fp32) device tensors replace the gate (K1)."""
+        st = MoeLayerStats() if stats else None
+        check(lib.moe_layer_forward_ids(self._h, layer, x.data_ptr(), ids.data_ptr(),
+                                        weights.data_ptr() if weights is not None else None, x.shape[0],
+                                        y.data_ptr(), plan_mode, iteration,
+                                        C.byref(st) if st is not None else None, stream or None))
+        return st
+
+    def last_plan(self):
+        """(n_e [E], segments [nseg, 3] = (first row, rows, weight slot), rows_local)
+        of the dispatch plan the device used for the most recent forward."""
+        n_e = np.zeros(self.E, np.int32)
+        segs = np.zeros((512, 3), np.int32)
+        n, rows = C.c_int(), C.c_int64()
+        check(lib.moe_last_plan(self._h, _p(n_e), _p(segs), 512, C.byref(n), C.byref(rows)))
+        return n_e, segs[:n.value].copy(), rows.value
+
+    def placement(self, layer: int) -> Tuple[np.ndarray, np.ndarray]:
+        """(replica_counts [E], replica_gpu [sum R]) in force for `layer`."""
+        rc = np.zeros(self.E, np.int32)
+        rg = np.zeros(512, np.int32)
+        n = C.c_int()
+        check(lib.moe_get_placement(self._h, layer, _p(rc), _p(rg), 512, C.byref(n)))
+        return rc, rg[:n.value].copy()
+
     def forward_host(self, layer: int, x_host: np.ndarray, y_host: np.ndarray,
                      plan_mode: int = MOE_PLAN_FIXED, iteration: int = 0, stats: bool = False):
         """HOST buffers in and out (H2D + forward + D2H): the e2e call."""

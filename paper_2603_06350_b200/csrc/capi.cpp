@@ -30,8 +30,13 @@ thread_local std::string g_last_error;
 // `stride` ints) into mapped host memory for the host planner (single GPU)
 void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, int32_t* pred_counts,
                 bool mirror = false, int stride = 0) {
-  require(L.has_gate, "gate weights not set for layer");
   CU_CHECK(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * c->count_stride, s));
+  if (c->ext_route) {  // caller-given routing (moe_layer_forward_ids) instead of K1
+    CU_CHECK(launch_route_ids(c->ext_ids, c->ext_wts, T, c->E, c->k, c->ids.p, c->wts.p, c->counts.p,
+                              c->block_counts.p, c->ids_err, s));
+    return;
+  }
+  require(L.has_gate, "gate weights not set for layer");
   if (c->fp32) {
     CU_CHECK(launch_gate_f32(reinterpret_cast<const float*>(x), T, c->d, reinterpret_cast<const float*>(L.wg.p), c->E,
                              c->k, c->ids.p, c->wts.p, c->counts.p, c->block_counts.p, s));
@@ -287,6 +292,15 @@ void stage_combine(moe_ctx* c, uint16_t* y, int T, cudaStream_t s) {
                           c->num_sms, s, c->pdl_combine()));
 }
 
+// invalid caller ids (moe_layer_forward_ids), flagged by route_ids_kernel
+void check_ids(moe_ctx* c) {
+  if (!c->ids_err || *reinterpret_cast<volatile int*>(c->ids_err) == 0) return;
+  const int t = *c->ids_err - 1;
+  *c->ids_err = 0;
+  throw std::invalid_argument("routing ids of token " + std::to_string(t) +
+                              " are invalid (expert out of range or chosen twice)");
+}
+
 void check_p2p(moe_ctx* c) {
   if (!c->p2p || !c->p2p_err || *reinterpret_cast<volatile int*>(c->p2p_err) == 0) return;
   const int v = *c->p2p_err - 1;
@@ -304,6 +318,7 @@ void flush_pending_plan(moe_ctx* c) {
   c->pending.active = false;
   CU_CHECK(cudaEventSynchronize(c->ev_counts));
   check_p2p(c);
+  check_ids(c);
   stage_plan(c, c->pending.layer, c->pending.mode, c->pending.iteration, c->h_counts, c->pending.stride);
   if (c->pending.gemm_slot >= 0) c->gemm_rows[c->pending.gemm_slot] = c->plan.rows_local;
 }
@@ -344,7 +359,8 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
     c->tmX_T = T;
   }
   mark(0);
-  const bool mirrored = c->G == 1 && !c->fp32 && T > 0;  // the gate publishes the histograms itself
+  // the gate publishes the histograms itself (not the caller-ids kernel)
+  const bool mirrored = c->G == 1 && !c->fp32 && T > 0 && !c->ext_route;
   stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr, mirrored, stride);
   if (c->G > 1 && c->p2p) {
     // every rank reads every histogram from its owner's slab
@@ -376,6 +392,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
     mark(1);
     CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram
     check_p2p(c);
+    check_ids(c);
     stage_plan(c, layer, plan_mode, iteration, c->h_counts, stride);
     mark(2);
     stage_dispatch(c, x, T, s);  // uploads the plan; P2P rows land in their owners' buffers
@@ -434,12 +451,12 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   flush_pending_plan(c);  // the previous call's deferred planner work
   // the fused predictor (K2) runs when the layer has predictor weights: its
   // histograms follow the gate's in the same counts buffer
-  const bool with_pred = c->n_pred > 0 && L.has_pred_weights;
+  const bool with_pred = c->n_pred > 0 && L.has_pred_weights && !c->ext_route;
   const int stride = with_pred ? c->count_stride : c->E;
   const bool ahead = c->G > 1 && c->p2p && !c->fp32 &&
                      (plan_mode == MOE_PLAN_FIXED || (plan_mode == MOE_PLAN_PREDICTED && L.plan_for == iteration));
   if (ahead) ensure_placement(c, layer);
-  if (c->use_graphs && !timed && (c->G == 1 || ahead) && !c->placed) {
+  if (c->use_graphs && !timed && (c->G == 1 || ahead) && !c->placed && !c->ext_route) {
     // Replay the layer's whole device sequence (8-14 kernels) as one CUDA
     // graph: captured once per (layer, tokens, buffers), then launched with a
     // single call — the launch-bound decode regime pays one launch, not ten.
@@ -478,6 +495,7 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   if (timed) {
     CU_CHECK(cudaEventSynchronize(ev.ev[8]));
     flush_pending_plan(c);
+    check_ids(c);
     st->gate_ms = ev.ms(0, 1);
     st->plan_ms = ev.ms(1, 2);
     st->dispatch_ms = ev.ms(2, 3);
@@ -561,6 +579,44 @@ int moe_layer_forward(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t*
     // a rank with no tokens still takes part in the exchange (x, y may be null)
     require(c && (T == 0 || (x && y)), "null argument");
     forward_device(c, layer, x, T, y, plan_mode, iteration, stats, pick(c, stream));
+  });
+}
+
+int moe_layer_forward_ids(moe_ctx* c, int layer, const uint16_t* x, const int32_t* ids, const float* weights,
+                          int T, uint16_t* y, int plan_mode, long iteration, moe_layer_stats* stats, void* stream) {
+  return guarded([&] {
+    require(c && (T == 0 || (x && y && ids)), "null argument");
+    require(c->k <= c->E, "top_k exceeds num_experts");
+    struct Restore {
+      moe_ctx* c;
+      ~Restore() { c->ext_route = false, c->ext_ids = nullptr, c->ext_wts = nullptr; }
+    } restore{c};
+    c->ext_route = true;
+    c->ext_ids = ids;
+    c->ext_wts = weights;
+    forward_device(c, layer, x, T, y, plan_mode, iteration, stats, pick(c, stream));
+  });
+}
+
+int moe_last_plan(moe_ctx* c, int32_t* n_e, int32_t* segs, int max_segs, int* nseg, int64_t* rows_local) {
+  return guarded([&] {
+    require(c && nseg, "null argument");
+    CU_CHECK(cudaSetDevice(c->desc.device));
+    CU_CHECK(cudaStreamSynchronize(c->stream));
+    flush_pending_plan(c);
+    DevPlan p;
+    CU_CHECK(cudaMemcpy(&p, c->dplan.p, sizeof(DevPlan), cudaMemcpyDeviceToHost));
+    require(p.nseg <= max_segs || !segs, "segment array too small");
+    if (n_e)
+      for (int e = 0; e < c->E; ++e) n_e[e] = p.n_e[e];
+    if (segs)
+      for (int i = 0; i < p.nseg; ++i) {
+        segs[3 * i] = p.segs[i].row_start;
+        segs[3 * i + 1] = p.segs[i].rows;
+        segs[3 * i + 2] = p.segs[i].slot;
+      }
+    *nseg = p.nseg;
+    if (rows_local) *rows_local = p.rows_local;
   });
 }
 

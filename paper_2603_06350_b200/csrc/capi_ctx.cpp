@@ -166,13 +166,24 @@ void plan_layer(moe_ctx* c, int layer, const std::vector<int64_t>& loads, long i
   cl.gpu_count = c->G;
   cl.gpu_mem_capacity_mb = c->desc.gpu_mem_capacity_mb > 0 ? c->desc.gpu_mem_capacity_mb : 180000.0;
   auto pr = moeless::place_experts(sp, cl, c->registry, iteration);
-  moeless::update_registry(c->registry, pr.placement, iteration);
-  L.warm = pr.warm_count;
-  L.cold = pr.cold_count;
+  // transactional: if the placement cannot be made resident (PLACED), the
+  // layer keeps its previous placement and the registry does not record it
+  std::vector<int32_t> old_counts = L.rep_counts, old_gpu = L.rep_gpu;
+  const bool had = L.has_placement;
   L.rep_counts.assign(sp.replica_counts.begin(), sp.replica_counts.end());
   L.rep_gpu.clear();
   for (auto& v : pr.placement.gpu_for) L.rep_gpu.insert(L.rep_gpu.end(), v.begin(), v.end());
-  placement_changed(c, layer);
+  try {
+    placement_changed(c, layer);
+  } catch (...) {
+    L.rep_counts.swap(old_counts);
+    L.rep_gpu.swap(old_gpu);
+    L.has_placement = had;
+    throw;
+  }
+  moeless::update_registry(c->registry, pr.placement, iteration);
+  L.warm = pr.warm_count;
+  L.cold = pr.cold_count;
 }
 
 Layer& layer_at(moe_ctx* c, int layer) {
@@ -391,6 +402,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     // mapped pinned control buffers, read/written by small SM copies (UVA pointers)
     CU_CHECK(cudaHostAlloc(&c->hplan, sizeof(DevPlan), cudaHostAllocMapped));
     CU_CHECK(cudaHostAlloc(&c->h_counts, pad16(sizeof(int32_t) * c->count_stride * c->G), cudaHostAllocMapped));
+    CU_CHECK(cudaHostAlloc(&c->ids_err, sizeof(int) * 4, cudaHostAllocMapped));
+    *c->ids_err = 0;
     c->events.create();
     CU_CHECK(cudaEventCreateWithFlags(&c->ev_counts, cudaEventDisableTiming));
     for (auto& tri : c->gemm_ev)
@@ -422,6 +435,7 @@ int moe_ctx_destroy(moe_ctx* c) {
     if (c->ev_peers_ready) cudaEventDestroy(c->ev_peers_ready);
     if (c->wstream) cudaStreamDestroy(c->wstream);
     if (c->p2p_err) cudaFreeHost(c->p2p_err);
+    if (c->ids_err) cudaFreeHost(c->ids_err);
     c->events.destroy();
     if (c->hplan) cudaFreeHost(c->hplan);
     if (c->h_counts) cudaFreeHost(c->h_counts);
@@ -707,6 +721,21 @@ int moe_set_placement(moe_ctx* c, int layer, const int32_t* rc, const int32_t* r
       L.has_placement = had;
       throw;
     }
+  });
+}
+
+int moe_get_placement(moe_ctx* c, int layer, int32_t* rc, int32_t* rg, int max_replicas, int* n_replicas) {
+  return guarded([&] {
+    Layer& L = layer_at(c, layer);
+    require(rc && n_replicas, "null argument");
+    flush_pending_plan(c);  // a deferred SYNC plan of the last forward lands first
+    ensure_placement(c, layer);
+    const int R = static_cast<int>(L.rep_gpu.size());
+    require(!rg || R <= max_replicas, "replica array too small");
+    for (int e = 0; e < c->E; ++e) rc[e] = L.rep_counts[e];
+    if (rg)
+      for (int i = 0; i < R; ++i) rg[i] = L.rep_gpu[i];
+    *n_replicas = R;
   });
 }
 

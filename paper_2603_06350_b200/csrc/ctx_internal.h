@@ -36,6 +36,8 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
                              int32_t* pred_counts, float* partial, cudaStream_t stream,
                              int32_t* host_counts = nullptr, int host_n = 0, unsigned* ticket = nullptr,
                              const float* pred_w2 = nullptr, unsigned mlp_mask = 0);
+cudaError_t launch_route_ids(const int32_t* ids_in, const float* w_in, int T, int E, int k, int32_t* ids, float* wts,
+                             int32_t* counts, int32_t* block_counts, int* err, cudaStream_t s);
 cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, const DevPlan* plan,
                                 int32_t* block_pre, cudaStream_t s, const int32_t* local_counts = nullptr,
                                 bool pdl = false);
@@ -376,6 +378,11 @@ struct moe_ctx {
   // single-GPU forward: host planner work deferred until the histogram lands
   PendingPlan pending;
   cudaEvent_t ev_counts = nullptr;
+  // caller-given routing (moe_layer_forward_ids): replaces K1 for one forward
+  bool ext_route = false;
+  const int32_t* ext_ids = nullptr;
+  const float* ext_wts = nullptr;
+  int* ids_err = nullptr;  // mapped pinned: 1 + first token with invalid ids (0 = none)
   // peer-memory exchange (MOE_EXCHANGE_P2P): one exported slab per rank
   bool p2p = false, p2p_ready = false;
   DevBuf<uint8_t> slab;

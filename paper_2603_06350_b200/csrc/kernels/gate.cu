@@ -47,6 +47,7 @@ constexpr int kBlockTokens = 32;  // tokens per CTA == per block_counts row
 constexpr int kWarps = 8;
 constexpr int kSlices = 4;        // K-slices per m-tile inside a CTA
 constexpr int kPerLane = 8;       // stacked logits per lane in the top-k (<= 256)
+constexpr int kMaxHistExperts = 256;
 
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                                uint32_t b0, uint32_t b1) {
@@ -329,6 +330,64 @@ gate_finish_kernel(const float* __restrict__ partial, int splits, int T, int E, 
   select_and_count<kLd, true, MLP>(red, hist, blk, tok0, kFinishTokens, T, E, n_pred, k, ids, wts, counts, block_counts,
                               pred_counts, mlp);
   publish_counts(counts, mirror);
+}
+
+// Caller-given routing (moe_layer_forward_ids — the SURVEY §8 c3 bridge: ids
+// replayed from the reference's route_tokens stream, workload.cpp:188-230,
+// enter the data path here instead of K1).  One CTA per 32-token block, one
+// thread per (token, slot): checks 0 <= id < E and that a token names each
+// expert once (route_tokens rejects duplicates, workload.cpp:221-226), copies
+// ids and weights (NULL weights: 1/k each) into the context's buffers, and
+// writes the same block histogram row + global histogram the gate writes, so
+// block prefix / dispatch / K4 / combine run unchanged.  A bad token is
+// replaced by experts 0..k-1 with weight 0 (memory-safe downstream) and
+// reported through *err = 1 + first bad token (the host raises MOE_EINVAL).
+__global__ void __launch_bounds__(256)
+route_ids_kernel(const int32_t* __restrict__ ids_in, const float* __restrict__ w_in, int T, int E, int k,
+                 int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
+                 int32_t* __restrict__ block_counts, int* __restrict__ err) {
+  __shared__ int hist[kMaxHistExperts];
+  __shared__ unsigned char bad[kBlockTokens];
+  const int blk = blockIdx.x;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
+  if (threadIdx.x < kBlockTokens) bad[threadIdx.x] = 0;
+  __syncthreads();
+  const int lt = threadIdx.x / k, j = threadIdx.x % k;
+  const int t = blk * kBlockTokens + lt;
+  const bool live = lt < kBlockTokens && t < T;
+  int id = 0;
+  if (live) {
+    id = __ldg(ids_in + (size_t)t * k + j);
+    bool ok = id >= 0 && id < E;
+    for (int q = 0; q < j; ++q) ok = ok && __ldg(ids_in + (size_t)t * k + q) != id;
+    if (!ok) bad[lt] = 1;
+  }
+  __syncthreads();
+  if (live) {
+    float w = w_in ? __ldg(w_in + (size_t)t * k + j) : 1.0f / static_cast<float>(k);
+    if (bad[lt]) {
+      id = j;
+      w = 0.0f;
+      if (j == 0) atomicCAS(err, 0, 1 + t);
+    }
+    ids[(size_t)t * k + j] = id;
+    wts[(size_t)t * k + j] = w;
+    atomicAdd(&hist[id], 1);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int h = hist[e];
+    block_counts[(size_t)blk * E + e] = h;
+    if (h) atomicAdd(counts + e, h);
+  }
+}
+
+cudaError_t launch_route_ids(const int32_t* ids_in, const float* w_in, int T, int E, int k, int32_t* ids, float* wts,
+                             int32_t* counts, int32_t* block_counts, int* err, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  if (k < 1 || k > 8 || k > E || E > kMaxHistExperts) return cudaErrorInvalidValue;
+  route_ids_kernel<<<(T + kBlockTokens - 1) / kBlockTokens, 256, 0, s>>>(ids_in, w_in, T, E, k, ids, wts, counts, block_counts, err);
+  return cudaGetLastError();
 }
 
 int gate_num_blocks(int T) { return (T + kBlockTokens - 1) / kBlockTokens; }

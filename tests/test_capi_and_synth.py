@@ -113,3 +113,29 @@ def test_exchange_plan_matches_oracle_dispatch():
                 assert np.all(np.isin(np.arange(off, off + n), mine))
             sent = sum(n for (_, _, _, n) in p["sends"])
             assert sent == p["rows_send"] == int(np.sum(per[rank][0] != rank))
+
+
+def test_oracle_generator_matches_product_generator():
+    """bench.py's reference arm synthesises its inputs with the oracle's
+    generator (oracle/workload.py) so it never loads the product; both must
+    produce the same bytes as paper_2603_06350_b200/workload.py."""
+    from oracle import workload as owl
+    for (T, d, E, seed, batch) in [(64, 1024, 8, 1, 3), (33, 2048, 64, 1, 1001), (5, 4096, 16, 7, 0)]:
+        assert np.array_equal(owl.tokens(T, d, E, seed, batch), wl.tokens(T, d, E, seed, batch))
+    for (E, d, s, seed, layer, it) in [(8, 1024, 1.2, 1, 0, 5), (64, 2048, 2.0, 1, 0, 17), (16, 4096, 1.2, 3, 2, 0)]:
+        assert np.array_equal(owl.gate_weights(E, d, s, seed, layer, it), wl.gate_weights(E, d, s, seed, layer, it))
+    for a, b in zip(owl.expert_weights(1024, 256, 1, 0, 3), wl.expert_weights(1024, 256, 1, 0, 3)):
+        assert np.array_equal(a, b)
+
+
+def test_cpu_reference_layer_matches_oracle():
+    """The CPU reference path of the bench (BLAS FFN) == the oracle layer (fp32)."""
+    from oracle import workload as owl
+    from oracle.cpu_path import CpuLayer
+    E, k, d, ff, T = 8, 2, 1024, 512, 300
+    ex = [owl.expert_weights(d, ff, 1, 0, e) for e in range(E)]
+    x, wg = owl.tokens(T, d, E, 1, 0), owl.gate_weights(E, d, 1.2, 1, 0, 0)
+    y, dt = CpuLayer(E, k, d, ff, ex).forward(x, wg)
+    yr, _, _, _ = oracle.layer_forward(x, wg, ex, [1] * E, k, round_h=False)
+    assert dt > 0
+    assert float(np.max(np.abs(y - yr)) / np.max(np.abs(yr))) <= 1e-4

@@ -1,10 +1,18 @@
-"""GPU parity at the BASELINE.json sizes, through size-independent properties.
+"""GPU parity at the BASELINE.json sizes, on the WHOLE batch.
 
-Full-size layers are too large for the oracle to recompute end to end in
-seconds, but every output row depends only on its own token (routing is
-per token; replica splits change where a row is computed, not its value), so
-the oracle recomputes a seeded sample of rows exactly, and the histogram /
-conservation / permutation properties are checked on the whole batch.
+cfg1 (T=2048), cfg2 Mixtral (T=16384), cfg3 Phi-3.5 shape (T=16384) and cfg5
+decode (T=256, Zipf s = 1.2 and 2.0), each one SYNC-planned forward through
+the C-ABI (straggler replicas added by the host planner):
+
+  * ids, weights and counts of the whole batch == oracle.gate (bit-exact ids and
+    counts; weights within expf ulps);
+  * row codes of the whole batch == oracle.dispatch with the placement the
+    context used (bit-exact: the stable permutation);
+  * the device plan (moe_last_plan): n_e == counts, one segment per active
+    expert in expert order, rows == counts, contiguous;
+  * per-row relative error <= 2e-2 on >= 1024 sampled tokens (all tokens at
+    cfg5): max_c |y[t,c] - y_ref[t,c]| / max_c |y_ref[t,c]| for every sampled
+    token t, against the oracle that mirrors the device's bf16 rounding of h.
 """
 import numpy as np
 import pytest
@@ -14,7 +22,24 @@ from paper_2603_06350_b200 import MOE_PLAN_SYNC, MoELayer
 from paper_2603_06350_b200 import workload as wl
 
 pytestmark = pytest.mark.gpu
-TOL_REL = 2e-2
+TOL_ROW = 2e-2
+
+
+def row_rel_err(y, y_ref):
+    """Per-token relative error: max over columns, normalised by the token's own scale."""
+    scale = np.maximum(np.max(np.abs(y_ref), axis=1), 1e-6)
+    return np.max(np.abs(y - y_ref), axis=1) / scale
+
+
+def check_plan(m, counts, E):
+    n_e, segs, rows_local = m.last_plan()
+    assert np.array_equal(n_e, counts)
+    active = [e for e in range(E) if counts[e] > 0]
+    assert segs[:, 2].tolist() == active  # one segment per active expert, expert order
+    assert segs[:, 1].tolist() == [int(counts[e]) for e in active]
+    starts = np.concatenate([[0], np.cumsum(segs[:, 1])[:-1]])
+    assert np.array_equal(segs[:, 0], starts)
+    assert rows_local == int(counts.sum())
 
 
 def _run(cuda, E, k, d, ff, T, extra, s, sample, seed=1, iteration=7):
@@ -33,33 +58,41 @@ def _run(cuda, E, k, d, ff, T, extra, s, sample, seed=1, iteration=7):
     torch.cuda.synchronize()
     y = oracle.bf16_to_f32(yd.cpu().numpy().view(np.uint16))
     ids = m.read_buffer(4, np.int32, (T, k))
+    wts = m.read_buffer(5, np.float32, (T, k))
     codes = m.read_buffer(6, np.uint32, (T, k)).astype(np.int64)
-    # conservation + histogram + permutation properties on the whole batch
-    counts = np.bincount(ids.reshape(-1), minlength=E)
-    assert counts.sum() == T * k
-    assert np.array_equal(np.array(st.counts[:E]), counts)
+    # whole batch: routing bit-exact against the oracle gate
+    ids_o, w_o, counts_o = oracle.gate(x, wg, k)
+    assert np.array_equal(ids, ids_o)
+    assert np.array_equal(np.array(st.counts[:E]), counts_o)
+    assert int(counts_o.sum()) == T * k
+    np.testing.assert_allclose(wts, w_o, rtol=1e-5, atol=1e-6)
+    # whole batch: the permutation bit-exact against the oracle dispatch under the
+    # placement the planner chose for this forward
+    rc, rg = m.placement(0)
+    assert int(rc.sum()) == len(rg) == st.replica_count
+    (dg, dr), = oracle.dispatch([ids_o], k, E, rc, rg)[0][:1]
+    assert np.array_equal(codes.reshape(-1), dr)
+    assert np.all(dg == 0)
+    check_plan(m, counts_o, E)
     assert st.rows_local == T * k
-    assert np.array_equal(np.sort(codes.reshape(-1)), np.arange(T * k))  # a permutation
-    for row in ids:
-        assert len(set(row.tolist())) == k  # distinct experts per token
-    # sampled rows recomputed by the oracle (replica split does not change values)
+    # sampled tokens recomputed by the oracle (a row depends only on its token)
     rng = np.random.default_rng(5)
     idx = np.sort(rng.choice(T, size=min(sample, T), replace=False))
-    y_ref, ids_o, w_o, counts_o = oracle.layer_forward(x[idx], wg, experts, [1] * E, k, round_h=True)
-    assert np.array_equal(ids[idx], ids_o)
-    err = float(np.max(np.abs(y[idx] - y_ref)) / np.max(np.abs(y_ref)))
-    assert err <= TOL_REL, err
+    y_ref, ids_s, _, _ = oracle.layer_forward(x[idx], wg, experts, [1] * E, k, round_h=True)
+    assert np.array_equal(ids[idx], ids_s)
+    err = row_rel_err(y[idx], y_ref)
+    assert float(err.max()) <= TOL_ROW, (float(err.max()), int(idx[int(err.argmax())]))
     m.close()
-    return st
+    return st, rc
 
 
 def test_cfg2_mixtral_full(cuda):
-    st = _run(cuda, E=8, k=2, d=4096, ff=14336, T=16384, extra=4, s=1.2, sample=24)
-    assert st.replica_count > 8  # the planner added straggler replicas
+    st, rc = _run(cuda, E=8, k=2, d=4096, ff=14336, T=16384, extra=4, s=1.2, sample=1024)
+    assert st.replica_count > 8 and int(rc.max()) > 1  # the planner added straggler replicas
 
 
 def test_cfg3_phi_shape_single_gpu(cuda):
-    _run(cuda, E=16, k=2, d=4096, ff=6400, T=16384, extra=8, s=1.2, sample=24)
+    _run(cuda, E=16, k=2, d=4096, ff=6400, T=16384, extra=8, s=1.2, sample=1024)
 
 
 @pytest.mark.parametrize("s", [1.2, 2.0])
