@@ -13,7 +13,7 @@
 #include "host/exchange_plan.h"
 #include "kernels/dispatch_plan.h"
 #include "moe_b200.h"
-#include "moeless/api.hpp"
+#include "host/moeless_api.hpp"
 
 namespace moe {
 uint64_t stream_key(uint64_t seed, uint64_t a, uint64_t b, uint64_t tag);

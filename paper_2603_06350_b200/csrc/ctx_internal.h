@@ -26,7 +26,7 @@
 #include "host/exchange_plan.h"
 #include "kernels/dispatch_plan.h"
 #include "moe_b200.h"
-#include "moeless/api.hpp"
+#include "host/moeless_api.hpp"
 
 namespace moe {
 // kernels

@@ -1,12 +1,17 @@
-// moeless/api.hpp — the reference's C++ planning/forward API, re-declared for
-// the B200 build.  Every signature here is the one a caller of the reference
-// (/root/reference/proj/include/moeless/*.hpp) compiles against, so existing
-// call sites (simulator.cpp:117-201, baselines.cpp:136,228) build unchanged.
-// The per-name headers next to this file (types.hpp, scaler.hpp, ...) only
-// forward here.  Implementation: paper_2603_06350_b200/csrc/host/planner.cpp.
+// host/moeless_api.hpp — INTERNAL declarations of the library's host planner:
+// a restatement, inside libmoe_b200.so, of the reference's planning functions
+// (/root/reference/proj/include/moeless/*.hpp: scale_experts, place_experts,
+// ReplicaRegistry, predict, layer_forward_time, route_tokens, static_plan, ...)
+// that the context runs for MOE_PLAN_SYNC / MOE_PLAN_PREDICTED and that the
+// C-ABI exports as moe_plan_* entry points.  Implementation: planner.cpp.
+//
+// This header is NOT installed and does not replace the reference's headers:
+// reference callers keep compiling against proj/include/moeless and reach the
+// GPU through include/moeless/b200_layer.hpp (C-ABI only).  The library
+// exports only the moe_* C symbols (csrc/exports.map), so these C++ symbols
+// never clash with a reference build linked into the same program.
 //
 // Behavioural contract kept from the reference:
-//   * inputs by const&, outputs by value; only ReplicaRegistry is mutable;
 //   * bad arguments throw std::invalid_argument, infeasible placements throw
 //     std::runtime_error naming the replica ("no GPU has memory for replica
 //     (e,r) of layer l", placer.cpp:100-104);

@@ -13,7 +13,7 @@
 #include <stdexcept>
 #include <string>
 
-#include "moeless/api.hpp"
+#include "host/moeless_api.hpp"
 
 namespace moeless {
 

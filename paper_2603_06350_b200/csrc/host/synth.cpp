@@ -15,7 +15,7 @@
 #include <cstdint>
 #include <cstring>
 
-#include "moeless/api.hpp"
+#include "host/moeless_api.hpp"
 
 namespace moe {
 
