@@ -388,6 +388,38 @@ int moe_plan_predict(int kind, const int64_t* actual, int num_experts, int layer
 double moe_measure_accuracy(const int64_t* predicted, const int64_t* actual, int num_experts);
 double moe_percentile(const double* values, int n, double q);
 
+/* static_plan (baselines.cpp:32-60): expert e -> GPU e mod G, one replica
+   each; gpu_out[E].  Throws the reference's "static placement does not fit
+   GPU g" as MOE_EINFEASIBLE. */
+int moe_static_plan(const int64_t* loads, int num_experts, int gpus, double expert_mem_mb,
+                    double gpu_mem_capacity_mb, int32_t* gpu_out);
+/* round_robin_placement (simulator.cpp:32-50): replica f (flattened
+   (expert, ordinal)) -> GPU f mod G; gpu_out[sum counts]. */
+int moe_round_robin_placement(const int32_t* counts, int num_experts, int gpus, double expert_mem_mb,
+                              double gpu_mem_capacity_mb, int32_t* gpu_out);
+/* gpu_comm_times (cost_model.cpp:67-89): beta x the shares hosted per GPU;
+   out[G].  Shares are plan_loads[e] / counts[e]. */
+int moe_gpu_comm_times(const int64_t* plan_loads, const int32_t* counts, const int32_t* gpu_flat,
+                       int num_experts, int gpus, double beta_ms_per_token, double* out);
+/* oracle_balance_time (baselines.cpp:141-154): the perfect-balance line;
+   out6 = compute, comm, forward, replicas, mem, cost (as moe_model_forward_time). */
+int moe_oracle_balance_time(const int64_t* actual, int num_experts, int gpus, double alpha, double beta,
+                            double t_misc, double m_misc, double expert_mem_mb, double* out6);
+/* verify_plan (scaler.cpp:99-173) on an explicit plan: replica counts[n_counts]
+   and shares (expert, ordinal, num/den)[n_shares]; *ok and the reference's
+   issue messages, newline-separated, in issues[cap]. */
+int moe_verify_plan(const int64_t* loads, int num_experts, const int32_t* counts, int n_counts,
+                    const int32_t* share_expert, const int32_t* share_ordinal, const int64_t* share_num,
+                    const int64_t* share_den, int n_shares, double alloc_mem_mb, double expert_mem_mb,
+                    double layer_mem_cap_mb, double cv_threshold, int exclude_zero, int* ok, char* issues,
+                    int cap);
+/* apply_layer_aware_finetuning (predictor.cpp:188-199) on a noisy profile's
+   per-layer accuracies (raised in place to the threshold h) -> fine_tuned[n]. */
+int moe_apply_finetuning(double* per_layer_accuracy, int n, double threshold, int32_t* fine_tuned);
+/* coefficient_of_variation / serverful_cost (cost_model.cpp:124-139); -1 on error. */
+double moe_coefficient_of_variation(const double* values, int n);
+double moe_serverful_cost(double total_ms, int num_layers, int num_experts, double expert_mem_mb, double m_misc_mb);
+
 /* route_tokens (workload.hpp:90-92) and the popularity profile behind it */
 int moe_route_tokens(int64_t tokens, int layer, long iteration, int num_experts, int num_layers,
                      double zipf_s, uint64_t seed, int top_k, int drift_period,

@@ -99,6 +99,13 @@ def ref():
             "ref_percentile": (dbl, [vp, C.c_int, dbl]),
             "ref_static_plan": (C.c_int, [vp, C.c_int, C.c_int, dbl, dbl, vp]),
             "ref_cpu_layer_path": (dbl, [i64, C.c_int, C.c_int, dbl, u64, C.c_int, dbl, dbl, C.c_int, vp]),
+            "ref_gpu_comm_times": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, dbl, vp]),
+            "ref_oracle_balance_time": (C.c_int, [vp, C.c_int, C.c_int, dbl, dbl, dbl, dbl, dbl, vp]),
+            "ref_verify_plan": (C.c_int, [vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, C.c_int, dbl, dbl, dbl, dbl,
+                                          C.c_int, vp, C.c_char_p, C.c_int]),
+            "ref_apply_finetuning": (C.c_int, [vp, C.c_int, dbl, vp]),
+            "ref_coefficient_of_variation": (dbl, [vp, C.c_int]),
+            "ref_serverful_cost": (dbl, [dbl, C.c_int, C.c_int, dbl, dbl]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_ref, name)

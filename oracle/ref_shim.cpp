@@ -257,6 +257,96 @@ int ref_static_plan(const std::int64_t* loads, int experts, int gpus, double exp
   } catch (const std::exception& e) { return fail(e); }
 }
 
+// gpu_comm_times (cost_model.cpp:67-89)
+int ref_gpu_comm_times(const std::int64_t* plan_loads, const int* counts, const int* gpu_flat, int experts,
+                       int gpus, double beta, double* out) {
+  try {
+    auto v = gpu_comm_times(plan_from(plan_loads, counts, experts, 0, 0.0),
+                            placement_from(counts, gpu_flat, experts, gpus, 0, 0.0), beta);
+    std::memcpy(out, v.data(), sizeof(double) * v.size());
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// oracle_balance_time (baselines.cpp:141-154)
+int ref_oracle_balance_time(const std::int64_t* actual, int experts, int gpus, double alpha, double beta,
+                            double t_misc, double m_misc, double expert_mem_mb, double* out6) {
+  try {
+    ClusterSpec c;
+    c.gpu_count = gpus;
+    c.alpha_ms_per_token = alpha;
+    c.beta_ms_per_token = beta;
+    c.t_misc_ms = t_misc;
+    c.m_misc_mb = m_misc;
+    ModelSpec m;
+    m.experts_per_layer = experts;
+    m.expert_mem_mb = expert_mem_mb;
+    auto r = oracle_balance_time(lv(actual, experts), c, m);
+    const double v[6] = {r.compute_ms, r.comm_ms, r.forward_ms, (double)r.replica_count, r.mem_mb, r.cost_mb_ms};
+    std::memcpy(out6, v, sizeof v);
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// verify_plan (scaler.cpp:99-173) on an explicit (possibly broken) plan
+int ref_verify_plan(const std::int64_t* loads, int experts, const int* counts, int n_counts, const int* s_expert,
+                    const int* s_ordinal, const std::int64_t* s_num, const std::int64_t* s_den, int n_shares,
+                    double alloc_mem_mb, double expert_mem_mb, double cap_mb, double cv_threshold,
+                    int exclude_zero, int* ok, char* issues, int cap) {
+  try {
+    ScalingPlan plan;
+    plan.replica_counts.assign(counts, counts + n_counts);
+    for (int i = 0; i < n_shares; ++i) plan.shares.push_back({s_expert[i], s_ordinal[i], Rational(s_num[i], s_den[i])});
+    plan.alloc_mem_mb = alloc_mem_mb;
+    plan.expert_mem_mb = expert_mem_mb;
+    ModelSpec m;
+    m.experts_per_layer = experts;
+    m.expert_mem_mb = expert_mem_mb;
+    m.layer_mem_cap_mb = cap_mb;
+    ScalerConfig cfg;
+    cfg.cv_threshold = cv_threshold;
+    cfg.exclude_zero_loads_from_cv = exclude_zero != 0;
+    auto rep = verify_plan(plan, lv(loads, experts), m, cfg);
+    *ok = rep.ok ? 1 : 0;
+    std::string all;
+    for (const auto& x : rep.issues) all += x + "\n";
+    const std::size_t n = std::min(all.size(), static_cast<std::size_t>(cap - 1));
+    std::memcpy(issues, all.data(), n);
+    issues[n] = 0;
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// apply_layer_aware_finetuning (predictor.cpp:188-199)
+int ref_apply_finetuning(double* acc, int n, double threshold, int* fine_tuned) {
+  try {
+    PredictorProfile p;
+    p.kind = PredictorKind::noisy;
+    p.per_layer_accuracy.assign(acc, acc + n);
+    p.accuracy_threshold = threshold;
+    apply_layer_aware_finetuning(p);
+    for (int l = 0; l < n; ++l) {
+      acc[l] = p.per_layer_accuracy[l];
+      fine_tuned[l] = p.fine_tuned[l] ? 1 : 0;
+    }
+    return 0;
+  } catch (const std::exception& e) { return fail(e); }
+}
+
+// coefficient_of_variation / serverful_cost (cost_model.cpp:124-139)
+double ref_coefficient_of_variation(const double* v, int n) {
+  try { return coefficient_of_variation(std::vector<double>(v, v + n)); } catch (const std::exception& e) { fail(e); return -1.0; }
+}
+double ref_serverful_cost(double total_ms, int layers, int experts, double expert_mem_mb, double m_misc) {
+  ModelSpec m;
+  m.num_layers = layers;
+  m.experts_per_layer = experts;
+  m.expert_mem_mb = expert_mem_mb;
+  ClusterSpec c;
+  c.m_misc_mb = m_misc;
+  return serverful_cost(total_ms, m, c);
+}
+
 // The reference simulator end to end (config.cpp:90 parse_config_text ->
 // workload.cpp:90 parse_trace -> simulator.cpp:71 run -> report.cpp:48
 // summary_json), for driving it with B200-calibrated alpha/beta/t_misc.

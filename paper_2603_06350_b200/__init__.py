@@ -147,6 +147,77 @@ def layer_forward_time(plan_loads, replica_counts, gpu_flat, actual, gpu_count, 
     return tuple(out.tolist())
 
 
+def static_plan(loads: Sequence[int], gpu_count: int, expert_mem_mb: float,
+                gpu_mem_capacity_mb: float = 180000.0) -> List[int]:
+    """Fixed placement, expert e -> GPU e mod G (reference baselines.cpp:32-60)."""
+    lv = _i64(loads)
+    out = np.zeros(max(len(lv), 1), np.int32)
+    check(lib.moe_static_plan(_p(lv), len(lv), gpu_count, expert_mem_mb, gpu_mem_capacity_mb, _p(out)))
+    return out[:len(lv)].tolist()
+
+
+def round_robin_placement(replica_counts: Sequence[int], gpu_count: int, expert_mem_mb: float,
+                          gpu_mem_capacity_mb: float = 180000.0) -> List[int]:
+    """Replica f -> GPU f mod G, flattened (reference simulator.cpp:32-50)."""
+    rc = _i32(replica_counts)
+    out = np.zeros(max(int(rc.sum()), 1), np.int32)
+    check(lib.moe_round_robin_placement(_p(rc), len(rc), gpu_count, expert_mem_mb, gpu_mem_capacity_mb,
+                                        _p(out)))
+    return out[:int(rc.sum())].tolist()
+
+
+def gpu_comm_times(plan_loads, replica_counts, gpu_flat, gpu_count: int, beta: float) -> List[float]:
+    """beta x shares hosted per GPU (reference cost_model.cpp:67-89)."""
+    lv, rc, g = _i64(plan_loads), _i32(replica_counts), _i32(gpu_flat)
+    out = np.zeros(gpu_count, np.float64)
+    check(lib.moe_gpu_comm_times(_p(lv), _p(rc), _p(g), len(rc), gpu_count, beta, _p(out)))
+    return out.tolist()
+
+
+def oracle_balance_time(actual, gpu_count, alpha, beta, t_misc, m_misc, expert_mem_mb) -> Tuple[float, ...]:
+    """Perfect-balance line (reference baselines.cpp:141-154): compute, comm, forward, replicas, mem, cost."""
+    a = _i64(actual)
+    out = np.zeros(6, np.float64)
+    check(lib.moe_oracle_balance_time(_p(a), len(a), gpu_count, alpha, beta, t_misc, m_misc, expert_mem_mb,
+                                      _p(out)))
+    return tuple(out.tolist())
+
+
+def verify_plan(loads, replica_counts, shares, alloc_mem_mb, expert_mem_mb, layer_mem_cap_mb,
+                cv_threshold=0.2, exclude_zero=False) -> Tuple[bool, List[str]]:
+    """verify_plan (reference scaler.cpp:99-173); shares = [(expert, ordinal, num, den)]."""
+    lv, rc = _i64(loads), _i32(replica_counts)
+    sh = np.asarray(shares, np.int64).reshape(-1, 4) if len(shares) else np.zeros((0, 4), np.int64)
+    se, so = _i32(sh[:, 0]), _i32(sh[:, 1])
+    sn, sd = _i64(sh[:, 2]), _i64(sh[:, 3])
+    ok = C.c_int()
+    buf = C.create_string_buffer(1 << 16)
+    check(lib.moe_verify_plan(_p(lv), len(lv), _p(rc) if len(rc) else None, len(rc), _p(se), _p(so), _p(sn),
+                              _p(sd), len(sh), alloc_mem_mb, expert_mem_mb, layer_mem_cap_mb, cv_threshold,
+                              int(exclude_zero), C.byref(ok), buf, len(buf)))
+    return bool(ok.value), [m for m in buf.value.decode().split("\n") if m]
+
+
+def apply_finetuning(per_layer_accuracy, threshold: float) -> Tuple[List[float], List[bool]]:
+    """apply_layer_aware_finetuning (reference predictor.cpp:188-199) on a noisy profile."""
+    acc = np.ascontiguousarray(np.asarray(per_layer_accuracy, np.float64)).copy()
+    ft = np.zeros(max(len(acc), 1), np.int32)
+    check(lib.moe_apply_finetuning(_p(acc), len(acc), threshold, _p(ft)))
+    return acc.tolist(), [bool(v) for v in ft[:len(acc)]]
+
+
+def coefficient_of_variation(values) -> float:
+    v = np.ascontiguousarray(np.asarray(values, np.float64))
+    r = lib.moe_coefficient_of_variation(_p(v) if len(v) else None, len(v))
+    if r < 0:
+        raise ValueError(lib.moe_last_error().decode())
+    return r
+
+
+def serverful_cost(total_ms, num_layers, experts, expert_mem_mb, m_misc_mb=0.0) -> float:
+    return lib.moe_serverful_cost(total_ms, num_layers, experts, expert_mem_mb, m_misc_mb)
+
+
 def predict(kind: int, actual: Sequence[int], layer: int = 0, history=(), accuracy=None,
             distance: int = 1, decay: float = 0.04, window: int = 8, iteration: int = 0,
             seed: int = 1, popularity=None) -> Tuple[List[int], bool]:

@@ -132,6 +132,15 @@ _sig("moe_measure_accuracy", dbl, vp, vp, C.c_int)
 _sig("moe_percentile", dbl, vp, C.c_int, dbl)
 _sig("moe_route_tokens", C.c_int, i64, C.c_int, C.c_long, C.c_int, C.c_int, dbl, u64, C.c_int, C.c_int, vp)
 _sig("moe_popularity", C.c_int, C.c_int, C.c_int, dbl, u64, C.c_int, C.c_long, C.c_int, vp, vp)
+_sig("moe_static_plan", C.c_int, vp, C.c_int, C.c_int, dbl, dbl, vp)
+_sig("moe_round_robin_placement", C.c_int, vp, C.c_int, C.c_int, dbl, dbl, vp)
+_sig("moe_gpu_comm_times", C.c_int, vp, vp, vp, C.c_int, C.c_int, dbl, vp)
+_sig("moe_oracle_balance_time", C.c_int, vp, C.c_int, C.c_int, dbl, dbl, dbl, dbl, dbl, vp)
+_sig("moe_verify_plan", C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, C.c_int, dbl, dbl, dbl, dbl, C.c_int,
+     P(C.c_int), C.c_char_p, C.c_int)
+_sig("moe_apply_finetuning", C.c_int, vp, C.c_int, dbl, vp)
+_sig("moe_coefficient_of_variation", dbl, vp, C.c_int)
+_sig("moe_serverful_cost", dbl, dbl, C.c_int, C.c_int, dbl, dbl)
 _sig("moe_stream_key", u64, u64, u64, u64, u64)
 _sig("moe_synth_tokens", C.c_int, u64, i64, i64, C.c_int, C.c_int, vp)
 _sig("moe_synth_gate", C.c_int, u64, C.c_int, C.c_int, vp, vp, vp)
@@ -149,7 +158,9 @@ EXPORTED = [
     "moe_forward_end", "moe_buffer", "moe_memcpy", "moe_exchange_plan", "moe_exchange_plan_direct", "moe_plan_scale",
     "moe_registry_create", "moe_registry_destroy", "moe_registry_size", "moe_plan_place",
     "moe_registry_update", "moe_model_forward_time", "moe_plan_predict", "moe_measure_accuracy",
-    "moe_percentile", "moe_route_tokens", "moe_popularity", "moe_stream_key", "moe_synth_tokens",
+    "moe_percentile", "moe_static_plan", "moe_round_robin_placement", "moe_gpu_comm_times",
+    "moe_oracle_balance_time", "moe_verify_plan", "moe_apply_finetuning", "moe_coefficient_of_variation",
+    "moe_serverful_cost", "moe_route_tokens", "moe_popularity", "moe_stream_key", "moe_synth_tokens",
     "moe_synth_gate", "moe_synth_expert",
 ]
 

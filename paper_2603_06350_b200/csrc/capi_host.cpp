@@ -284,4 +284,126 @@ int moe_synth_expert(uint64_t key, int d, int ff, uint16_t* w1, uint16_t* w3, ui
   });
 }
 
+// ------------------------------------------------ baselines / cost model rows
+int moe_static_plan(const int64_t* loads, int E, int G, double mem, double gpu_mem, int32_t* gpu_out) {
+  return guarded([&] {
+    require(loads && gpu_out, "null argument");
+    moeless::ModelSpec ms;
+    ms.experts_per_layer = E;
+    ms.expert_mem_mb = mem;
+    moeless::ClusterSpec cl;
+    cl.gpu_count = G;
+    cl.gpu_mem_capacity_mb = gpu_mem;
+    auto sp = moeless::static_plan(moeless::LoadVector{0, std::vector<int64_t>(loads, loads + E)}, ms, cl);
+    for (int e = 0; e < E; ++e) gpu_out[e] = sp.second.gpu_for[e][0];
+  });
+}
+
+int moe_round_robin_placement(const int32_t* counts, int E, int G, double mem, double gpu_mem, int32_t* gpu_out) {
+  return guarded([&] {
+    require(counts && gpu_out, "null argument");
+    moeless::ScalingPlan plan;
+    plan.replica_counts.assign(counts, counts + E);
+    plan.expert_mem_mb = mem;
+    moeless::ClusterSpec cl;
+    cl.gpu_count = G;
+    cl.gpu_mem_capacity_mb = gpu_mem;
+    auto pl = moeless::round_robin_placement(plan, cl);
+    int i = 0;
+    for (const auto& v : pl.gpu_for)
+      for (int g : v) gpu_out[i++] = g;
+  });
+}
+
+int moe_gpu_comm_times(const int64_t* loads, const int32_t* counts, const int32_t* gpu, int E, int G, double beta,
+                       double* out) {
+  return guarded([&] {
+    require(loads && counts && gpu && out, "null argument");
+    auto v = moeless::gpu_comm_times(plan_of(loads, counts, E, 0, 0.0), placement_of(counts, gpu, E, G, 0, 0.0), beta);
+    std::copy(v.begin(), v.end(), out);
+  });
+}
+
+int moe_oracle_balance_time(const int64_t* actual, int E, int G, double alpha, double beta, double t_misc,
+                            double m_misc, double mem, double* out6) {
+  return guarded([&] {
+    require(actual && out6, "null argument");
+    moeless::ClusterSpec cl;
+    cl.gpu_count = G;
+    cl.alpha_ms_per_token = alpha;
+    cl.beta_ms_per_token = beta;
+    cl.t_misc_ms = t_misc;
+    cl.m_misc_mb = m_misc;
+    moeless::ModelSpec ms;
+    ms.experts_per_layer = E;
+    ms.expert_mem_mb = mem;
+    auto m = moeless::oracle_balance_time(moeless::LoadVector{0, std::vector<int64_t>(actual, actual + E)}, cl, ms);
+    const double v[6] = {m.compute_ms, m.comm_ms, m.forward_ms, static_cast<double>(m.replica_count), m.mem_mb,
+                         m.cost_mb_ms};
+    std::copy(v, v + 6, out6);
+  });
+}
+
+int moe_verify_plan(const int64_t* loads, int E, const int32_t* counts, int n_counts, const int32_t* share_expert,
+                    const int32_t* share_ordinal, const int64_t* share_num, const int64_t* share_den, int n_shares,
+                    double alloc_mem_mb, double mem, double layer_cap_mb, double cv_threshold, int exclude_zero,
+                    int* ok, char* issues, int cap) {
+  return guarded([&] {
+    require(loads && ok && (n_counts == 0 || counts), "null argument");
+    moeless::ScalingPlan plan;
+    plan.replica_counts.assign(counts, counts + n_counts);
+    for (int i = 0; i < n_shares; ++i)
+      plan.shares.push_back({share_expert[i], share_ordinal[i], moeless::Rational(share_num[i], share_den[i])});
+    plan.alloc_mem_mb = alloc_mem_mb;
+    plan.expert_mem_mb = mem;
+    moeless::ModelSpec ms;
+    ms.experts_per_layer = E;
+    ms.expert_mem_mb = mem;
+    ms.layer_mem_cap_mb = layer_cap_mb;
+    moeless::ScalerConfig sc;
+    sc.cv_threshold = cv_threshold;
+    sc.exclude_zero_loads_from_cv = exclude_zero != 0;
+    auto rep = moeless::verify_plan(plan, moeless::LoadVector{0, std::vector<int64_t>(loads, loads + E)}, ms, sc);
+    *ok = rep.ok ? 1 : 0;
+    std::string all;
+    for (const auto& m : rep.issues) all += m + "\n";
+    if (issues && cap > 0) {
+      const size_t n = std::min(all.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(issues, all.data(), n);
+      issues[n] = 0;
+    }
+  });
+}
+
+int moe_apply_finetuning(double* accuracy, int n, double threshold, int32_t* fine_tuned) {
+  return guarded([&] {
+    require(accuracy && fine_tuned, "null argument");
+    moeless::PredictorProfile p;
+    p.kind = moeless::PredictorKind::noisy;
+    p.per_layer_accuracy.assign(accuracy, accuracy + n);
+    p.accuracy_threshold = threshold;
+    moeless::apply_layer_aware_finetuning(p);
+    for (int l = 0; l < n; ++l) {
+      accuracy[l] = p.per_layer_accuracy[l];
+      fine_tuned[l] = p.fine_tuned[l] ? 1 : 0;
+    }
+  });
+}
+
+double moe_coefficient_of_variation(const double* values, int n) {
+  double r = -1.0;
+  const int rc = guarded([&] { r = moeless::coefficient_of_variation(std::vector<double>(values, values + n)); });
+  return rc == MOE_OK ? r : -1.0;
+}
+
+double moe_serverful_cost(double total_ms, int num_layers, int E, double mem, double m_misc) {
+  moeless::ModelSpec ms;
+  ms.num_layers = num_layers;
+  ms.experts_per_layer = E;
+  ms.expert_mem_mb = mem;
+  moeless::ClusterSpec cl;
+  cl.m_misc_mb = m_misc;
+  return moeless::serverful_cost(total_ms, ms, cl);
+}
+
 }  // extern "C"

@@ -255,6 +255,9 @@ std::pair<ScalingPlan, Placement> static_plan(const LoadVector& loads, const Mod
                                               const ClusterSpec& cluster);
 LayerMetrics oracle_balance_time(const LoadVector& actual, const ClusterSpec& cluster,
                                  const ModelSpec& model);
+// replica f (flattened (expert, ordinal)) -> GPU f mod G: the simulator's
+// static_rr placement ablation (simulator.cpp:32-50)
+Placement round_robin_placement(const ScalingPlan& plan, const ClusterSpec& cluster);
 
 // -------------------------------------------------------------- report.hpp
 double percentile(std::vector<double> values, double q);

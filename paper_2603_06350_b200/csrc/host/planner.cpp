@@ -302,7 +302,8 @@ double measure_accuracy(const LoadVector& predicted, const LoadVector& actual) {
 void apply_layer_aware_finetuning(PredictorProfile& profile) {
   if (profile.kind != PredictorKind::noisy)
     throw std::invalid_argument("fine-tuning applies to the noisy predictor only");
-  profile.fine_tuned.resize(profile.per_layer_accuracy.size(), false);
+  if (profile.fine_tuned.size() != profile.per_layer_accuracy.size())  // a mismatched mask restarts
+    profile.fine_tuned.assign(profile.per_layer_accuracy.size(), false);
   for (std::size_t l = 0; l < profile.per_layer_accuracy.size(); ++l)
     if (profile.per_layer_accuracy[l] < profile.accuracy_threshold) {
       profile.per_layer_accuracy[l] = profile.accuracy_threshold;
@@ -648,16 +649,37 @@ LayerMetrics oracle_balance_time(const LoadVector& actual, const ClusterSpec& cl
                                  const ModelSpec& model) {
   cluster.validate();
   model.validate();
-  const double per_gpu = static_cast<double>(actual.total()) / cluster.gpu_count;
+  // every token's work spread evenly over the GPUs: the straggler-free bound
+  const double tokens = static_cast<double>(actual.total());
   LayerMetrics m;
-  m.compute_ms = cluster.alpha_ms_per_token * static_cast<double>(actual.total()) / cluster.gpu_count;
-  m.comm_ms = cluster.beta_ms_per_token * static_cast<double>(actual.total()) / cluster.gpu_count;
-  (void)per_gpu;
+  m.compute_ms = cluster.alpha_ms_per_token * tokens / cluster.gpu_count;
+  m.comm_ms = cluster.beta_ms_per_token * tokens / cluster.gpu_count;
   m.forward_ms = m.compute_ms + 2.0 * m.comm_ms + cluster.t_misc_ms;
   m.replica_count = cluster.gpu_count;
   m.mem_mb = m.replica_count * model.expert_mem_mb;
   m.cost_mb_ms = (m.compute_ms + 2.0 * m.comm_ms) * m.mem_mb + cluster.t_misc_ms * cluster.m_misc_mb;
   return m;
+}
+
+Placement round_robin_placement(const ScalingPlan& plan, const ClusterSpec& cluster) {
+  const int G = cluster.gpu_count;
+  if (G < 1) throw std::invalid_argument("gpu_count must be >= 1");
+  Placement pl;
+  pl.layer = plan.layer;
+  pl.per_gpu_mem_mb.assign(G, 0.0);
+  int f = 0;  // flat replica index in (expert, ordinal) order
+  for (int c : plan.replica_counts) {
+    std::vector<int> gpus(std::max(c, 0));
+    for (int& g : gpus) {
+      g = f++ % G;
+      pl.per_gpu_mem_mb[g] += plan.expert_mem_mb;
+    }
+    pl.gpu_for.push_back(std::move(gpus));
+  }
+  for (int g = 0; g < G; ++g)
+    if (pl.per_gpu_mem_mb[g] > cluster.gpu_mem_capacity_mb + 1e-9)
+      throw std::runtime_error("round-robin placement does not fit GPU " + to_string(g));
+  return pl;
 }
 
 // ============================================================== report

@@ -240,3 +240,145 @@ def test_route_and_percentile_live(ref):
         v = rng.random(int(rng.integers(1, 300)))
         q = float(rng.random())
         assert pk.percentile(v, q) == ref.ref_percentile(oracle.P(v), len(v), q)
+
+
+# ------------------------------------ baselines / cost-model rows (a8, a10, a11)
+def _ref_or_skip():
+    ref = oracle.ref()
+    if ref is None:
+        pytest.skip("reference library not built")
+    return ref
+
+
+def _random_plan(rng, E, G):
+    loads = rng.integers(0, 5000, E).astype(np.int64)
+    rc = rng.integers(1, 4, E).astype(np.int32)
+    gpu = rng.integers(0, G, int(rc.sum())).astype(np.int32)
+    return loads, rc, gpu
+
+
+def test_static_plan_matches_reference():  # baselines.cpp:32-60
+    ref = _ref_or_skip()
+    rng = np.random.default_rng(11)
+    for _ in range(200):
+        E, G = int(rng.integers(1, 70)), int(rng.integers(1, 9))
+        loads = rng.integers(0, 10000, E).astype(np.int64)
+        want = np.zeros(E, np.int32)
+        assert ref.ref_static_plan(oracle.P(loads), E, G, 22.0, 180000.0, oracle.P(want)) == 0
+        assert pk.static_plan(loads, G, 22.0) == want.tolist()
+    # a placement that does not fit: the reference's wording
+    with pytest.raises(MoeError, match="static placement does not fit GPU 0"):
+        pk.static_plan([1, 2, 3], 1, 100.0, 250.0)
+
+
+def test_round_robin_placement_semantics():  # simulator.cpp:32-50 (anonymous there: restated)
+    assert pk.round_robin_placement([2, 1, 3], 2, 10.0) == [0, 1, 0, 1, 0, 1]
+    assert pk.round_robin_placement([1] * 5, 3, 10.0) == [0, 1, 2, 0, 1]
+    # one replica per expert: identical to the reference's static_plan
+    ref = _ref_or_skip()
+    rng = np.random.default_rng(12)
+    for _ in range(50):
+        E, G = int(rng.integers(1, 70)), int(rng.integers(1, 9))
+        want = np.zeros(E, np.int32)
+        assert ref.ref_static_plan(oracle.P(np.zeros(E, np.int64)), E, G, 1.0, 1e9, oracle.P(want)) == 0
+        assert pk.round_robin_placement([1] * E, G, 1.0) == want.tolist()
+    with pytest.raises(MoeError, match="round-robin placement does not fit GPU 0"):
+        pk.round_robin_placement([3, 1], 2, 100.0, 150.0)
+
+
+def test_gpu_comm_times_matches_reference():  # cost_model.cpp:67-89
+    ref = _ref_or_skip()
+    rng = np.random.default_rng(13)
+    for _ in range(300):
+        E, G = int(rng.integers(1, 40)), int(rng.integers(1, 9))
+        loads, rc, gpu = _random_plan(rng, E, G)
+        beta = float(rng.choice([0.0, 0.002, 0.005, 1.0]))
+        want = np.zeros(G)
+        assert ref.ref_gpu_comm_times(oracle.P(loads), oracle.P(rc), oracle.P(gpu), E, G, beta, oracle.P(want)) == 0
+        assert pk.gpu_comm_times(loads, rc, gpu, G, beta) == want.tolist()  # bit-identical doubles
+
+
+def test_oracle_balance_time_matches_reference():  # baselines.cpp:141-154
+    ref = _ref_or_skip()
+    rng = np.random.default_rng(14)
+    for _ in range(300):
+        E, G = int(rng.integers(1, 70)), int(rng.integers(1, 9))
+        actual = rng.integers(0, 20000, E).astype(np.int64)
+        args = (G, float(rng.random()), float(rng.random() * 0.01), float(rng.random()), float(rng.random() * 100),
+                float(rng.choice([22.0, 352.0])))
+        want = np.zeros(6)
+        assert ref.ref_oracle_balance_time(oracle.P(actual), E, *args, oracle.P(want)) == 0
+        assert list(pk.oracle_balance_time(actual, *args)) == want.tolist()
+
+
+def _ref_verify(ref, loads, rc, shares, alloc, mem, cap, cv, excl):
+    sh = np.asarray(shares, np.int64).reshape(-1, 4)
+    se, so = np.ascontiguousarray(sh[:, 0], np.int32), np.ascontiguousarray(sh[:, 1], np.int32)
+    sn, sd = np.ascontiguousarray(sh[:, 2]), np.ascontiguousarray(sh[:, 3])
+    la, rca = np.ascontiguousarray(loads, np.int64), np.ascontiguousarray(rc, np.int32)
+    ok = np.zeros(1, np.int32)
+    buf = oracle.C.create_string_buffer(1 << 16)
+    assert ref.ref_verify_plan(oracle.P(la), len(la), oracle.P(rca), len(rca), oracle.P(se), oracle.P(so),
+                               oracle.P(sn), oracle.P(sd), len(sh), alloc, mem, cap, cv, int(excl), oracle.P(ok),
+                               buf, len(buf)) == 0
+    return bool(ok[0]), [m for m in buf.value.decode().split("\n") if m]
+
+
+def test_verify_plan_matches_reference():  # scaler.cpp:99-173, incl. broken plans
+    ref = _ref_or_skip()
+    rng = np.random.default_rng(15)
+    n_bad = 0
+    for i in range(400):
+        E = int(rng.integers(1, 20))
+        loads = rng.integers(0, 3000, E).astype(np.int64)
+        mem, cap = 1.0, float(rng.integers(0, 2 * E))
+        plan = pk.scale_experts(loads, mem, cap, 0.2)
+        rc = list(plan.replica_counts)
+        shares = [[e, r, int(loads[e]), rc[e]] for e in range(E) for r in range(rc[e])]
+        alloc = float(plan.alloc_mem_mb)
+        mut = i % 8
+        if mut == 1:
+            rc[int(rng.integers(E))] += 1                      # share count mismatch
+        elif mut == 2 and shares:
+            shares[int(rng.integers(len(shares)))][1] = 99     # out-of-range ordinal
+        elif mut == 3 and shares:
+            shares[int(rng.integers(len(shares)))][2] += 1     # unequal / non-conserving shares
+        elif mut == 4:
+            alloc += 1.0                                       # alloc mismatch
+        elif mut == 5:
+            rc[int(rng.integers(E))] = 0                       # replica count < 1
+        elif mut == 6 and shares:
+            shares[0][0] = E + 3                               # unknown expert
+        elif mut == 7:
+            rc = rc[:-1]                                       # wrong length
+        got = pk.verify_plan(loads, rc, shares, alloc, mem, cap)
+        want = _ref_verify(ref, loads, rc, shares, alloc, mem, cap, 0.2, False)
+        assert got == want, (i, got, want)
+        n_bad += not want[0]
+    assert n_bad > 100  # the mutations exercised the failure paths
+
+
+def test_apply_finetuning_matches_reference():  # predictor.cpp:188-199
+    ref = _ref_or_skip()
+    rng = np.random.default_rng(16)
+    for _ in range(100):
+        n = int(rng.integers(0, 40))
+        acc = rng.random(n)
+        h = float(rng.random())
+        want_acc, want_ft = acc.copy(), np.zeros(max(n, 1), np.int32)
+        assert ref.ref_apply_finetuning(oracle.P(want_acc), n, h, oracle.P(want_ft)) == 0
+        got_acc, got_ft = pk.apply_finetuning(acc, h)
+        assert got_acc == want_acc.tolist() and got_ft == [bool(v) for v in want_ft[:n]]
+
+
+def test_cv_and_serverful_cost_match_reference():  # cost_model.cpp:124-139
+    ref = _ref_or_skip()
+    rng = np.random.default_rng(17)
+    for _ in range(200):
+        v = np.ascontiguousarray(rng.random(int(rng.integers(1, 50))) * rng.choice([0.0, 1.0, 1e3]))
+        assert pk.coefficient_of_variation(v) == ref.ref_coefficient_of_variation(oracle.P(v), len(v))
+        args = (float(rng.random() * 1e4), int(rng.integers(1, 33)), int(rng.integers(1, 65)),
+                float(rng.random() * 400), float(rng.random() * 100))
+        assert pk.serverful_cost(*args) == ref.ref_serverful_cost(*args)
+    with pytest.raises(ValueError, match="CV of an empty sample"):
+        pk.coefficient_of_variation([])
