@@ -67,8 +67,15 @@ enum {
    P2P:      peer memory over NVLink (or ranks sharing one device): dispatch
              stores rows straight into the owning rank's receive buffer and
              combine reads expert outputs from the owner; flags in device
-             memory order the phases.  Requires moe_p2p_export/import. */
-enum { MOE_EXCHANGE_NCCL = 0, MOE_EXCHANGE_EXTERNAL = 1, MOE_EXCHANGE_P2P = 2 };
+             memory order the phases.  Requires moe_p2p_export/import.
+   COPY:     the NCCL path's chunked exchange (same chunk lists and message
+             order) over a copy-engine transport for ranks of ONE process
+             (threads; any devices, peers on one GPU included): a host
+             rendezvous per step, then cudaMemcpyAsync pulls.  The group is
+             the 128 bytes in nccl_unique_id (any value shared by the ranks).
+             Built for multi-rank testing on one GPU and for a single process
+             driving several GPUs. */
+enum { MOE_EXCHANGE_NCCL = 0, MOE_EXCHANGE_EXTERNAL = 1, MOE_EXCHANGE_P2P = 2, MOE_EXCHANGE_COPY = 3 };
 
 /* planning modes for moe_layer_forward */
 enum {

@@ -23,7 +23,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _capi
-from ._capi import (MOE_EXCHANGE_EXTERNAL, MOE_EXCHANGE_NCCL, MOE_EXCHANGE_P2P, MOE_PLAN_FIXED, MOE_PLAN_PREDICTED,
+from ._capi import (MOE_EXCHANGE_COPY, MOE_EXCHANGE_EXTERNAL, MOE_EXCHANGE_NCCL, MOE_EXCHANGE_P2P, MOE_PLAN_FIXED, MOE_PLAN_PREDICTED,
                     MOE_PLAN_SYNC, MoeChunk, MoeCtxDesc, MoeError, MoeLayerStats, MoeP2PHandle, check, lib)
 
 __all__ = [
@@ -33,7 +33,7 @@ __all__ = [
     "MoELayer", "ScalingPlan", "PlaceResult", "synth_tokens", "synth_gate", "synth_expert",
     "stream_key", "nccl_unique_id", "PinnedArray", "MoeError", "MOE_PLAN_FIXED", "MOE_PLAN_SYNC",
     "MOE_PLAN_PREDICTED", "MOE_EXCHANGE_NCCL",
-    "MOE_EXCHANGE_EXTERNAL", "MOE_EXCHANGE_P2P", "LIB_PATH",
+    "MOE_EXCHANGE_EXTERNAL", "MOE_EXCHANGE_P2P", "MOE_EXCHANGE_COPY", "LIB_PATH",
 ]
 LIB_PATH = _capi.LIB_PATH
 

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmoe_b200.so")
 
 MOE_OK, MOE_EINVAL, MOE_EINFEASIBLE, MOE_ECUDA, MOE_ENCCL, MOE_ESTATE = range(6)
-MOE_EXCHANGE_NCCL, MOE_EXCHANGE_EXTERNAL, MOE_EXCHANGE_P2P = 0, 1, 2
+MOE_EXCHANGE_NCCL, MOE_EXCHANGE_EXTERNAL, MOE_EXCHANGE_P2P, MOE_EXCHANGE_COPY = 0, 1, 2, 3
 MOE_PLAN_FIXED, MOE_PLAN_SYNC, MOE_PLAN_PREDICTED = 0, 1, 2
 MOE_PRECISION_BF16, MOE_PRECISION_FP32 = 0, 1
 MOE_RESIDENCY_ALL, MOE_RESIDENCY_PLACED = 0, 1

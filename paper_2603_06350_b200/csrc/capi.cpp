@@ -162,26 +162,20 @@ void stage_exchange(moe_ctx* c, bool forward, cudaStream_t s) {
     CU_CHECK(launch_p2p_wait(c->peers.flags[c->rank], c->G, kind, c->epoch_dev.p, c->p2p_timeout_ns, c->p2p_err, s));
     return;
   }
-  if (c->desc.exchange_mode != MOE_EXCHANGE_NCCL) return;
+  if (!c->transport) return;  // MOE_EXCHANGE_EXTERNAL: the caller moves the chunks
+  // one message per (peer, replica) chunk, in the plan's order on both sides:
+  // forward  = my send buffer -> the owners' received-rows buffers,
+  // backward = my expert outputs -> the sources' return buffers
   const size_t w = static_cast<size_t>(c->xw);  // row width in 16-bit units (bf16 or fp32 rows)
   const size_t row_bytes = w * 2;
-  g_nccl.check(g_nccl.GroupStart(), "ncclGroupStart");
-  if (forward) {
-    for (const Chunk& ch : c->plan.sends)
-      g_nccl.check(g_nccl.Send(c->send.p + ch.row_offset * w, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
-                   "ncclSend");
-    for (const Chunk& ch : c->plan.recvs)
-      g_nccl.check(g_nccl.Recv(c->xp.p + ch.row_offset * w, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
-                   "ncclRecv");
-  } else {
-    for (const Chunk& ch : c->plan.recvs)
-      g_nccl.check(g_nccl.Send(c->yp.p + ch.row_offset * w, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
-                   "ncclSend");
-    for (const Chunk& ch : c->plan.sends)
-      g_nccl.check(g_nccl.Recv(c->ret.p + ch.row_offset * w, ch.rows * row_bytes, ncclUint8, ch.peer, c->comm, s),
-                   "ncclRecv");
-  }
-  g_nccl.check(g_nccl.GroupEnd(), "ncclGroupEnd");
+  std::vector<Msg> sends, recvs;
+  const auto& out = forward ? c->plan.sends : c->plan.recvs;
+  const auto& in = forward ? c->plan.recvs : c->plan.sends;
+  uint16_t* out_base = forward ? c->send.p : c->yp.p;
+  uint16_t* in_base = forward ? c->xp.p : c->ret.p;
+  for (const Chunk& ch : out) sends.push_back(Msg{out_base + ch.row_offset * w, ch.rows * row_bytes, ch.peer});
+  for (const Chunk& ch : in) recvs.push_back(Msg{in_base + ch.row_offset * w, ch.rows * row_bytes, ch.peer});
+  c->transport->exchange(sends, recvs, s);
 }
 
 // K4: which = 0 -> GEMM1 (X -> H, SwiGLU epilogue), 1 -> GEMM2 (H -> Y).
@@ -376,8 +370,8 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
     }
     CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
   } else if (c->G > 1) {
-    require(c->desc.exchange_mode == MOE_EXCHANGE_NCCL, "staged API required for external exchange");
-    g_nccl.check(g_nccl.AllGather(c->counts.p, c->counts_all.p, stride, ncclInt32, c->comm, s), "ncclAllGather");
+    require(c->transport != nullptr, "staged API required for external exchange");
+    c->transport->all_gather(c->counts.p, c->counts_all.p, stride, s);
     CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
   } else if (!mirrored) {
     CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * stride), s));

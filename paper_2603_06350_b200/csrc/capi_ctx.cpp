@@ -291,6 +291,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_PDL_FRONT")) c->pdl_front = std::atoi(v);
     if (const char* v = std::getenv("MOE_SWAP_WPOL")) g_swap_wpol.store(std::atoi(v));
     if (const char* v = std::getenv("MOE_GATE_MAX_SPLITS")) g_gate_max_splits.store(std::max(1, std::atoi(v)));
+    if (const char* v = std::getenv("MOE_P2P_TIMEOUT_MS")) c->p2p_timeout_ns = std::strtoull(v, nullptr, 10) * 1000000ull;
+    require(D.exchange_mode >= MOE_EXCHANGE_NCCL && D.exchange_mode <= MOE_EXCHANGE_COPY, "unknown exchange mode");
     c->registry = moeless::ReplicaRegistry(std::max(0, D.keep_alive_iters));
     c->layers.resize(D.num_layers);
     require(D.precision == MOE_PRECISION_BF16 || D.precision == MOE_PRECISION_FP32, "unknown precision");
@@ -377,7 +379,6 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
         CU_CHECK(cudaStreamCreateWithFlags(&c->wstream, cudaStreamNonBlocking));
         CU_CHECK(cudaEventCreateWithFlags(&c->ev_peers_ready, cudaEventDisableTiming));
       }
-      if (const char* v = std::getenv("MOE_P2P_TIMEOUT_MS")) c->p2p_timeout_ns = std::strtoull(v, nullptr, 10) * 1000000ull;
     }
     c->dplan.alloc(1);
     c->gemm_sched.alloc(4);
@@ -414,6 +415,9 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
       ncclUniqueId id;
       std::memcpy(&id, D.nccl_unique_id, sizeof(id));
       g_nccl.check(g_nccl.CommInitRank(&c->comm, c->G, id, c->rank), "ncclCommInitRank");
+      c->transport = make_nccl_transport(c->comm);
+    } else if (c->G > 1 && D.exchange_mode == MOE_EXCHANGE_COPY) {
+      c->transport = make_copy_transport(D.nccl_unique_id, c->G, c->rank, D.device, c->p2p_timeout_ns);
     }
     *out = c.release();
   });
@@ -424,6 +428,7 @@ int moe_ctx_destroy(moe_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->desc.device);
     cudaStreamSynchronize(c->stream);
+    c->transport.reset();
     if (c->comm) g_nccl.CommDestroy(c->comm);
     for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
     if (c->wstream) cudaStreamSynchronize(c->wstream);

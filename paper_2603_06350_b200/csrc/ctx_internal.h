@@ -26,6 +26,7 @@
 #include "host/exchange_plan.h"
 #include "kernels/dispatch_plan.h"
 #include "moe_b200.h"
+#include "transport.h"
 #include "host/moeless_api.hpp"
 
 namespace moe {
@@ -343,6 +344,7 @@ struct moe_ctx {
   int64_t gemm_seq = 0;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
+  std::unique_ptr<Transport> transport;  // chunked exchange (NCCL / COPY); null for P2P and EXTERNAL
   std::vector<Layer> layers;
   // workspace
   DevBuf<int32_t> ids, counts, counts_all, block_counts, block_pre, pred_counts;
