@@ -443,6 +443,21 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   EventSet& ev = c->events;
   const bool timed = st != nullptr;
   flush_pending_plan(c);  // the previous call's deferred planner work
+  // A caller stream: context uploads (placement table, staged gate weights,
+  // weights) are enqueued on c->stream, so the forward first waits for them,
+  // and later uploads wait for the forward (ForeignStreamOrder's destructor)
+  struct ForeignStreamOrder {
+    moe_ctx* c;
+    cudaStream_t s;
+    ~ForeignStreamOrder() {
+      if (s != c->stream && cudaEventRecord(c->ev_fwd_tail, s) == cudaSuccess)
+        cudaStreamWaitEvent(c->stream, c->ev_fwd_tail, 0);
+    }
+  } order{c, s};
+  if (s != c->stream) {
+    CU_CHECK(cudaEventRecord(c->ev_ctx_tail, c->stream));
+    CU_CHECK(cudaStreamWaitEvent(s, c->ev_ctx_tail, 0));
+  }
   // the fused predictor (K2) runs when the layer has predictor weights: its
   // histograms follow the gate's in the same counts buffer
   const bool with_pred = c->n_pred > 0 && L.has_pred_weights && !c->ext_route;

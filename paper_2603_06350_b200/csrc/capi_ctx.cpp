@@ -407,6 +407,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     *c->ids_err = 0;
     c->events.create();
     CU_CHECK(cudaEventCreateWithFlags(&c->ev_counts, cudaEventDisableTiming));
+    CU_CHECK(cudaEventCreateWithFlags(&c->ev_ctx_tail, cudaEventDisableTiming));
+    CU_CHECK(cudaEventCreateWithFlags(&c->ev_fwd_tail, cudaEventDisableTiming));
     for (auto& tri : c->gemm_ev)
       for (cudaEvent_t& e : tri) CU_CHECK(cudaEventCreate(&e));
     if (c->G > 1 && D.exchange_mode == MOE_EXCHANGE_NCCL) {
@@ -447,6 +449,8 @@ int moe_ctx_destroy(moe_ctx* c) {
     if (c->wg_stage) cudaFreeHost(c->wg_stage);
     if (c->ev_wg_staged) cudaEventDestroy(c->ev_wg_staged);
     if (c->ev_counts) cudaEventDestroy(c->ev_counts);
+    if (c->ev_ctx_tail) cudaEventDestroy(c->ev_ctx_tail);
+    if (c->ev_fwd_tail) cudaEventDestroy(c->ev_fwd_tail);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     for (auto& tri : c->gemm_ev)
       for (cudaEvent_t e : tri)

@@ -380,6 +380,8 @@ struct moe_ctx {
   // single-GPU forward: host planner work deferred until the histogram lands
   PendingPlan pending;
   cudaEvent_t ev_counts = nullptr;
+  // forwards on a caller stream: ordered against the ctx stream's uploads
+  cudaEvent_t ev_ctx_tail = nullptr, ev_fwd_tail = nullptr;
   // caller-given routing (moe_layer_forward_ids): replaces K1 for one forward
   bool ext_route = false;
   const int32_t* ext_ids = nullptr;

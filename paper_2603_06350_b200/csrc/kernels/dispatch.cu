@@ -45,13 +45,18 @@ __global__ void __launch_bounds__(512)
 block_prefix_kernel(const int32_t* __restrict__ block_counts, int nblk, int E,
                     const DevPlan* __restrict__ plan, int32_t* __restrict__ block_pre,
                     const int32_t* __restrict__ local_counts, DevPlan* __restrict__ local_plan) {
-  griddep_wait();               // launched programmatically behind the gate
-  griddep_launch_dependents();  // dispatch CTAs may be scheduled now (they wait for this grid)
+  griddep_wait();  // launched programmatically behind the gate
   const int e = blockIdx.x;
   if (e == E) {
+    // the plan CTA lets dependents start only once the plan is written: with
+    // T == 0 no dispatch runs, and GEMM1 (PDL) reads the segment list early
     plan_local_body(local_counts, E, local_plan);
+    __threadfence();
+    __syncthreads();
+    griddep_launch_dependents();
     return;
   }
+  griddep_launch_dependents();  // dispatch CTAs may be scheduled now (they wait for this grid)
   const int tid = threadIdx.x;
   const int per = (nblk + blockDim.x - 1) / blockDim.x;
   const int b0 = tid * per, b1 = min(nblk, b0 + per);

@@ -800,12 +800,6 @@ cudaError_t launch_grouped_gemm_m256(int epi, const CUtensorMap* tmA, const CUte
                                      const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                      __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream) {
   if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(grouped_gemm_m256_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes4);
-    cudaFuncSetAttribute(grouped_gemm_m256_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes4);
-    configured = true;
-  }
   if (epi == EPI_SWIGLU)
     grouped_gemm_m256_kernel<EPI_SWIGLU><<<num_ctas, kThreads, kSmemBytes4, stream>>>(
         *tmA, *tmB, segs, nseg, n_total, k_total, b_rows_per_slot, out, out_ld);
@@ -1189,14 +1183,6 @@ cudaError_t launch_swap(int which, const CUtensorMap* tmA1, const CUtensorMap* t
                         const CUtensorMap* tmB2, const GemmSeg* segs, const int* nseg, const SwapPass& g1,
                         const SwapPass& g2, int* ready, int ready_n, int num_ctas, cudaStream_t stream, bool pdl) {
   using C = SwapCfg<SNv>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(grouped_gemm_swap_kernel<false, SNv>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::kSmemBytes);
-    cudaFuncSetAttribute(grouped_gemm_swap_kernel<true, SNv>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::kSmemBytes);
-    configured = true;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_ctas);
   cfg.blockDim = dim3(kThreads);
@@ -1240,12 +1226,6 @@ cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUten
                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                     __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream) {
   if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(grouped_gemm_2sm_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes2);
-    cudaFuncSetAttribute(grouped_gemm_2sm_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes2);
-    configured = true;
-  }
   const int grid = num_ctas & ~1;
   if (epi == EPI_SWIGLU)
     grouped_gemm_2sm_kernel<EPI_SWIGLU><<<grid, kThreads, kSmemBytes2, stream>>>(
@@ -1263,12 +1243,6 @@ cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorM
                                 __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, int* sched,
                                 bool pdl, const int32_t* a_gather, int group_m, const FusedCombine& fc) {
   if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(grouped_gemm_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    configured = true;
-  }
   // programmatic dependent launch: the kernel starts while the previous one
   // drains (it waits in griddepcontrol.wait before reading A)
   cudaLaunchConfig_t cfg = {};
@@ -1291,7 +1265,29 @@ cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorM
 // Load every kernel of this file now (CUDA 12 loads kernels lazily on first
 // launch, and a lazy load may wait for the whole context — including a
 // peer-exchange kernel spinning on another rank that shares the context).
+//
+// Also sets the dynamic shared-memory opt-in of every K4 kernel.  The
+// attribute is per device, so this runs for every context after its
+// cudaSetDevice (moe_ctx_create), not once per process.
 cudaError_t preload_gemm_kernels() {
+  const struct {
+    const void* fn;
+    size_t smem;
+  } opt_in[] = {{reinterpret_cast<const void*>(grouped_gemm_kernel<EPI_SWIGLU>), kSmemBytes},
+                {reinterpret_cast<const void*>(grouped_gemm_kernel<EPI_STORE>), kSmemBytes},
+                {reinterpret_cast<const void*>(grouped_gemm_2sm_kernel<EPI_SWIGLU>), kSmemBytes2},
+                {reinterpret_cast<const void*>(grouped_gemm_2sm_kernel<EPI_STORE>), kSmemBytes2},
+                {reinterpret_cast<const void*>(grouped_gemm_m256_kernel<EPI_SWIGLU>), kSmemBytes4},
+                {reinterpret_cast<const void*>(grouped_gemm_m256_kernel<EPI_STORE>), kSmemBytes4},
+                {reinterpret_cast<const void*>(grouped_gemm_swap_kernel<false, 64>), SwapCfg<64>::kSmemBytes},
+                {reinterpret_cast<const void*>(grouped_gemm_swap_kernel<true, 64>), SwapCfg<64>::kSmemBytes},
+                {reinterpret_cast<const void*>(grouped_gemm_swap_kernel<false, 128>), SwapCfg<128>::kSmemBytes},
+                {reinterpret_cast<const void*>(grouped_gemm_swap_kernel<true, 128>), SwapCfg<128>::kSmemBytes}};
+  for (const auto& k : opt_in) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem));
+    if (e != cudaSuccess) return e;
+  }
   cudaFuncAttributes a;
   const void* fns[] = {reinterpret_cast<const void*>(grouped_gemm_kernel<0>),
                        reinterpret_cast<const void*>(grouped_gemm_kernel<1>),

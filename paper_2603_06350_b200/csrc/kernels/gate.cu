@@ -33,6 +33,7 @@
 // Exactness: on the synthetic grid every partial sum is a
 // multiple of 2^-16 below 2^6, so any fp32 summation order — the MMA's
 // included — yields the exact logit, and ids match the CPU oracle bit for bit.
+#include <algorithm>
 #include <cfloat>
 #include <atomic>
 #include <cstdint>
@@ -399,7 +400,8 @@ std::atomic<int> g_gate_max_splits{16};  // env MOE_GATE_MAX_SPLITS (A/B); set a
 int gate_splits(int T, int d) {
   const int nblk = gate_num_blocks(T);
   int s = 1;
-  const int max_s = g_gate_max_splits.load(std::memory_order_relaxed);
+  // gate_finish_kernel sums at most kMaxSplits slices: never split further
+  const int max_s = std::min(g_gate_max_splits.load(std::memory_order_relaxed), kMaxSplits);
   while (s < max_s && nblk * s * 2 <= 2 * 148 && d % (kSlices * 32 * s * 2) == 0) s *= 2;
   return s;
 }

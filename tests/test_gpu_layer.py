@@ -261,3 +261,56 @@ def test_device_gate_update_matches_host_upload(cuda):
         m.close()
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+def test_forward_on_caller_stream_sees_uploads(cuda):
+    """Gate / placement uploads go on the context's stream; a forward on a
+    caller stream issued right after them must see them (and a later upload
+    must not overtake the forward)."""
+    import torch
+    E, k, d, ff, T = 8, 2, 1024, 1408, 512
+    x, wg, experts = _build(E, k, d, ff, T, seed=21)
+    wg2 = wl.gate_weights(E, d, 2.0, 21, 0, 9)
+    m = MoELayer(1, E, k, d, ff, max_tokens=T)
+    ref = MoELayer(1, E, k, d, ff, max_tokens=T)
+    for mm in (m, ref):
+        for e, (w1, w3, w2) in enumerate(experts):
+            mm.load_expert(0, e, w1, w3, w2)
+    xd = _to_dev(x, torch)
+    side = torch.cuda.Stream()
+    outs = []
+    for it, (g, rc) in enumerate([(wg, [1] * E), (wg2, [2, 1, 1, 1, 3, 1, 1, 1]), (wg, [1] * E)]):
+        m.set_gate(0, g)
+        m.set_placement(0, rc, [0] * sum(rc))
+        y = torch.zeros((T, d), dtype=torch.int16, device=cuda)
+        m.forward(0, xd, y, MOE_PLAN_FIXED, it, stream=side.cuda_stream)
+        outs.append(y)
+    torch.cuda.synchronize()
+    for g, y in zip((wg, wg2, wg), outs):
+        ref.set_gate(0, g)
+        y1 = torch.zeros_like(y)
+        ref.forward(0, xd, y1)
+        ref.sync()
+        assert torch.equal(y, y1)
+    m.close()
+    ref.close()
+
+
+def test_empty_forward_then_full(cuda):
+    """T = 0 launches no dispatch; the next forward must not see a stale plan."""
+    import torch
+    E, k, d, ff, T = 8, 2, 1024, 1408, 300
+    x, wg, experts = _build(E, k, d, ff, T, seed=22)
+    m = MoELayer(1, E, k, d, ff, max_tokens=T)
+    m.set_gate(0, wg)
+    for e, (w1, w3, w2) in enumerate(experts):
+        m.load_expert(0, e, w1, w3, w2)
+    xd = _to_dev(x, torch)
+    ys = []
+    for t in (T, 0, T, 0, 0, T):
+        y = torch.zeros((max(t, 1), d), dtype=torch.int16, device=cuda)[:t]
+        m.forward(0, xd[:t], y, MOE_PLAN_FIXED, 0)  # eager, no timing events: PDL chain intact
+        ys.append(y)
+    torch.cuda.synchronize()
+    assert torch.equal(ys[0], ys[2]) and torch.equal(ys[0], ys[5])
+    m.close()
