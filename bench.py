@@ -341,6 +341,10 @@ def run_ours(args):
         local = 0
     torch.cuda.set_device(local)
     dist = None
+    if G > 1 and args.exchange == "nccl":
+        # communicator lines (nRanks, channels, NVLS) on stderr for the driver's check
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if G > 1:
         import torch.distributed as dist
         if shared:

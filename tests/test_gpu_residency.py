@@ -13,6 +13,8 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 import pytest
 
+import oracle
+
 from paper_2603_06350_b200 import (MOE_EXCHANGE_P2P, MOE_PLAN_FIXED, MOE_PLAN_PREDICTED, MOE_PLAN_SYNC, MoeError,
                                    MoELayer)
 from paper_2603_06350_b200 import _capi
@@ -43,6 +45,37 @@ def _parallel(ms, fn):
         return list(ex.map(fn, range(len(ms))))
 
 
+def _check_oracle(x, wg, experts, k, y_dev, ids_dev_layer=None):
+    """Output of one rank vs the CPU oracle on its tokens: per-token relative error <= 2e-2."""
+    y = oracle.bf16_to_f32(y_dev.cpu().numpy().view(np.uint16))
+    y_ref, ids_o, _, counts_o = oracle.layer_forward(x, wg, experts, [1] * len(experts), k, round_h=True)
+    scale = np.maximum(np.max(np.abs(y_ref), axis=1), 1e-6)
+    assert float(np.max(np.max(np.abs(y - y_ref), axis=1) / scale)) <= 2e-2
+    return counts_o
+
+
+class RefPlanner:
+    """The compiled reference's scale_experts -> place_experts -> update_registry
+    sequence (placer.cpp:11-43,45-130) on the all-gathered loads."""
+
+    def __init__(self, keep_alive=50):
+        self.ref = oracle.ref()
+        self.reg = self.ref.ref_registry_new(keep_alive) if self.ref else None
+
+    def step(self, loads, E, G, mem, cap, it):
+        ref = self.ref
+        la = np.ascontiguousarray(loads, np.int64)
+        rc = np.zeros(E, np.int32)
+        assert ref.ref_scale_experts(oracle.P(la), E, 0, mem, cap, 0.2, 0, oracle.P(rc), None, None, None, 0,
+                                     None, None) == 0
+        gpu = np.zeros(int(rc.sum()), np.int32)
+        warm, cold = np.zeros(1, np.int32), np.zeros(1, np.int32)
+        assert ref.ref_place_experts(self.reg, oracle.P(la), oracle.P(rc), E, 0, mem, G, 180000.0, it, 0, 0.0, 1.0,
+                                     oracle.P(gpu), oracle.P(warm), oracle.P(cold)) == 0
+        assert ref.ref_update_registry(self.reg, oracle.P(rc), oracle.P(gpu), E, G, 0, it) == 0
+        return rc, gpu, int(warm[0]), int(cold[0])
+
+
 def _check_residency(m, layer, rc, rg, G, rank):
     slot_of, n_slots = m.residency(layer)
     E = len(rc)
@@ -69,8 +102,12 @@ def test_placed_sync_planner_bit_identical(cuda):
     for m in ms + [one]:
         for e in range(E):
             m.load_expert(0, e, *wl.expert_weights(d, ff, 1, 0, e))
-    xd = [torch.from_numpy(wl.tokens(T, d, E, 1, 90 + r).view(np.int16)).to(cuda) for r in range(G)]
+    xs = [wl.tokens(T, d, E, 1, 90 + r) for r in range(G)]
+    xd = [torch.from_numpy(x.view(np.int16)).to(cuda) for x in xs]
     yd = [torch.zeros((T, d), dtype=torch.int16, device=cuda) for _ in range(G)]
+    experts = [wl.expert_weights(d, ff, 1, 0, e) for e in range(E)]
+    mem = 3.0 * d * ff * 2 / 1e6
+    refp = RefPlanner(50)
     copies, hits = 0, 0
     for it in range(6):
         wg = wl.gate_weights(E, d, 1.6, 1, 0, it // 2)  # the routing changes every other iteration
@@ -78,6 +115,16 @@ def test_placed_sync_planner_bit_identical(cuda):
             m.set_gate(0, wg)
         sts = _parallel(ms, lambda r: ms[r].forward(0, xd[r], yd[r], MOE_PLAN_SYNC, it, stats=True))
         torch.cuda.synchronize()
+        # outputs and histograms vs the oracle; the placement and its warm/cold split
+        # vs the compiled reference's planner + registry on the same global loads
+        loads = sum(_check_oracle(xs[r], wg, experts, k, yd[r]).astype(np.int64) for r in range(G))
+        if refp.ref is not None:
+            rc, gpu, warm, cold = refp.step(loads, E, G, mem, (E + 6) * mem, it)
+            prc, prg = ms[0].placement(0)
+            assert np.array_equal(prc, rc) and np.array_equal(prg, gpu), it
+            assert (sts[0].warm_count, sts[0].cold_count) == (warm, cold), it
+            for r in range(G):  # a replica off its home rank is resident after the forward
+                _check_residency(ms[r], 0, rc, gpu, G, r)
         for r in range(G):
             st = sts[r]
             copies += st.weight_copies
@@ -104,7 +151,10 @@ def test_placed_eviction_with_small_cache(cuda):
         for e in range(E):
             m.load_expert(0, e, *wl.expert_weights(d, ff, 1, 0, e))
         m.set_gate(0, wl.gate_weights(E, d, 1.2, 1, 0, 0))
-    xd = [torch.from_numpy(wl.tokens(T, d, E, 1, 700 + r).view(np.int16)).to(cuda) for r in range(G)]
+    xs = [wl.tokens(T, d, E, 1, 700 + r) for r in range(G)]
+    xd = [torch.from_numpy(x.view(np.int16)).to(cuda) for x in xs]
+    experts = [wl.expert_weights(d, ff, 1, 0, e) for e in range(E)]
+    wg = wl.gate_weights(E, d, 1.2, 1, 0, 0)
     yd = [torch.zeros((T, d), dtype=torch.int16, device=cuda) for _ in range(G)]
     # odd experts are home on rank 1; each placement moves two of them to rank 0
     moves = [(1, 3), (5, 7), (1, 5), (3, 7), (1, 3)]
@@ -122,6 +172,7 @@ def test_placed_eviction_with_small_cache(cuda):
         assert (sts[0].weight_copies, sts[0].weight_hits) == [(2, 0), (2, 0), (1, 1), (2, 0), (1, 1)][it]
         assert sts[1].weight_copies == 0
         for r in range(G):
+            _check_oracle(xs[r], wg, experts, k, yd[r])  # copied-in weights compute the oracle's layer
             y1 = torch.zeros_like(yd[r])
             one.forward(0, xd[r], y1, MOE_PLAN_FIXED, it)
             one.sync()
