@@ -179,19 +179,21 @@ void stage_exchange(moe_ctx* c, bool forward, cudaStream_t s) {
 }
 
 // K4: which = 0 -> GEMM1 (X -> H, SwiGLU epilogue), 1 -> GEMM2 (H -> Y).
-// Default: the 1-SM kernel.  The 2-SM (cta_group::2, 256-row tile) kernel
-// reaches ~88% tensor-pipe utilisation per clock vs ~80%, but under the
-// B200's 1 kW cap it settles ~190 MHz lower and nets ~4% less throughput on
-// the Mixtral layer (profiles/ab_gemm_variants_r01.md), so it is opt-in
-// (MOE_GEMM_VARIANT=2sm) until it is made more energy-efficient.
+// Prefill default: the 2-SM (cta_group::2, 256-row tile) kernel, launched
+// programmatically like the 1-SM kernel (it lost ~4% to it under the 1 kW cap
+// before it had PDL, profiles/ab_gemm_variants_r01.md; with PDL it wins,
+// profiles/ab_2sm_pdl_r02.md).  MOE_GEMM_VARIANT=1sm / mc select the 1-SM
+// kernel or its cluster-multicast form.
 // Swap-AB tiles (weights as the M operand, tokens as N; GEMM1 and GEMM2 in one
 // launch): 64-token tiles when the batch leaves a few dozen rows per expert
 // (decode: 128-row tiles would be mostly padding), 128-token tiles for
 // mid-size batches (same MMA work per stage as the 1-SM kernel, no tail
-// between the GEMMs).  Returns the tile's token rows, 0 = the 1-SM kernel
+// between the GEMMs).  Returns the tile's token rows, 0 = the 128/256-row kernels
 // (profiles/ab_swap_r01.md).
 int use_swap(const moe_ctx* c, int T) {
-  if (c->fp32 || T <= 0 || c->gemm_variant == 1 || c->gemm_variant == 2 || c->gemm_variant == 3) return 0;
+  if (c->fp32 || T <= 0 || c->gemm_variant == 1 || c->gemm_variant == 2 || c->gemm_variant == 3 ||
+      c->gemm_variant == 7)
+    return 0;
   const int64_t mean_rows = static_cast<int64_t>(T) * c->k * c->G / std::max(1, c->E);  // balanced EP
   if (c->gemm_variant == 5) return 64;
   if (c->gemm_variant == 6) return 128;
@@ -229,9 +231,34 @@ void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t r
     }
     return;
   }
-  const bool two_sm = c->gemm_variant == 2, m256 = c->gemm_variant == 3;
-  if (two_sm || m256) {
-    auto fn = two_sm ? launch_grouped_gemm_2sm : launch_grouped_gemm_m256;
+  if (c->gemm_variant == 7) {  // cluster pairs sharing B through TMA multicast
+    const int n = which == 0 ? 2 * c->ff : c->d, kk = which == 0 ? c->d : c->ff;
+    CU_CHECK(launch_grouped_gemm_mc(which == 0 ? 0 : 1, which == 0 ? &c->tmA1 : &c->tmA2,
+                                    which == 0 ? &L.tmB1h : &L.tmB2h, c->dplan.p->segs, &c->dplan.p->nseg, n, kk, n,
+                                    reinterpret_cast<__nv_bfloat16*>(which == 0 ? c->h.p : c->yp.p),
+                                    which == 0 ? c->ff : c->d, c->num_sms, s, c->use_pdl, c->group_m[which]));
+    return;
+  }
+  // default (auto) for batches past the swap-AB range: the 2-SM cta_group::2
+  // kernel (256-row tiles, B split across the SM pair, PDL behind its
+  // producer) — +4-5% tokens/s at cfg2 over the 1-SM kernel in short and
+  // 150-step runs alike (profiles/ab_2sm_pdl_r02.md); the 1-SM kernel keeps the
+  // opt-in gather / fused-combine / dynamic-scheduler paths
+  const bool two_sm = c->gemm_variant == 2 || (c->gemm_variant == 0 && !gather && !fused_y && !c->dyn_sched);
+  const bool m256 = c->gemm_variant == 3;
+  if (two_sm) {
+    if (which == 0)
+      CU_CHECK(launch_grouped_gemm_2sm(0, &c->tmA1, &L.tmB1h, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d,
+                                       2 * c->ff, reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, c->num_sms, s,
+                                       c->use_pdl, c->group_m[0]));
+    else
+      CU_CHECK(launch_grouped_gemm_2sm(1, &c->tmA2, &L.tmB2h, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
+                                       reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s, c->use_pdl,
+                                       c->group_m[1]));
+    return;
+  }
+  if (m256) {
+    auto fn = launch_grouped_gemm_m256;
     const CUtensorMap* a1 = m256 ? &c->tmA1w : &c->tmA1;
     const CUtensorMap* a2 = m256 ? &c->tmA2w : &c->tmA2;
     if (which == 0)

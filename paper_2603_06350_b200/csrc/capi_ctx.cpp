@@ -283,6 +283,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
                         : s == "swap"   ? 4
                         : s == "swap64" ? 5
                         : s == "swap128" ? 6
+                        : s == "mc"     ? 7
                                          : 0;
     }
     if (const char* v = std::getenv("MOE_GEMM_SWAP_ROWS")) c->swap_rows = std::atoi(v);

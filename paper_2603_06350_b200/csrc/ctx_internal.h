@@ -78,7 +78,12 @@ cudaError_t launch_grouped_gemm_m256(int epi, const CUtensorMap* tmA, const CUte
                                      __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream);
 cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
-                                    __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream);
+                                    __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl = false,
+                                    int group_m = 0);
+cudaError_t launch_grouped_gemm_mc(int epi, const CUtensorMap* tmA, const CUtensorMap* tmBh, const GemmSeg* segs,
+                                   const int* nseg, int n_total, int k_total, int b_rows_per_slot,
+                                   __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl,
+                                   int group_m);
 cudaError_t launch_grouped_gemm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                 const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                 __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, int* sched,
@@ -295,7 +300,7 @@ struct EventSet {
 struct moe_ctx {
   moe_ctx_desc desc{};
   int E = 0, k = 0, d = 0, ff = 0, G = 1, rank = 0, Tmax = 0, n_pred = 0, num_sms = 148;
-  int gemm_variant = 0;  // 0 auto, 1 force 1-SM, 2 force 2-SM, 3 m256, 4 swap-AB, 5 swap64, 6 swap128 (MOE_GEMM_VARIANT)
+  int gemm_variant = 0;  // 0 auto, 1 force 1-SM, 2 force 2-SM, 3 m256, 4 swap-AB, 5 swap64, 6 swap128, 7 mc (MOE_GEMM_VARIANT)
   int swap_rows = 64;    // auto: 64-token swap-AB tiles when the mean rows per expert <= this (MOE_GEMM_SWAP_ROWS)
   int swap128_rows = 1024;  // auto: 128-token swap-AB tiles (fused GEMMs) up to this mean (MOE_GEMM_SWAP128_ROWS)
   int gemm_T = 0;        // tokens of the forward whose GEMMs are being enqueued

@@ -447,36 +447,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   }
 }
 
-// ===================================================================
-// 2-CTA variant: a cluster of 2 SMs computes a 256x256 tile with
-// tcgen05.mma.cta_group::2 (M=256).  Each CTA stages its own 128 A rows and
-// HALF of the 256 B rows (the W1 block on CTA 0, the W3 block on CTA 1 for
-// GEMM1), so per SM and k-block it moves 32 KB instead of 48 KB through
-// L2 -> smem for the same MMA work; both CTAs' TMA bytes land on the leader's
-// full barrier, the leader's single MMA thread issues for the pair, commits
-// multicast to both CTAs' empty / tmem-full barriers, and both CTAs' epilogue
-// warps (each reading its own TMEM: 128 rows x 256 cols) release the
-// accumulator on the leader's tmem-empty barrier (8 arrivals).
-constexpr int BM2 = 256;                 // rows per cluster tile
-constexpr int STAGES2 = 6;
-constexpr uint32_t kHalfA = 128 * BK * 2, kHalfB = 128 * BK * 2;  // 16 KB each, per CTA
-constexpr uint32_t kStage2 = kHalfA + kHalfB;
-
-template <int EPI> constexpr int kGroupM2 = EPI == 0 ? 16 : 8;  // in 256-row tiles
-
-struct SmemLayout2 {
-  static constexpr uint32_t a = 0;
-  static constexpr uint32_t b = a + STAGES2 * kHalfA;
-  static constexpr uint32_t bars = b + STAGES2 * kHalfB;
-  static constexpr uint32_t n_bars = 2 * STAGES2 + 4;
-  static constexpr uint32_t tmem_slot = bars + n_bars * 8;
-  static constexpr uint32_t seg_tiles = tmem_slot + 16;
-  static constexpr uint32_t segs = seg_tiles + (kMaxSegs + 1) * 4 + 12;
-  static constexpr uint32_t end = ((segs + 15) / 16) * 16 + kMaxSegs * 16;
-};
-constexpr uint32_t kSmemBytes2 = SmemLayout2::end + 1024;
-static_assert(kSmemBytes2 <= 232448, "smem budget (2-CTA)");
-
+// One epilogue warp's 32 rows of a 128x256 accumulator -> bf16 (SwiGLU: the
+// 128 gate/up column pairs -> 128 columns of H).
 template <int EPI>
 __device__ __forceinline__ void store_accumulator(uint32_t taddr, __nv_bfloat16* __restrict__ out, size_t grow,
                                                   bool valid, int n, int out_ld) {
@@ -520,11 +492,252 @@ __device__ __forceinline__ void store_accumulator(uint32_t taddr, __nv_bfloat16*
   }
 }
 
+// ===================================================================
+// Cluster-multicast variant ("mc"): a cluster of 2 CTAs computes the two
+// vertically adjacent 128x256 tiles m = 2p, 2p+1 of one segment and n tile
+// with the 1-SM MMA (cta_group::1, M=128, N=256, own TMEM accumulators).  The
+// B tile both need is read from L2 ONCE: each CTA's TMA fetches one 128-row
+// half and multicasts it into both CTAs' shared memory, so per SM and k-block
+// 16 KB of A + 16 KB of B cross L2 -> SM instead of 48 KB, while every MMA
+// operand stays in the CTA's own smem (the cta_group::2 kernel instead reads
+// half of B from the peer SM on every MMA).  A stage is free once BOTH CTAs'
+// MMAs have read it: each MMA commit arrives multicast on the empty barriers
+// of the two CTAs (count 2).  When a segment has an odd number of m-tiles the
+// last pair's second CTA has no rows: it loads and multicasts its half of B,
+// skips A and the MMAs, and releases each stage with plain cluster arrives.
+template <int EPI> constexpr int kGroupMmc = EPI == 0 ? 16 : 8;  // in 256-row pairs
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+grouped_gemm_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
+                       const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total, int k_total,
+                       int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld, int group_m) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout::bars);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint64_t* ring_full = bars + 2 * STAGES + 4;
+  uint64_t* ring_empty = ring_full + kTileRing;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SmemLayout::tmem_slot);
+  volatile int* ring = reinterpret_cast<volatile int*>(smem + SmemLayout::tile_ring);
+  int* seg_tiles = reinterpret_cast<int*>(smem + SmemLayout::seg_tiles);
+  int4* segs = reinterpret_cast<int4*>(smem + SmemLayout::segs);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  const int rank = static_cast<int>(cluster_ctarank());
+  const int cluster = blockIdx.x >> 1, num_clusters = gridDim.x >> 1;
+  const int nseg = min(*nseg_g, kMaxSegs);
+  const int n_tiles = n_total / BN;
+
+  for (int i = threadIdx.x; i < nseg; i += kThreads) segs[i] = reinterpret_cast<const int4*>(segs_g)[i];
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmBh);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 2); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    for (int r = 0; r < kTileRing; ++r) { mbar_init(&ring_full[r], 1); mbar_init(&ring_empty[r], 5); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int s = 0; s < nseg; ++s) {
+      seg_tiles[s] = acc;
+      acc += ((segs[s].y + 2 * BM - 1) / (2 * BM)) * n_tiles;
+    }
+    seg_tiles[nseg] = acc;
+  }
+  tc_fence_before();
+  cluster_sync();  // both CTAs' barriers exist before any multicast or remote arrive
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_tiles = nseg > 0 ? seg_tiles[nseg] : 0;
+  const int num_kb = k_total / BK;
+  griddep_launch_dependents();
+
+  // this CTA's m-tile of pair tile t, and whether it has any rows
+  auto my_tile = [&](int t, TileCoord& c) {
+    c = decode_tile<kGroupMmc<EPI>, 2 * BM>(t, seg_tiles, segs, nseg, n_tiles, group_m);
+    c.m = 2 * c.m + rank;
+    return c.m * BM < segs[c.seg].y;
+  };
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int rslot = 0;
+      uint32_t rphase = 0;
+      const uint64_t pol_b = policy_evict_last();
+      bool first = true;
+      for (int t = cluster;; t += num_clusters) {
+        mbar_wait(&ring_empty[rslot], rphase ^ 1);
+        ring[rslot] = t < total_tiles ? t : -1;
+        mbar_arrive(&ring_full[rslot]);
+        if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
+        if (t >= total_tiles) break;
+        TileCoord c;
+        const bool mine = my_tile(t, c);
+        const int a_row = segs[c.seg].x + c.m * BM;
+        const int b_row = segs[c.seg].z * b_rows_per_slot + c.n * BN + rank * (BN / 2);
+        const uint32_t bytes = (mine ? kStageBytesA : 0u) + kStageBytesB;
+        const uint32_t b_off = static_cast<uint32_t>(rank) * (kStageBytesB / 2);
+        int kb0 = 0;
+        if (first) {
+          // weights first (they do not depend on the previous kernel), then A
+          first = false;
+          kb0 = num_kb < STAGES ? num_kb : STAGES;
+          for (int kb = 0; kb < kb0; ++kb) {
+            mbar_arrive_expect_tx(&full[kb], bytes);
+            tma_load_2d_mc(smem + SmemLayout::b + kb * kStageBytesB + b_off, &tmBh, &full[kb], kb * BK, b_row, 0x3,
+                           pol_b);
+          }
+          griddep_wait();
+          if (mine)
+            for (int kb = 0; kb < kb0; ++kb)
+              tma_load_2d(smem + SmemLayout::a + kb * kStageBytesA, &tmA, &full[kb], kb * BK, a_row);
+          stage = kb0 == STAGES ? 0 : kb0;
+          phase = kb0 == STAGES ? 1u : 0u;
+        }
+        for (int kb = kb0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);  // both CTAs have consumed this stage
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          if (mine) tma_load_2d(smem + SmemLayout::a + stage * kStageBytesA, &tmA, &full[stage], kb * BK, a_row);
+          tma_load_2d_mc(smem + SmemLayout::b + stage * kStageBytesB + b_off, &tmBh, &full[stage], kb * BK, b_row,
+                         0x3, pol_b);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      const uint32_t peer_empty0 = mapa_shared(smem_u32(&empty[0]), static_cast<uint32_t>(rank ^ 1));
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      const uint32_t a_base = smem_u32(smem + SmemLayout::a);
+      const uint32_t b_base = smem_u32(smem + SmemLayout::b);
+      int rslot = 0;
+      uint32_t rphase = 0;
+      while (true) {
+        mbar_wait(&ring_full[rslot], rphase);
+        const int t = ring[rslot];
+        mbar_arrive(&ring_empty[rslot]);
+        if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
+        if (t < 0) break;
+        TileCoord c;
+        if (!my_tile(t, c)) {
+          // no rows here: release each stage of the shared B on both CTAs
+          for (int kb = 0; kb < num_kb; ++kb) {
+            mbar_wait(&full[stage], phase);
+            mbar_arrive(&empty[stage]);
+            mbar_arrive_cluster(peer_empty0 + stage * 8);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          continue;
+        }
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = umma_desc_sw128(a_base + stage * kStageBytesA);
+          const uint64_t bdesc = umma_desc_sw128(b_base + stage * kStageBytesB);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            tc_mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          tc_commit_mc(&empty[stage], 0x3);  // this CTA has read the stage: tell both producers
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // --------------------------------------------------------- epilogue
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int rslot = 0;
+    uint32_t rphase = 0;
+    while (true) {
+      mbar_wait(&ring_full[rslot], rphase);
+      const int t = ring[rslot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ring_empty[rslot]);
+      if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
+      if (t < 0) break;
+      TileCoord c;
+      if (!my_tile(t, c)) continue;
+      const int4 sg = segs[c.seg];
+      const int row = c.m * BM + quarter * 32 + lane;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      if (c.m * BM + quarter * 32 < sg.y) {
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+        store_accumulator<EPI>(taddr, out, static_cast<size_t>(sg.x + row), row < sg.y, c.n, out_ld);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  griddep_wait();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer must not exit while this CTA still multicasts into it
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// ===================================================================
+// 2-CTA variant: a cluster of 2 SMs computes a 256x256 tile with
+// tcgen05.mma.cta_group::2 (M=256).  Each CTA stages its own 128 A rows and
+// HALF of the 256 B rows (the W1 block on CTA 0, the W3 block on CTA 1 for
+// GEMM1), so per SM and k-block it moves 32 KB instead of 48 KB through
+// L2 -> smem for the same MMA work; both CTAs' TMA bytes land on the leader's
+// full barrier, the leader's single MMA thread issues for the pair, commits
+// multicast to both CTAs' empty / tmem-full barriers, and both CTAs' epilogue
+// warps (each reading its own TMEM: 128 rows x 256 cols) release the
+// accumulator on the leader's tmem-empty barrier (8 arrivals).
+constexpr int BM2 = 256;                 // rows per cluster tile
+constexpr int STAGES2 = 6;
+constexpr uint32_t kHalfA = 128 * BK * 2, kHalfB = 128 * BK * 2;  // 16 KB each, per CTA
+constexpr uint32_t kStage2 = kHalfA + kHalfB;
+
+template <int EPI> constexpr int kGroupM2 = EPI == 0 ? 16 : 8;  // in 256-row tiles
+
+struct SmemLayout2 {
+  static constexpr uint32_t a = 0;
+  static constexpr uint32_t b = a + STAGES2 * kHalfA;
+  static constexpr uint32_t bars = b + STAGES2 * kHalfB;
+  static constexpr uint32_t n_bars = 2 * STAGES2 + 4;
+  static constexpr uint32_t tmem_slot = bars + n_bars * 8;
+  static constexpr uint32_t seg_tiles = tmem_slot + 16;
+  static constexpr uint32_t segs = seg_tiles + (kMaxSegs + 1) * 4 + 12;
+  static constexpr uint32_t end = ((segs + 15) / 16) * 16 + kMaxSegs * 16;
+};
+constexpr uint32_t kSmemBytes2 = SmemLayout2::end + 1024;
+static_assert(kSmemBytes2 <= 232448, "smem budget (2-CTA)");
+
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total, int k_total,
-                        int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld) {
+                        int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld, int group_m) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout2::bars);
@@ -568,6 +781,9 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = nseg > 0 ? seg_tiles[nseg] : 0;
   const int num_kb = k_total / BK;
+  // the next kernel (GEMM2 after GEMM1) may launch now and stream its weights
+  // while this grid's CTAs retire
+  griddep_launch_dependents();
 
   if (warp == 0) {
     // ---------------------------------------------------------- producer (both CTAs)
@@ -577,11 +793,28 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
       // A tiles are reused by every n tile of the group: evict_first here made
       // GEMM1 re-read them from HBM (21 GB per launch instead of 3 GB)
       const uint64_t pol_a = policy_evict_normal(), pol_b = policy_evict_last();
+      bool first = true;
       for (int t = cluster; t < total_tiles; t += num_clusters) {
-        const TileCoord c = decode_tile<kGroupM2<EPI>, BM2>(t, seg_tiles, segs, nseg, n_tiles);
+        const TileCoord c = decode_tile<kGroupM2<EPI>, BM2>(t, seg_tiles, segs, nseg, n_tiles, group_m);
         const int a_row = segs[c.seg].x + c.m * BM2 + static_cast<int>(rank) * 128;
         const int b_row = segs[c.seg].z * b_rows_per_slot + c.n * BN + static_cast<int>(rank) * 128;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        int kb0 = 0;
+        if (first) {
+          // launched programmatically behind the kernel that produces A: stream
+          // the first weight stages while it drains, then wait for it
+          first = false;
+          kb0 = num_kb < STAGES2 ? num_kb : STAGES2;
+          for (int kb = 0; kb < kb0; ++kb) {
+            if (leader) mbar_arrive_expect_tx(&full[kb], 2 * kStage2);  // fresh stages: no empty wait
+            tma_load_2d_2sm(smem + SmemLayout2::b + kb * kHalfB, &tmB, &full[kb], kb * BK, b_row, pol_b);
+          }
+          griddep_wait();
+          for (int kb = 0; kb < kb0; ++kb)
+            tma_load_2d_2sm(smem + SmemLayout2::a + kb * kHalfA, &tmA, &full[kb], kb * BK, a_row, pol_a);
+          stage = kb0 == STAGES2 ? 0 : kb0;
+          phase = kb0 == STAGES2 ? 1u : 0u;
+        }
+        for (int kb = kb0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStage2);
           tma_load_2d_2sm(smem + SmemLayout2::a + stage * kHalfA, &tmA, &full[stage], kb * BK, a_row, pol_a);
@@ -626,7 +859,7 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cluster; t < total_tiles; t += num_clusters) {
-      const TileCoord c = decode_tile<kGroupM2<EPI>, BM2>(t, seg_tiles, segs, nseg, n_tiles);
+      const TileCoord c = decode_tile<kGroupM2<EPI>, BM2>(t, seg_tiles, segs, nseg, n_tiles, group_m);
       const int4 sg = segs[c.seg];
       const int row = c.m * BM2 + static_cast<int>(rank) * 128 + quarter * 32 + lane;
       mbar_wait(&tfull[acc], acc_phase);
@@ -639,6 +872,7 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
+  griddep_wait();  // a CTA without tiles never waited: keep stream order for later kernels
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // the peer must not exit while the leader still multicasts to it
@@ -1224,16 +1458,49 @@ static_assert(kSmemBytes <= 232448, "smem budget");
 
 cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
-                                    __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream) {
+                                    __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl,
+                                    int group_m) {
   if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
-  const int grid = num_ctas & ~1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_ctas & ~1);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes2;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int gp = group_m > 0 ? (group_m + 1) / 2 : 0;  // m-tiles -> 256-row tiles
   if (epi == EPI_SWIGLU)
-    grouped_gemm_2sm_kernel<EPI_SWIGLU><<<grid, kThreads, kSmemBytes2, stream>>>(
-        *tmA, *tmB, segs, nseg, n_total, k_total, b_rows_per_slot, out, out_ld);
-  else
-    grouped_gemm_2sm_kernel<EPI_STORE><<<grid, kThreads, kSmemBytes2, stream>>>(
-        *tmA, *tmB, segs, nseg, n_total, k_total, b_rows_per_slot, out, out_ld);
-  return cudaGetLastError();
+    return cudaLaunchKernelEx(&cfg, grouped_gemm_2sm_kernel<EPI_SWIGLU>, *tmA, *tmB, segs, nseg, n_total, k_total,
+                              b_rows_per_slot, out, out_ld, gp);
+  return cudaLaunchKernelEx(&cfg, grouped_gemm_2sm_kernel<EPI_STORE>, *tmA, *tmB, segs, nseg, n_total, k_total,
+                            b_rows_per_slot, out, out_ld, gp);
+}
+
+cudaError_t launch_grouped_gemm_mc(int epi, const CUtensorMap* tmA, const CUtensorMap* tmBh, const GemmSeg* segs,
+                                   const int* nseg, int n_total, int k_total, int b_rows_per_slot,
+                                   __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl,
+                                   int group_m) {
+  if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_ctas & ~1);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // group_m counts m-tiles; the kernel sweeps pairs of them
+  const int gp = group_m > 0 ? (group_m + 1) / 2 : 0;
+  if (epi == EPI_SWIGLU)
+    return cudaLaunchKernelEx(&cfg, grouped_gemm_mc_kernel<EPI_SWIGLU>, *tmA, *tmBh, segs, nseg, n_total, k_total,
+                              b_rows_per_slot, out, out_ld, gp);
+  return cudaLaunchKernelEx(&cfg, grouped_gemm_mc_kernel<EPI_STORE>, *tmA, *tmBh, segs, nseg, n_total, k_total,
+                            b_rows_per_slot, out, out_ld, gp);
 }
 
 int gemm_smem_bytes() { return static_cast<int>(kSmemBytes); }
@@ -1275,6 +1542,8 @@ cudaError_t preload_gemm_kernels() {
     size_t smem;
   } opt_in[] = {{reinterpret_cast<const void*>(grouped_gemm_kernel<EPI_SWIGLU>), kSmemBytes},
                 {reinterpret_cast<const void*>(grouped_gemm_kernel<EPI_STORE>), kSmemBytes},
+                {reinterpret_cast<const void*>(grouped_gemm_mc_kernel<EPI_SWIGLU>), kSmemBytes},
+                {reinterpret_cast<const void*>(grouped_gemm_mc_kernel<EPI_STORE>), kSmemBytes},
                 {reinterpret_cast<const void*>(grouped_gemm_2sm_kernel<EPI_SWIGLU>), kSmemBytes2},
                 {reinterpret_cast<const void*>(grouped_gemm_2sm_kernel<EPI_STORE>), kSmemBytes2},
                 {reinterpret_cast<const void*>(grouped_gemm_m256_kernel<EPI_SWIGLU>), kSmemBytes4},

@@ -291,6 +291,26 @@ __device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// cta_group::1 TMA load delivered to every CTA of the cluster in `mask`, at the
+// same shared-memory offset, signalling the mbarrier at the same offset in each
+__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const void* desc, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+      : "memory");
+}
+
+// cta_group::1 commit whose mbarrier arrive lands in every CTA of `mask`
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 // --------------------------------------------------------------- misc
 __device__ __forceinline__ int4 ld_nc_v4(const void* p) {
   int4 r;

@@ -54,8 +54,9 @@ def test_variants_agree_and_match_oracle(cuda, E, k, d, ff, T, rc):
     _, _, _, y5 = _run(cuda, "swap", E, k, d, ff, T, rc, env={"MOE_SWAP_FUSE": "0"})
     _, _, _, y6 = _run(cuda, "swap64", E, k, d, ff, T, rc)
     _, _, _, y7 = _run(cuda, "swap128", E, k, d, ff, T, rc)
+    _, _, _, y8 = _run(cuda, "mc", E, k, d, ff, T, rc)  # cluster pairs, B multicast
     y_ref = oracle.layer_forward(x, wg, experts, rc, k)[0]
-    for y in (y1, y2, y3, y4, y5, y6, y7):
+    for y in (y1, y2, y3, y4, y5, y6, y7, y8):
         err = float(np.max(np.abs(y - y_ref)) / np.max(np.abs(y_ref)))
         assert err <= 2e-2, err
     # same K order per output element, same fp32 accumulation: bit-identical outputs
@@ -64,6 +65,7 @@ def test_variants_agree_and_match_oracle(cuda, E, k, d, ff, T, rc):
     assert np.array_equal(y1, y4), float(np.max(np.abs(y1 - y4)))
     assert np.array_equal(y1, y5), float(np.max(np.abs(y1 - y5)))
     assert np.array_equal(y1, y6) and np.array_equal(y1, y7)
+    assert np.array_equal(y1, y8)  # multicast B: the same MMAs on the same operands
 
 
 def test_swap_fused_repeated_forwards(cuda):
