@@ -570,7 +570,7 @@ def run_ours(args):
             # plan upload, prefix, dispatch, GEMM1, GEMM2, combine (NCCL's own kernels and the
             # gate-weight memcpy not counted)
             "gpu_launches": (12 if p2p else (8 if G > 1 else 6 + (1 if T <= 32 * 148 else 0))) * args.steps,
-            "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel (GEMM1 SwiGLU + GEMM2)",
+            "roofline": {"bound": "tensor", "kernel": "grouped_gemm_2sm_kernel (GEMM1 SwiGLU + GEMM2)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "peak_source": peak_src + ", bf16 sustained", "burst_peak": peaks.get("bf16_tflops"),
                          "algorithmic_flops_per_step": statistics.median(gflop),

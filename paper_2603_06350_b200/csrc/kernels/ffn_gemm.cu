@@ -737,7 +737,7 @@ template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total, int k_total,
-                        int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld, int group_m) {
+                        int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld, int group_m, int l2pol) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout2::bars);
@@ -792,7 +792,12 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
       uint32_t phase = 0;
       // A tiles are reused by every n tile of the group: evict_first here made
       // GEMM1 re-read them from HBM (21 GB per launch instead of 3 GB)
-      const uint64_t pol_a = policy_evict_normal(), pol_b = policy_evict_last();
+      // l2pol (MOE_GEMM_L2POL, A/B): bits 0-1 A, bits 2-3 B: 0 evict_normal,
+      // 1 evict_last, 2 evict_first; default A normal, B evict_last
+      auto pol = [](int v) {
+        return v == 1 ? policy_evict_last() : v == 2 ? policy_evict_first() : policy_evict_normal();
+      };
+      const uint64_t pol_a = pol(l2pol & 3), pol_b = pol((l2pol >> 2) & 3);
       bool first = true;
       for (int t = cluster; t < total_tiles; t += num_clusters) {
         const TileCoord c = decode_tile<kGroupM2<EPI>, BM2>(t, seg_tiles, segs, nseg, n_tiles, group_m);
@@ -1410,6 +1415,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
   }
 }
 
+std::atomic<int> g_gemm_l2pol{-1};  // 2-SM K4 L2 policies (env MOE_GEMM_L2POL: GEMM1 bits 0-3, GEMM2 bits 4-7; -1 default)
 std::atomic<int> g_swap_wpol{1};  // L2 policy of the swap kernel's weight stream: 1 evict_first (default), 0 evict_last, 2 normal (env MOE_SWAP_WPOL)
 
 template <int SNv>
@@ -1472,11 +1478,13 @@ cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUten
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int gp = group_m > 0 ? (group_m + 1) / 2 : 0;  // m-tiles -> 256-row tiles
+  const int pol = g_gemm_l2pol.load(std::memory_order_relaxed);
+  const int l2pol = pol >= 0 ? (epi == EPI_SWIGLU ? pol & 15 : (pol >> 4) & 15) : 1 << 2;
   if (epi == EPI_SWIGLU)
     return cudaLaunchKernelEx(&cfg, grouped_gemm_2sm_kernel<EPI_SWIGLU>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                              b_rows_per_slot, out, out_ld, gp);
+                              b_rows_per_slot, out, out_ld, gp, l2pol);
   return cudaLaunchKernelEx(&cfg, grouped_gemm_2sm_kernel<EPI_STORE>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                            b_rows_per_slot, out, out_ld, gp);
+                            b_rows_per_slot, out, out_ld, gp, l2pol);
 }
 
 cudaError_t launch_grouped_gemm_mc(int epi, const CUtensorMap* tmA, const CUtensorMap* tmBh, const GemmSeg* segs,

@@ -38,6 +38,8 @@
 #include <atomic>
 #include <cstdint>
 
+#include <cooperative_groups.h>
+
 #include "sm100_ptx.cuh"
 
 namespace moe {
@@ -201,12 +203,12 @@ struct CountsMirror {
   int n;
 };
 
-__device__ __forceinline__ void publish_counts(const int32_t* counts, const CountsMirror& m) {
+__device__ __forceinline__ void publish_counts(const int32_t* counts, const CountsMirror& m, unsigned n_ctas) {
   if (!m.host) return;
   __shared__ bool last;
   __threadfence();  // this CTA's histogram atomics are visible device-wide
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(m.ticket, 1u) == gridDim.x * gridDim.y - 1;
+  if (threadIdx.x == 0) last = atomicAdd(m.ticket, 1u) == n_ctas - 1;
   __syncthreads();
   if (last) {
     __threadfence();
@@ -222,13 +224,20 @@ __device__ __forceinline__ void publish_counts(const int32_t* counts, const Coun
 // zeroes), block_counts [ceil(T/32), E] i32, pred_counts [n_pred, E] (atomic).
 // NT = n-tiles of 8 stacked logits (E * (1 + n_pred) <= 8 * NT).  With
 // gridDim.y > 1 the CTA covers a 1/gridDim.y share of d and writes its
-// partial logits to `partial` instead of selecting.
+// partial logits to `partial` instead of selecting — or, launched as clusters
+// of gridDim.y CTAs (cluster_reduce), the y-rank-0 CTA of each cluster sums
+// the other CTAs' partial logits out of their shared memory (DSMEM) in slice
+// order, the finish kernel's arithmetic, and selects: no second launch and no
+// round trip of the partials through global memory.
+constexpr int kMaxClusterSplits = 8;
+
 template <int NT, bool MLP>
 __global__ void __launch_bounds__(kWarps * 32)
 gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_bfloat16* __restrict__ w_all, int E,
                  int n_pred, int k, int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
                  int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts, float* __restrict__ partial,
-                 const __grid_constant__ CountsMirror mirror, const __grid_constant__ PredictorMlp mlp) {
+                 const __grid_constant__ CountsMirror mirror, const __grid_constant__ PredictorMlp mlp,
+                 int cluster_reduce) {
   constexpr int kCols = 8 * NT;
   constexpr int kLd = kCols + 4;  // padded row of the reduction buffer
   __shared__ float red[kBlockTokens * kLd];
@@ -280,6 +289,34 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_b
     }
     __syncthreads();
   }
+  if (gridDim.y > 1 && cluster_reduce) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();  // every slice's partial logits are in its CTA's shared memory
+    if (blockIdx.y == 0) {
+      const int S = gridDim.y;
+      const float* peer[kMaxClusterSplits];
+#pragma unroll
+      for (int q = 1; q < kMaxClusterSplits; ++q) peer[q] = q < S ? cl.map_shared_rank(red, q) : red;
+      for (int i = threadIdx.x; i < kBlockTokens * kLd; i += blockDim.x) {
+        float v[kMaxClusterSplits];
+#pragma unroll
+        for (int q = 1; q < kMaxClusterSplits; ++q) v[q] = q < S ? peer[q][i] : 0.0f;  // all loads in flight
+        float a = red[i];
+#pragma unroll
+        for (int q = 1; q < kMaxClusterSplits; ++q)
+          if (q < S) a += v[q];
+        red[i] = a;
+      }
+    }
+    cl.sync();  // the peers' shared memory stays alive until it has been read
+    if (blockIdx.y != 0) return;
+    griddep_launch_dependents();
+    select_and_count<kLd, false, MLP>(red, hist, blk, 0, kBlockTokens, T, E, n_pred, k, ids, wts, counts,
+                                      block_counts, pred_counts, mlp);
+    publish_counts(counts, mirror, gridDim.x);
+    return;
+  }
   if (gridDim.y > 1) {
     float* dst = partial + ((size_t)blockIdx.y * gridDim.x + blk) * kBlockTokens * kCols;
     for (int i = threadIdx.x; i < kBlockTokens * kCols; i += blockDim.x) dst[i] = red[(i / kCols) * kLd + i % kCols];
@@ -291,7 +328,7 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_b
   griddep_launch_dependents();  // the block-prefix launch may be scheduled (it waits for this grid)
   select_and_count<kLd, false, MLP>(red, hist, blk, 0, kBlockTokens, T, E, n_pred, k, ids, wts, counts, block_counts,
                                pred_counts, mlp);
-  publish_counts(counts, mirror);
+  publish_counts(counts, mirror, gridDim.x * gridDim.y);
 }
 
 // Sums the split-K partial logits of kFinishTokens tokens of one 32-token
@@ -330,7 +367,7 @@ gate_finish_kernel(const float* __restrict__ partial, int splits, int T, int E, 
   griddep_launch_dependents();
   select_and_count<kLd, true, MLP>(red, hist, blk, tok0, kFinishTokens, T, E, n_pred, k, ids, wts, counts, block_counts,
                               pred_counts, mlp);
-  publish_counts(counts, mirror);
+  publish_counts(counts, mirror, gridDim.x * gridDim.y);
 }
 
 // Caller-given routing (moe_layer_forward_ids — the SURVEY §8 c3 bridge: ids
@@ -396,13 +433,19 @@ int gate_num_blocks(int T) { return (T + kBlockTokens - 1) / kBlockTokens; }
 // K-splits for a batch: enough CTAs to cover the SMs twice, d/(4 S) a
 // multiple of 32, at most 16.
 std::atomic<int> g_gate_max_splits{16};  // env MOE_GATE_MAX_SPLITS (A/B); set at ctx creation
+std::atomic<int> g_gate_cluster{0};      // env MOE_GATE_CLUSTER: 1 = split-K reduced inside a cluster (DSMEM), 0 = finish kernel (default: profiles/ab_gate_cluster_r02.md)
+std::atomic<int> g_gate_min_splits{1};   // env MOE_GATE_MIN_SPLITS: split large batches too (A/B)
 
 int gate_splits(int T, int d) {
   const int nblk = gate_num_blocks(T);
   int s = 1;
-  // gate_finish_kernel sums at most kMaxSplits slices: never split further
-  const int max_s = std::min(g_gate_max_splits.load(std::memory_order_relaxed), kMaxSplits);
+  // the finish kernel sums at most kMaxSplits slices, a cluster holds at most
+  // kMaxClusterSplits (portable cluster size): never split further
+  const int cap = g_gate_cluster.load(std::memory_order_relaxed) ? kMaxClusterSplits : kMaxSplits;
+  const int max_s = std::min(g_gate_max_splits.load(std::memory_order_relaxed), cap);
   while (s < max_s && nblk * s * 2 <= 2 * 148 && d % (kSlices * 32 * s * 2) == 0) s *= 2;
+  const int min_s = g_gate_min_splits.load(std::memory_order_relaxed);
+  while (s < min_s && s * 2 <= max_s && d % (kSlices * 32 * s * 2) == 0) s *= 2;
   return s;
 }
 
@@ -428,11 +471,26 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
   const int splits = partial ? gate_splits(T, d) : 1;
   const dim3 grid(nblk, splits), block(kWarps * 32);
   const bool with_mlp = pred_w2 != nullptr && (mlp_mask & ((n_pred >= 32 ? 0u : (1u << n_pred)) - 1u)) != 0;
+  const bool in_cluster = splits > 1 && g_gate_cluster.load(std::memory_order_relaxed) != 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = splits;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = in_cluster ? 1 : 0;
 #define MOE_GATE_LAUNCH(NT_, MLP_)                                                                          \
   {                                                                                                         \
+    if (in_cluster)                                                                                         \
+      return cudaLaunchKernelEx(&cfg, gate_topk_kernel<NT_, MLP_>, x, T, d, w_all, E, n_pred, k, ids, wts,  \
+                                counts, block_counts, pred_counts, partial, mirror, mlp, 1);               \
     gate_topk_kernel<NT_, MLP_><<<grid, block, 0, stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts, \
                                                             block_counts, pred_counts, partial,            \
-                                                            splits > 1 ? CountsMirror{} : mirror, mlp);    \
+                                                            splits > 1 ? CountsMirror{} : mirror, mlp, 0); \
     if (splits > 1)                                                                                         \
       gate_finish_kernel<NT_, MLP_><<<dim3(nblk, kBlockTokens / kFinishTokens), block, 0, stream>>>(        \
           partial, splits, T, E, n_pred, k, ids, wts, counts, block_counts, pred_counts, mirror, mlp);      \
