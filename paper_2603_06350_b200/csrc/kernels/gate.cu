@@ -51,6 +51,10 @@ constexpr int kWarps = 8;
 constexpr int kSlices = 4;        // K-slices per m-tile inside a CTA
 constexpr int kPerLane = 8;       // stacked logits per lane in the top-k (<= 256)
 constexpr int kMaxHistExperts = 256;
+#ifndef MOE_GATE_UNROLL
+#define MOE_GATE_UNROLL 2
+#endif
+constexpr int kGateUnroll = MOE_GATE_UNROLL;  // K-loop iterations in flight per warp (two 16-byte x loads each)
 
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                                uint32_t b0, uint32_t b1) {
@@ -260,7 +264,7 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_b
 #pragma unroll
   for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
   const int4 zero = make_int4(0, 0, 0, 0);
-#pragma unroll 2
+#pragma unroll kGateUnroll
   for (int kb = k_begin; kb < k_end; kb += 32) {
     const int f = kb + 8 * c;  // this lane's 8 consecutive features of the 32-feature block
     const int4 a_lo = v0 ? ld_nc_v4(x0 + f) : zero;
