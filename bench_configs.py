@@ -89,31 +89,42 @@ def run_stack(name, iters, warmup, layers=None):
     E, k, d, ff, T = c["E"], c["k"], c["d"], c["ff"], c["T"]
     st = MoEStack(L, E, k, d, ff, T, extra_replicas=c["extra_replicas"], zipf_s=c["s"], distance=1)
     pool = [torch.from_numpy(wl.tokens(T, d, E, 1, i).view(np.int16)).cuda() for i in range(4)]
-    ys = [torch.empty((T, d), dtype=torch.int16, device="cuda") for _ in range(2)]
+    y = torch.empty((T, d), dtype=torch.int16, device="cuda")
+    hs = [torch.empty((T, d), dtype=torch.int16, device="cuda") for _ in range(2)]  # residual stream
     stream = torch.cuda.ExternalStream(st.layer.stream_ptr)
 
-    def xs_for(it):  # layer l reads its own batch: predictions are made on other tokens
-        return [pool[(it + l) % 4] for l in range(L)]
+    def run_iteration(it, stats=False, ev_row=None):
+        # The residual stream of a real stack: layer l + 1 reads h + y of layer l (bf16 add on
+        # the layer's stream), so layer l's fused predictor scores layer l + 1 on the hidden
+        # state the next layer actually sees, one residual update earlier.
+        x, out = pool[it % 4], []
+        with torch.cuda.stream(stream):
+            for l in range(L):
+                if ev_row is not None:
+                    ev_row[l][0].record(stream)
+                r = st.layer.forward(l, x, y, 2, it, stats=stats)
+                if ev_row is not None:
+                    ev_row[l][1].record(stream)
+                out.append(r)
+                h = hs[l % 2]
+                torch.add(x.view(torch.bfloat16), y.view(torch.bfloat16), out=h.view(torch.bfloat16))
+                x = h
+        return out
 
     for it in range(warmup):
-        st.forward(xs_for(it), [ys[l % 2] for l in range(L)], it)
+        run_iteration(it)
     torch.cuda.synchronize()
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
           for _ in range(iters)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for i in range(iters):
-        it = warmup + i
-        xs = xs_for(it)
-        for l in range(L):
-            ev[i][l][0].record(stream)
-            st.layer.forward(l, xs[l], ys[l % 2], 2, it)
-            ev[i][l][1].record(stream)
+        run_iteration(warmup + i, ev_row=ev[i])
     t1.record(stream)
     torch.cuda.synchronize()
-    lat = [a.elapsed_time(b) for row in ev for a, b in row]  # all (iteration, layer) samples
+    lat = [a.elapsed_time(b) for row in ev for a, b in row]  # all (iteration, layer) samples (MoE layer only)
     total = t0.elapsed_time(t1)
-    stats = st.forward(xs_for(warmup + iters), [ys[l % 2] for l in range(L)], warmup + iters, stats=True)
+    stats = run_iteration(warmup + iters, stats=True)
     acc = [s.predictor_accuracy for s in stats[1:]]
     res = {
         "config": name, "layers": L, "gpus": 1, "shape": c, "iterations": iters,
@@ -122,7 +133,9 @@ def run_stack(name, iters, warmup, layers=None):
         "tokens_per_s_per_layer": T * iters * L / (total * 1e-3),
         "predictor_accuracy_mean": sum(acc) / len(acc), "predictor_accuracy_min": min(acc),
         "plan_sources": [s.plan_source for s in stats], "replicas": [s.replica_count for s in stats],
-        "note": "per-GPU shape at G=1 (named config is G=8); planning from the fused predictor, distance 1",
+        "note": "per-GPU shape at G=1 (named config is G=8); planning from the fused predictor, distance 1; "
+                "layers chained through the residual stream h_{l+1} = h_l + y_l (ms_per_stack includes the adds, "
+                "the layer samples do not)",
     }
     st.close()
     return res

@@ -96,6 +96,7 @@ cudaError_t launch_grouped_gemm_swap(int which, int sn, const CUtensorMap* tmA1,
 extern std::atomic<int> g_gate_max_splits;  // K1 split-K bound (env MOE_GATE_MAX_SPLITS)
 extern std::atomic<int> g_gate_cluster;     // K1 split-K reduced in a cluster (env MOE_GATE_CLUSTER)
 extern std::atomic<int> g_gate_min_splits;  // K1 split-K floor (env MOE_GATE_MIN_SPLITS)
+extern std::atomic<int> g_gate_stream;      // K1 persistent streaming kernel for large batches (env MOE_GATE_STREAM)
 extern std::atomic<int> g_gemm_l2pol;  // 2-SM K4 L2 policies (env MOE_GEMM_L2POL)
 extern std::atomic<int> g_swap_wpol;  // swap-AB weight-stream L2 policy (env MOE_SWAP_WPOL)
 cudaError_t preload_gate_kernels();

@@ -146,7 +146,7 @@ __device__ __forceinline__ void mlp_scores_inplace(float* seg, int E, const floa
 // memory (row stride LD, row 0 = tok0); warp w handles ntok / kWarps tokens.
 // ACCUM: the block's histogram row is shared with other CTAs (atomic adds
 // into a zeroed row) instead of being written whole.
-template <int LD, bool ACCUM, bool MLP>
+template <int LD, bool ACCUM, bool MLP, int BAR = 0>
 __device__ __forceinline__ void select_and_count(const float* red, int* hist, int blk, int tok0, int ntok, int T,
                                                  int E, int n_pred, int k, int32_t* __restrict__ ids,
                                                  float* __restrict__ wts, int32_t* __restrict__ counts,
@@ -186,8 +186,9 @@ __device__ __forceinline__ void select_and_count(const float* red, int* hist, in
       }
     }
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+  // BAR = 0: the whole CTA; otherwise named barrier BAR over the kWarps consumer warps
+  if (BAR == 0) __syncthreads(); else named_bar_sync(BAR, kWarps * 32);
+  for (int e = threadIdx.x; e < E; e += kWarps * 32) {
     const int h = hist[e];
     if (ACCUM) {
       if (h) atomicAdd(block_counts + (size_t)blk * E + e, h);
@@ -335,6 +336,126 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_b
   publish_counts(counts, mirror, gridDim.x * gridDim.y);
 }
 
+// Large batches (prefill): a persistent streaming gate.  One CTA per SM walks
+// the 32-token blocks b = blockIdx.x, + gridDim.x, ...; a producer warp streams
+// each block through a 4-stage shared-memory ring in K-chunks of 512 features
+// (32 rows x 1 KB per stage, one cp.async.bulk per row, rows padded to 1088 B
+// so the consumers' 16-byte fragment loads are bank-conflict free), so ~128 KB
+// per SM stay in flight — against the 1-2 us loaded HBM latency that is what
+// the per-block kernel (3-4 blocks resident per SM, ~56 KB in flight, 3.46
+// blocks per SM on average -> a 4-block tail) could not keep.  8 consumer warps
+// = 2 m-tiles x 4 K-slices of 128 features per stage run the same m16n8k16
+// MMAs on the same fragment mapping; at a block's end the K-slices are summed
+// in order (deterministic) and the same top-k / softmax / histogram runs while
+// the producer is already streaming the next block.
+constexpr int kStreamK = 512;                      // features per stage
+constexpr int kStreamRow = kStreamK * 2 + 64;      // padded row bytes in shared memory
+constexpr int kStreamStages = 4;
+constexpr int kStreamStageBytes = kBlockTokens * kStreamRow;
+constexpr int kStreamThreads = (kWarps + 1) * 32;  // + producer warp
+
+template <int NT, bool MLP>
+__global__ void __launch_bounds__(kStreamThreads, 1)
+gate_stream_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_bfloat16* __restrict__ w_all, int E,
+                   int n_pred, int k, int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
+                   int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts,
+                   const __grid_constant__ CountsMirror mirror, const __grid_constant__ PredictorMlp mlp) {
+  constexpr int kCols = 8 * NT;
+  constexpr int kLd = kCols + 4;
+  extern __shared__ __align__(128) uint8_t stream_smem[];
+  __shared__ float red[kBlockTokens * kLd];
+  __shared__ int hist[256];
+  __shared__ __align__(8) uint64_t full[kStreamStages], empty[kStreamStages];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int nblk = (T + kBlockTokens - 1) / kBlockTokens;
+  const int n_chunks = d / kStreamK;
+  const int Etot = E * (1 + n_pred);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStreamStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kWarps); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  griddep_launch_dependents();  // the block-prefix launch may be scheduled (it waits for this grid)
+
+  if (warp == kWarps) {
+    // ------------------------------------------------------------ producer
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+      const int t = b * kBlockTokens + lane;
+      const int rows = min(kBlockTokens, T - b * kBlockTokens);
+      for (int ch = 0; ch < n_chunks; ++ch) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* dst = stream_smem + stage * kStreamStageBytes;
+        if (lane == 0) mbar_arrive_expect_tx(&full[stage], static_cast<uint32_t>(rows) * kStreamK * 2);
+        __syncwarp();
+        if (lane < rows)
+          bulk_load(dst + lane * kStreamRow, x + (size_t)t * d + ch * kStreamK, kStreamK * 2, &full[stage]);
+        if (++stage == kStreamStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    // ----------------------------------------------------- consumers (8 warps)
+    const int g = lane >> 2, c = lane & 3;
+    const int mt = warp & 1, ks = warp >> 1;
+    int stage = 0;
+    uint32_t phase = 0;
+    const int4 zero = make_int4(0, 0, 0, 0);
+    for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+      for (int i = threadIdx.x; i < E; i += kWarps * 32) hist[i] = 0;
+      const int r0 = b * kBlockTokens + mt * 16 + g;
+      const bool v0 = r0 < T, v1 = r0 + 8 < T;
+      float acc[NT][4];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
+      for (int ch = 0; ch < n_chunks; ++ch) {
+        mbar_wait(&full[stage], phase);
+        const uint8_t* base = stream_smem + stage * kStreamStageBytes;
+        const uint8_t* row0 = base + (mt * 16 + g) * kStreamRow;
+        const uint8_t* row1 = row0 + 8 * kStreamRow;
+#pragma unroll
+        for (int q = 0; q < kStreamK / kSlices / 32; ++q) {
+          const int fl = ks * (kStreamK / kSlices) + q * 32 + 8 * c;  // feature within the chunk
+          const int f = ch * kStreamK + fl;
+          const int4 a_lo = v0 ? *reinterpret_cast<const int4*>(row0 + fl * 2) : zero;
+          const int4 a_hi = v1 ? *reinterpret_cast<const int4*>(row1 + fl * 2) : zero;
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            const int e = n * 8 + g;
+            const int4 bw = e < Etot ? __ldg(reinterpret_cast<const int4*>(w_all + (size_t)e * d + f)) : zero;
+            mma_bf16_16816(acc[n], a_lo.x, a_hi.x, a_lo.y, a_hi.y, bw.x, bw.y);
+            mma_bf16_16816(acc[n], a_lo.z, a_hi.z, a_lo.w, a_hi.w, bw.z, bw.w);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == kStreamStages) { stage = 0; phase ^= 1; }
+      }
+      // ordered K-slice reduction (consumers only: named barrier 1)
+      for (int s = 0; s < kSlices; ++s) {
+        if (ks == s) {
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            float* p0 = red + (mt * 16 + g) * kLd + n * 8 + 2 * c;
+            float* p1 = p0 + 8 * kLd;
+            if (s == 0) {
+              p0[0] = acc[n][0]; p0[1] = acc[n][1]; p1[0] = acc[n][2]; p1[1] = acc[n][3];
+            } else {
+              p0[0] += acc[n][0]; p0[1] += acc[n][1]; p1[0] += acc[n][2]; p1[1] += acc[n][3];
+            }
+          }
+        }
+        named_bar_sync(1, kWarps * 32);
+      }
+      select_and_count<kLd, false, MLP, 1>(red, hist, b, 0, kBlockTokens, T, E, n_pred, k, ids, wts, counts,
+                                           block_counts, pred_counts, mlp);
+      named_bar_sync(1, kWarps * 32);  // red / hist are reused by the next block
+    }
+  }
+  __syncthreads();
+  publish_counts(counts, mirror, gridDim.x);
+}
+
 // Sums the split-K partial logits of kFinishTokens tokens of one 32-token
 // block in slice order (deterministic; all slices are loaded before the
 // first add, so the sum costs one memory latency, not `splits`), then top-k /
@@ -439,6 +560,7 @@ int gate_num_blocks(int T) { return (T + kBlockTokens - 1) / kBlockTokens; }
 std::atomic<int> g_gate_max_splits{16};  // env MOE_GATE_MAX_SPLITS (A/B); set at ctx creation
 std::atomic<int> g_gate_cluster{0};      // env MOE_GATE_CLUSTER: 1 = split-K reduced inside a cluster (DSMEM), 0 = finish kernel (default: profiles/ab_gate_cluster_r02.md)
 std::atomic<int> g_gate_min_splits{1};   // env MOE_GATE_MIN_SPLITS: split large batches too (A/B)
+std::atomic<int> g_gate_stream{1};       // env MOE_GATE_STREAM: 0 = the per-block kernel for large batches (A/B)
 
 int gate_splits(int T, int d) {
   const int nblk = gate_num_blocks(T);
@@ -476,6 +598,10 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
   const dim3 grid(nblk, splits), block(kWarps * 32);
   const bool with_mlp = pred_w2 != nullptr && (mlp_mask & ((n_pred >= 32 ? 0u : (1u << n_pred)) - 1u)) != 0;
   const bool in_cluster = splits > 1 && g_gate_cluster.load(std::memory_order_relaxed) != 0;
+  // prefill: the persistent streaming gate (one CTA per SM, 4-stage ring)
+  const bool stream_gate = splits == 1 && nblk >= 148 && d % kStreamK == 0 && Etot <= 32 &&
+                           g_gate_stream.load(std::memory_order_relaxed) != 0;
+  const int stream_grid = nblk < 148 ? nblk : 148;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -489,6 +615,14 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
   cfg.numAttrs = in_cluster ? 1 : 0;
 #define MOE_GATE_LAUNCH(NT_, MLP_)                                                                          \
   {                                                                                                         \
+    if (stream_gate) {                                                                                      \
+      if constexpr (NT_ <= 4) {                                                                             \
+        gate_stream_kernel<NT_, MLP_><<<stream_grid, kStreamThreads, kStreamStages * kStreamStageBytes,     \
+                                        stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,           \
+                                                  block_counts, pred_counts, mirror, mlp);                  \
+        return cudaGetLastError();                                                                          \
+      }                                                                                                     \
+    }                                                                                                       \
     if (in_cluster)                                                                                         \
       return cudaLaunchKernelEx(&cfg, gate_topk_kernel<NT_, MLP_>, x, T, d, w_all, E, n_pred, k, ids, wts,  \
                                 counts, block_counts, pred_counts, partial, mirror, mlp, 1);               \
@@ -520,6 +654,17 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
 // launch, and a lazy load may wait for the whole context — including a
 // peer-exchange kernel spinning on another rank that shares the context).
 cudaError_t preload_gate_kernels() {
+  // the streaming gate's ring is dynamic shared memory beyond 48 KB (per device)
+  const void* stream_fns[] = {
+#define MOE_STREAM_FNS(NT_) \
+  reinterpret_cast<const void*>(gate_stream_kernel<NT_, false>), reinterpret_cast<const void*>(gate_stream_kernel<NT_, true>)
+      MOE_STREAM_FNS(1), MOE_STREAM_FNS(2), MOE_STREAM_FNS(4)};
+#undef MOE_STREAM_FNS
+  for (const void* f : stream_fns) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamStages * kStreamStageBytes);
+    if (e != cudaSuccess) return e;
+  }
   cudaFuncAttributes a;
   const void* fns[] = {
 #define MOE_GATE_FNS(NT_)                                                                               \

@@ -11,9 +11,13 @@ prediction and bootstrap from their load history (simulator.cpp:146-151).
 
 Synthetic stand-ins (no checkpoint offline): every layer's gate carries its own
 Zipf popularity permutation (workload.cpp:30-57); the predictor for layer l+d
-is that layer's gate; each layer reads its own token batch, so a prediction is
-made on different tokens than the ones it is scored against.  All layers share
-one set of random expert weights (loaded per layer; the data path is unchanged).
+is that layer's gate.  `forward` takes one input per layer: the tests give each
+layer its own token batch (outputs checked per layer against the oracle), and
+bench_configs.py cfg4 chains the layers through the residual stream
+h_{l+1} = h_l + y_l, so layer l's predictor scores layer l+1 on the hidden
+state that layer actually sees one residual update earlier — the accuracy it
+reports measures that drift instead of comparing two iid Zipf draws.  All
+layers share one set of random expert weights (loaded per layer).
 """
 from __future__ import annotations
 
