@@ -181,6 +181,15 @@ def nearest_rank(values, q):
     return percentile(values, q)
 
 
+def single_gpu_launches(T, k, E):
+    """Kernels of one G = 1 forward (capi.cpp enqueue_forward, default knobs)."""
+    nblk = (T + 31) // 32
+    split = nblk * 4 <= 2 * 148          # gate_splits: small batches split K (+ finish kernel)
+    fused_plan = nblk <= 32              # dispatch builds prefix + plan itself
+    swap = T * k / E <= 1024             # swap-AB tiles: GEMM1 + GEMM2 in one launch
+    return 1 + split + (0 if fused_plan else 1) + 1 + (1 if swap else 2) + 1
+
+
 def config_dict(G, c):
     """The `config` of both arms' lines (identical for the same workload and N)."""
     E, k, d, ff, T = c["E"], c["k"], c["d"], c["ff"], c["T"]
@@ -564,12 +573,13 @@ def run_ours(args):
             "phase_ms_median": phases, "replicas_median": replicas,
             # our kernels per step.  G=1: K1 gate (+ its split-K finish for small
             # batches; it also mirrors the histograms to the host), block prefix + on-device
-            # plan (one launch), K3 dispatch, K4 GEMM1, K4 GEMM2, K5 combine.  P2P (host-planned
-            # SYNC steps): gate, counts gather, counts SM copy, plan upload, prefix, dispatch,
-            # rows wait, GEMM1, GEMM2, outputs signal + wait, combine.  NCCL: gate, counts copy,
-            # plan upload, prefix, dispatch, GEMM1, GEMM2, combine (NCCL's own kernels and the
-            # gate-weight memcpy not counted)
-            "gpu_launches": (12 if p2p else (8 if G > 1 else 6 + (1 if T <= 32 * 148 else 0))) * args.steps,
+            # plan (one launch; folded into dispatch for <= 32 token blocks), K3 dispatch,
+            # K4 GEMM1 + GEMM2 (one launch for the swap-AB tiles of small batches), K5 combine.
+            # P2P (host-planned SYNC steps): gate, counts gather, counts SM copy, plan upload,
+            # prefix, dispatch, rows wait, GEMM1, GEMM2, outputs signal + wait, combine.  NCCL:
+            # gate, counts copy, plan upload, prefix, dispatch, GEMM1, GEMM2, combine (NCCL's own
+            # kernels and the gate-weight memcpy not counted)
+            "gpu_launches": (12 if p2p else (8 if G > 1 else single_gpu_launches(T, k, E))) * args.steps,
             "roofline": {"bound": "tensor", "kernel": "grouped_gemm_2sm_kernel (GEMM1 SwiGLU + GEMM2)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "peak_source": peak_src + ", bf16 sustained", "burst_peak": peaks.get("bf16_tflops"),

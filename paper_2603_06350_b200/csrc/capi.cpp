@@ -42,11 +42,21 @@ void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, 
                              c->k, c->ids.p, c->wts.p, c->counts.p, c->block_counts.p, s));
     return;
   }
+  // the prefill gate streams x through TMA boxes: one map per (x, T), rebuilt when they change
+  const CUtensorMap* tmx = nullptr;
+  if (T >= 148 * 32 && c->d % 512 == 0) {
+    if (c->tmGate_ptr != x || c->tmGate_T != T) {
+      c->tmGate = make_kmajor_map(x, T, c->d, 32);
+      c->tmGate_ptr = x;
+      c->tmGate_T = T;
+    }
+    tmx = &c->tmGate;
+  }
   CU_CHECK(launch_gate_topk(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
                             reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, pred_counts ? c->n_pred : 0,
                             c->k, c->ids.p, c->wts.p, c->counts.p, c->block_counts.p,
                             pred_counts ? pred_counts : c->pred_counts.p, c->gate_partial.p, s,
-                            mirror ? c->h_counts : nullptr, stride, c->gate_ticket.p, L.pred_w2.p, L.mlp_mask));
+                            mirror ? c->h_counts : nullptr, stride, c->gate_ticket.p, L.pred_w2.p, L.mlp_mask, tmx));
 }
 
 // buf: [G][stride] int32 from the gate — per rank, E actual counts followed by
@@ -122,8 +132,11 @@ void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool u
   if (upload_plan)
     CU_CHECK(launch_small_copy(c->dplan.p, c->hplan, sizeof(DevPlan), s));  // SM copy from mapped pinned memory
   const int nblk = gate_num_blocks(T);
-  CU_CHECK(launch_block_prefix(c->block_counts.p, nblk, c->E, c->dplan.p, c->block_pre.p, s,
-                               local_plan ? c->counts.p : nullptr, c->pdl_prefix()));
+  // single GPU, few blocks (decode): the dispatch grid builds prefix + plan itself
+  const bool fuse_plan = local_plan && !gather && !fused && c->fuse_plan && dispatch_fuses_plan(T);
+  if (!fuse_plan)
+    CU_CHECK(launch_block_prefix(c->block_counts.p, nblk, c->E, c->dplan.p, c->block_pre.p, s,
+                                 local_plan ? c->counts.p : nullptr, c->pdl_prefix()));
   // rows move as opaque 16-byte chunks: the row width in 16-bit units covers fp32 rows too
   RowTargets t{};
   PeerSignal sig{};
@@ -143,7 +156,8 @@ void stage_dispatch(moe_ctx* c, const uint16_t* x, int T, cudaStream_t s, bool u
   }
   CU_CHECK(launch_dispatch(reinterpret_cast<const __nv_bfloat16*>(x), T, c->xw, c->E, c->k, c->ids.p, c->block_pre.p,
                            c->dplan.p, t, c->row_code.p, sig, s, gather ? c->perm_src.p : nullptr,
-                           fused ? c->row_owner.p : nullptr, c->pdl_prefix()));
+                           fused ? c->row_owner.p : nullptr, c->pdl_prefix(), fuse_plan ? c->counts.p : nullptr,
+                           c->block_counts.p, c->dplan.p));
 }
 
 // The exchange step of one direction.  NCCL: grouped send/recv, forward: my

@@ -289,6 +289,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_GEMM_SWAP_ROWS")) c->swap_rows = std::atoi(v);
     if (const char* v = std::getenv("MOE_GEMM_SWAP128_ROWS")) c->swap128_rows = std::atoi(v);
     if (const char* v = std::getenv("MOE_SWAP_FUSE")) c->swap_fuse = std::string(v) != "0";
+    if (const char* v = std::getenv("MOE_FUSE_PLAN")) c->fuse_plan = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_PDL_FRONT")) c->pdl_front = std::atoi(v);
     if (const char* v = std::getenv("MOE_SWAP_WPOL")) g_swap_wpol.store(std::atoi(v));
     if (const char* v = std::getenv("MOE_GEMM_L2POL")) g_gemm_l2pol.store(std::atoi(v));

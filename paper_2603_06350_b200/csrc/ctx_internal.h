@@ -36,7 +36,8 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
                              int k, int32_t* ids, float* wts, int32_t* counts, int32_t* block_counts,
                              int32_t* pred_counts, float* partial, cudaStream_t stream,
                              int32_t* host_counts = nullptr, int host_n = 0, unsigned* ticket = nullptr,
-                             const float* pred_w2 = nullptr, unsigned mlp_mask = 0);
+                             const float* pred_w2 = nullptr, unsigned mlp_mask = 0,
+                             const CUtensorMap* tmx = nullptr);
 cudaError_t launch_route_ids(const int32_t* ids_in, const float* w_in, int T, int E, int k, int32_t* ids, float* wts,
                              int32_t* counts, int32_t* block_counts, int* err, cudaStream_t s);
 cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, const DevPlan* plan,
@@ -45,7 +46,9 @@ cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, co
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
                             const int32_t* block_pre, const DevPlan* plan, const RowTargets& targets,
                             uint32_t* row_code, const PeerSignal& sig, cudaStream_t s, int32_t* perm_src,
-                            int32_t* row_owner, bool pdl = false);
+                            int32_t* row_owner, bool pdl = false, const int32_t* local_counts = nullptr,
+                            const int32_t* block_counts = nullptr, DevPlan* plan_out = nullptr);
+bool dispatch_fuses_plan(int T);  // single GPU: dispatch builds prefix + plan itself (few blocks)
 // K6 over peer memory (p2p.cu)
 constexpr int kMaxRanks = 8;
 enum { kFlagCounts = 0, kFlagRows = 1, kFlagOutputs = 2, kFlagKinds = 4 };
@@ -315,6 +318,7 @@ struct moe_ctx {
   bool pdl_prefix() const { return (pdl_front & (capturing ? 4 : 1)) != 0; }
   bool pdl_combine() const { return (pdl_front & (capturing ? 8 : 2)) != 0; }
   bool swap_fuse = true;  // swap-AB: GEMM1 and GEMM2 in one launch (MOE_SWAP_FUSE=0: two)
+  bool fuse_plan = true;  // single GPU, <= 32 blocks: dispatch builds prefix + plan (MOE_FUSE_PLAN=0: block-prefix launch)
   DevBuf<int> swap_ready; // its per-(segment, m-tile) GEMM1-done counters (+ CTA counter)
   int pred_distance = 1;  // predictor slot 0 scores layer + pred_distance
   int count_stride = 0;   // ints per rank in the counts buffer: E * (1 + n_pred)
@@ -342,6 +346,9 @@ struct moe_ctx {
   int group_m[2] = {0, 0};  // K4 m-tiles per n sweep (0: the kernel's default; MOE_GEMM_GROUP_M=g1,g2)
   DevBuf<int32_t> perm_src;    // gathered GEMM1: permuted row -> token
   CUtensorMap tmX;             // gather4 map over the current x ({64, 1} box)
+  CUtensorMap tmGate;          // the streaming gate's map over the current x ({64, 32} boxes)
+  const void* tmGate_ptr = nullptr;
+  int tmGate_T = -1;
   const void* tmX_ptr = nullptr;
   int tmX_T = -1;
   DevBuf<int> gemm_sched;      // [GEMM1 next, done, GEMM2 next, done], zero between launches

@@ -91,13 +91,26 @@ block_prefix_kernel(const int32_t* __restrict__ block_counts, int nblk, int E,
 }
 
 // ------------------------------------------------------------- dispatch
+// Single GPU with few 32-token blocks (decode): the dispatch CTAs build their
+// own prefix row and the local plan from the gate's histograms, so the
+// block-prefix launch disappears.  Every CTA sums block_counts[b' < b] for its
+// block and scans the expert totals (one warp, 32 experts per step); CTA
+// (0, 0) also writes the DevPlan the GEMMs read after their griddepcontrol.wait
+// on this grid.  Same rows, same codes as block_prefix_kernel + plan_local_body.
+struct LocalPlan {
+  const int32_t* counts;        // [E] gate histogram; nullptr: read block_pre / plan as usual
+  const int32_t* block_counts;  // [nblk][E]
+  DevPlan* out;                 // written by CTA (0, 0)
+};
+constexpr int kFusedPlanMaxBlocks = 32;
+
 template <int K>
 __global__ void __launch_bounds__(128)
 dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const int32_t* __restrict__ ids,
                 const int32_t* __restrict__ block_pre, const DevPlan* __restrict__ plan,
                 const __grid_constant__ RowTargets targets, uint32_t* __restrict__ row_code,
                 const __grid_constant__ PeerSignal sig, int32_t* __restrict__ perm_src,
-                int32_t* __restrict__ row_owner) {
+                int32_t* __restrict__ row_owner, const __grid_constant__ LocalPlan lp) {
   __shared__ uint32_t codes[32 * K];
   // the block's prefix row and the plan tables the ranking reads, staged once
   // (coalesced) so the ranking never waits on L2
@@ -111,17 +124,73 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int t_base = b * 32;
   const int ntok = min(32, T - t_base);
-  const int R = plan->R;
-  for (int i = threadIdx.x; i < E; i += blockDim.x) {
-    s_pre[i] = block_pre[(size_t)b * E + i];
-    s_n[i] = plan->n_e[i];
-    s_rbase[i] = plan->rep_base[i];
-    s_mask[i] = 0u;
-  }
-  if (threadIdx.x == 0) s_rbase[E] = plan->rep_base[E];
-  for (int i = threadIdx.x; i < R; i += blockDim.x) {
-    s_rrow[i] = plan->rep_row_base[i];
-    s_rrem[i] = static_cast<unsigned char>(plan->rep_remote[i]);
+  if (lp.counts) {
+    // fused local plan: one merged replica per expert, rows in expert order
+    for (int i = threadIdx.x; i < E; i += blockDim.x) {
+      int pre = 0;
+      for (int bb = 0; bb < b; ++bb) pre += lp.block_counts[(size_t)bb * E + i];
+      s_pre[i] = pre;
+      s_rbase[i] = i;
+      s_rrem[i] = 0;
+      s_mask[i] = 0u;
+    }
+    if (warp == 0) {
+      const bool writer = blockIdx.x == 0 && blockIdx.y == 0;
+      int row_carry = 0, seg_carry = 0;
+      for (int e0 = 0; e0 < E; e0 += 32) {
+        const int e = e0 + lane;
+        const int n = e < E ? lp.counts[e] : 0;
+        int incl = n;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += v;
+        }
+        const uint32_t active = __ballot_sync(0xffffffffu, n > 0);
+        const int row0 = row_carry + incl - n;
+        if (e < E) {
+          s_n[e] = n;
+          s_rrow[e] = row0;
+          if (writer) {
+            lp.out->n_e[e] = n;
+            lp.out->src_off[e] = 0;
+            lp.out->rep_base[e] = e;
+            lp.out->rep_row_base[e] = row0;
+            lp.out->rep_remote[e] = 0;
+            if (n > 0) lp.out->segs[seg_carry + __popc(active & ((1u << lane) - 1u))] = GemmSeg{row0, n, e, 0};
+          }
+        }
+        row_carry += __shfl_sync(0xffffffffu, incl, 31);
+        seg_carry += __popc(active);
+      }
+      if (writer && lane == 0) {
+        lp.out->E = E;
+        lp.out->R = E;
+        lp.out->G = 1;
+        lp.out->rank = 0;
+        lp.out->nseg = seg_carry;
+        lp.out->rows_local = row_carry;
+        lp.out->rows_send = 0;
+        lp.out->rep_base[E] = E;
+      }
+      // the GEMMs (launched programmatically behind this grid) read the segment
+      // list before their griddepcontrol.wait: publish it before this CTA triggers
+      if (writer) __threadfence();
+    }
+    if (threadIdx.x == 0) s_rbase[E] = E;
+  } else {
+    const int R = plan->R;
+    for (int i = threadIdx.x; i < E; i += blockDim.x) {
+      s_pre[i] = block_pre[(size_t)b * E + i];
+      s_n[i] = plan->n_e[i];
+      s_rbase[i] = plan->rep_base[i];
+      s_mask[i] = 0u;
+    }
+    if (threadIdx.x == 0) s_rbase[E] = plan->rep_base[E];
+    for (int i = threadIdx.x; i < R; i += blockDim.x) {
+      s_rrow[i] = plan->rep_row_base[i];
+      s_rrem[i] = static_cast<unsigned char>(plan->rep_remote[i]);
+    }
   }
 #pragma unroll
   for (int i = 0; i < kMaxTargets; ++i)  // constant indices: the table stays in parameter space
@@ -473,18 +542,22 @@ cudaError_t launch_block_prefix(const int32_t* block_counts, int nblk, int E, co
 cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, const int32_t* ids,
                             const int32_t* block_pre, const DevPlan* plan, const RowTargets& targets,
                             uint32_t* row_code, const PeerSignal& sig, cudaStream_t s, int32_t* perm_src,
-                            int32_t* row_owner, bool pdl) {
+                            int32_t* row_owner, bool pdl, const int32_t* local_counts,
+                            const int32_t* block_counts, DevPlan* plan_out) {
   if (T <= 0) return cudaSuccess;
   if (d % 8) return cudaErrorInvalidValue;
   const int nblk = (T + 31) / 32;
+  const LocalPlan lp{local_counts, block_counts, plan_out};
   // at least ~2 CTAs per SM: split each row's chunks when there are few blocks
   // (ranking only when GEMM1 gathers the rows itself)
   const int split = perm_src ? 1 : std::max(1, std::min((2 * 148 + nblk - 1) / nblk, d / 8 / 16));
   const dim3 grid(nblk, split);
   MOE_SWITCH_K(k, return launch_pdl(pdl, dispatch_kernel<KK>, grid, dim3(128), s, x, T, d, E, ids, block_pre, plan,
-                                    targets, row_code, sig, perm_src, row_owner));
+                                    targets, row_code, sig, perm_src, row_owner, lp));
   return cudaSuccess;
 }
+
+bool dispatch_fuses_plan(int T) { return T > 0 && (T + 31) / 32 <= kFusedPlanMaxBlocks; }
 
 cudaError_t launch_combine(const RowTargets& sources, int T, int d, int k, const uint32_t* row_code,
                            const float* wts, __nv_bfloat16* y, int num_sms, cudaStream_t s, bool pdl) {

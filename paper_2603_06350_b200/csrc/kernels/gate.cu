@@ -39,6 +39,7 @@
 #include <cstdint>
 
 #include <cooperative_groups.h>
+#include <cuda.h>
 
 #include "sm100_ptx.cuh"
 
@@ -68,7 +69,10 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
 // Top-k over logits [base, base+E) of one token's stacked row in shared
 // memory; lane l looks at l, l+32, ...  Every lane returns the same result.
 // Top-k over per-lane values own[s] = value of expert lane + 32 s.
-__device__ __forceinline__ void warp_topk_vals(const float (&own)[kPerLane], int E, int k, int (&ids_out)[8],
+// S = logits per lane actually held (ceil(columns / 32)): the decode shape
+// (64 experts) scans 2 slots per round, not kPerLane.
+template <int S>
+__device__ __forceinline__ void warp_topk_vals(const float (&own)[S], int E, int k, int (&ids_out)[8],
                                                float (&logit_out)[8]) {
   const int lane = lane_id();
   uint32_t taken = 0;
@@ -78,7 +82,7 @@ __device__ __forceinline__ void warp_topk_vals(const float (&own)[kPerLane], int
     float bv = -FLT_MAX;
     int bi = 0x7fffffff;
 #pragma unroll
-    for (int s = 0; s < kPerLane; ++s) {
+    for (int s = 0; s < S; ++s) {
       const int e = lane + 32 * s;
       if (e < E && !((taken >> s) & 1u))
         if (own[s] > bv || (own[s] == bv && e < bi)) { bv = own[s]; bi = e; }
@@ -95,12 +99,13 @@ __device__ __forceinline__ void warp_topk_vals(const float (&own)[kPerLane], int
   }
 }
 
+template <int S>
 __device__ __forceinline__ void warp_topk(const float* row, int base, int E, int k, int (&ids_out)[8],
                                           float (&logit_out)[8]) {
   const int lane = lane_id();
-  float own[kPerLane];
+  float own[S];
 #pragma unroll
-  for (int s = 0; s < kPerLane; ++s) {
+  for (int s = 0; s < S; ++s) {
     const int e = lane + 32 * s;
     own[s] = e < E ? row[base + e] : -FLT_MAX;
   }
@@ -118,11 +123,12 @@ struct PredictorMlp {
   uint32_t mask;    // bit p: slot p is an MLP
 };
 
+template <int S>
 __device__ __forceinline__ void mlp_scores_inplace(float* seg, int E, const float* __restrict__ w2) {
   const int lane = lane_id();
-  float own[kPerLane];
+  float own[S];
 #pragma unroll
-  for (int s = 0; s < kPerLane; ++s) {
+  for (int s = 0; s < S; ++s) {
     const int e = lane + 32 * s;
     float acc = 0.0f;
     if (e < E) {
@@ -136,7 +142,7 @@ __device__ __forceinline__ void mlp_scores_inplace(float* seg, int E, const floa
   }
   __syncwarp();
 #pragma unroll
-  for (int s = 0; s < kPerLane; ++s)
+  for (int s = 0; s < S; ++s)
     if (lane + 32 * s < E) seg[lane + 32 * s] = own[s];
   __syncwarp();
 }
@@ -153,6 +159,7 @@ __device__ __forceinline__ void select_and_count(const float* red, int* hist, in
                                                  int32_t* __restrict__ block_counts,
                                                  int32_t* __restrict__ pred_counts, const PredictorMlp& mlp) {
   const int warp = threadIdx.x >> 5, lane = lane_id();
+  constexpr int S = (LD - 4 + 31) / 32;  // E * (1 + n_pred) <= LD - 4 columns
   const int per = ntok / kWarps;
   for (int q = 0; q < per; ++q) {
     const int lt = warp * per + q;
@@ -163,8 +170,8 @@ __device__ __forceinline__ void select_and_count(const float* red, int* hist, in
       int sel[8];
       float lg[8];
       if (MLP && gi > 0 && ((mlp.mask >> (gi - 1)) & 1u))
-        mlp_scores_inplace(const_cast<float*>(row) + gi * E, E, mlp.w2 + (size_t)(gi - 1) * E * E);
-      warp_topk(row, gi * E, E, k, sel, lg);
+        mlp_scores_inplace<S>(const_cast<float*>(row) + gi * E, E, mlp.w2 + (size_t)(gi - 1) * E * E);
+      warp_topk<S>(row, gi * E, E, k, sel, lg);
       if (lane == 0) {
         if (gi == 0) {
           float z = 0.0f, p[8];
@@ -339,9 +346,9 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_b
 // Large batches (prefill): a persistent streaming gate.  One CTA per SM walks
 // the 32-token blocks b = blockIdx.x, + gridDim.x, ...; a producer warp streams
 // each block through a 4-stage shared-memory ring in K-chunks of 512 features
-// (32 rows x 1 KB per stage, one cp.async.bulk per row, rows padded to 1088 B
-// so the consumers' 16-byte fragment loads are bank-conflict free), so ~128 KB
-// per SM stay in flight — against the 1-2 us loaded HBM latency that is what
+// (32 rows x 1 KB per stage = eight 32 x 64 TMA boxes with the 128-byte
+// swizzle, so the consumers' 16-byte fragment loads are bank-conflict free),
+// so ~128 KB per SM stay in flight — against the 1-2 us loaded HBM latency that is what
 // the per-block kernel (3-4 blocks resident per SM, ~56 KB in flight, 3.46
 // blocks per SM on average -> a 4-block tail) could not keep.  8 consumer warps
 // = 2 m-tiles x 4 K-slices of 128 features per stage run the same m16n8k16
@@ -349,20 +356,22 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_b
 // in order (deterministic) and the same top-k / softmax / histogram runs while
 // the producer is already streaming the next block.
 constexpr int kStreamK = 512;                      // features per stage
-constexpr int kStreamRow = kStreamK * 2 + 64;      // padded row bytes in shared memory
+constexpr int kStreamBox = kBlockTokens * 128;     // one 32-row x 64-feature TMA box (4 KB)
 constexpr int kStreamStages = 4;
-constexpr int kStreamStageBytes = kBlockTokens * kStreamRow;
+constexpr int kStreamStageBytes = (kStreamK / 64) * kStreamBox;
 constexpr int kStreamThreads = (kWarps + 1) * 32;  // + producer warp
+constexpr int kStreamSmem = kStreamStages * kStreamStageBytes + 1024;  // + 1024-byte alignment slack
 
 template <int NT, bool MLP>
 __global__ void __launch_bounds__(kStreamThreads, 1)
-gate_stream_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_bfloat16* __restrict__ w_all, int E,
+gate_stream_kernel(const __grid_constant__ CUtensorMap tmx, int T, int d, const __nv_bfloat16* __restrict__ w_all, int E,
                    int n_pred, int k, int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
                    int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts,
                    const __grid_constant__ CountsMirror mirror, const __grid_constant__ PredictorMlp mlp) {
   constexpr int kCols = 8 * NT;
   constexpr int kLd = kCols + 4;
-  extern __shared__ __align__(128) uint8_t stream_smem[];
+  extern __shared__ uint8_t stream_raw[];
+  uint8_t* stream_smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(stream_raw) + 1023) & ~uintptr_t(1023));
   __shared__ float red[kBlockTokens * kLd];
   __shared__ int hist[256];
   __shared__ __align__(8) uint64_t full[kStreamStages], empty[kStreamStages];
@@ -379,19 +388,20 @@ gate_stream_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv
 
   if (warp == kWarps) {
     // ------------------------------------------------------------ producer
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
-      const int t = b * kBlockTokens + lane;
-      const int rows = min(kBlockTokens, T - b * kBlockTokens);
-      for (int ch = 0; ch < n_chunks; ++ch) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* dst = stream_smem + stage * kStreamStageBytes;
-        if (lane == 0) mbar_arrive_expect_tx(&full[stage], static_cast<uint32_t>(rows) * kStreamK * 2);
-        __syncwarp();
-        if (lane < rows)
-          bulk_load(dst + lane * kStreamRow, x + (size_t)t * d + ch * kStreamK, kStreamK * 2, &full[stage]);
-        if (++stage == kStreamStages) { stage = 0; phase ^= 1; }
+    if (lane == 0) {
+      tma_prefetch_desc(&tmx);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+        for (int ch = 0; ch < n_chunks; ++ch) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* dst = stream_smem + stage * kStreamStageBytes;
+          mbar_arrive_expect_tx(&full[stage], kStreamStageBytes);  // rows past T are zero-filled
+#pragma unroll
+          for (int j = 0; j < kStreamK / 64; ++j)
+            tma_load_2d(dst + j * kStreamBox, &tmx, &full[stage], ch * kStreamK + j * 64, b * kBlockTokens);
+          if (++stage == kStreamStages) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else {
@@ -411,14 +421,16 @@ gate_stream_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv
       for (int ch = 0; ch < n_chunks; ++ch) {
         mbar_wait(&full[stage], phase);
         const uint8_t* base = stream_smem + stage * kStreamStageBytes;
-        const uint8_t* row0 = base + (mt * 16 + g) * kStreamRow;
-        const uint8_t* row1 = row0 + 8 * kStreamRow;
+        const int ra = mt * 16 + g, rb = ra + 8;  // rows of this lane's A fragments
 #pragma unroll
         for (int q = 0; q < kStreamK / kSlices / 32; ++q) {
           const int fl = ks * (kStreamK / kSlices) + q * 32 + 8 * c;  // feature within the chunk
           const int f = ch * kStreamK + fl;
-          const int4 a_lo = v0 ? *reinterpret_cast<const int4*>(row0 + fl * 2) : zero;
-          const int4 a_hi = v1 ? *reinterpret_cast<const int4*>(row1 + fl * 2) : zero;
+          // box fl / 64, 16-byte chunk (fl % 64) / 8 of the row, 128B-swizzled
+          const uint8_t* box = base + (fl >> 6) * kStreamBox;
+          const int chunk = (fl & 63) >> 3;
+          const int4 a_lo = v0 ? *reinterpret_cast<const int4*>(box + ra * 128 + ((chunk ^ (ra & 7)) << 4)) : zero;
+          const int4 a_hi = v1 ? *reinterpret_cast<const int4*>(box + rb * 128 + ((chunk ^ (rb & 7)) << 4)) : zero;
 #pragma unroll
           for (int n = 0; n < NT; ++n) {
             const int e = n * 8 + g;
@@ -560,7 +572,7 @@ int gate_num_blocks(int T) { return (T + kBlockTokens - 1) / kBlockTokens; }
 std::atomic<int> g_gate_max_splits{16};  // env MOE_GATE_MAX_SPLITS (A/B); set at ctx creation
 std::atomic<int> g_gate_cluster{0};      // env MOE_GATE_CLUSTER: 1 = split-K reduced inside a cluster (DSMEM), 0 = finish kernel (default: profiles/ab_gate_cluster_r02.md)
 std::atomic<int> g_gate_min_splits{1};   // env MOE_GATE_MIN_SPLITS: split large batches too (A/B)
-std::atomic<int> g_gate_stream{1};       // env MOE_GATE_STREAM: 0 = the per-block kernel for large batches (A/B)
+std::atomic<int> g_gate_stream{0};       // env MOE_GATE_STREAM=1: the persistent streaming gate for large batches (opt-in: 47 vs 39 us at cfg2, profiles/ab_gate_stream_r02.md)
 
 int gate_splits(int T, int d) {
   const int nblk = gate_num_blocks(T);
@@ -587,7 +599,7 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
                              int n_pred, int k, int32_t* ids, float* wts, int32_t* counts,
                              int32_t* block_counts, int32_t* pred_counts, float* partial, cudaStream_t stream,
                              int32_t* host_counts, int host_n, unsigned* ticket, const float* pred_w2,
-                             unsigned mlp_mask) {
+                             unsigned mlp_mask, const CUtensorMap* tmx) {
   if (T <= 0) return cudaSuccess;
   const CountsMirror mirror{host_counts, ticket, host_n};
   const PredictorMlp mlp{pred_w2, mlp_mask};
@@ -599,7 +611,7 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
   const bool with_mlp = pred_w2 != nullptr && (mlp_mask & ((n_pred >= 32 ? 0u : (1u << n_pred)) - 1u)) != 0;
   const bool in_cluster = splits > 1 && g_gate_cluster.load(std::memory_order_relaxed) != 0;
   // prefill: the persistent streaming gate (one CTA per SM, 4-stage ring)
-  const bool stream_gate = splits == 1 && nblk >= 148 && d % kStreamK == 0 && Etot <= 32 &&
+  const bool stream_gate = tmx != nullptr && splits == 1 && nblk >= 148 && d % kStreamK == 0 && Etot <= 32 &&
                            g_gate_stream.load(std::memory_order_relaxed) != 0;
   const int stream_grid = nblk < 148 ? nblk : 148;
   cudaLaunchConfig_t cfg = {};
@@ -617,8 +629,8 @@ cudaError_t launch_gate_topk(const __nv_bfloat16* x, int T, int d, const __nv_bf
   {                                                                                                         \
     if (stream_gate) {                                                                                      \
       if constexpr (NT_ <= 4) {                                                                             \
-        gate_stream_kernel<NT_, MLP_><<<stream_grid, kStreamThreads, kStreamStages * kStreamStageBytes,     \
-                                        stream>>>(x, T, d, w_all, E, n_pred, k, ids, wts, counts,           \
+        gate_stream_kernel<NT_, MLP_><<<stream_grid, kStreamThreads, kStreamSmem,                           \
+                                        stream>>>(*tmx, T, d, w_all, E, n_pred, k, ids, wts, counts,        \
                                                   block_counts, pred_counts, mirror, mlp);                  \
         return cudaGetLastError();                                                                          \
       }                                                                                                     \
@@ -662,7 +674,7 @@ cudaError_t preload_gate_kernels() {
 #undef MOE_STREAM_FNS
   for (const void* f : stream_fns) {
     const cudaError_t e =
-        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamStages * kStreamStageBytes);
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem);
     if (e != cudaSuccess) return e;
   }
   cudaFuncAttributes a;
