@@ -64,8 +64,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--pool", type=int, default=4, help="distinct token batches cycled per rank")
-    ap.add_argument("--cpu-sample-tokens", type=int, default=2048,
-                    help="tokens of the step's batch the reference arm runs per step (~2-3 s of host work)")
+    ap.add_argument("--cpu-sample-tokens", type=int, default=4096,
+                    help="tokens of the step's batch the reference arm runs per step (~2-4 s of host work)")
     ap.add_argument("--cpu-full-layer", type=int, default=1,
                     help="reference arm: also time one full-batch layer after the steps (0: skip)")
     ap.add_argument("--cpu-baseline-tokens", type=int, default=1024,
@@ -267,7 +267,7 @@ def cpu_cfg1_full_layer():
 
 def run_reference(args):
     """--impl reference: the CPU path of this metric on the host's cores, rank 0
-    only.  Each step runs a bounded sample of the step's batch (default 2048 of
+    only.  Each step runs a bounded sample of the step's batch (default 4096 of
     16384 tokens: every token's routing and FFN rows are independent, so the
     cost is linear in tokens); one full 16384-token layer is also timed once
     after the steps and reported beside the per-step rate."""

@@ -289,3 +289,40 @@ def test_p2p_predicted_planning_distance_two(cuda):
                 assert torch.equal(yd[r][l], y1), (it, r, l)
     for m in ms + [one]:
         m.close()
+
+
+@pytest.mark.parametrize("variant", ["2sm", "1sm"])
+def test_p2p_prefill_kernels_bit_identical(cuda, monkeypatch, variant):
+    """The prefill K4 kernels (the 2-SM default and the 1-SM one) behind the
+    peer-memory exchange: G=2 ranks with straggler replicas split across them,
+    every rank's output bit-identical to one GPU running the same kernel."""
+    import torch
+    monkeypatch.setenv("MOE_GEMM_VARIANT", variant)
+    G, E, k, d, ff, T = 2, 8, 2, 1024, 1408, 1500
+    rc, rg = [2, 1, 1, 3, 1, 1, 1, 1], [0, 1, 1, 0, 1, 0, 1, 0, 0, 1, 1]
+    ms = _ranks(G, E, k, d, ff, T)
+    one = _single(E, k, d, ff, T)
+    wg = wl.gate_weights(E, d, 1.3, 1, 0, 0)
+    for m in ms + [one]:
+        m.set_gate(0, wg)
+        for e in range(E):
+            m.load_expert(0, e, *wl.expert_weights(d, ff, 1, 0, e))
+    for m in ms:
+        m.set_placement(0, rc, rg)
+    xs = [wl.tokens(T, d, E, 1, 300 + r) for r in range(G)]
+    xd = [torch.from_numpy(x.view(np.int16)).to(cuda) for x in xs]
+    yd = [torch.zeros((T, d), dtype=torch.int16, device=cuda) for _ in range(G)]
+    for it in range(2):
+        sts = _parallel(ms, lambda r: ms[r].forward(0, xd[r], yd[r], MOE_PLAN_FIXED, it, stats=True))
+        torch.cuda.synchronize()
+        assert sum(st.rows_local for st in sts) == k * G * T and sts[0].rows_sent > 0
+        for r in range(G):
+            y1 = torch.zeros_like(yd[r])
+            one.forward(0, xd[r], y1, MOE_PLAN_FIXED, it)
+            one.sync()
+            assert torch.equal(yd[r], y1), (variant, it, r)
+    y = oracle.bf16_to_f32(yd[0].cpu().numpy().view(np.uint16))
+    y_ref = oracle.layer_forward(xs[0], wg, [wl.expert_weights(d, ff, 1, 0, e) for e in range(E)], [1] * E, k)[0]
+    assert float(np.max(np.abs(y - y_ref)) / np.max(np.abs(y_ref))) <= 2e-2
+    for m in ms + [one]:
+        m.close()
