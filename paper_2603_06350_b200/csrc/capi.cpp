@@ -258,17 +258,17 @@ void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t r
   // producer) — +4-5% tokens/s at cfg2 over the 1-SM kernel in short and
   // 150-step runs alike (profiles/ab_2sm_pdl_r02.md); the 1-SM kernel keeps the
   // opt-in gather / fused-combine / dynamic-scheduler paths
-  const bool two_sm = c->gemm_variant == 2 || (c->gemm_variant == 0 && !gather && !fused_y && !c->dyn_sched);
+  const bool two_sm = c->gemm_variant == 2 || (c->gemm_variant == 0 && !gather && !fused_y);
   const bool m256 = c->gemm_variant == 3;
   if (two_sm) {
     if (which == 0)
       CU_CHECK(launch_grouped_gemm_2sm(0, &c->tmA1, &L.tmB1h, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d,
                                        2 * c->ff, reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, c->num_sms, s,
-                                       c->use_pdl, c->group_m[0]));
+                                       c->use_pdl, c->group_m[0], c->dyn_sched ? c->gemm_sched.p : nullptr));
     else
       CU_CHECK(launch_grouped_gemm_2sm(1, &c->tmA2, &L.tmB2h, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
                                        reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s, c->use_pdl,
-                                       c->group_m[1]));
+                                       c->group_m[1], c->dyn_sched ? c->gemm_sched.p + 2 : nullptr));
     return;
   }
   if (m256) {

@@ -82,7 +82,7 @@ cudaError_t launch_grouped_gemm_m256(int epi, const CUtensorMap* tmA, const CUte
 cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                     __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl = false,
-                                    int group_m = 0);
+                                    int group_m = 0, int* sched = nullptr);
 cudaError_t launch_grouped_gemm_mc(int epi, const CUtensorMap* tmA, const CUtensorMap* tmBh, const GemmSeg* segs,
                                    const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                    __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl,

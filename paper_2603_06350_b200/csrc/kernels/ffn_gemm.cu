@@ -712,7 +712,12 @@ grouped_gemm_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_con
 // full barrier, the leader's single MMA thread issues for the pair, commits
 // multicast to both CTAs' empty / tmem-full barriers, and both CTAs' epilogue
 // warps (each reading its own TMEM: 128 rows x 256 cols) release the
-// accumulator on the leader's tmem-empty barrier (8 arrivals).
+// accumulator on the leader's tmem-empty barrier (8 arrivals).  Tiles reach
+// both CTAs through a ring the leader's producer fills: statically (cluster c
+// takes c, c + clusters, ...) or, with a scheduler counter (MOE_GEMM_SCHED=
+// dynamic), claimed in tile order so the clusters in flight always cover one
+// contiguous window of tiles; every consumer of both CTAs frees a slot on the
+// leader's ring-empty barrier (10 arrivals).
 constexpr int BM2 = 256;                 // rows per cluster tile
 constexpr int STAGES2 = 6;
 constexpr uint32_t kHalfA = 128 * BK * 2, kHalfB = 128 * BK * 2;  // 16 KB each, per CTA
@@ -724,9 +729,10 @@ struct SmemLayout2 {
   static constexpr uint32_t a = 0;
   static constexpr uint32_t b = a + STAGES2 * kHalfA;
   static constexpr uint32_t bars = b + STAGES2 * kHalfB;
-  static constexpr uint32_t n_bars = 2 * STAGES2 + 4;
+  static constexpr uint32_t n_bars = 2 * STAGES2 + 4 + 2 * kTileRing;
   static constexpr uint32_t tmem_slot = bars + n_bars * 8;
-  static constexpr uint32_t seg_tiles = tmem_slot + 16;
+  static constexpr uint32_t tile_ring = tmem_slot + 16;              // int[kTileRing]
+  static constexpr uint32_t seg_tiles = tile_ring + kTileRing * 4;
   static constexpr uint32_t segs = seg_tiles + (kMaxSegs + 1) * 4 + 12;
   static constexpr uint32_t end = ((segs + 15) / 16) * 16 + kMaxSegs * 16;
 };
@@ -737,7 +743,8 @@ template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total, int k_total,
-                        int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld, int group_m, int l2pol) {
+                        int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld, int group_m, int l2pol,
+                        int* __restrict__ sched) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout2::bars);
@@ -745,6 +752,9 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
   uint64_t* empty = bars + STAGES2;           // per CTA
   uint64_t* tfull = bars + 2 * STAGES2;       // per CTA
   uint64_t* tempty = bars + 2 * STAGES2 + 2;  // used on the leader only (8 arrivals)
+  uint64_t* ring_full = bars + 2 * STAGES2 + 4;      // per CTA (1 arrival: the leader's producer)
+  uint64_t* ring_empty = ring_full + kTileRing;      // used on the leader only (10 arrivals)
+  volatile int* ring = reinterpret_cast<volatile int*>(smem + SmemLayout2::tile_ring);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SmemLayout2::tmem_slot);
   int* seg_tiles = reinterpret_cast<int*>(smem + SmemLayout2::seg_tiles);
   int4* segs = reinterpret_cast<int4*>(smem + SmemLayout2::segs);
@@ -763,6 +773,7 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+    for (int r = 0; r < kTileRing; ++r) { mbar_init(&ring_full[r], 1); mbar_init(&ring_empty[r], 10); }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_2sm<kTmemCols>(tmem_slot);
@@ -798,8 +809,29 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
         return v == 1 ? policy_evict_last() : v == 2 ? policy_evict_first() : policy_evict_normal();
       };
       const uint64_t pol_a = pol(l2pol & 3), pol_b = pol((l2pol >> 2) & 3);
+      const uint32_t peer_ring = mapa_shared(smem_u32(const_cast<int*>(ring)), 1);
+      const uint32_t peer_ring_full0 = mapa_shared(smem_u32(&ring_full[0]), 1);
+      const uint32_t leader_ring_empty0 = mapa_shared(smem_u32(&ring_empty[0]), 0);
+      int rslot = 0;
+      uint32_t rphase = 0;
       bool first = true;
-      for (int t = cluster; t < total_tiles; t += num_clusters) {
+      for (int k_static = 0;; ++k_static) {
+        int t;
+        if (leader) {  // claim the next tile and hand it to both CTAs
+          mbar_wait(&ring_empty[rslot], rphase ^ 1);
+          t = sched ? atomicAdd(sched, 1) : cluster + k_static * num_clusters;
+          if (t >= total_tiles) t = -1;
+          ring[rslot] = t;
+          st_shared_cluster(peer_ring + rslot * 4, t);
+          mbar_arrive(&ring_full[rslot]);
+          mbar_arrive_cluster(peer_ring_full0 + rslot * 8);  // release: the store above is visible first
+        } else {
+          mbar_wait(&ring_full[rslot], rphase);
+          t = ring[rslot];
+          mbar_arrive_cluster(leader_ring_empty0 + rslot * 8);
+        }
+        if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
+        if (t < 0) break;
         const TileCoord c = decode_tile<kGroupM2<EPI>, BM2>(t, seg_tiles, segs, nseg, n_tiles, group_m);
         const int a_row = segs[c.seg].x + c.m * BM2 + static_cast<int>(rank) * 128;
         const int b_row = segs[c.seg].z * b_rows_per_slot + c.n * BN + static_cast<int>(rank) * 128;
@@ -827,6 +859,10 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
           if (++stage == STAGES2) { stage = 0; phase ^= 1; }
         }
       }
+      if (leader && sched && atomicAdd(sched + 1, 1) == num_clusters - 1) {
+        sched[0] = 0;  // every cluster has made its last claim: reset for the next launch
+        sched[1] = 0;
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------- MMA issuer (leader)
@@ -838,7 +874,14 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
       uint32_t acc_phase = 0;
       const uint32_t a_base = smem_u32(smem + SmemLayout2::a);
       const uint32_t b_base = smem_u32(smem + SmemLayout2::b);
-      for (int t = cluster; t < total_tiles; t += num_clusters) {
+      int rslot = 0;
+      uint32_t rphase = 0;
+      while (true) {
+        mbar_wait(&ring_full[rslot], rphase);
+        const int t = ring[rslot];
+        mbar_arrive(&ring_empty[rslot]);
+        if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
+        if (t < 0) break;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -861,9 +904,18 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
     // --------------------------------------------------------- epilogue (both CTAs)
     const int quarter = warp & 3;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    const uint32_t leader_ring_empty0 = mapa_shared(smem_u32(&ring_empty[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cluster; t < total_tiles; t += num_clusters) {
+    int rslot = 0;
+    uint32_t rphase = 0;
+    while (true) {
+      mbar_wait(&ring_full[rslot], rphase);
+      const int t = ring[rslot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_ring_empty0 + rslot * 8);
+      if (++rslot == kTileRing) { rslot = 0; rphase ^= 1; }
+      if (t < 0) break;
       const TileCoord c = decode_tile<kGroupM2<EPI>, BM2>(t, seg_tiles, segs, nseg, n_tiles, group_m);
       const int4 sg = segs[c.seg];
       const int row = c.m * BM2 + static_cast<int>(rank) * 128 + quarter * 32 + lane;
@@ -1465,7 +1517,7 @@ static_assert(kSmemBytes <= 232448, "smem budget");
 cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                     __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl,
-                                    int group_m) {
+                                    int group_m, int* sched) {
   if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_ctas & ~1);
@@ -1482,9 +1534,9 @@ cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUten
   const int l2pol = pol >= 0 ? (epi == EPI_SWIGLU ? pol & 15 : (pol >> 4) & 15) : 1 << 2;
   if (epi == EPI_SWIGLU)
     return cudaLaunchKernelEx(&cfg, grouped_gemm_2sm_kernel<EPI_SWIGLU>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                              b_rows_per_slot, out, out_ld, gp, l2pol);
+                              b_rows_per_slot, out, out_ld, gp, l2pol, sched);
   return cudaLaunchKernelEx(&cfg, grouped_gemm_2sm_kernel<EPI_STORE>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                            b_rows_per_slot, out, out_ld, gp, l2pol);
+                            b_rows_per_slot, out, out_ld, gp, l2pol, sched);
 }
 
 cudaError_t launch_grouped_gemm_mc(int epi, const CUtensorMap* tmA, const CUtensorMap* tmBh, const GemmSeg* segs,

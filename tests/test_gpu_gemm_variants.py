@@ -55,8 +55,9 @@ def test_variants_agree_and_match_oracle(cuda, E, k, d, ff, T, rc):
     _, _, _, y6 = _run(cuda, "swap64", E, k, d, ff, T, rc)
     _, _, _, y7 = _run(cuda, "swap128", E, k, d, ff, T, rc)
     _, _, _, y8 = _run(cuda, "mc", E, k, d, ff, T, rc)  # cluster pairs, B multicast
+    _, _, _, y9 = _run(cuda, "2sm", E, k, d, ff, T, rc, env={"MOE_GEMM_SCHED": "dynamic"})  # claimed tiles
     y_ref = oracle.layer_forward(x, wg, experts, rc, k)[0]
-    for y in (y1, y2, y3, y4, y5, y6, y7, y8):
+    for y in (y1, y2, y3, y4, y5, y6, y7, y8, y9):
         err = float(np.max(np.abs(y - y_ref)) / np.max(np.abs(y_ref)))
         assert err <= 2e-2, err
     # same K order per output element, same fp32 accumulation: bit-identical outputs
@@ -66,6 +67,7 @@ def test_variants_agree_and_match_oracle(cuda, E, k, d, ff, T, rc):
     assert np.array_equal(y1, y5), float(np.max(np.abs(y1 - y5)))
     assert np.array_equal(y1, y6) and np.array_equal(y1, y7)
     assert np.array_equal(y1, y8)  # multicast B: the same MMAs on the same operands
+    assert np.array_equal(y1, y9)  # tile order does not change any tile's arithmetic
 
 
 def test_swap_fused_repeated_forwards(cuda):
