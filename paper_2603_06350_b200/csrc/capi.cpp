@@ -264,11 +264,11 @@ void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t r
     if (which == 0)
       CU_CHECK(launch_grouped_gemm_2sm(0, &c->tmA1, &L.tmB1h, c->dplan.p->segs, &c->dplan.p->nseg, 2 * c->ff, c->d,
                                        2 * c->ff, reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff, c->num_sms, s,
-                                       c->use_pdl, c->group_m[0], c->dyn_sched ? c->gemm_sched.p : nullptr));
+                                       c->use_pdl, c->group_m[0], c->sched_2sm() ? c->gemm_sched.p : nullptr));
     else
       CU_CHECK(launch_grouped_gemm_2sm(1, &c->tmA2, &L.tmB2h, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
                                        reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s, c->use_pdl,
-                                       c->group_m[1], c->dyn_sched ? c->gemm_sched.p + 2 : nullptr));
+                                       c->group_m[1], c->sched_2sm() ? c->gemm_sched.p + 2 : nullptr));
     return;
   }
   if (m256) {
@@ -284,7 +284,7 @@ void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t r
     return;
   }
   // 1-SM kernel with the dynamic tile scheduler (counter pair per GEMM)
-  int* sched = c->dyn_sched ? c->gemm_sched.p + 2 * which : nullptr;
+  int* sched = c->sched_1sm() ? c->gemm_sched.p + 2 * which : nullptr;
   if (which == 0)
     CU_CHECK(launch_grouped_gemm(0, gather ? &c->tmX : &c->tmA1, &L.tmB1, c->dplan.p->segs, &c->dplan.p->nseg,
                                  2 * c->ff, c->d, 2 * c->ff, reinterpret_cast<__nv_bfloat16*>(c->h.p), c->ff,

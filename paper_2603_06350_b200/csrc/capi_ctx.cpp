@@ -270,7 +270,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->use_graphs = D.use_cuda_graphs != 0;
     if (const char* v = std::getenv("MOE_CUDA_GRAPHS")) c->use_graphs = std::string(v) == "1";
     c->num_sms = prop.multiProcessorCount;
-    if (const char* v = std::getenv("MOE_GEMM_SCHED")) c->dyn_sched = std::string(v) == "dynamic";
+    if (const char* v = std::getenv("MOE_GEMM_SCHED")) c->sched_mode = std::string(v) == "dynamic" ? 2 : std::string(v) == "static" ? 1 : 0;
     if (const char* v = std::getenv("MOE_PDL")) c->use_pdl = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_GATHER")) c->gather = std::string(v) == "1";
     if (const char* v = std::getenv("MOE_FUSED_COMBINE")) c->fuse_combine = std::string(v) == "1";

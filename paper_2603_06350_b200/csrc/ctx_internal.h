@@ -328,7 +328,12 @@ struct moe_ctx {
   DevBuf<float> gu_f32;   // fp32 GEMM1 output [rows_cap][2 ff]
   DevBuf<float> gate_partial;  // split-K gate scratch (small batches)
   bool use_graphs = false;     // replay single-GPU forwards as CUDA graphs
-  bool dyn_sched = false;      // K4 claims tiles from a global counter (MOE_GEMM_SCHED=dynamic; A/B: no gain)
+  // K4 tile scheduler (MOE_GEMM_SCHED): 0 auto = the 2-SM kernel claims tiles from a global
+  // counter (-24% DRAM bytes at cfg2, profiles/ab_2sm_sched_r02.md), the 1-SM kernel walks
+  // them statically; 1 static everywhere; 2 dynamic everywhere (1-SM A/B: no gain)
+  int sched_mode = 0;
+  bool sched_2sm() const { return sched_mode != 1; }
+  bool sched_1sm() const { return sched_mode == 2; }
   bool use_pdl = true;         // K4 launched programmatically behind its producer (MOE_PDL=0: off)
   // single GPU: GEMM1 gathers its A rows from x with TMA gather4 and the
   // dispatch kernel only ranks (MOE_GATHER=1).  Opt-in: bit-identical, but 32
