@@ -141,17 +141,22 @@ class ClockSampler:
                 reasons = N.nvmlDeviceGetCurrentClocksEventReasons(h)
                 self.rows.append(dict(sm=N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM), smax=smax,
                                       power=N.nvmlDeviceGetPowerUsage(h) / 1000.0, reasons=reasons))
+                self.ready.set()
                 self.stop.wait(self.period)
             if self.e0 is not None:
                 self.energy_j = (N.nvmlDeviceGetTotalEnergyConsumption(h) - self.e0) / 1000.0
         except Exception as e:  # no NVML: report unsampled
             self.err = repr(e)
+        finally:
+            self.ready.set()
 
     def __enter__(self):
         import threading
         self.stop = threading.Event()
+        self.ready = threading.Event()
         self.th = threading.Thread(target=self._loop, daemon=True)
         self.th.start()
+        self.ready.wait(timeout=10)  # NVML initialised and sampling before the timed region starts
         return self
 
     def __exit__(self, *a):

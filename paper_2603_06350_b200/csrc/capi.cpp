@@ -394,6 +394,16 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
     c->tmX_T = T;
   }
   mark(0);
+  // decode: pull the first experts' weights into L2 on a side stream while the
+  // front end runs (the swap-AB K4 streams them in expert order)
+  const bool prefetch = swap && c->prefetch_mb > 0 && c->G == 1 && !c->fp32 && L.w13.p;
+  if (prefetch) {
+    CU_CHECK(cudaEventRecord(c->ev_pf_fork, s));
+    CU_CHECK(cudaStreamWaitEvent(c->pstream, c->ev_pf_fork, 0));
+    const size_t bytes = std::min(static_cast<size_t>(c->prefetch_mb) << 20, L.w13.n * sizeof(uint16_t));
+    CU_CHECK(launch_l2_prefetch(L.w13.p, bytes, c->pstream));
+    CU_CHECK(cudaEventRecord(c->ev_pf_join, c->pstream));
+  }
   // the gate publishes the histograms itself (not the caller-ids kernel)
   const bool mirrored = c->G == 1 && !c->fp32 && T > 0 && !c->ext_route;
   stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr, mirrored, stride);
@@ -463,6 +473,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   stage_exchange(c, false, s);
   mark(7);
   if (!fused) stage_combine(c, y, T, s);
+  if (prefetch) CU_CHECK(cudaStreamWaitEvent(s, c->ev_pf_join, 0));  // the side stream rejoins
   mark(8);
   if (deferred && !capturing) c->pending = PendingPlan{true, layer, plan_mode, iteration, stride, ahead ? gslot : -1};
 }

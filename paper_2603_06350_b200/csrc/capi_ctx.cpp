@@ -290,6 +290,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_GEMM_SWAP128_ROWS")) c->swap128_rows = std::atoi(v);
     if (const char* v = std::getenv("MOE_SWAP_FUSE")) c->swap_fuse = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_FUSE_PLAN")) c->fuse_plan = std::string(v) != "0";
+    if (const char* v = std::getenv("MOE_DECODE_PREFETCH_MB")) c->prefetch_mb = std::max(0, std::atoi(v));
     if (const char* v = std::getenv("MOE_PDL_FRONT")) c->pdl_front = std::atoi(v);
     if (const char* v = std::getenv("MOE_SWAP_WPOL")) g_swap_wpol.store(std::atoi(v));
     if (const char* v = std::getenv("MOE_GEMM_L2POL")) g_gemm_l2pol.store(std::atoi(v));
@@ -414,6 +415,9 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     c->events.create();
     CU_CHECK(cudaEventCreateWithFlags(&c->ev_counts, cudaEventDisableTiming));
     CU_CHECK(cudaEventCreateWithFlags(&c->ev_ctx_tail, cudaEventDisableTiming));
+    CU_CHECK(cudaStreamCreateWithFlags(&c->pstream, cudaStreamNonBlocking));
+    CU_CHECK(cudaEventCreateWithFlags(&c->ev_pf_fork, cudaEventDisableTiming));
+    CU_CHECK(cudaEventCreateWithFlags(&c->ev_pf_join, cudaEventDisableTiming));
     CU_CHECK(cudaEventCreateWithFlags(&c->ev_fwd_tail, cudaEventDisableTiming));
     for (auto& tri : c->gemm_ev)
       for (cudaEvent_t& e : tri) CU_CHECK(cudaEventCreate(&e));
@@ -456,6 +460,12 @@ int moe_ctx_destroy(moe_ctx* c) {
     if (c->ev_wg_staged) cudaEventDestroy(c->ev_wg_staged);
     if (c->ev_counts) cudaEventDestroy(c->ev_counts);
     if (c->ev_ctx_tail) cudaEventDestroy(c->ev_ctx_tail);
+    if (c->pstream) {
+      cudaStreamSynchronize(c->pstream);
+      cudaStreamDestroy(c->pstream);
+    }
+    for (cudaEvent_t e : {c->ev_pf_fork, c->ev_pf_join})
+      if (e) cudaEventDestroy(e);
     if (c->ev_fwd_tail) cudaEventDestroy(c->ev_fwd_tail);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     for (auto& tri : c->gemm_ev)

@@ -63,6 +63,7 @@ cudaError_t launch_p2p_wait(const uint32_t* my_flags, int G, int kind, const uin
 cudaError_t launch_p2p_counts(const PeerSlabs& peers, int G, int rank, int stride, uint32_t* epoch,
                               uint64_t timeout_ns, int* err, int32_t* counts_all, cudaStream_t s);
 cudaError_t launch_small_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
+cudaError_t launch_l2_prefetch(const void* base, size_t bytes, cudaStream_t s);
 cudaError_t launch_plan_exchange(const int32_t* counts_all, int stride, int G, int rank, const PlacementTable* pt,
                                  DevPlan* plan, cudaStream_t s);
 // K7 fp32 path
@@ -319,6 +320,11 @@ struct moe_ctx {
   bool pdl_combine() const { return (pdl_front & (capturing ? 8 : 2)) != 0; }
   bool swap_fuse = true;  // swap-AB: GEMM1 and GEMM2 in one launch (MOE_SWAP_FUSE=0: two)
   bool fuse_plan = true;  // single GPU, <= 32 blocks: dispatch builds prefix + plan (MOE_FUSE_PLAN=0: block-prefix launch)
+  // decode (swap-AB K4): MB of the first experts' weights prefetched into L2 on a side
+  // stream while the front end runs (MOE_DECODE_PREFETCH_MB; 0 = off)
+  int prefetch_mb = 0;
+  cudaStream_t pstream = nullptr;
+  cudaEvent_t ev_pf_fork = nullptr, ev_pf_join = nullptr;
   DevBuf<int> swap_ready; // its per-(segment, m-tile) GEMM1-done counters (+ CTA counter)
   int pred_distance = 1;  // predictor slot 0 scores layer + pred_distance
   int count_stride = 0;   // ints per rank in the counts buffer: E * (1 + n_pred)

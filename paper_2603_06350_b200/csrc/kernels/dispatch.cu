@@ -491,6 +491,24 @@ __global__ void __launch_bounds__(256) small_copy_kernel(int4* __restrict__ dst,
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
 
+// Decode: the first expert weights the swap-AB K4 will stream, pulled into L2
+// on a side stream while the gate / dispatch front end runs (they use little
+// HBM bandwidth).  One thread per CTA issues bulk prefetches of 256 KB pieces.
+__global__ void __launch_bounds__(32) l2_prefetch_kernel(const uint8_t* __restrict__ base, size_t bytes) {
+  constexpr size_t kPiece = 256 * 1024;
+  if (threadIdx.x != 0) return;
+  for (size_t off = static_cast<size_t>(blockIdx.x) * kPiece; off < bytes; off += static_cast<size_t>(gridDim.x) * kPiece) {
+    const size_t n = bytes - off < kPiece ? bytes - off : kPiece;
+    bulk_prefetch_l2(base + off, static_cast<uint32_t>(n & ~size_t(15)));
+  }
+}
+
+cudaError_t launch_l2_prefetch(const void* base, size_t bytes, cudaStream_t s) {
+  if (!base || bytes < 16) return cudaSuccess;
+  l2_prefetch_kernel<<<16, 32, 0, s>>>(static_cast<const uint8_t*>(base), bytes);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_small_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   if (bytes == 0) return cudaSuccess;
   if ((bytes & 15) || (reinterpret_cast<uintptr_t>(dst) & 15) || (reinterpret_cast<uintptr_t>(src) & 15))
@@ -579,6 +597,7 @@ cudaError_t preload_dispatch_kernels() {
   cudaFuncAttributes a;
   const void* fns[] = {
       reinterpret_cast<const void*>(block_prefix_kernel),  reinterpret_cast<const void*>(dispatch_kernel<1>),
+      reinterpret_cast<const void*>(l2_prefetch_kernel),
       reinterpret_cast<const void*>(dispatch_kernel<2>),   reinterpret_cast<const void*>(dispatch_kernel<4>),
       reinterpret_cast<const void*>(dispatch_kernel<6>),   reinterpret_cast<const void*>(dispatch_kernel<8>),
       reinterpret_cast<const void*>(combine_kernel<1>),    reinterpret_cast<const void*>(combine_kernel<2>),

@@ -315,6 +315,12 @@ __device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// bulk L2 prefetch of [p, p + bytes) (bytes a multiple of 16), no shared memory
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
+               : "memory");
+}
+
 // --------------------------------------------------------------- misc
 __device__ __forceinline__ int4 ld_nc_v4(const void* p) {
   int4 r;

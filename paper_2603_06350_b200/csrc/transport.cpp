@@ -7,6 +7,7 @@
 #include <condition_variable>
 #include <cstring>
 #include <deque>
+#include <iterator>
 #include <map>
 #include <mutex>
 #include <string>
@@ -69,6 +70,8 @@ std::map<std::string, std::weak_ptr<CopyHub>> g_hubs;
 std::shared_ptr<CopyHub> hub_for(const void* group, int G) {
   const std::string key(static_cast<const char*>(group), 128);
   std::lock_guard<std::mutex> l(g_hubs_mu);
+  for (auto it = g_hubs.begin(); it != g_hubs.end();)  // groups whose ranks are all gone
+    it = it->second.expired() && it->first != key ? g_hubs.erase(it) : std::next(it);
   auto h = g_hubs[key].lock();
   if (!h) {
     h = std::make_shared<CopyHub>(G);
