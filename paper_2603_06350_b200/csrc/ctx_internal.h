@@ -321,8 +321,8 @@ struct moe_ctx {
   bool swap_fuse = true;  // swap-AB: GEMM1 and GEMM2 in one launch (MOE_SWAP_FUSE=0: two)
   bool fuse_plan = true;  // single GPU, <= 32 blocks: dispatch builds prefix + plan (MOE_FUSE_PLAN=0: block-prefix launch)
   // decode (swap-AB K4): MB of the first experts' weights prefetched into L2 on a side
-  // stream while the front end runs (MOE_DECODE_PREFETCH_MB; 0 = off)
-  int prefetch_mb = 0;
+  // stream while the front end runs (MOE_DECODE_PREFETCH_MB, default 64; 0 = off)
+  int prefetch_mb = 64;
   cudaStream_t pstream = nullptr;
   cudaEvent_t ev_pf_fork = nullptr, ev_pf_join = nullptr;
   DevBuf<int> swap_ready; // its per-(segment, m-tile) GEMM1-done counters (+ CTA counter)
