@@ -192,7 +192,8 @@ def single_gpu_launches(T, k, E):
     split = nblk * 4 <= 2 * 148          # gate_splits: small batches split K (+ finish kernel)
     fused_plan = nblk <= 32              # dispatch builds prefix + plan itself
     swap = T * k / E <= 1024             # swap-AB tiles: GEMM1 + GEMM2 in one launch
-    return 1 + split + (0 if fused_plan else 1) + 1 + (1 if swap else 2) + 1
+    prefetch = swap                      # + the side-stream L2 prefetch of the first weights
+    return 1 + split + (0 if fused_plan else 1) + 1 + (1 if swap else 2) + 1 + prefetch
 
 
 def config_dict(G, c):
