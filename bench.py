@@ -77,6 +77,11 @@ def parse():
                          "owners' buffers) or NCCL grouped send/recv")
     ap.add_argument("--workload", choices=["cfg2", "cfg1", "cfg3", "cfg5", "cfg5s12"], default="cfg2",
                     help="layer shape (cfg2 = the headline Mixtral layer)")
+    ap.add_argument("--plan", choices=["sync", "predicted"], default=None,
+                    help="sync: scale/place on each step's actual loads (a host round trip per layer at N>1); "
+                         "predicted: MoEless planning off the critical path (the layer's historical bootstrap "
+                         "plans its next forward, which then runs device-planned).  Default: sync at N=1 (no "
+                         "round trip there: the planner bookkeeping is deferred), predicted at N>1")
     ap.add_argument("--residency", choices=["all", "placed"], default="all",
                     help="N>1 expert weights: every expert resident on every GPU, or only home experts + "
                          "replica cache slots with cold replicas copied from their home GPU over NVLink")
@@ -196,14 +201,18 @@ def single_gpu_launches(T, k, E):
     return 1 + split + (0 if fused_plan else 1) + 1 + (1 if swap else 2) + 1 + prefetch
 
 
-def config_dict(G, c):
+PLANNER = {"sync": "MOE_PLAN_SYNC (scale_experts + place_experts on actual loads)",
+           "predicted": "MOE_PLAN_PREDICTED (historical bootstrap planned one step ahead; device-planned forwards)"}
+
+
+def config_dict(G, c, plan="sync"):
     """The `config` of both arms' lines (identical for the same workload and N)."""
     E, k, d, ff, T = c["E"], c["k"], c["d"], c["ff"], c["T"]
     return {"workload": WORKLOAD, "global_batch": G * T, "tokens_per_gpu": T, "seq_len": None,
             "parallelism": f"ep{G}", "experts": E, "top_k": k, "d_model": d, "d_ff": ff,
             "l2": f"inputs larger than L2 ({E * 3 * d * ff * 2 / 1e9:.2f} GB of expert weights + "
                   f"{T * d * 2 / 1e6:.0f} MB of tokens per step vs 126 MB of L2)",
-            "planner": "MOE_PLAN_SYNC (scale_experts + place_experts on actual loads)"}
+            "planner": PLANNER[plan]}
 
 
 def host_cpu():
@@ -306,7 +315,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (the same keyed inputs as the GPU arm, from the oracle's generator)",
-        "config": config_dict(G, c),
+        "config": config_dict(G, c, args.plan),
         "p50_ms": statistics.median(ms), "p99_ms": pct(ms, 0.99) if pct else max(ms),
         "latency_note": "per-layer latency scaled from the sample to the full batch",
         "sample": {"tokens_per_step": sample, "tokens_per_layer": c["T"],
@@ -343,7 +352,8 @@ def run_ours(args):
     import numpy as np
     import torch
 
-    from paper_2603_06350_b200 import (MOE_EXCHANGE_NCCL, MOE_EXCHANGE_P2P, MOE_PLAN_SYNC, MoELayer, nccl_unique_id,
+    from paper_2603_06350_b200 import (MOE_EXCHANGE_NCCL, MOE_EXCHANGE_P2P, MOE_PLAN_PREDICTED, MOE_PLAN_SYNC,
+                                       MoELayer, nccl_unique_id,
                                        percentile)
     from paper_2603_06350_b200 import workload as wl
 
@@ -368,6 +378,7 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = CFG
     E, k, d, ff, T = c["E"], c["k"], c["d"], c["ff"], c["T"]
+    plan_mode = MOE_PLAN_PREDICTED if args.plan == "predicted" else MOE_PLAN_SYNC
     uid = None
     p2p = G > 1 and args.exchange == "p2p"
     mem = 3.0 * d * ff * 2 / 1e6
@@ -434,7 +445,7 @@ def run_ours(args):
 
     def step(it, stats=True):
         m.set_gate_device(0, gates[it])
-        return m.forward(0, pool[it % args.pool], y, MOE_PLAN_SYNC, it, stats=stats)
+        return m.forward(0, pool[it % args.pool], y, plan_mode, it, stats=stats)
 
     def barrier():
         torch.cuda.synchronize()
@@ -532,7 +543,7 @@ def run_ours(args):
         tickets = []
         for i in range(2):  # warm the staging buffers / streams
             m.set_gate_device(0, gates[i])
-            tickets.append(m.forward_host_async(0, xh[i % len(xh)], yh[i % 3], MOE_PLAN_SYNC, i))
+            tickets.append(m.forward_host_async(0, xh[i % len(xh)], yh[i % 3], plan_mode, i))
         for t in tickets:
             m.wait(t)
         barrier()
@@ -543,7 +554,7 @@ def run_ours(args):
             if i >= 3:
                 m.wait(tickets[i - 3])  # its output buffer is about to be reused
             m.set_gate_device(0, gates[it])
-            tickets.append(m.forward_host_async(0, xh[i % len(xh)], yh[i % 3], MOE_PLAN_SYNC, it))
+            tickets.append(m.forward_host_async(0, xh[i % len(xh)], yh[i % 3], plan_mode, it))
         for t in tickets[-3:]:
             m.wait(t)
         e2e_ms = (time.perf_counter() - t0) * 1e3  # host-visible: every result is in host memory
@@ -571,7 +582,7 @@ def run_ours(args):
             "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (keyed Zipf-skewed gate inputs, random-init expert weights)",
-            "config": config_dict(G, c),
+            "config": config_dict(G, c, args.plan),
             "exchange": (exchange_note or ("peer memory (P2P)" if p2p else "NCCL send/recv")) if G > 1
                         else "none (G=1)",
             "p50_ms": p50, "p99_ms": p99,
@@ -635,6 +646,8 @@ def run_ours(args):
 def main():
     global CFG, WORKLOAD
     args = parse()
+    if args.plan is None:
+        args.plan = "predicted" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "sync"
     if args.workload != "cfg2":
         CFG, WORKLOAD = OTHER_WORKLOADS[args.workload]
     if args.impl == "reference":

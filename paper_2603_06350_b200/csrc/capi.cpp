@@ -85,6 +85,11 @@ void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int3
     // synchronous planning on the actual loads (oracle predictor, distance 0)
     plan_layer(c, layer, total, iteration);
     L.plan_source = 1;
+  } else if (plan_mode == MOE_PLAN_PREDICTED && L.plan_for != iteration && L.boot_ready) {
+    // the bootstrap placement planned at the previous forward's flush (below)
+    L.boot_ready = false;
+    L.plan_source = 3;
+    ++L.bootstraps;
   } else if (plan_mode == MOE_PLAN_PREDICTED && L.plan_for != iteration) {
     // no prediction reached this layer (l < d, simulator.cpp:146-151): bootstrap
     // from the layer's load history with the historical predictor
@@ -123,6 +128,23 @@ void stage_plan(moe_ctx* c, int layer, int plan_mode, long iteration, const int3
   if (c->plan.rows_local > c->rows_cap || (!c->p2p && c->plan.rows_send > c->send_cap))
     throw Status(MOE_EINFEASIBLE, "received rows exceed workspace capacity");
   *c->hplan = c->plan.dev;
+  // MoEless plans off the critical path.  A layer no predictor reaches (l < d)
+  // bootstraps from its load history (simulator.cpp:146-151) — and the history
+  // is all that needs, so the placement of its NEXT forward is planned here, and
+  // that forward takes the device-planned path instead of a host round trip.
+  // The target total is this batch's (the reference takes the incoming batch's:
+  // the same for fixed batch sizes).  Not with PLACED residency: the copies a
+  // new placement may start must be ordered after this forward's GEMMs.
+  const bool upstream = layer >= c->pred_distance && c->n_pred > 0 &&
+                        c->layers[layer - c->pred_distance].has_pred_weights;
+  L.boot_ready = false;
+  if (plan_mode == MOE_PLAN_PREDICTED && !upstream && !c->placed) {
+    moeless::PredictorProfile hp;
+    hp.kind = moeless::PredictorKind::historical;
+    const auto guess = moeless::predict({layer, total}, L.history, hp, iteration + 1, 1);
+    plan_layer(c, layer, guess.loads, iteration + 1);
+    L.boot_ready = true;
+  }
 }
 
 // local_plan (single GPU): the scan launch also builds the dispatch plan from
@@ -515,7 +537,8 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
   const bool with_pred = c->n_pred > 0 && L.has_pred_weights && !c->ext_route;
   const int stride = with_pred ? c->count_stride : c->E;
   const bool ahead = c->G > 1 && c->p2p && !c->fp32 &&
-                     (plan_mode == MOE_PLAN_FIXED || (plan_mode == MOE_PLAN_PREDICTED && L.plan_for == iteration));
+                     (plan_mode == MOE_PLAN_FIXED ||
+                      (plan_mode == MOE_PLAN_PREDICTED && (L.plan_for == iteration || L.boot_ready)));
   if (ahead) ensure_placement(c, layer);
   if (c->use_graphs && !timed && (c->G == 1 || ahead) && !c->placed && !c->ext_route) {
     // Replay the layer's whole device sequence (8-14 kernels) as one CUDA

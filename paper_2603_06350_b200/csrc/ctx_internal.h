@@ -243,6 +243,7 @@ struct Layer {
   std::vector<int64_t> pred_loads;          // predicted loads for this layer (made d layers earlier)
   bool pred_valid = false;
   long plan_for = -1;                       // iteration whose placement was planned ahead
+  bool boot_ready = false;                  // bootstrap placement of the next forward already planned
   double last_accuracy = -1.0, acc_sum = 0.0;
   long acc_n = 0, bootstraps = 0;
   int plan_source = 0;                      // 0 fixed, 1 actual, 2 predicted, 3 historical bootstrap
