@@ -1,0 +1,39 @@
+"""Small forwards for compute-sanitizer runs over the round-2 paths:
+  default  gate (+split-K finish), dispatch with the fused local plan, swap-AB K4
+           with the side-stream L2 prefetch, combine
+  2sm      the 2-SM cta_group::2 K4 with claimed tiles (MOE_GEMM_VARIANT=2sm)
+  ids      moe_layer_forward_ids (route_ids kernel instead of the gate)
+  stream   the streaming prefill gate (MOE_GATE_STREAM=1, T >= 148 blocks)
+  python profiles/sanitize_forward_r02.py <scenario>"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2603_06350_b200 import MOE_PLAN_SYNC, MoELayer  # noqa: E402
+from paper_2603_06350_b200 import workload as wl  # noqa: E402
+
+scenario = sys.argv[1] if len(sys.argv) > 1 else "default"
+E, k, d, ff, T = 8, 2, 256, 256, 200
+if scenario == "2sm":
+    os.environ["MOE_GEMM_VARIANT"] = "2sm"
+    T = 600
+if scenario == "stream":
+    os.environ["MOE_GATE_STREAM"] = "1"
+    d, T = 512, 148 * 32 + 17
+m = MoELayer(1, E, k, d, ff, max_tokens=T, expert_mem_mb=1.0, layer_mem_cap_mb=3.0)
+m.set_gate(0, wl.gate_weights(E, d, 1.2, 1, 0, 0))
+for e in range(E):
+    m.load_expert(0, e, *wl.expert_weights(d, ff, 1, 0, e))
+x = torch.from_numpy(wl.tokens(T, d, E, 1, 0).view(np.int16)).cuda()
+y = torch.zeros((T, d), dtype=torch.int16, device="cuda")
+for it in range(2):
+    if scenario == "ids":
+        ids = torch.from_numpy(np.stack([np.arange(T) % E, (np.arange(T) + 3) % E], 1).astype(np.int32)).cuda()
+        m.forward_ids(0, x, ids, y, None, MOE_PLAN_SYNC, it)
+    else:
+        m.forward(0, x, y, MOE_PLAN_SYNC, it)
+m.sync()
+print(scenario, "forward ok", float(y.float().abs().sum()))
