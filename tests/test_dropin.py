@@ -93,3 +93,53 @@ def test_reference_run_with_the_b200_layer(cuda):
     assert b_sum["p99_forward_ms"] < 50.0
     print(f"sim_b200: p50 {b_sum['p50_forward_ms']:.4f} ms, p99 {b_sum['p99_forward_ms']:.4f} ms "
           f"(analytic reference: {ref_sum['p50_forward_ms']:.4f} / {ref_sum['p99_forward_ms']:.4f})")
+
+
+CPP_IDS_TEST = r"""
+#include <cstdio>
+#include <random>
+#include <set>
+#include "moeless/b200_layer.hpp"
+int main() {
+  std::mt19937_64 rng(7);
+  for (int trial = 0; trial < 500; ++trial) {
+    const int E = 1 + rng() % 64, k = 1 + rng() % std::min(E, 8);
+    const long T = rng() % 300;
+    // random histogram with sum T*k and every load <= T: k distinct experts per token
+    std::vector<std::int64_t> loads(E, 0);
+    for (long t = 0; t < T; ++t) {
+      std::set<int> pick;
+      while ((int)pick.size() < k) pick.insert(rng() % E);
+      for (int e : pick) ++loads[e];
+    }
+    std::int64_t tokens = -1;
+    const auto ids = moeless::b200::ids_for_loads(loads, k, &tokens);
+    if (tokens != T) return 1;
+    std::vector<std::int64_t> h(E, 0);
+    for (long t = 0; t < T; ++t) {
+      std::set<int> row;
+      for (int j = 0; j < k; ++j) { row.insert(ids[t * k + j]); ++h[ids[t * k + j]]; }
+      if ((int)row.size() != k) return 2;  // distinct experts per token
+    }
+    if (h != loads) return 3;             // the histogram is exactly the loads
+  }
+  try { moeless::b200::ids_for_loads({5, 1}, 2, nullptr); return 4; } catch (const std::invalid_argument&) {}
+  std::puts("ids_for_loads ok");
+  return 0;
+}
+"""
+
+
+def test_ids_for_loads_reproduces_any_histogram(tmp_path):
+    """b200::layer_forward_time turns the reference's per-expert loads into
+    per-token ids: the histogram must be exact and no token may repeat an expert
+    (route_tokens draws without replacement, workload.cpp:221-226)."""
+    if not os.path.exists("/root/reference/proj/include/moeless/types.hpp"):
+        pytest.skip("reference headers absent")
+    src = tmp_path / "ids.cpp"
+    src.write_text(CPP_IDS_TEST)
+    exe = tmp_path / "ids"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I/root/reference/proj/include", "-I" + os.path.join(ROOT, "include"),
+                    "-I/usr/local/cuda/include", str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0 and "ids_for_loads ok" in out.stdout, (out.returncode, out.stdout)
