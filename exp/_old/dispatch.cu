@@ -197,44 +197,39 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
     if (threadIdx.x == i) s_tgt[i] = static_cast<__nv_bfloat16*>(targets.base[i]);
   __syncthreads();
 
-  {
+  if (warp == 0) {
     // stable rank of (token, expert) inside the block = number of EARLIER
-    // tokens of the block that chose the same expert: one bit per token.  The
-    // K slots are spread over the CTA's warps (slot j on warp j mod kRankWarps):
-    // every warp first sets its slots' bits, then ranks them.
-    constexpr int kRankWarps = 4;  // blockDim.x / 32
-    constexpr int kMine = (K + kRankWarps - 1) / kRankWarps;
+    // tokens of the block that chose the same expert: one bit per token
     const int t = t_base + lane;
     const bool live = lane < ntok;
-    int my[kMine];
+    int my[K];
 #pragma unroll
-    for (int q = 0; q < kMine; ++q) {
-      const int j = warp + q * kRankWarps;
-      my[q] = live && j < K ? ids[(size_t)t * K + j] : -1;
-      if (my[q] >= 0) atomicOr(&s_mask[my[q]], 1u << lane);
-    }
-    __syncthreads();  // every slot's bit is in the masks
+    for (int j = 0; j < K; ++j) my[j] = live ? ids[(size_t)t * K + j] : -1;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (live) atomicOr(&s_mask[my[j]], 1u << lane);
+    __syncwarp();
     const uint32_t lt = (1u << lane) - 1u;
+    if (live) {
 #pragma unroll
-    for (int q = 0; q < kMine; ++q) {
-      const int j = warp + q * kRankWarps;
-      const int e = my[q];
-      if (e < 0) continue;
-      const int gr = s_pre[e] + __popc(s_mask[e] & lt);
-      // integer replica split: replica r owns floor(n/R) + [r < n mod R] ranks
-      const int Re = s_rbase[e + 1] - s_rbase[e];
-      int r = 0;
-      if (Re > 1) {
-        const int n = s_n[e], qq = n / Re, rem = n % Re;
-        r = gr < rem * (qq + 1) ? gr / (qq + 1) : rem + (gr - rem * (qq + 1)) / qq;
+      for (int j = 0; j < K; ++j) {
+        const int e = my[j];
+        const int gr = s_pre[e] + __popc(s_mask[e] & lt);
+        // integer replica split: replica r owns floor(n/R) + [r < n mod R] ranks
+        const int Re = s_rbase[e + 1] - s_rbase[e];
+        int r = 0;
+        if (Re > 1) {
+          const int n = s_n[e], q = n / Re, rem = n % Re;
+          r = gr < rem * (q + 1) ? gr / (q + 1) : rem + (gr - rem * (q + 1)) / q;
+        }
+        const int f = s_rbase[e] + r;
+        const uint32_t code =
+            static_cast<uint32_t>(s_rrow[f] + gr) | (static_cast<uint32_t>(s_rrem[f]) << kTargetShift);
+        codes[lane * K + j] = code;
+        if (blockIdx.y == 0) row_code[(size_t)t * K + j] = code;
+        if (perm_src) perm_src[code & kRowMask] = t;  // gathered GEMM1: row -> token
+        if (row_owner) row_owner[code & kRowMask] = t * K + j;  // fused combine: row -> (token, slot)
       }
-      const int f = s_rbase[e] + r;
-      const uint32_t code =
-          static_cast<uint32_t>(s_rrow[f] + gr) | (static_cast<uint32_t>(s_rrem[f]) << kTargetShift);
-      codes[lane * K + j] = code;
-      if (blockIdx.y == 0) row_code[(size_t)t * K + j] = code;
-      if (perm_src) perm_src[code & kRowMask] = t;  // gathered GEMM1: row -> token
-      if (row_owner) row_owner[code & kRowMask] = t * K + j;  // fused combine: row -> (token, slot)
     }
   }
   if (perm_src) {  // single GPU, gathered GEMM1: the rows are read from x in place
