@@ -449,6 +449,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 
 // One epilogue warp's 32 rows of a 128x256 accumulator -> bf16 (SwiGLU: the
 // 128 gate/up column pairs -> 128 columns of H).
+#ifndef MOE_EPI_NOSTORE
+#define MOE_EPI_NOSTORE 0  // 1: skip the global stores (A/B of the epilogue's cost only; wrong outputs)
+#endif
 template <int EPI>
 __device__ __forceinline__ void store_accumulator(uint32_t taddr, __nv_bfloat16* __restrict__ out, size_t grow,
                                                   bool valid, int n, int out_ld) {
@@ -467,7 +470,7 @@ __device__ __forceinline__ void store_accumulator(uint32_t taddr, __nv_bfloat16*
         const float h1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
         packed[i] = pack_bf16(h0, h1);
       }
-      if (valid) {
+      if (valid && !MOE_EPI_NOSTORE) {
         int4* p = reinterpret_cast<int4*>(dst + ch * 32);
 #pragma unroll
         for (int v = 0; v < 4; ++v) p[v] = make_int4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
@@ -483,7 +486,7 @@ __device__ __forceinline__ void store_accumulator(uint32_t taddr, __nv_bfloat16*
       uint32_t packed[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) packed[i] = pack_bf16(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-      if (valid) {
+      if (valid && !MOE_EPI_NOSTORE) {
         int4* p = reinterpret_cast<int4*>(dst + ch * 32);
 #pragma unroll
         for (int v = 0; v < 4; ++v) p[v] = make_int4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
