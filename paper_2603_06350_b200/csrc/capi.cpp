@@ -419,50 +419,73 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   // decode: pull the first experts' weights into L2 on a side stream while the
   // front end runs (the swap-AB K4 streams them in expert order)
   const bool prefetch = swap && c->prefetch_mb > 0 && c->G == 1 && !c->fp32 && L.w13.p;
-  if (prefetch) {
+  const size_t prefetch_bytes =
+      prefetch ? std::min(static_cast<size_t>(c->prefetch_mb) << 20, L.w13.n * sizeof(uint16_t)) : 0;
+  // single GPU, small batch: gate, top-k, plan and dispatch in one cooperative
+  // launch (the weight prefetch folded in)
+  const int Etot = with_pred ? c->count_stride : c->E;
+  const bool front = c->frontend && c->G == 1 && !c->fp32 && !c->ext_route && !gather && !fused && L.has_gate &&
+                     frontend_applies(T, c->d, Etot, c->k, c->num_sms);
+  const bool inline_prefetch = prefetch && front && c->front_prefetch_inline;
+  if (prefetch && !inline_prefetch) {
     CU_CHECK(cudaEventRecord(c->ev_pf_fork, s));
     CU_CHECK(cudaStreamWaitEvent(c->pstream, c->ev_pf_fork, 0));
-    const size_t bytes = std::min(static_cast<size_t>(c->prefetch_mb) << 20, L.w13.n * sizeof(uint16_t));
-    CU_CHECK(launch_l2_prefetch(L.w13.p, bytes, c->pstream));
+    CU_CHECK(launch_l2_prefetch(L.w13.p, prefetch_bytes, c->pstream));
     CU_CHECK(cudaEventRecord(c->ev_pf_join, c->pstream));
   }
   // the gate publishes the histograms itself (not the caller-ids kernel)
   const bool mirrored = c->G == 1 && !c->fp32 && T > 0 && !c->ext_route;
-  stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr, mirrored, stride);
-  if (c->G > 1 && c->p2p) {
-    // every rank reads every histogram from its owner's slab
-    CU_CHECK(launch_p2p_counts(c->peers, c->G, c->rank, stride, c->epoch_dev.p, c->p2p_timeout_ns, c->p2p_err,
-                               c->counts_all.p, s));
-    if (c->placed && !c->peers_ready) {
-      // every rank has entered its first forward, so every home expert is
-      // loaded: weight copies from peers may start from here on
-      CU_CHECK(cudaEventRecord(c->ev_peers_ready, s));
-      CU_CHECK(cudaStreamWaitEvent(c->wstream, c->ev_peers_ready, 0));
-      c->peers_ready = true;
-      for (size_t l = 0; l < c->layers.size(); ++l) issue_weight_copies(c, static_cast<int>(l));
-    }
-    CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
-  } else if (c->G > 1) {
-    require(c->transport != nullptr, "staged API required for external exchange");
-    c->transport->all_gather(c->counts.p, c->counts_all.p, stride, s);
-    CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
-  } else if (!mirrored) {
-    CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * stride), s));
-  }
-  if (deferred) {
-    CU_CHECK(cudaEventRecordWithFlags(c->ev_counts, s, rec));
+  if (front) {
+    CU_CHECK(launch_frontend(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
+                             reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, with_pred ? c->n_pred : 0, c->k,
+                             c->ids.p, c->wts.p, c->counts.p, c->block_counts.p, c->gate_partial.p, c->h_counts,
+                             L.pred_w2.p, L.mlp_mask, reinterpret_cast<__nv_bfloat16*>(c->xp.p), c->row_code.p,
+                             c->dplan.p, inline_prefetch ? L.w13.p : nullptr, prefetch_bytes, c->front_trace.p, s));
+    // "counts are in host memory" on a side branch: an event node between the
+    // front end and the GEMM would cut their programmatic edge
+    CU_CHECK(cudaEventRecord(c->ev_front, s));
+    CU_CHECK(cudaStreamWaitEvent(c->pstream, c->ev_front, 0));
+    CU_CHECK(cudaEventRecordWithFlags(c->ev_counts, c->pstream, rec));
+    CU_CHECK(cudaEventRecord(c->ev_pf_join, c->pstream));
     mark(1);
-    if (c->G > 1) CU_CHECK(launch_plan_exchange(c->counts_all.p, stride, c->G, c->rank, L.ptab.p, c->dplan.p, s));
     mark(2);
-    stage_dispatch(c, x, T, s, /*upload_plan=*/false, gather, fused, /*local_plan=*/c->G == 1);
   } else {
-    mark(1);
-    CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram
-    check_p2p(c);
-    check_ids(c);
-    stage_plan(c, layer, plan_mode, iteration, c->h_counts, stride);
-    mark(2);
-    stage_dispatch(c, x, T, s);  // uploads the plan; P2P rows land in their owners' buffers
+    stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr, mirrored, stride);
+    if (c->G > 1 && c->p2p) {
+      // every rank reads every histogram from its owner's slab
+      CU_CHECK(launch_p2p_counts(c->peers, c->G, c->rank, stride, c->epoch_dev.p, c->p2p_timeout_ns, c->p2p_err,
+                                 c->counts_all.p, s));
+      if (c->placed && !c->peers_ready) {
+        // every rank has entered its first forward, so every home expert is
+        // loaded: weight copies from peers may start from here on
+        CU_CHECK(cudaEventRecord(c->ev_peers_ready, s));
+        CU_CHECK(cudaStreamWaitEvent(c->wstream, c->ev_peers_ready, 0));
+        c->peers_ready = true;
+        for (size_t l = 0; l < c->layers.size(); ++l) issue_weight_copies(c, static_cast<int>(l));
+      }
+      CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
+    } else if (c->G > 1) {
+      require(c->transport != nullptr, "staged API required for external exchange");
+      c->transport->all_gather(c->counts.p, c->counts_all.p, stride, s);
+      CU_CHECK(launch_small_copy(c->h_counts, c->counts_all.p, pad16(sizeof(int32_t) * c->G * stride), s));
+    } else if (!mirrored) {
+      CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * stride), s));
+    }
+    if (deferred) {
+      CU_CHECK(cudaEventRecordWithFlags(c->ev_counts, s, rec));
+      mark(1);
+      if (c->G > 1) CU_CHECK(launch_plan_exchange(c->counts_all.p, stride, c->G, c->rank, L.ptab.p, c->dplan.p, s));
+      mark(2);
+      stage_dispatch(c, x, T, s, /*upload_plan=*/false, gather, fused, /*local_plan=*/c->G == 1);
+    } else {
+      mark(1);
+      CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram
+      check_p2p(c);
+      check_ids(c);
+      stage_plan(c, layer, plan_mode, iteration, c->h_counts, stride);
+      mark(2);
+      stage_dispatch(c, x, T, s);  // uploads the plan; P2P rows land in their owners' buffers
+    }
   }
   // x is not read after dispatch (after GEMM1 when GEMM1 gathers from it)
   if (x_consumed && !gather) CU_CHECK(cudaEventRecordWithFlags(x_consumed, s, rec));
@@ -495,7 +518,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   stage_exchange(c, false, s);
   mark(7);
   if (!fused) stage_combine(c, y, T, s);
-  if (prefetch) CU_CHECK(cudaStreamWaitEvent(s, c->ev_pf_join, 0));  // the side stream rejoins
+  if (prefetch || front) CU_CHECK(cudaStreamWaitEvent(s, c->ev_pf_join, 0));  // the side stream rejoins
   mark(8);
   if (deferred && !capturing) c->pending = PendingPlan{true, layer, plan_mode, iteration, stride, ahead ? gslot : -1};
 }
@@ -857,6 +880,7 @@ int moe_buffer(moe_ctx* c, int which, void** ptr, int64_t* rows) {
       case 9: *ptr = c->p2p ? c->slab.p + c->off_flags : nullptr; r = kFlagKinds * kMaxRanks; break;  // P2P flags
       case 10: *ptr = c->epoch_dev.p; r = 1; break;  // P2P device epoch
       case 11: *ptr = c->perm_src.p; r = c->plan.rows_local; break;  // gathered GEMM1: row -> token
+      case 12: *ptr = c->front_trace.p; r = c->front_trace.p ? 148 : 0; break;  // MOE_FRONT_TRACE stamps [148][16] u64
       default: throw std::invalid_argument("unknown buffer id");
     }
     if (rows) *rows = r;

@@ -290,6 +290,12 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_GEMM_SWAP128_ROWS")) c->swap128_rows = std::atoi(v);
     if (const char* v = std::getenv("MOE_SWAP_FUSE")) c->swap_fuse = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_FUSE_PLAN")) c->fuse_plan = std::string(v) != "0";
+    if (const char* v = std::getenv("MOE_FRONTEND")) c->frontend = std::string(v) != "0";
+    if (const char* v = std::getenv("MOE_FRONT_PREFETCH")) c->front_prefetch_inline = std::string(v) != "side";
+    if (const char* v = std::getenv("MOE_FRONT_TRACE"); v && std::string(v) == "1") {
+      c->front_trace.alloc(148 * 16);
+      CU_CHECK(cudaMemset(c->front_trace.p, 0, 148 * 16 * sizeof(unsigned long long)));
+    }
     if (const char* v = std::getenv("MOE_DECODE_PREFETCH_MB")) c->prefetch_mb = std::max(0, std::atoi(v));
     if (const char* v = std::getenv("MOE_PDL_FRONT")) c->pdl_front = std::atoi(v);
     if (const char* v = std::getenv("MOE_SWAP_WPOL")) g_swap_wpol.store(std::atoi(v));
@@ -330,6 +336,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     // load every kernel now, not lazily at first launch (see preload_*)
     CU_CHECK(preload_gate_kernels());
     CU_CHECK(preload_dispatch_kernels());
+    CU_CHECK(preload_frontend_kernels());
     CU_CHECK(preload_gemm_kernels());
     CU_CHECK(preload_fp32_kernels());
     CU_CHECK(preload_p2p_kernels());
@@ -417,6 +424,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     CU_CHECK(cudaEventCreateWithFlags(&c->ev_ctx_tail, cudaEventDisableTiming));
     CU_CHECK(cudaStreamCreateWithFlags(&c->pstream, cudaStreamNonBlocking));
     CU_CHECK(cudaEventCreateWithFlags(&c->ev_pf_fork, cudaEventDisableTiming));
+    CU_CHECK(cudaEventCreateWithFlags(&c->ev_front, cudaEventDisableTiming));
     CU_CHECK(cudaEventCreateWithFlags(&c->ev_pf_join, cudaEventDisableTiming));
     CU_CHECK(cudaEventCreateWithFlags(&c->ev_fwd_tail, cudaEventDisableTiming));
     for (auto& tri : c->gemm_ev)
@@ -464,7 +472,7 @@ int moe_ctx_destroy(moe_ctx* c) {
       cudaStreamSynchronize(c->pstream);
       cudaStreamDestroy(c->pstream);
     }
-    for (cudaEvent_t e : {c->ev_pf_fork, c->ev_pf_join})
+    for (cudaEvent_t e : {c->ev_pf_fork, c->ev_pf_join, c->ev_front})
       if (e) cudaEventDestroy(e);
     if (c->ev_fwd_tail) cudaEventDestroy(c->ev_fwd_tail);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);

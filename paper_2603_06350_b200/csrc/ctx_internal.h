@@ -49,6 +49,14 @@ cudaError_t launch_dispatch(const __nv_bfloat16* x, int T, int d, int E, int k, 
                             int32_t* row_owner, bool pdl = false, const int32_t* local_counts = nullptr,
                             const int32_t* block_counts = nullptr, DevPlan* plan_out = nullptr);
 bool dispatch_fuses_plan(int T);  // single GPU: dispatch builds prefix + plan itself (few blocks)
+// decode front end in one cooperative launch (kernels/frontend.cu): gate + top-k + plan + dispatch
+bool frontend_applies(int T, int d, int Etot, int k, int num_sms);
+cudaError_t launch_frontend(const __nv_bfloat16* x, int T, int d, const __nv_bfloat16* w_all, int E, int n_pred, int k,
+                            int32_t* ids, float* wts, int32_t* counts, int32_t* block_counts, float* partial,
+                            int32_t* host_counts, const float* pred_w2, unsigned mlp_mask, __nv_bfloat16* xp,
+                            uint32_t* row_code, DevPlan* plan, const void* prefetch, size_t prefetch_bytes,
+                            unsigned long long* trace, cudaStream_t stream);
+cudaError_t preload_frontend_kernels();
 // K6 over peer memory (p2p.cu)
 constexpr int kMaxRanks = 8;
 enum { kFlagCounts = 0, kFlagRows = 1, kFlagOutputs = 2, kFlagKinds = 4 };
@@ -320,12 +328,17 @@ struct moe_ctx {
   bool pdl_prefix() const { return (pdl_front & (capturing ? 4 : 1)) != 0; }
   bool pdl_combine() const { return (pdl_front & (capturing ? 8 : 2)) != 0; }
   bool swap_fuse = true;  // swap-AB: GEMM1 and GEMM2 in one launch (MOE_SWAP_FUSE=0: two)
+  // single GPU, <= 32 token blocks: gate, top-k, plan and dispatch in ONE cooperative launch
+  // (kernels/frontend.cu; MOE_FRONTEND=0: the gate / finish / dispatch launches)
+  bool frontend = true;
+  bool front_prefetch_inline = true;  // the front end issues the decode weight prefetch itself (MOE_FRONT_PREFETCH=side: side stream)
+  DevBuf<unsigned long long> front_trace;  // MOE_FRONT_TRACE=1: phase stamps of the fused front end (moe_buffer 12)
   bool fuse_plan = true;  // single GPU, <= 32 blocks: dispatch builds prefix + plan (MOE_FUSE_PLAN=0: block-prefix launch)
   // decode (swap-AB K4): MB of the first experts' weights prefetched into L2 on a side
   // stream while the front end runs (MOE_DECODE_PREFETCH_MB, default 64; 0 = off)
   int prefetch_mb = 64;
   cudaStream_t pstream = nullptr;
-  cudaEvent_t ev_pf_fork = nullptr, ev_pf_join = nullptr;
+  cudaEvent_t ev_pf_fork = nullptr, ev_pf_join = nullptr, ev_front = nullptr;
   DevBuf<int> swap_ready; // its per-(segment, m-tile) GEMM1-done counters (+ CTA counter)
   int pred_distance = 1;  // predictor slot 0 scores layer + pred_distance
   int count_stride = 0;   // ints per rank in the counts buffer: E * (1 + n_pred)

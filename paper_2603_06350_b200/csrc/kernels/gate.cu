@@ -41,111 +41,12 @@
 #include <cooperative_groups.h>
 #include <cuda.h>
 
+#include "gate_common.cuh"
 #include "sm100_ptx.cuh"
 
 namespace moe {
 
 namespace {
-
-constexpr int kBlockTokens = 32;  // tokens per CTA == per block_counts row
-constexpr int kWarps = 8;
-constexpr int kSlices = 4;        // K-slices per m-tile inside a CTA
-constexpr int kPerLane = 8;       // stacked logits per lane in the top-k (<= 256)
-constexpr int kMaxHistExperts = 256;
-#ifndef MOE_GATE_UNROLL
-#define MOE_GATE_UNROLL 2
-#endif
-constexpr int kGateUnroll = MOE_GATE_UNROLL;  // K-loop iterations in flight per warp (two 16-byte x loads each)
-
-__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                               uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-// Top-k over logits [base, base+E) of one token's stacked row in shared
-// memory; lane l looks at l, l+32, ...  Every lane returns the same result.
-// Top-k over per-lane values own[s] = value of expert lane + 32 s.
-// S = logits per lane actually held (ceil(columns / 32)): the decode shape
-// (64 experts) scans 2 slots per round, not kPerLane.
-template <int S>
-__device__ __forceinline__ void warp_topk_vals(const float (&own)[S], int E, int k, int (&ids_out)[8],
-                                               float (&logit_out)[8]) {
-  const int lane = lane_id();
-  uint32_t taken = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    if (j >= k) break;
-    float bv = -FLT_MAX;
-    int bi = 0x7fffffff;
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const int e = lane + 32 * s;
-      if (e < E && !((taken >> s) & 1u))
-        if (own[s] > bv || (own[s] == bv && e < bi)) { bv = own[s]; bi = e; }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-    }
-    if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-    ids_out[j] = bi;
-    logit_out[j] = bv;
-  }
-}
-
-template <int S>
-__device__ __forceinline__ void warp_topk(const float* row, int base, int E, int k, int (&ids_out)[8],
-                                          float (&logit_out)[8]) {
-  const int lane = lane_id();
-  float own[S];
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const int e = lane + 32 * s;
-    own[s] = e < E ? row[base + e] : -FLT_MAX;
-  }
-  warp_topk_vals(own, E, k, ids_out, logit_out);
-}
-
-// The batched predictor MLP (K2 with a hidden layer): its E hidden units are
-// the slot's stacked rows (computed in the same read of x as the gate), so
-// per token the warp turns them in place into out[e] = sum_j W2[e][j]
-// relu(hidden_j) — an fmaf chain in j order, reproducible bit for bit on the
-// CPU — and the usual top-k runs on out.  W2 [E][E] fp32 per slot.  A
-// separate instantiation (MLP = true): the linear path keeps its registers.
-struct PredictorMlp {
-  const float* w2;  // [n_pred][E][E]; nullptr: every slot linear
-  uint32_t mask;    // bit p: slot p is an MLP
-};
-
-template <int S>
-__device__ __forceinline__ void mlp_scores_inplace(float* seg, int E, const float* __restrict__ w2) {
-  const int lane = lane_id();
-  float own[S];
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const int e = lane + 32 * s;
-    float acc = 0.0f;
-    if (e < E) {
-      const float* w = w2 + (size_t)e * E;
-      for (int j = 0; j < E; ++j) {
-        const float h = seg[j];
-        acc = fmaf(__ldg(w + j), h > 0.0f ? h : 0.0f, acc);
-      }
-    }
-    own[s] = acc;
-  }
-  __syncwarp();
-#pragma unroll
-  for (int s = 0; s < S; ++s)
-    if (lane + 32 * s < E) seg[lane + 32 * s] = own[s];
-  __syncwarp();
-}
 
 // top-k, softmax and histograms for `ntok` tokens of one 32-token block,
 // starting at token tok0 of the block, whose stacked logits sit in shared
@@ -254,53 +155,11 @@ gate_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, const __nv_b
   constexpr int kLd = kCols + 4;  // padded row of the reduction buffer
   __shared__ float red[kBlockTokens * kLd];
   __shared__ int hist[256];
-  const int warp = threadIdx.x >> 5, lane = lane_id();
-  const int g = lane >> 2, c = lane & 3;
-  const int mt = warp & 1, ks = warp >> 1;
   const int blk = blockIdx.x;
   const int Etot = E * (1 + n_pred);
   for (int i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
 
-  // ---- skinny GEMM: 16 tokens x 8*NT logits over this warp's K-slice
-  const int r0 = blk * kBlockTokens + mt * 16 + g, r1 = r0 + 8;
-  const bool v0 = r0 < T, v1 = r1 < T;
-  const __nv_bfloat16* x0 = x + (size_t)(v0 ? r0 : 0) * d;
-  const __nv_bfloat16* x1 = x + (size_t)(v1 ? r1 : 0) * d;
-  const int slice = d / (kSlices * gridDim.y);  // multiple of 32 (checked by the launcher)
-  const int k_begin = (blockIdx.y * kSlices + ks) * slice, k_end = k_begin + slice;
-  float acc[NT][4];
-#pragma unroll
-  for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
-  const int4 zero = make_int4(0, 0, 0, 0);
-#pragma unroll kGateUnroll
-  for (int kb = k_begin; kb < k_end; kb += 32) {
-    const int f = kb + 8 * c;  // this lane's 8 consecutive features of the 32-feature block
-    const int4 a_lo = v0 ? ld_nc_v4(x0 + f) : zero;
-    const int4 a_hi = v1 ? ld_nc_v4(x1 + f) : zero;
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      const int e = n * 8 + g;
-      const int4 b = e < Etot ? __ldg(reinterpret_cast<const int4*>(w_all + (size_t)e * d + f)) : zero;
-      mma_bf16_16816(acc[n], a_lo.x, a_hi.x, a_lo.y, a_hi.y, b.x, b.y);  // features f .. f+3
-      mma_bf16_16816(acc[n], a_lo.z, a_hi.z, a_lo.w, a_hi.w, b.z, b.w);  // features f+4 .. f+7
-    }
-  }
-  // ---- ordered K-slice reduction into shared memory (deterministic)
-  for (int s = 0; s < kSlices; ++s) {
-    if (ks == s) {
-#pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        float* p0 = red + (mt * 16 + g) * kLd + n * 8 + 2 * c;
-        float* p1 = p0 + 8 * kLd;
-        if (s == 0) {
-          p0[0] = acc[n][0]; p0[1] = acc[n][1]; p1[0] = acc[n][2]; p1[1] = acc[n][3];
-        } else {
-          p0[0] += acc[n][0]; p0[1] += acc[n][1]; p1[0] += acc[n][2]; p1[1] += acc[n][3];
-        }
-      }
-    }
-    __syncthreads();
-  }
+  block_partial_logits<NT>(x, T, d, w_all, Etot, blk, blockIdx.y, gridDim.y, red);
   if (gridDim.y > 1 && cluster_reduce) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
