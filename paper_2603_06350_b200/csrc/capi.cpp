@@ -422,7 +422,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   const size_t prefetch_bytes =
       prefetch ? std::min(static_cast<size_t>(c->prefetch_mb) << 20, L.w13.n * sizeof(uint16_t)) : 0;
   // single GPU, small batch: gate, top-k, plan and dispatch in one cooperative
-  // launch (the weight prefetch folded in)
+  // launch (kernels/frontend.cu)
   const int Etot = with_pred ? c->count_stride : c->E;
   const bool front = c->frontend && c->G == 1 && !c->fp32 && !c->ext_route && !gather && !fused && L.has_gate &&
                      frontend_applies(T, c->d, Etot, c->k, c->num_sms);
@@ -517,7 +517,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   mark(6);
   stage_exchange(c, false, s);
   mark(7);
-  if (!fused) stage_combine(c, y, T, s);
+  if (!fused && !c->skip_combine) stage_combine(c, y, T, s);
   if (prefetch || front) CU_CHECK(cudaStreamWaitEvent(s, c->ev_pf_join, 0));  // the side stream rejoins
   mark(8);
   if (deferred && !capturing) c->pending = PendingPlan{true, layer, plan_mode, iteration, stride, ahead ? gslot : -1};

@@ -291,7 +291,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_SWAP_FUSE")) c->swap_fuse = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_FUSE_PLAN")) c->fuse_plan = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_FRONTEND")) c->frontend = std::string(v) != "0";
-    if (const char* v = std::getenv("MOE_FRONT_PREFETCH")) c->front_prefetch_inline = std::string(v) != "side";
+    if (const char* v = std::getenv("MOE_DEBUG_SKIP_COMBINE")) c->skip_combine = std::string(v) == "1";
+    if (const char* v = std::getenv("MOE_FRONT_PREFETCH")) c->front_prefetch_inline = std::string(v) == "inline";
     if (const char* v = std::getenv("MOE_FRONT_TRACE"); v && std::string(v) == "1") {
       c->front_trace.alloc(148 * 16);
       CU_CHECK(cudaMemset(c->front_trace.p, 0, 148 * 16 * sizeof(unsigned long long)));

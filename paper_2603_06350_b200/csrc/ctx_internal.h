@@ -331,7 +331,9 @@ struct moe_ctx {
   // single GPU, <= 32 token blocks: gate, top-k, plan and dispatch in ONE cooperative launch
   // (kernels/frontend.cu; MOE_FRONTEND=0: the gate / finish / dispatch launches)
   bool frontend = true;
-  bool front_prefetch_inline = true;  // the front end issues the decode weight prefetch itself (MOE_FRONT_PREFETCH=side: side stream)
+  // decode weight prefetch with the fused front end (MOE_FRONT_PREFETCH): the side-stream
+  // kernel (default), or "inline": the front end's CTAs issue the bulk prefetches themselves
+  bool front_prefetch_inline = false;
   DevBuf<unsigned long long> front_trace;  // MOE_FRONT_TRACE=1: phase stamps of the fused front end (moe_buffer 12)
   bool fuse_plan = true;  // single GPU, <= 32 blocks: dispatch builds prefix + plan (MOE_FUSE_PLAN=0: block-prefix launch)
   // decode (swap-AB K4): MB of the first experts' weights prefetched into L2 on a side
@@ -365,6 +367,7 @@ struct moe_ctx {
   // short-K shapes (the late rows' sums serialise on 4 epilogue warps),
   // profiles/ab_fused_combine_r01.md
   bool fuse_combine = false;
+  bool skip_combine = false;  // MOE_DEBUG_SKIP_COMBINE=1: timing experiments only (y is not written)
   DevBuf<unsigned> gate_ticket;  // CTAs of the gate grid done (histogram mirror, self-resetting)
   DevBuf<int32_t> row_owner;  // [rows_cap] row -> t * k + j
   DevBuf<int32_t> comb_cnt;   // [Tmax * d / 256] arrivals per (token, GEMM2 n tile)

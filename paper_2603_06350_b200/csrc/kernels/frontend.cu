@@ -12,8 +12,9 @@
 //
 //   A  split-K partial logits of (32-token block, K split) -> L2 scratch
 //      (block_partial_logits, the gate kernel's fragment mapping and ordered
-//      K-slice sum); the first CTAs also pull the first experts' weights into
-//      L2 for the GEMM that follows (the side-stream prefetch, folded in).
+//      K-slice sum).  (The decode weight prefetch stays on its side stream:
+//      issued from here it delays this phase more than it saves in the GEMM,
+//      profiles/ab_frontend_r02.md.)
 //   B  token t on CTA t mod nctas, one warp: sums the splits' partial logits in
 //      slice order (the finish kernel's arithmetic), top-k (lowest index wins
 //      ties), softmax over the k, ids / weights; predictor slots add into their
