@@ -28,19 +28,37 @@ thread_local std::string g_last_error;
 
 // mirror: the gate's last CTA also copies the histograms (gate + predictor,
 // `stride` ints) into mapped host memory for the host planner (single GPU)
-void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, int32_t* pred_counts,
+// Returns true when the histograms still have to be mirrored to the host (the
+// tcgen05 gate leaves that to a side-stream copy, off the layer's critical path).
+bool stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, int32_t* pred_counts,
                 bool mirror = false, int stride = 0) {
   CU_CHECK(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * c->count_stride, s));
   if (c->ext_route) {  // caller-given routing (moe_layer_forward_ids) instead of K1
     CU_CHECK(launch_route_ids(c->ext_ids, c->ext_wts, T, c->E, c->k, c->ids.p, c->wts.p, c->counts.p,
                               c->block_counts.p, c->ids_err, s));
-    return;
+    return false;
   }
   require(L.has_gate, "gate weights not set for layer");
   if (c->fp32) {
     CU_CHECK(launch_gate_f32(reinterpret_cast<const float*>(x), T, c->d, reinterpret_cast<const float*>(L.wg.p), c->E,
                              c->k, c->ids.p, c->wts.p, c->counts.p, c->block_counts.p, s));
-    return;
+    return false;
+  }
+  // prefill: the tcgen05 gate (128-token tiles of x through TMA); one x map per (x, T)
+  const int n_pred_used = pred_counts ? c->n_pred : 0;
+  const int Etot = c->E * (1 + n_pred_used);
+  const bool mlp = L.pred_w2.p != nullptr && (L.mlp_mask & ((n_pred_used >= 32 ? 0u : (1u << n_pred_used)) - 1u)) != 0;
+  if (gate_tc_applies(T, c->d, Etot, c->k, mlp)) {
+    if (c->tmGateTc_ptr != x || c->tmGateTc_T != T) {
+      c->tmGateTc = make_kmajor_map(x, T, c->d, 128);
+      c->tmGateTc_ptr = x;
+      c->tmGateTc_T = T;
+    }
+    const CUtensorMap tmw = make_kmajor_map(L.wg.p, Etot, c->d, Etot <= 16 ? 16 : 32);  // rows past Etot: zero fill
+    CU_CHECK(launch_gate_tc(&c->tmGateTc, &tmw, T, c->d, c->E, n_pred_used, c->k, c->ids.p, c->wts.p, c->counts.p,
+                            c->block_counts.p, pred_counts ? pred_counts : c->pred_counts.p, nullptr, stride,
+                            c->gate_ticket.p, c->num_sms, s, c->front_trace.p));
+    return mirror;
   }
   // the prefill gate streams x through TMA boxes: one map per (x, T), rebuilt when they change
   const CUtensorMap* tmx = nullptr;
@@ -57,6 +75,7 @@ void stage_gate(moe_ctx* c, Layer& L, const uint16_t* x, int T, cudaStream_t s, 
                             c->k, c->ids.p, c->wts.p, c->counts.p, c->block_counts.p,
                             pred_counts ? pred_counts : c->pred_counts.p, c->gate_partial.p, s,
                             mirror ? c->h_counts : nullptr, stride, c->gate_ticket.p, L.pred_w2.p, L.mlp_mask, tmx));
+  return false;
 }
 
 // buf: [G][stride] int32 from the gate — per rank, E actual counts followed by
@@ -435,6 +454,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   }
   // the gate publishes the histograms itself (not the caller-ids kernel)
   const bool mirrored = c->G == 1 && !c->fp32 && T > 0 && !c->ext_route;
+  bool side_mirror = false;
   if (front) {
     CU_CHECK(launch_frontend(reinterpret_cast<const __nv_bfloat16*>(x), T, c->d,
                              reinterpret_cast<const __nv_bfloat16*>(L.wg.p), c->E, with_pred ? c->n_pred : 0, c->k,
@@ -450,7 +470,16 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
     mark(1);
     mark(2);
   } else {
-    stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr, mirrored, stride);
+    side_mirror = stage_gate(c, L, x, T, s, with_pred ? c->counts.p + c->E : nullptr, mirrored, stride);
+    if (side_mirror) {
+      // the histograms to mapped host memory on the side stream: the PCIe writes
+      // and their flush stay off the layer's critical path
+      CU_CHECK(cudaEventRecord(c->ev_front, s));
+      CU_CHECK(cudaStreamWaitEvent(c->pstream, c->ev_front, 0));
+      CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * stride), c->pstream));
+      CU_CHECK(cudaEventRecordWithFlags(c->ev_counts, c->pstream, rec));
+      CU_CHECK(cudaEventRecord(c->ev_pf_join, c->pstream));
+    }
     if (c->G > 1 && c->p2p) {
       // every rank reads every histogram from its owner's slab
       CU_CHECK(launch_p2p_counts(c->peers, c->G, c->rank, stride, c->epoch_dev.p, c->p2p_timeout_ns, c->p2p_err,
@@ -472,7 +501,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
       CU_CHECK(launch_small_copy(c->h_counts, c->counts.p, pad16(sizeof(int32_t) * stride), s));
     }
     if (deferred) {
-      CU_CHECK(cudaEventRecordWithFlags(c->ev_counts, s, rec));
+      if (!side_mirror) CU_CHECK(cudaEventRecordWithFlags(c->ev_counts, s, rec));
       mark(1);
       if (c->G > 1) CU_CHECK(launch_plan_exchange(c->counts_all.p, stride, c->G, c->rank, L.ptab.p, c->dplan.p, s));
       mark(2);
@@ -518,7 +547,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   stage_exchange(c, false, s);
   mark(7);
   if (!fused && !c->skip_combine) stage_combine(c, y, T, s);
-  if (prefetch || front) CU_CHECK(cudaStreamWaitEvent(s, c->ev_pf_join, 0));  // the side stream rejoins
+  if (prefetch || front || side_mirror) CU_CHECK(cudaStreamWaitEvent(s, c->ev_pf_join, 0));  // the side stream rejoins
   mark(8);
   if (deferred && !capturing) c->pending = PendingPlan{true, layer, plan_mode, iteration, stride, ahead ? gslot : -1};
 }

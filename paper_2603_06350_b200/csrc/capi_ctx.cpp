@@ -304,6 +304,8 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_GATE_MAX_SPLITS")) g_gate_max_splits.store(std::max(1, std::atoi(v)));
     if (const char* v = std::getenv("MOE_GATE_CLUSTER")) g_gate_cluster.store(std::atoi(v) != 0);
     if (const char* v = std::getenv("MOE_GATE_STREAM")) g_gate_stream.store(std::atoi(v) != 0);
+    if (const char* v = std::getenv("MOE_GATE_TC")) g_gate_tc.store(std::atoi(v) != 0);
+    if (const char* v = std::getenv("MOE_GATE_TC_BKS")) g_gate_tc_bks.store(std::atoi(v));
     if (const char* v = std::getenv("MOE_GATE_MIN_SPLITS")) g_gate_min_splits.store(std::max(1, std::atoi(v)));
     if (const char* v = std::getenv("MOE_P2P_TIMEOUT_MS")) c->p2p_timeout_ns = std::strtoull(v, nullptr, 10) * 1000000ull;
     require(D.exchange_mode >= MOE_EXCHANGE_NCCL && D.exchange_mode <= MOE_EXCHANGE_COPY, "unknown exchange mode");

@@ -57,6 +57,13 @@ cudaError_t launch_frontend(const __nv_bfloat16* x, int T, int d, const __nv_bfl
                             uint32_t* row_code, DevPlan* plan, const void* prefetch, size_t prefetch_bytes,
                             unsigned long long* trace, cudaStream_t stream);
 cudaError_t preload_frontend_kernels();
+// prefill gate on tcgen05 (kernels/gate.cu): 128-token tiles, TMA-streamed x
+bool gate_tc_applies(int T, int d, int Etot, int k, bool mlp);
+cudaError_t launch_gate_tc(const CUtensorMap* tmx, const CUtensorMap* tmw, int T, int d, int E, int n_pred, int k,
+                           int32_t* ids, float* wts, int32_t* counts, int32_t* block_counts, int32_t* pred_counts,
+                           int32_t* host_counts, int host_n, unsigned* ticket, int num_sms, cudaStream_t stream,
+                           unsigned long long* trace = nullptr);
+extern std::atomic<int> g_gate_tc, g_gate_tc_bks;
 // K6 over peer memory (p2p.cu)
 constexpr int kMaxRanks = 8;
 enum { kFlagCounts = 0, kFlagRows = 1, kFlagOutputs = 2, kFlagKinds = 4 };
@@ -375,6 +382,9 @@ struct moe_ctx {
   DevBuf<int32_t> perm_src;    // gathered GEMM1: permuted row -> token
   CUtensorMap tmX;             // gather4 map over the current x ({64, 1} box)
   CUtensorMap tmGate;          // the streaming gate's map over the current x ({64, 32} boxes)
+  CUtensorMap tmGateTc;        // the tcgen05 gate's map over the current x ({64, 128} boxes)
+  const void* tmGateTc_ptr = nullptr;
+  int tmGateTc_T = -1;
   const void* tmGate_ptr = nullptr;
   int tmGate_T = -1;
   const void* tmX_ptr = nullptr;

@@ -37,6 +37,7 @@
 #include <cfloat>
 #include <atomic>
 #include <cstdint>
+#include <utility>
 
 #include <cooperative_groups.h>
 #include <cuda.h>
@@ -327,6 +328,252 @@ gate_stream_kernel(const __grid_constant__ CUtensorMap tmx, int T, int d, const 
   publish_counts(counts, mirror, gridDim.x);
 }
 
+// Large batches (prefill), tensor-core gate: 128-token tiles of x stream
+// through an 8-stage TMA ring (64-feature boxes, 128-byte swizzle, L2
+// evict_first) beside the matching 64-feature slice of the stacked gate /
+// predictor rows (N = Etot rounded up to 16 <= 32, L2 evict_last; the rows
+// past Etot are the map's zero fill); one elected thread issues
+// tcgen05.mma (M = 128 tokens, N, K = 16) x4 per stage into a double-buffered
+// TMEM accumulator.  Four epilogue warps each own one 32-token block: a
+// tcgen05.ld gives every thread its token's Etot logits, so top-k, softmax and
+// the block histogram (ballots, one per expert) need no shared memory and no
+// shuffles.  The per-block kernel above keeps ~56 KB per SM in flight through
+// register-direct 16-byte loads; here ~160 KB per SM are in flight and x is
+// read once in 64-feature rows.  Exactness as for the other gate kernels: on
+// the synthetic grid every partial sum is exact in fp32, whatever the order.
+std::atomic<int> g_gate_tc{1};      // env MOE_GATE_TC=0: prefill batches keep the per-block mma.sync gate
+std::atomic<int> g_gate_tc_bks{2};  // env MOE_GATE_TC_BKS: 64-feature k-blocks per ring stage (1, 2, 4)
+constexpr int kTcTile = 128;                              // tokens per tile (UMMA M)
+constexpr uint32_t kTcXBytes = kTcTile * 64 * 2;          // 16 KB x box (64 features)
+constexpr int kTcThreads = 192;                           // producer, MMA, 4 epilogue warps
+constexpr uint32_t kTcRowLd = 33;                         // epilogue staging row (floats), conflict-free
+constexpr uint32_t kTcRingBudget = 196 * 1024;
+// NC accumulator columns (16 or 32 >= Etot); BKS 64-feature k-blocks per stage
+// (adjacent k-blocks of a row are requested together: 128 B -> BKS x 128 B
+// of each token row per DRAM visit)
+template <int NC, int BKS>
+struct TcCfg {
+  static constexpr uint32_t kWBytes = NC * 64 * 2;
+  static constexpr uint32_t kStage = BKS * (kTcXBytes + kWBytes);
+  static constexpr int kStages = kTcRingBudget / kStage < 16 ? kTcRingBudget / kStage : 16;
+  static constexpr uint32_t kSmem = kStages * kStage + 256 + 4 * 32 * kTcRowLd * 4 + 1024;
+};
+template <int NC, int BKS>
+__global__ void __launch_bounds__(kTcThreads, 1)
+gate_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw, int T, int d,
+               int E, int n_pred, int k, int32_t* __restrict__ ids, float* __restrict__ wts,
+               int32_t* __restrict__ counts, int32_t* __restrict__ block_counts, int32_t* __restrict__ pred_counts,
+               const __grid_constant__ CountsMirror mirror, unsigned long long* __restrict__ trace) {
+  extern __shared__ uint8_t tc_raw[];
+  // MOE_FRONT_TRACE: %globaltimer stamps per CTA (start, prologue, first / last stage, epilogue, end)
+  auto stamp = [&](int i) {
+    if (trace) {
+      unsigned long long v;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+      trace[blockIdx.x * 16 + i] = v;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
+  using C = TcCfg<NC, BKS>;
+  constexpr int kTcStages = C::kStages;
+  constexpr uint32_t kTcStageBytes = C::kStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * kTcStageBytes);
+  uint64_t* empty = full + kTcStages;
+  uint64_t* tfull = empty + kTcStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* rows = reinterpret_cast<float*>(smem + kTcStages * kTcStageBytes + 256);  // [4 warps][32][kTcRowLd]
+  __shared__ int s_hist[32];  // this CTA's gate + predictor histograms (Etot <= 32)
+  if (threadIdx.x < 32) s_hist[threadIdx.x] = 0;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int n_tiles = (T + kTcTile - 1) / kTcTile;
+  const int num_kb = d / (64 * BKS);  // stages per tile
+  // this CTA's stages: (tile, k-stage) pairs i = 0 .. n_mine * num_kb - 1
+  const int n_mine = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int pre = min(kTcStages, n_mine * num_kb);  // issued before the CTA-wide sync
+  auto issue = [&](int i, int stage, uint64_t pol_x, uint64_t pol_w) {
+    const int t = blockIdx.x + (i / num_kb) * gridDim.x, kb = i % num_kb;
+    uint8_t* st = smem + stage * kTcStageBytes;
+    mbar_arrive_expect_tx(&full[stage], kTcStageBytes);  // OOB rows are zero-filled
+#pragma unroll
+    for (int q = 0; q < BKS; ++q)
+      tma_load_2d_hint(st + q * kTcXBytes, &tmx, &full[stage], (kb * BKS + q) * 64, t * kTcTile, pol_x);
+#pragma unroll
+    for (int q = 0; q < BKS; ++q)
+      tma_load_2d_hint(st + BKS * kTcXBytes + q * C::kWBytes, &tmw, &full[stage], (kb * BKS + q) * 64, 0, pol_w);
+  };
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmx);
+    tma_prefetch_desc(&tmw);
+    for (int s = 0; s < kTcStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    fence_barrier_init();
+    // the first stages go out before TMEM allocation and the CTA sync (fresh
+    // stages need no empty wait): the first HBM round trip starts at once
+    const uint64_t pol_x = policy_evict_first(), pol_w = policy_evict_last();
+    for (int i = 0; i < pre; ++i) issue(i, i, pol_x, pol_w);
+  }
+  if (warp == 1) tmem_alloc<64>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_launch_dependents();  // the block-prefix launch may be scheduled (it waits for this grid)
+  if (threadIdx.x == 0) stamp(1);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_x = policy_evict_first(), pol_w = policy_evict_last();
+      int stage = pre % kTcStages;
+      uint32_t phase = pre == kTcStages ? 1u : 0u;
+      for (int i = pre; i < n_mine * num_kb; ++i) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        issue(i, stage, pol_x, pol_w);
+        if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = umma_idesc_bf16(kTcTile, NC);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      const uint32_t base = smem_u32(smem);
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem_base + acc * 32;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (kb == 0) stamp(2);
+          if (kb == num_kb - 1) stamp(3);
+#pragma unroll
+          for (int b = 0; b < BKS; ++b) {
+            const uint64_t xa = umma_desc_sw128(base + stage * kTcStageBytes + b * kTcXBytes);
+            const uint64_t wb = umma_desc_sw128(base + stage * kTcStageBytes + BKS * kTcXBytes + b * C::kWBytes);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              tc_mma_bf16(dcol, xa + 2 * q, wb + 2 * q, idesc, (kb | b | q) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // epilogue: warp w owns TMEM lanes 32 (w % 4) .. + 31 = one 32-token block of the tile
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * 32, r);
+      tc_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      const int blk = tile * (kTcTile / kBlockTokens) + quarter;
+      const int t = blk * kBlockTokens + lane;
+      const bool live = t < T;
+      // the token's logits to a private shared-memory row: slot gi's E logits are
+      // then read at a runtime offset without dynamic register indexing
+      float* row = rows + (quarter * 32 + lane) * kTcRowLd;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) row[c] = __uint_as_float(r[c]);
+      for (int gi = 0; gi <= n_pred; ++gi) {
+        // arg-max rounds on order keys, lowest expert on ties (warp_topk_vals' rule)
+        uint32_t key[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) key[e] = e < E ? logit_key(row[gi * E + e]) : 0u;
+        int sel[8];
+        float lg[8];
+        uint32_t chosen = 0;  // bit e: this token chose expert e
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j >= k) break;
+          uint32_t best = 0u;
+          int be = 0;
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (key[e] > best) { best = key[e]; be = e; }
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (e == be) key[e] = 0u;
+          sel[j] = be;
+          lg[j] = key_logit(best);
+          chosen |= 1u << be;
+        }
+        if (!live) chosen = 0u;
+        if (gi == 0 && live) {
+          float z = 0.0f, p[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < k) { p[j] = expf(lg[j] - lg[0]); z += p[j]; }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < k) {
+              ids[(size_t)t * k + j] = sel[j];
+              wts[(size_t)t * k + j] = p[j] / z;
+            }
+        }
+        // the block's histogram: one ballot per expert, lane e publishes expert e
+        int mine = 0;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          if (e >= E) break;
+          const int c = __popc(__ballot_sync(0xffffffffu, (chosen >> e) & 1u));
+          if (lane == e) mine = c;
+        }
+        if (gi == 0 && lane < E && blk * kBlockTokens < T) block_counts[(size_t)blk * E + lane] = mine;
+        if (lane < E && mine) atomicAdd(&s_hist[gi * E + lane], mine);  // one global add per CTA and slot
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < E * (1 + n_pred) && s_hist[threadIdx.x])
+    atomicAdd(threadIdx.x < E ? counts + threadIdx.x : pred_counts + (threadIdx.x - E), s_hist[threadIdx.x]);
+  if (threadIdx.x == 0) stamp(4);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<64>(tmem_base);
+  }
+  publish_counts(counts, mirror, gridDim.x);
+  if (threadIdx.x == 0) stamp(5);
+}
+
+bool gate_tc_applies(int T, int d, int Etot, int k, bool mlp) {
+  return g_gate_tc.load(std::memory_order_relaxed) != 0 && T >= 64 * kTcTile && d % 256 == 0 && Etot <= 32 &&
+         k <= 8 && !mlp;
+}
+
+cudaError_t launch_gate_tc(const CUtensorMap* tmx, const CUtensorMap* tmw, int T, int d, int E, int n_pred, int k,
+                           int32_t* ids, float* wts, int32_t* counts, int32_t* block_counts, int32_t* pred_counts,
+                           int32_t* host_counts, int host_n, unsigned* ticket, int num_sms, cudaStream_t stream,
+                           unsigned long long* trace) {
+  const CountsMirror mirror{host_counts, ticket, host_n};
+  const int Etot = E * (1 + n_pred);
+  const int tiles = (T + kTcTile - 1) / kTcTile;
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  const int bks = g_gate_tc_bks.load(std::memory_order_relaxed);
+#define MOE_TC_LAUNCH(NC_, BKS_)                                                                              \
+  gate_tc_kernel<NC_, BKS_><<<grid, kTcThreads, TcCfg<NC_, BKS_>::kSmem, stream>>>(                           \
+      *tmx, *tmw, T, d, E, n_pred, k, ids, wts, counts, block_counts, pred_counts, mirror, trace)
+  if (Etot <= 16) {
+    if (bks == 4) MOE_TC_LAUNCH(16, 4); else if (bks == 2) MOE_TC_LAUNCH(16, 2); else MOE_TC_LAUNCH(16, 1);
+  } else {
+    if (bks == 4) MOE_TC_LAUNCH(32, 4); else if (bks == 2) MOE_TC_LAUNCH(32, 2); else MOE_TC_LAUNCH(32, 1);
+  }
+#undef MOE_TC_LAUNCH
+  return cudaGetLastError();
+}
+
 // Sums the split-K partial logits of kFinishTokens tokens of one 32-token
 // block in slice order (deterministic; all slices are loaded before the
 // first add, so the sum costs one memory latency, not `splits`), then top-k /
@@ -531,6 +778,14 @@ cudaError_t preload_gate_kernels() {
   reinterpret_cast<const void*>(gate_stream_kernel<NT_, false>), reinterpret_cast<const void*>(gate_stream_kernel<NT_, true>)
       MOE_STREAM_FNS(1), MOE_STREAM_FNS(2), MOE_STREAM_FNS(4)};
 #undef MOE_STREAM_FNS
+  const std::pair<const void*, uint32_t> tc_fns[] = {
+#define MOE_TC_FN(NC_, BKS_) {reinterpret_cast<const void*>(gate_tc_kernel<NC_, BKS_>), TcCfg<NC_, BKS_>::kSmem}
+      MOE_TC_FN(16, 1), MOE_TC_FN(16, 2), MOE_TC_FN(16, 4), MOE_TC_FN(32, 1), MOE_TC_FN(32, 2), MOE_TC_FN(32, 4)};
+#undef MOE_TC_FN
+  for (const auto& f : tc_fns) {
+    const cudaError_t e = cudaFuncSetAttribute(f.first, cudaFuncAttributeMaxDynamicSharedMemorySize, f.second);
+    if (e != cudaSuccess) return e;
+  }
   for (const void* f : stream_fns) {
     const cudaError_t e =
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem);
