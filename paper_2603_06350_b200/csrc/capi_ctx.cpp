@@ -296,6 +296,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_FRONT_TRACE"); v && std::string(v) == "1") {
       c->front_trace.alloc(148 * 16);
       CU_CHECK(cudaMemset(c->front_trace.p, 0, 148 * 16 * sizeof(unsigned long long)));
+      CU_CHECK(set_swap_trace(c->front_trace.p));
     }
     if (const char* v = std::getenv("MOE_DECODE_PREFETCH_MB")) c->prefetch_mb = std::max(0, std::atoi(v));
     if (const char* v = std::getenv("MOE_PDL_FRONT")) c->pdl_front = std::atoi(v);

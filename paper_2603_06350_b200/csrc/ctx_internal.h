@@ -57,6 +57,7 @@ cudaError_t launch_frontend(const __nv_bfloat16* x, int T, int d, const __nv_bfl
                             uint32_t* row_code, DevPlan* plan, const void* prefetch, size_t prefetch_bytes,
                             unsigned long long* trace, cudaStream_t stream);
 cudaError_t preload_frontend_kernels();
+cudaError_t set_swap_trace(unsigned long long* p);  // MOE_FRONT_TRACE: swap-AB K4 CTA start / end stamps
 // prefill gate on tcgen05 (kernels/gate.cu): 128-token tiles, TMA-streamed x
 bool gate_tc_applies(int T, int d, int Etot, int k, bool mlp);
 cudaError_t launch_gate_tc(const CUtensorMap* tmx, const CUtensorMap* tmw, int T, int d, int E, int n_pred, int k,

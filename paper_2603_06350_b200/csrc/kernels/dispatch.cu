@@ -613,7 +613,12 @@ cudaError_t preload_dispatch_kernels() {
     const cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
   }
-  return cudaSuccess;
+  // The decode weight prefetch runs beside the front end and the swap-AB K4
+  // (~200 KB of shared memory per CTA): with the default carveout an SM that
+  // hosts a prefetch CTA cannot take a K4 CTA until it drains and reconfigures
+  // (K4 CTAs on those SMs started ~8 us late, profiles/ab_frontend_r02.md).
+  return cudaFuncSetAttribute(reinterpret_cast<const void*>(l2_prefetch_kernel),
+                              cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
 }
 
 }  // namespace moe

@@ -1214,6 +1214,18 @@ __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence
 // anything: no deadlock even when the grid is not fully resident (other
 // kernels on the GPU).  The last CTA to finish zeroes the counters.  GEMM2's weights start streaming while GEMM1's
 // last wave drains, and there is no tail between the two GEMMs.
+// MOE_FRONT_TRACE: %globaltimer at each swap-kernel CTA's start / end ([cta][12], [cta][13] of the trace)
+__device__ unsigned long long* g_swap_trace = nullptr;
+__device__ __forceinline__ void swap_stamp(int i) {
+  unsigned long long* tr = g_swap_trace;
+  if (tr && threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    tr[blockIdx.x * 16 + i] = v;
+  }
+}
+cudaError_t set_swap_trace(unsigned long long* p) { return cudaMemcpyToSymbol(g_swap_trace, &p, sizeof(p)); }
+
 template <bool FUSED, int SNv>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
@@ -1240,6 +1252,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
 
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
+  swap_stamp(12);
   const int nseg = min(*nseg_g, kMaxSegs);
 
   for (int i = threadIdx.x; i < nseg; i += kThreads) segs[i] = reinterpret_cast<const int4*>(segs_g)[i];
@@ -1468,6 +1481,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem_base);
   }
+  swap_stamp(13);
 }
 
 std::atomic<int> g_gemm_l2pol{-1};  // 2-SM K4 L2 policies (env MOE_GEMM_L2POL: GEMM1 bits 0-3, GEMM2 bits 4-7; -1 default)

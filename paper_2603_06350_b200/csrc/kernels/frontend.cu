@@ -392,7 +392,11 @@ cudaError_t preload_frontend_kernels() {
       MOE_FRONT_FNS(1), MOE_FRONT_FNS(2), MOE_FRONT_FNS(4), MOE_FRONT_FNS(8), MOE_FRONT_FNS(16)};
 #undef MOE_FRONT_FNS
   for (const void* f : fns) {
-    const cudaError_t e = cudaFuncGetAttributes(&fa, f);
+    cudaError_t e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) return e;
+    // the same shared-memory carveout as the GEMM that follows (PDL): its CTAs
+    // may then share an SM with this grid's CTAs without a reconfiguration
+    e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
