@@ -268,7 +268,8 @@ void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t r
                                       c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, 2 * c->ff, c->d,
                                       reinterpret_cast<__nv_bfloat16*>(c->h.p),
                                       reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->swap_ready.p,
-                                      static_cast<int>(c->swap_ready.n), c->num_sms, s, c->use_pdl));
+                                      static_cast<int>(c->swap_ready.n), c->num_sms, s, c->use_pdl,
+                                      c->swap_half2 ? &L.tmB2h : nullptr));
     return;
   }
   if (c->fp32) {  // K7: SIMT fp32 grouped GEMMs (+ SwiGLU pass between them)

@@ -289,6 +289,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_GEMM_SWAP_ROWS")) c->swap_rows = std::atoi(v);
     if (const char* v = std::getenv("MOE_GEMM_SWAP128_ROWS")) c->swap128_rows = std::atoi(v);
     if (const char* v = std::getenv("MOE_SWAP_FUSE")) c->swap_fuse = std::string(v) != "0";
+    if (const char* v = std::getenv("MOE_SWAP_HALF2")) c->swap_half2 = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_FUSE_PLAN")) c->fuse_plan = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_FRONTEND")) c->frontend = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_DEBUG_SKIP_COMBINE")) c->skip_combine = std::string(v) == "1";

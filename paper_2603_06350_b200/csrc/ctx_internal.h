@@ -112,7 +112,7 @@ cudaError_t launch_grouped_gemm_swap(int which, int sn, const CUtensorMap* tmA1,
                                      const CUtensorMap* tmA2, const CUtensorMap* tmB2, const GemmSeg* segs,
                                      const int* nseg, int d, int ff, int b_rows1, int b_rows2, __nv_bfloat16* h,
                                      __nv_bfloat16* yp, int* ready, int ready_n, int num_ctas, cudaStream_t stream,
-                                     bool pdl);
+                                     bool pdl, const CUtensorMap* tmB2half = nullptr);
 extern std::atomic<int> g_gate_max_splits;  // K1 split-K bound (env MOE_GATE_MAX_SPLITS)
 extern std::atomic<int> g_gate_cluster;     // K1 split-K reduced in a cluster (env MOE_GATE_CLUSTER)
 extern std::atomic<int> g_gate_min_splits;  // K1 split-K floor (env MOE_GATE_MIN_SPLITS)
@@ -335,7 +335,10 @@ struct moe_ctx {
   bool capturing = false;  // enqueue_forward is recording a CUDA graph
   bool pdl_prefix() const { return (pdl_front & (capturing ? 4 : 1)) != 0; }
   bool pdl_combine() const { return (pdl_front & (capturing ? 8 : 2)) != 0; }
-  bool swap_fuse = true;  // swap-AB: GEMM1 and GEMM2 in one launch (MOE_SWAP_FUSE=0: two)
+  bool swap_fuse = true;
+  // swap-AB GEMM2 in 128-row weight tiles (MOE_SWAP_HALF2=1; default 256 rows: the half tiles
+  // re-read each tile's H rows and cost cfg5 +8 us, profiles/ab_frontend_r02.md)
+  bool swap_half2 = false;  // swap-AB: GEMM1 and GEMM2 in one launch (MOE_SWAP_FUSE=0: two)
   // single GPU, <= 32 token blocks: gate, top-k, plan and dispatch in ONE cooperative launch
   // (kernels/frontend.cu; MOE_FRONTEND=0: the gate / finish / dispatch launches)
   bool frontend = true;

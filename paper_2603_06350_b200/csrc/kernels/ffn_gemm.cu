@@ -1164,6 +1164,7 @@ __device__ __forceinline__ void store_token_pairs(const float (&v)[32], int lane
 struct SwapPass {
   __nv_bfloat16* out;
   int n_tiles, num_kb, b_rows_per_slot, out_ld, epi;
+  int wrows;  // weight rows per tile: 256 (two M=128 halves), or 128 for GEMM2 (half tiles: a shorter tail)
 };
 
 struct SwapTile {
@@ -1312,8 +1313,8 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
         const int a_row = segs[c.seg].x + c.m * SN;
         const int rows = min(SN, segs[c.seg].y - c.m * SN);
         const int nbox = (rows + SBOX - 1) / SBOX;
-        const uint32_t bytes = kStageWS + nbox * kBoxBytesS;
-        const int b_row = segs[c.seg].z * p.b_rows_per_slot + c.n * BN;
+        const uint32_t bytes = p.wrows * BK * 2 + nbox * kBoxBytesS;
+        const int b_row = segs[c.seg].z * p.b_rows_per_slot + c.n * p.wrows;
         const int num_kb = p.num_kb;
         int kb0 = 0;
         if (first || (FUSED && c.pass == 1)) {
@@ -1376,6 +1377,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
         }
         const SwapTile c = swap_tile<SN>(t, mt_prefix, nseg, mt_total, p0, p1);
         const int num_kb = (c.pass ? p1 : p0).num_kb;
+        const bool two_halves = (c.pass ? p1 : p0).wrows == 256;
         const int rows = min(SN, segs[c.seg].y - c.m * SN);
         const uint32_t idesc = umma_idesc_bf16(128, static_cast<uint32_t>((rows + 15) & ~15));
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -1392,7 +1394,7 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
           for (int k = 0; k < BK / 16; ++k) {
             const uint32_t accf = (kb | k) != 0 ? 1u : 0u;
             tc_mma_bf16(d0, w_top + 2 * k, tdesc + 2 * k, idesc, accf);
-            tc_mma_bf16(d1, w_bot + 2 * k, tdesc + 2 * k, idesc, accf);
+            if (two_halves) tc_mma_bf16(d1, w_bot + 2 * k, tdesc + 2 * k, idesc, accf);
           }
           tc_commit(&empty[stage]);
           if (++stage == STAGES_S) { stage = 0; phase ^= 1; }
@@ -1441,13 +1443,13 @@ grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_
           store_token_pairs(v, lane, j0, rows, p.out, row0, p.out_ld, c.n * (BN / 2) + (f & ~1));
         } else {
 #pragma unroll 1
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < p.wrows / 128; ++h) {
             uint32_t r[32];
             tmem_ld_32x32b_x32(taddr + h * SN + j0, r);
             tc_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-            store_token_pairs(v, lane, j0, rows, p.out, row0, p.out_ld, c.n * BN + h * 128 + (f & ~1));
+            store_token_pairs(v, lane, j0, rows, p.out, row0, p.out_ld, c.n * p.wrows + h * 128 + (f & ~1));
           }
         }
       }
@@ -1518,10 +1520,12 @@ cudaError_t launch_grouped_gemm_swap(int which, int sn, const CUtensorMap* tmA1,
                                      const CUtensorMap* tmA2, const CUtensorMap* tmB2, const GemmSeg* segs,
                                      const int* nseg, int d, int ff, int b_rows1, int b_rows2, __nv_bfloat16* h,
                                      __nv_bfloat16* yp, int* ready, int ready_n, int num_ctas, cudaStream_t stream,
-                                     bool pdl) {
+                                     bool pdl, const CUtensorMap* tmB2half) {
   if ((2 * ff) % BN || d % BN || d % BK || ff % BK || (sn != 64 && sn != 128)) return cudaErrorInvalidValue;
-  const SwapPass g1{h, 2 * ff / BN, d / BK, b_rows1, ff, EPI_SWIGLU};
-  const SwapPass g2{yp, d / BN, ff / BK, b_rows2, d, EPI_STORE};
+  const int w2rows = tmB2half ? 128 : 256;
+  const SwapPass g1{h, 2 * ff / BN, d / BK, b_rows1, ff, EPI_SWIGLU, 256};
+  const SwapPass g2{yp, d / w2rows, ff / BK, b_rows2, d, EPI_STORE, w2rows};
+  if (tmB2half) tmB2 = tmB2half;
   return sn == 64 ? launch_swap<64>(which, tmA1, tmB1, tmA2, tmB2, segs, nseg, g1, g2, ready, ready_n, num_ctas,
                                     stream, pdl)
                   : launch_swap<128>(which, tmA1, tmB1, tmA2, tmB2, segs, nseg, g1, g2, ready, ready_n, num_ctas,
