@@ -1,6 +1,9 @@
 """Small forwards for compute-sanitizer runs over the round-2 paths:
-  default  gate (+split-K finish), dispatch with the fused local plan, swap-AB K4
-           with the side-stream L2 prefetch, combine
+  default  the fused decode front end (gate + top-k + plan + dispatch, one
+           cooperative launch), swap-AB K4 with the side-stream L2 prefetch, combine
+  frontpred  the same with a predictor MLP slot and a linear slot (64 stacked rows)
+  gatetc   the tcgen05 prefill gate (T >= 8192) + side-stream histogram copy
+  threek   MOE_FRONTEND=0: split-K gate + finish + dispatch (the three-kernel path)
   2sm      the 2-SM cta_group::2 K4 with claimed tiles (MOE_GEMM_VARIANT=2sm)
   ids      moe_layer_forward_ids (route_ids kernel instead of the gate)
   stream   the streaming prefill gate (MOE_GATE_STREAM=1, T >= 148 blocks)
@@ -23,8 +26,17 @@ if scenario == "2sm":
 if scenario == "stream":
     os.environ["MOE_GATE_STREAM"] = "1"
     d, T = 512, 148 * 32 + 17
-m = MoELayer(1, E, k, d, ff, max_tokens=T, expert_mem_mb=1.0, layer_mem_cap_mb=3.0)
+if scenario == "gatetc":
+    T = 8192 + 17
+if scenario == "threek":
+    os.environ["MOE_FRONTEND"] = "0"
+npred = 2 if scenario == "frontpred" else 0
+m = MoELayer(1, E, k, d, ff, max_tokens=T, expert_mem_mb=1.0, layer_mem_cap_mb=3.0, num_predictor_targets=npred)
 m.set_gate(0, wl.gate_weights(E, d, 1.2, 1, 0, 0))
+if npred:
+    m.set_predictor_mlp(0, 0, wl.gate_weights(E, d, 1.2, 1, 1, 0),
+                        np.random.default_rng(0).standard_normal((E, E)).astype(np.float32))
+    m.set_predictor(0, 1, wl.gate_weights(E, d, 1.2, 1, 2, 0))
 for e in range(E):
     m.load_expert(0, e, *wl.expert_weights(d, ff, 1, 0, e))
 x = torch.from_numpy(wl.tokens(T, d, E, 1, 0).view(np.int16)).cuda()
