@@ -197,7 +197,7 @@ def single_gpu_launches(T, k, E, d=4096):
     swap = T * k / E <= 1024             # swap-AB tiles: GEMM1 + GEMM2 in one launch
     prefetch = swap                      # + the side-stream L2 prefetch of the first weights
     k4 = 1 if swap else 2
-    if nblk <= 32:                       # fused front end: gate + top-k + plan + dispatch, one launch
+    if nblk <= 148 and d % 256 == 0 and E <= 128:  # fused front end: gate + top-k + plan + dispatch
         return 1 + k4 + 1 + prefetch
     tc_gate = T >= 8192 and d % 256 == 0  # tcgen05 gate (+ its side-stream histogram copy to the host)
     split = not tc_gate and nblk * 4 <= 2 * 148  # small batches split K (+ finish kernel)

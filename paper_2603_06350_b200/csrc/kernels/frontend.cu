@@ -1,6 +1,6 @@
 // frontend.cu — the decode front end in ONE launch: K1 gate (+ K2 predictor)
 // -> top-k -> K3 dispatch plan, ranking and row scatter, for a single GPU and
-// small batches (<= 32 token blocks, e.g. cfg5: 256 tokens).
+// small batches (up to 148 token blocks: cfg5's 256 tokens, cfg1's 2048).
 //
 // At decode the separate launches (split-K gate, gate finish, dispatch) each
 // move a few hundred KB to a few MB, so each costs its launch latency, one
@@ -204,7 +204,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) frontend_kernel(const __grid_c
       v0[u] = ld_nc_v4(a.x + (size_t)(t_base + tk) * a.d + (size_t)(c_begin + it - tk * nch) * 8);
     }
   }
-  for (int e = threadIdx.x; e < E; e += blockDim.x) s_mask[e] = 0u;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    s_mask[e] = 0u;
+    s_pre[e] = 0;
+  }
   stamp(a, cta, 5);
   grid_barrier();
   stamp(a, cta, 7);
@@ -215,17 +218,23 @@ __global__ void __launch_bounds__(kWarps * 32, 1) frontend_kernel(const __grid_c
   const int t = t_base + lane;
   const bool live = lane < ntok;
   const int my = warp < k && live ? __ldcg(a.ids + (size_t)t * k + warp) : -1;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    s_cnt[e] = __ldcg(a.counts + e);
-    int pre = 0;
-    for (int b0 = 0; b0 < b; b0 += 8) {  // 8 independent loads per round (b < 32)
-      int v[8];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) s_cnt[e] = __ldcg(a.counts + e);
+  {
+    // P threads per expert sum rows q, q + P, ... < b, 8 loads in flight each
+    // (consecutive threads read consecutive experts of one row)
+    const int P = max(1, static_cast<int>(blockDim.x) / E);
+    for (int i = threadIdx.x; i < E * P; i += blockDim.x) {
+      const int e = i % E, q = i / E;
+      int pre = 0;
+      for (int b0 = q; b0 < b; b0 += 8 * P) {
+        int v[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = b0 + q < b ? __ldcg(a.block_counts + (size_t)(b0 + q) * E + e) : 0;
+        for (int u = 0; u < 8; ++u) v[u] = b0 + u * P < b ? __ldcg(a.block_counts + (size_t)(b0 + u * P) * E + e) : 0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) pre += v[q];
+        for (int u = 0; u < 8; ++u) pre += v[u];
+      }
+      if (pre) atomicAdd(&s_pre[e], pre);
     }
-    s_pre[e] = pre;
   }
   if (my >= 0) atomicOr(&s_mask[my], 1u << lane);  // tokens of block b that chose expert e
   __syncthreads();
@@ -315,18 +324,21 @@ __global__ void __launch_bounds__(kWarps * 32, 1) frontend_kernel(const __grid_c
 
 }  // namespace
 
-int gate_splits(int T, int d);
 int gate_num_blocks(int T);
-constexpr int kFrontMaxBlocks = 32;
+// The fused front end applies to single-GPU bf16 batches with <= 128 stacked
+// logit columns whose split-K grid (token blocks x K splits) fits on the SMs at
+// once: up to 148 blocks (4736 tokens; cfg5 8 x 16 CTAs, cfg1 64 x 2).
+// K splits: the most (<= 16, a power of two) that keep the grid on the SMs
+static int front_splits(int nblk, int d, int num_sms) {
+  int s = 1;
+  while (s < 16 && nblk * s * 2 <= num_sms && d % (kSlices * 32 * s * 2) == 0) s *= 2;
+  return s;
+}
 
-// The fused front end applies to single-GPU bf16 batches of <= 32 token blocks
-// with <= 128 stacked logit columns whose split-K grid fits on the SMs at once.
 bool frontend_applies(int T, int d, int Etot, int k, int num_sms) {
   if (T <= 0 || k < 1 || k > 8 || Etot > 128 || d % 256) return false;
   const int nblk = gate_num_blocks(T);
-  if (nblk > kFrontMaxBlocks) return false;
-  const int splits = gate_splits(T, d);
-  return splits <= 16 && nblk * splits <= num_sms && d % (kSlices * 32 * splits) == 0;
+  return nblk <= num_sms && nblk * front_splits(nblk, d, num_sms) <= num_sms;
 }
 
 cudaError_t launch_frontend(const __nv_bfloat16* x, int T, int d, const __nv_bfloat16* w_all, int E, int n_pred, int k,
@@ -336,7 +348,12 @@ cudaError_t launch_frontend(const __nv_bfloat16* x, int T, int d, const __nv_bfl
                             unsigned long long* trace, cudaStream_t stream) {
   const int Etot = E * (1 + n_pred);
   const int nblk = gate_num_blocks(T);
-  const int splits = gate_splits(T, d);
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int splits = front_splits(nblk, d, sms);
   FrontArgs a{};
   a.x = x;
   a.w_all = w_all;

@@ -1,4 +1,4 @@
-"""The fused decode front end (kernels/frontend.cu: gate + top-k + plan +
+"""The fused front end (kernels/frontend.cu: gate + top-k + plan +
 dispatch in one cooperative launch) against the oracle and against the
 three-kernel path it replaces (MOE_FRONTEND=0), bit for bit: ids, weights,
 counts (gate and predictor histograms), row codes, the permuted rows, the
@@ -55,6 +55,8 @@ CASES = [
     (16, 4, 2048, 256, 1000, 1.2, 2, True),   # 32 blocks (the limit), predictor MLP + linear slot
     (64, 8, 2048, 256, 77, 2.0, 1, False),    # 128 stacked logit columns, ragged
     (32, 6, 1024, 256, 500, 1.2, 0, False),   # k = 6
+    (8, 2, 1024, 3584, 2048, 1.2, 0, False),  # cfg1: 64 blocks x 2 K splits
+    (16, 2, 2048, 256, 4000, 1.2, 1, False),  # 125 blocks, no K split, predictor
 ]
 
 
