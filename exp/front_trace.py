@@ -8,7 +8,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["MOE_FRONT_TRACE"] = "1"
+os.environ["MOE_FRONT_TRACE"] = os.environ.get("MOE_FRONT_TRACE", "1")
 from paper_2603_06350_b200 import MOE_PLAN_SYNC, MoELayer  # noqa: E402
 from paper_2603_06350_b200 import workload as wl  # noqa: E402
 
@@ -25,9 +25,15 @@ y = torch.empty((T, d), dtype=torch.int16, device="cuda")
 names = ["A done", "bar1 arrive", "bar1 release", "B loads", "B done", "bar2 arrive", "bar2 release", "hist", "plan+trigger", "scatter done"]
 rows = []
 k4 = []
+stream = torch.cuda.ExternalStream(m.stream_ptr)
+evs = []
 for it in range(40):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
     m.forward(0, xs[it % 4], y, MOE_PLAN_SYNC, it)
+    e1.record(stream)
     torch.cuda.synchronize()
+    evs.append(e0.elapsed_time(e1) * 1e3)
     tr = m.read_buffer(12, np.uint64, (148, 16)).astype(np.int64)
     k4t = tr[:, 12:14].copy()
     n = int((tr[:, 0] > 0).sum())
@@ -37,7 +43,8 @@ for it in range(40):
                  for i in range(11)])
     if k4t[:, 0].min() > 0:
         st, en = (k4t[:, 0] - t0) / 1e3, np.sort((k4t[:, 1] - t0) / 1e3)
-        k4.append([st.min(), st.max(), en[0], en[len(en) // 2], en[-10], en[-1]])
+        k4.append([st.min(), st.max(), en[0], en[len(en) // 2], en[-10], en[-1], (tr[0, 14] - t0) / 1e3,
+                   (tr[0, 15] - t0) / 1e3 if tr[0, 15] > 0 else np.nan])
 r = np.median(np.array(rows[5:], dtype=np.float64), axis=0) / 1e3
 print(f"{cfg} ({'graph' if graphs else 'eager'}): {n} CTAs; start spread {r[0][1]:.2f} us")
 for i, nm in enumerate(names):
@@ -47,4 +54,5 @@ for i, nm in enumerate(names):
 if k4:
     q = np.median(np.array(k4[5:]), axis=0)
     print(f"  K4 (swap) CTA start {q[0]:.1f}..{q[1]:.1f} us; CTA end first {q[2]:.1f}, median {q[3]:.1f}, "
-          f"10th-last {q[4]:.1f}, last {q[5]:.1f} us")
+          f"10th-last {q[4]:.1f}, last {q[5]:.1f} us; combine end {q[6]:.1f} us; marker {q[7]:.1f} us")
+print(f"  event-timed layer: median {np.median(evs[5:]):.1f} us")

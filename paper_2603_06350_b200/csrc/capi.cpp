@@ -436,6 +436,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
     c->tmX_T = T;
   }
   mark(0);
+  if (c->trace_marker) CU_CHECK(launch_trace_marker(s));
   // decode: pull the first experts' weights into L2 on a side stream while the
   // front end runs (the swap-AB K4 streams them in expert order)
   const bool prefetch = swap && c->prefetch_mb > 0 && c->G == 1 && !c->fp32 && L.w13.p;

@@ -294,10 +294,12 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_FRONTEND")) c->frontend = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_DEBUG_SKIP_COMBINE")) c->skip_combine = std::string(v) == "1";
     if (const char* v = std::getenv("MOE_FRONT_PREFETCH")) c->front_prefetch_inline = std::string(v) == "inline";
-    if (const char* v = std::getenv("MOE_FRONT_TRACE"); v && std::string(v) == "1") {
+    if (const char* v = std::getenv("MOE_FRONT_TRACE"); v && (std::string(v) == "1" || std::string(v) == "2")) {
+      c->trace_marker = std::string(v) == "2";
       c->front_trace.alloc(148 * 16);
       CU_CHECK(cudaMemset(c->front_trace.p, 0, 148 * 16 * sizeof(unsigned long long)));
       CU_CHECK(set_swap_trace(c->front_trace.p));
+      CU_CHECK(set_combine_trace(c->front_trace.p));
     }
     if (const char* v = std::getenv("MOE_DECODE_PREFETCH_MB")) c->prefetch_mb = std::max(0, std::atoi(v));
     if (const char* v = std::getenv("MOE_PDL_FRONT")) c->pdl_front = std::atoi(v);

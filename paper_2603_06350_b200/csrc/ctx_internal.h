@@ -57,7 +57,9 @@ cudaError_t launch_frontend(const __nv_bfloat16* x, int T, int d, const __nv_bfl
                             uint32_t* row_code, DevPlan* plan, const void* prefetch, size_t prefetch_bytes,
                             unsigned long long* trace, cudaStream_t stream);
 cudaError_t preload_frontend_kernels();
-cudaError_t set_swap_trace(unsigned long long* p);  // MOE_FRONT_TRACE: swap-AB K4 CTA start / end stamps
+cudaError_t set_swap_trace(unsigned long long* p);
+cudaError_t set_combine_trace(unsigned long long* p);
+cudaError_t launch_trace_marker(cudaStream_t s);  // MOE_FRONT_TRACE: swap-AB K4 CTA start / end stamps
 // prefill gate on tcgen05 (kernels/gate.cu): 128-token tiles, TMA-streamed x
 bool gate_tc_applies(int T, int d, int Etot, int k, bool mlp);
 cudaError_t launch_gate_tc(const CUtensorMap* tmx, const CUtensorMap* tmw, int T, int d, int E, int n_pred, int k,
@@ -345,6 +347,7 @@ struct moe_ctx {
   // decode weight prefetch with the fused front end (MOE_FRONT_PREFETCH): the side-stream
   // kernel (default), or "inline": the front end's CTAs issue the bulk prefetches themselves
   bool front_prefetch_inline = false;
+  bool trace_marker = false;  // MOE_FRONT_TRACE=2: + a marker kernel at the layer's start
   DevBuf<unsigned long long> front_trace;  // MOE_FRONT_TRACE=1: phase stamps of the fused front end (moe_buffer 12)
   bool fuse_plan = true;  // single GPU, <= 32 blocks: dispatch builds prefix + plan (MOE_FUSE_PLAN=0: block-prefix launch)
   // decode (swap-AB K4): MB of the first experts' weights prefetched into L2 on a side

@@ -298,6 +298,23 @@ dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int E, const 
 }
 
 // -------------------------------------------------------------- combine
+// MOE_FRONT_TRACE: the latest combine CTA end (%globaltimer, atomicMax into trace[14])
+__device__ unsigned long long* g_combine_trace = nullptr;
+cudaError_t set_combine_trace(unsigned long long* p) { return cudaMemcpyToSymbol(g_combine_trace, &p, sizeof(p)); }
+
+// MOE_FRONT_TRACE=2: a one-thread marker stamped first in the layer's sequence (trace[15])
+__global__ void trace_marker_kernel() {
+  if (g_combine_trace) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    g_combine_trace[15] = v;
+  }
+}
+cudaError_t launch_trace_marker(cudaStream_t s) {
+  trace_marker_kernel<<<1, 32, 0, s>>>();
+  return cudaGetLastError();
+}
+
 template <int K>
 __global__ void __launch_bounds__(256)
 combine_kernel(const __grid_constant__ RowTargets sources, int T, int d, const uint32_t* __restrict__ row_code,
@@ -348,6 +365,11 @@ combine_kernel(const __grid_constant__ RowTargets sources, int T, int d, const u
       o.w = pack_bf16(acc[6], acc[7]);
       st_v4(out + (size_t)c0 * 8, o);
     }
+  }
+  if (g_combine_trace && threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    atomicMax(g_combine_trace + 14, v);
   }
 }
 
