@@ -358,6 +358,42 @@ struct TcCfg {
   static constexpr int kStages = kTcRingBudget / kStage < 16 ? kTcRingBudget / kStage : 16;
   static constexpr uint32_t kSmem = kStages * kStage + 256 + 4 * 32 * kTcRowLd * 4 + 1024;
 };
+// One token's top-k over slot gi's E <= W logits: order keys packed with
+// W - 1 - e in 64 bits, k arg-max rounds as log2(W)-deep trees (the max is the
+// largest logit and, on ties, the lowest expert: warp_topk_vals' rule).  Slot
+// 0 reads the TMEM registers directly; predictor slots (runtime offset gi * E)
+// the token's shared-memory row.  Returns the chosen-expert mask.
+template <int W>
+__device__ __forceinline__ uint32_t tc_token_topk(const uint32_t (&r)[32], const float* row, int gi, int E, int k,
+                                                  int (&sel)[8], float (&lg)[8]) {
+  uint64_t key[W];
+#pragma unroll
+  for (int c = 0; c < W; ++c) {
+    const float v = gi == 0 ? __uint_as_float(r[c]) : row[gi * E + c];
+    key[c] = c < E ? (static_cast<uint64_t>(logit_key(v)) << 32) | static_cast<uint32_t>(W - 1 - c) : 0ull;
+  }
+  uint32_t chosen = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j >= k) break;
+    uint64_t m[W / 2];
+#pragma unroll
+    for (int c = 0; c < W / 2; ++c) m[c] = key[2 * c] > key[2 * c + 1] ? key[2 * c] : key[2 * c + 1];
+#pragma unroll
+    for (int w = W / 4; w >= 1; w /= 2)
+#pragma unroll
+      for (int c = 0; c < w; ++c) m[c] = m[c] > m[c + w] ? m[c] : m[c + w];
+    const int be = W - 1 - static_cast<int>(m[0] & 0xffffffffu);
+    sel[j] = be;
+    lg[j] = key_logit(static_cast<uint32_t>(m[0] >> 32));
+    chosen |= 1u << be;
+#pragma unroll
+    for (int c = 0; c < W; ++c)
+      if (c == be) key[c] = 0ull;
+  }
+  return chosen;
+}
+
 template <int NC, int BKS>
 __global__ void __launch_bounds__(kTcThreads, 1)
 gate_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw, int T, int d,
@@ -374,6 +410,9 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
     }
   };
   if (threadIdx.x == 0) stamp(0);
+  auto cstamp = [&](int i) {
+    if (trace) trace[blockIdx.x * 16 + i] = clock64();
+  };
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
   using C = TcCfg<NC, BKS>;
   constexpr int kTcStages = C::kStages;
@@ -460,6 +499,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
           if (++stage == kTcStages) { stage = 0; phase ^= 1; }
         }
         tc_commit(&tfull[acc]);
+        stamp(9);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -471,9 +511,11 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (warp == 2 && lane == 0) stamp(6);
       uint32_t r[32];
       tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * 32, r);
       tc_wait_ld();
+      if (warp == 2 && lane == 0) { stamp(7); cstamp(13); }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -481,51 +523,50 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
       const int blk = tile * (kTcTile / kBlockTokens) + quarter;
       const int t = blk * kBlockTokens + lane;
       const bool live = t < T;
-      // the token's logits to a private shared-memory row: slot gi's E logits are
-      // then read at a runtime offset without dynamic register indexing
+      // Slot gi's E logits -> NC order keys in registers (gi = 0 straight from
+      // the TMEM load; predictor slots through a private shared-memory row, as
+      // their offset gi * E is a runtime value), then k arg-max rounds as
+      // log2(NC)-deep trees over (key, NC - 1 - e) packed in 64 bits: the max
+      // is the largest logit and, on ties, the lowest expert (warp_topk_vals'
+      // rule).  The serial 32-step scan this replaces was a dependent chain of
+      // ~2.5k cycles per tile at the end of every CTA.
       float* row = rows + (quarter * 32 + lane) * kTcRowLd;
+      if (n_pred > 0) {
 #pragma unroll
-      for (int c = 0; c < NC; ++c) row[c] = __uint_as_float(r[c]);
+        for (int c = 0; c < NC; ++c) row[c] = __uint_as_float(r[c]);
+      }
       for (int gi = 0; gi <= n_pred; ++gi) {
-        // arg-max rounds on order keys, lowest expert on ties (warp_topk_vals' rule)
-        uint32_t key[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) key[e] = e < E ? logit_key(row[gi * E + e]) : 0u;
         int sel[8];
         float lg[8];
-        uint32_t chosen = 0;  // bit e: this token chose expert e
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (j >= k) break;
-          uint32_t best = 0u;
-          int be = 0;
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (key[e] > best) { best = key[e]; be = e; }
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (e == be) key[e] = 0u;
-          sel[j] = be;
-          lg[j] = key_logit(best);
-          chosen |= 1u << be;
-        }
+        uint32_t chosen;  // bit e: this token chose expert e
+        if (E <= 8)
+          chosen = tc_token_topk<8>(r, row, gi, E, k, sel, lg);
+        else
+          chosen = tc_token_topk<NC>(r, row, gi, E, k, sel, lg);
         if (!live) chosen = 0u;
+        if (warp == 2 && lane == 0 && gi == 0) { stamp(11); cstamp(14); }
         if (gi == 0 && live) {
           float z = 0.0f, p[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             if (j < k) { p[j] = expf(lg[j] - lg[0]); z += p[j]; }
+          if (k == 2) {  // the Mixtral / Phi shapes: one 8-byte store each
+            reinterpret_cast<int2*>(ids)[t] = make_int2(sel[0], sel[1]);
+            reinterpret_cast<float2*>(wts)[t] = make_float2(p[0] / z, p[1] / z);
+          } else {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (j < k) {
-              ids[(size_t)t * k + j] = sel[j];
-              wts[(size_t)t * k + j] = p[j] / z;
-            }
+            for (int j = 0; j < 8; ++j)
+              if (j < k) {
+                ids[(size_t)t * k + j] = sel[j];
+                wts[(size_t)t * k + j] = p[j] / z;
+              }
+          }
         }
+        if (warp == 2 && lane == 0 && gi == 0) { stamp(12); cstamp(15); }
         // the block's histogram: one ballot per expert, lane e publishes expert e
         int mine = 0;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
+        for (int e = 0; e < NC; ++e) {
           if (e >= E) break;
           const int c = __popc(__ballot_sync(0xffffffffu, (chosen >> e) & 1u));
           if (lane == e) mine = c;
@@ -533,6 +574,7 @@ gate_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
         if (gi == 0 && lane < E && blk * kBlockTokens < T) block_counts[(size_t)blk * E + lane] = mine;
         if (lane < E && mine) atomicAdd(&s_hist[gi * E + lane], mine);  // one global add per CTA and slot
       }
+      if (warp == 2 && lane == 0) stamp(8);
     }
   }
   tc_fence_before();
