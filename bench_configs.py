@@ -39,13 +39,22 @@ def run_config(name, steps, warmup, graphs=False):
     y = torch.empty((T, d), dtype=torch.int16, device="cuda")
     stream = torch.cuda.ExternalStream(m.stream_ptr)
 
+    # the layer reads a static input buffer, refilled from the pool before each
+    # step (as a serving engine feeds its captured decode graph): one CUDA graph
+    # per (layer, tokens, buffers) is replayed; cycling graph executables per
+    # pool buffer instead costs ~6 us per launch (profiles/ab_graph_stack_r02.md)
+    x_static = torch.empty_like(pool[0])
+
     def step(it, stats=False, ev_start=None):
-        # device-resident per-iteration gates re-route every step; the upload is
-        # not part of the layer (K1 .. K5), so the layer's start event follows it
+        # device-resident per-iteration gates re-route every step; the gate and
+        # token uploads are not part of the layer (K1 .. K5), so the layer's start
+        # event follows them
+        with torch.cuda.stream(stream):
+            x_static.copy_(pool[it % 4])
         m.set_gate_device(0, gates[it])
         if ev_start is not None:
             ev_start.record(stream)
-        return m.forward(0, pool[it % 4], y, MOE_PLAN_SYNC, it, stats=stats)
+        return m.forward(0, x_static, y, MOE_PLAN_SYNC, it, stats=stats)
 
     for it in range(warmup):
         step(it)
@@ -75,6 +84,66 @@ def run_config(name, steps, warmup, graphs=False):
         "k4_tflops": flops / (gemm * 1e-3) / 1e12, "k4_weight_gbs": wbytes / (gemm * 1e-3) / 1e9,
         "active_experts": active, "replicas_median": statistics.median(x.replica_count for x in st),
         "gpus": 1, "note": "per-GPU shape at G=1" if c["G"] > 1 else "", "cuda_graphs": graphs,
+    }
+
+
+def run_graph_stack(name, n_layers, steps, warmup):
+    """A decode step over `n_layers` layers of the named shape recorded as ONE CUDA
+    graph (moe_graph_begin / moe_graph_end; one graph launch per step, as a serving
+    engine replays a whole decode step): per-layer latency = graph time / n_layers.
+    Every layer has its own expert weights in HBM (1.07 GB each at cfg5, far above
+    L2) and its own gate, re-routed every step by device-to-device gate updates
+    that sit outside the timed window; layer inputs are independent synthetic
+    batches (the routing statistics of the single-layer config)."""
+    import numpy as np
+    import torch
+
+    from paper_2603_06350_b200 import MOE_PLAN_FIXED, MoELayer, percentile
+    from paper_2603_06350_b200 import workload as wl
+    c = dict(wl.CONFIGS[name])
+    E, k, d, ff, T, s = c["E"], c["k"], c["d"], c["ff"], c["T"], c["s"]
+    m = MoELayer(n_layers, E, k, d, ff, max_tokens=T)
+    host_experts = [wl.expert_weights(d, ff, 1, 0, e) for e in range(E)]
+    for l in range(n_layers):  # same values, separate HBM copies per layer
+        for e in range(E):
+            m.load_expert(l, e, *host_experts[e])
+    pool = [torch.from_numpy(wl.tokens(T, d, E, 1, i).view(np.int16)).cuda() for i in range(4)]
+    ys = [torch.empty((T, d), dtype=torch.int16, device="cuda") for _ in range(n_layers)]
+    n_gate_sets = 16
+    gates = torch.from_numpy(np.stack([np.stack([wl.gate_weights(E, d, s, 1, l, g) for l in range(n_layers)])
+                                       for g in range(n_gate_sets)]).view(np.int16)).cuda()
+    stream = torch.cuda.ExternalStream(m.stream_ptr)
+
+    def set_gates(it):
+        for l in range(n_layers):
+            m.set_gate_device(l, gates[it % n_gate_sets, l])
+
+    set_gates(0)
+    m.graph_begin()
+    for l in range(n_layers):
+        m.forward(l, pool[l % 4], ys[l], MOE_PLAN_FIXED, 0)
+    gid = m.graph_end()
+    for it in range(warmup):
+        set_gates(it)
+        m.graph_launch(gid)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        set_gates(warmup + i)
+        ev[i][0].record(stream)
+        m.graph_launch(gid)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    per_layer = [t / n_layers for t in step_ms]
+    m.close()
+    return {
+        "config": name, "mode": "graph_stack", "layers": n_layers, "shape": c, "steps": steps,
+        "p50_layer_ms": percentile(per_layer, 0.5), "p99_layer_ms": percentile(per_layer, 0.99),
+        "p50_step_ms": percentile(step_ms, 0.5), "p99_step_ms": percentile(step_ms, 0.99),
+        "tokens_per_s_per_layer": T * n_layers * steps / (sum(step_ms) * 1e-3), "gpus": 1,
+        "note": "per-GPU shape at G=1; one CUDA graph of %d layer forwards per step (moe_graph_begin/end), "
+                "per-layer = graph time / layers; gate re-routing uploads outside the window" % n_layers,
     }
 
 
@@ -151,9 +220,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--out", default="")
     ap.add_argument("--graphs", action="store_true", help="replay single-GPU forwards as CUDA graphs")
+    ap.add_argument("--stack-graph", type=int, default=0,
+                    help="record this many layers of each config as one CUDA graph per step (decode stack)")
     a = ap.parse_args()
-    res = [run_stack(n, max(2, a.steps // 10), 1) if n == "cfg4" else run_config(n, a.steps, a.warmup, a.graphs)
-           for n in a.configs.split(",")]
+    if a.stack_graph:
+        res = [run_graph_stack(n, a.stack_graph, a.steps, a.warmup) for n in a.configs.split(",")]
+    else:
+        res = [run_stack(n, max(2, a.steps // 10), 1) if n == "cfg4" else run_config(n, a.steps, a.warmup, a.graphs)
+               for n in a.configs.split(",")]
     for r in res:
         print(json.dumps(r), flush=True)
     if a.out:

@@ -255,6 +255,20 @@ int moe_predict_loads(moe_ctx* ctx, int layer, const uint16_t* x_dev, int tokens
 int moe_layer_forward(moe_ctx* ctx, int layer, const uint16_t* x_dev, int tokens, uint16_t* y_dev,
                       int plan_mode, long iteration, moe_layer_stats* stats, void* stream);
 
+/* Several forwards as ONE CUDA graph (a decode step over many layers pays one
+   graph launch, not one per layer): moe_graph_begin starts capturing the
+   context's stream; the moe_layer_forward calls that follow (stream NULL,
+   stats NULL, device-planned: G == 1, or FIXED / PREDICTED-ahead at G > 1;
+   not with MOE_RESIDENCY_PLACED) are recorded instead of run; moe_graph_end
+   instantiates them and returns *graph_id.  moe_graph_launch replays the
+   graph on `stream` (NULL: the context's stream), ordered after the
+   context's uploads.  Replays re-read each layer's current gate weights and
+   inputs but do not run the host planner's per-forward bookkeeping (the
+   device plans every layer).  Graphs are freed by moe_destroy. */
+int moe_graph_begin(moe_ctx* ctx);
+int moe_graph_end(moe_ctx* ctx, int* graph_id);
+int moe_graph_launch(moe_ctx* ctx, int graph_id, void* stream);
+
 /* The layer on caller-given routing (the SURVEY §8 c3 bridge): ids_dev [T, k]
    int32 expert ids and weights_dev [T, k] fp32 (NULL: 1/k each) replace K1, so
    routing produced outside the gate — e.g. the reference's route_tokens stream

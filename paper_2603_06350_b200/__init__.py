@@ -494,6 +494,20 @@ class MoELayer:
                                     iteration, C.byref(st) if st is not None else None, stream or None))
         return st
 
+    def graph_begin(self) -> None:
+        """Start recording forwards into one CUDA graph (moe_graph_begin): the
+        forward() calls until graph_end() are captured, not run."""
+        check(lib.moe_graph_begin(self._h))
+
+    def graph_end(self) -> int:
+        """Instantiate the recorded forwards; returns the graph id."""
+        gid = C.c_int(-1)
+        check(lib.moe_graph_end(self._h, C.byref(gid)))
+        return gid.value
+
+    def graph_launch(self, graph_id: int, stream: int = 0) -> None:
+        check(lib.moe_graph_launch(self._h, graph_id, stream or None))
+
     def forward_ids(self, layer: int, x, ids, y, weights=None, plan_mode: int = MOE_PLAN_FIXED,
                     iteration: int = 0, stats: bool = False, stream: int = 0) -> Optional[MoeLayerStats]:
         """The layer on caller-given routing: ids [T, k] int32 (and optional

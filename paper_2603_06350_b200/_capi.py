@@ -98,6 +98,9 @@ _sig("moe_set_placement", C.c_int, vp, C.c_int, vp, vp)
 _sig("moe_gate_topk", C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp)
 _sig("moe_predict_loads", C.c_int, vp, C.c_int, vp, C.c_int, vp, vp)
 _sig("moe_layer_forward", C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int, C.c_long, P(MoeLayerStats), vp)
+_sig("moe_graph_begin", C.c_int, vp)
+_sig("moe_graph_end", C.c_int, vp, P(C.c_int))
+_sig("moe_graph_launch", C.c_int, vp, C.c_int, vp)
 _sig("moe_layer_forward_ids", C.c_int, vp, C.c_int, vp, vp, vp, C.c_int, vp, C.c_int, C.c_long, P(MoeLayerStats),
      vp)
 _sig("moe_last_plan", C.c_int, vp, vp, vp, C.c_int, P(C.c_int), P(i64))
@@ -152,7 +155,7 @@ EXPORTED = [
     "moe_ctx_sync", "moe_p2p_export", "moe_p2p_import", "moe_load_expert_weights", "moe_set_gate_weights",
     "moe_load_expert_weights_f32", "moe_set_gate_weights_f32", "moe_set_gate_weights_device",
     "moe_set_predictor_weights", "moe_set_predictor_mlp", "moe_set_placement", "moe_gate_topk", "moe_predict_loads",
-    "moe_layer_forward", "moe_layer_forward_ids", "moe_last_plan", "moe_get_placement", "moe_layer_forward_host", "moe_layer_forward_host_async", "moe_wait",
+    "moe_layer_forward", "moe_graph_begin", "moe_graph_end", "moe_graph_launch", "moe_layer_forward_ids", "moe_last_plan", "moe_get_placement", "moe_layer_forward_host", "moe_layer_forward_host_async", "moe_wait",
     "moe_host_alloc", "moe_host_free", "moe_gemm_times", "moe_residency",
     "moe_forward_begin", "moe_forward_expert",
     "moe_forward_end", "moe_buffer", "moe_memcpy", "moe_exchange_plan", "moe_exchange_plan_direct", "moe_plan_scale",

@@ -594,6 +594,16 @@ void forward_device(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t* y
                      (plan_mode == MOE_PLAN_FIXED ||
                       (plan_mode == MOE_PLAN_PREDICTED && (L.plan_for == iteration || L.boot_ready)));
   if (ahead) ensure_placement(c, layer);
+  if (c->user_capture) {
+    // recorded into the caller's multi-forward graph (moe_graph_begin)
+    require(s == c->stream, "moe_graph_begin: forwards inside a capture must use the context's stream");
+    require(!timed, "moe_graph_begin: stats cannot be taken inside a capture");
+    require((c->G == 1 || ahead) && !c->placed && !c->ext_route,
+            "moe_graph_begin: only device-planned forwards (G == 1, or FIXED / PREDICTED ahead) can be captured");
+    enqueue_forward(c, L, layer, x, T, y, plan_mode, iteration, s, with_pred, stride, x_consumed, ahead, true,
+                    [](int) {});
+    return;
+  }
   if (c->use_graphs && !timed && (c->G == 1 || ahead) && !c->placed && !c->ext_route) {
     // Replay the layer's whole device sequence (8-14 kernels) as one CUDA
     // graph: captured once per (layer, tokens, buffers), then launched with a
@@ -717,6 +727,59 @@ int moe_layer_forward(moe_ctx* c, int layer, const uint16_t* x, int T, uint16_t*
     // a rank with no tokens still takes part in the exchange (x, y may be null)
     require(c && (T == 0 || (x && y)), "null argument");
     forward_device(c, layer, x, T, y, plan_mode, iteration, stats, pick(c, stream));
+  });
+}
+
+int moe_graph_begin(moe_ctx* c) {
+  return guarded([&] {
+    require(c != nullptr, "null argument");
+    require(!c->user_capture, "moe_graph_begin: a capture is already open");
+    CU_CHECK(cudaSetDevice(c->desc.device));
+    flush_pending_plan(c);  // the previous forward's planner work, before the stream is captured
+    CU_CHECK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    c->user_capture = true;
+    c->capturing = true;
+  });
+}
+
+int moe_graph_end(moe_ctx* c, int* graph_id) {
+  return guarded([&] {
+    require(c && graph_id, "null argument");
+    require(c->user_capture, "moe_graph_end: no capture is open");
+    c->user_capture = false;
+    c->capturing = false;
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (e != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      CU_CHECK(e);
+    }
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    CU_CHECK(ei);
+    CU_CHECK(cudaGraphUpload(ex, c->stream));
+    c->user_graphs.push_back(ex);
+    *graph_id = static_cast<int>(c->user_graphs.size()) - 1;
+  });
+}
+
+int moe_graph_launch(moe_ctx* c, int graph_id, void* stream) {
+  return guarded([&] {
+    require(c != nullptr, "null argument");
+    require(graph_id >= 0 && graph_id < static_cast<int>(c->user_graphs.size()), "moe_graph_launch: unknown graph");
+    require(!c->user_capture, "moe_graph_launch: a capture is open");
+    CU_CHECK(cudaSetDevice(c->desc.device));
+    cudaStream_t s = pick(c, stream);
+    if (s != c->stream) {  // after the context's uploads; later uploads after the replay
+      CU_CHECK(cudaEventRecord(c->ev_ctx_tail, c->stream));
+      CU_CHECK(cudaStreamWaitEvent(s, c->ev_ctx_tail, 0));
+    }
+    CU_CHECK(cudaGraphLaunch(c->user_graphs[graph_id], s));
+    if (s != c->stream) {
+      CU_CHECK(cudaEventRecord(c->ev_fwd_tail, s));
+      CU_CHECK(cudaStreamWaitEvent(c->stream, c->ev_fwd_tail, 0));
+    }
   });
 }
 

@@ -483,6 +483,7 @@ int moe_ctx_destroy(moe_ctx* c) {
       if (e) cudaEventDestroy(e);
     if (c->ev_fwd_tail) cudaEventDestroy(c->ev_fwd_tail);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    for (cudaGraphExec_t g : c->user_graphs) cudaGraphExecDestroy(g);
     for (auto& tri : c->gemm_ev)
       for (cudaEvent_t e : tri)
         if (e) cudaEventDestroy(e);

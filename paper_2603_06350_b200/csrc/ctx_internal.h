@@ -398,6 +398,8 @@ struct moe_ctx {
   int tmX_T = -1;
   DevBuf<int> gemm_sched;      // [GEMM1 next, done, GEMM2 next, done], zero between launches
   std::map<GraphKey, cudaGraphExec_t> graphs;
+  bool user_capture = false;                // between moe_graph_begin and moe_graph_end
+  std::vector<cudaGraphExec_t> user_graphs;  // moe_graph_end's graphs (id = index)
   // K4 timing ring: events around GEMM1 / GEMM2 of every forward (no sync)
   static constexpr int kGemmRing = 64;
   cudaEvent_t gemm_ev[kGemmRing][3] = {};
