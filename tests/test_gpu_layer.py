@@ -13,6 +13,7 @@ import pytest
 import oracle
 from paper_2603_06350_b200 import MOE_PLAN_FIXED, MoELayer, exchange_plan
 from paper_2603_06350_b200 import workload as wl
+from tolerance import row_rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -78,7 +79,7 @@ def _layer_case(cuda, E, k, d, ff, T, rc, seed=3):
 
 
 def _rel_err(y, y_ref):
-    return float(np.max(np.abs(y - y_ref)) / max(np.max(np.abs(y_ref)), 1e-30))
+    return row_rel_err(y, y_ref)
 
 
 @pytest.mark.parametrize("E,k,d,ff,T,rc", [

@@ -23,6 +23,7 @@ import torch.multiprocessing as mp
 import oracle
 import paper_2603_06350_b200 as pk
 from paper_2603_06350_b200 import workload as wl
+from tolerance import row_rel_err
 
 E, K, D, FF = 8, 2, 256, 256
 
@@ -109,7 +110,7 @@ def _worker(rank, world, port, rc, rg, tokens_per_rank, q):
                 y[t] += w[t, j] * oracle.bf16_to_f32(all_y[tgt][row])
         y_ref, ids_ref, _, _ = oracle.layer_forward(x, wg, experts, [1] * E, K)
         assert np.array_equal(ids, ids_ref)
-        err = float(np.max(np.abs(y - y_ref)) / np.max(np.abs(y_ref))) if T else 0.0
+        err = row_rel_err(y, y_ref)
         q.put((rank, err, plan["rows_local"], plan["rows_send"]))
         dist.barrier()
         dist.destroy_process_group()
