@@ -327,3 +327,47 @@ def test_p2p_prefill_kernels_bit_identical(cuda, monkeypatch, variant):
     assert row_rel_err(y, y_ref) <= 2e-2
     for m in ms + [one]:
         m.close()
+
+
+def test_p2p_forwards_replayed_as_cuda_graphs(cuda):
+    """Two ranks on the peer-memory exchange, FIXED placement (device-planned):
+    each rank records its forward as a CUDA graph (moe_graph_begin / end) and the
+    replays — re-routed between them by device-side gate updates — stay
+    bit-identical to single-GPU eager forwards on the same tokens (the epoch
+    lives in device memory, so every replay opens a fresh exchange epoch)."""
+    import torch
+    G, E, k, d, ff = 2, 8, 2, 1024, 1408
+    tokens = [256, 200]
+    rc, rg = [1] * E, [e % G for e in range(E)]
+    experts = [wl.expert_weights(d, ff, 1, 0, e) for e in range(E)]
+    gates = [wl.gate_weights(E, d, 1.2, 1, 0, it) for it in range(3)]
+    gd = [torch.from_numpy(g.view(np.int16)).to(cuda) for g in gates]
+    ms = _ranks(G, E, k, d, ff, max(tokens))
+    one = _single(E, k, d, ff, max(tokens))
+    for m in ms + [one]:
+        m.set_gate(0, gates[0])
+        for e, w in enumerate(experts):
+            m.load_expert(0, e, *w)
+    for m in ms:
+        m.set_placement(0, rc, rg)
+    xd = [torch.from_numpy(wl.tokens(tokens[r], d, E, 1, 90 + r).view(np.int16)).to(cuda) for r in range(G)]
+    yd = [torch.zeros((t, d), dtype=torch.int16, device=cuda) for t in tokens]
+    _parallel(ms, lambda r: ms[r].forward(0, xd[r], yd[r], MOE_PLAN_FIXED, 0))  # warm: placement tables in place
+    torch.cuda.synchronize()
+    gids = []
+    for r in range(G):
+        ms[r].graph_begin()
+        ms[r].forward(0, xd[r], yd[r], MOE_PLAN_FIXED, 0)
+        gids.append(ms[r].graph_end())
+    for it in (1, 2, 0, 1):
+        for m in ms + [one]:
+            m.set_gate_device(0, gd[it])
+        _parallel(ms, lambda r: ms[r].graph_launch(gids[r]))
+        torch.cuda.synchronize()
+        for r in range(G):
+            y1 = torch.zeros_like(yd[r])
+            one.forward(0, xd[r], y1, MOE_PLAN_FIXED, it)
+            one.sync()
+            assert torch.equal(yd[r], y1), (it, r)
+    for m in ms + [one]:
+        m.close()
