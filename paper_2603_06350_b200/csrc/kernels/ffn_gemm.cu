@@ -452,6 +452,80 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #ifndef MOE_EPI_NOSTORE
 #define MOE_EPI_NOSTORE 0  // 1: skip the global stores (A/B of the epilogue's cost only; wrong outputs)
 #endif
+// Line-coalesced form (stage: this warp's 32 x 144 B shared-memory staging
+// rows): per 64 output columns every lane parks its row's 128 bytes in smem,
+// then each store instruction writes 4 whole 128-byte row segments (8 lanes x
+// 16 B per row) instead of 32 half-sectors of 32 different rows: half the L2
+// write transactions, +1-2 % tokens/s at cfg2 (profiles/ab_epi_store_r02.md,
+// which also measures what GEMM2's output writes cost the board's clock).
+// Row stride 144 B: the row writes and the transposed reads are both
+// bank-conflict free per phase.
+constexpr uint32_t kStageRow = 144;
+constexpr uint32_t kStageWarp = 32 * kStageRow;  // bytes per epilogue warp
+#ifndef MOE_EPI_STAGED
+#define MOE_EPI_STAGED 1  // 0: direct per-lane row stores (A/B)
+#endif
+
+__device__ __forceinline__ void st_shared_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ int4 ld_shared_v4(uint32_t a) {
+  int4 r;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a) : "memory");
+  return r;
+}
+template <int EPI>
+__device__ __forceinline__ void store_accumulator_staged(uint32_t taddr, __nv_bfloat16* __restrict__ out, size_t grow,
+                                                         bool valid, int n, int out_ld, uint32_t stage) {
+  constexpr int kOutCols = EPI == EPI_SWIGLU ? BN / 2 : BN;
+  const int lane = lane_id();
+  const size_t grow0 = __shfl_sync(0xffffffffu, grow, 0);  // the warp's rows are grow0 + 0..31
+  const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+  __nv_bfloat16* dst0 = out + grow0 * out_ld + n * kOutCols;
+  const uint32_t my_row = stage + lane * kStageRow;
+  const int jr = lane >> 3, c = lane & 7;  // read side: row 4 i + jr, 16-byte chunk c
+#pragma unroll 1
+  for (int g = 0; g < kOutCols / 64; ++g) {
+    uint32_t packed[32];
+    if constexpr (EPI == EPI_SWIGLU) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t gt[32], up[32];
+        tmem_ld_32x32b_x32(taddr + (2 * g + h) * 32, gt);
+        tmem_ld_32x32b_x32(taddr + BN / 2 + (2 * g + h) * 32, up);
+        tc_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float h0 = silu(__uint_as_float(gt[2 * i])) * __uint_as_float(up[2 * i]);
+          const float h1 = silu(__uint_as_float(gt[2 * i + 1])) * __uint_as_float(up[2 * i + 1]);
+          packed[16 * h + i] = pack_bf16(h0, h1);
+        }
+      }
+    } else {
+      uint32_t r0[32], r1[32];
+      tmem_ld_32x32b_x32(taddr + g * 64, r0);
+      tmem_ld_32x32b_x32(taddr + g * 64 + 32, r1);
+      tc_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        packed[i] = pack_bf16(__uint_as_float(r0[2 * i]), __uint_as_float(r0[2 * i + 1]));
+        packed[16 + i] = pack_bf16(__uint_as_float(r1[2 * i]), __uint_as_float(r1[2 * i + 1]));
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+      st_shared_v4(my_row + 16 * v, packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int j = 4 * i + jr;
+      const int4 w = ld_shared_v4(stage + j * kStageRow + 16 * c);
+      if (((vmask >> j) & 1u) && !MOE_EPI_NOSTORE) st_v4(dst0 + static_cast<size_t>(j) * out_ld + g * 64 + c * 8, w);
+    }
+    __syncwarp();  // the next group overwrites the staging rows
+  }
+}
+
 template <int EPI>
 __device__ __forceinline__ void store_accumulator(uint32_t taddr, __nv_bfloat16* __restrict__ out, size_t grow,
                                                   bool valid, int n, int out_ld) {
@@ -737,7 +811,8 @@ struct SmemLayout2 {
   static constexpr uint32_t tile_ring = tmem_slot + 16;              // int[kTileRing]
   static constexpr uint32_t seg_tiles = tile_ring + kTileRing * 4;
   static constexpr uint32_t segs = seg_tiles + (kMaxSegs + 1) * 4 + 12;
-  static constexpr uint32_t end = ((segs + 15) / 16) * 16 + kMaxSegs * 16;
+  static constexpr uint32_t epi_stage = ((segs + 15) / 16) * 16 + kMaxSegs * 16;  // 4 epilogue warps
+  static constexpr uint32_t end = epi_stage + 4 * kStageWarp;
 };
 constexpr uint32_t kSmemBytes2 = SmemLayout2::end + 1024;
 static_assert(kSmemBytes2 <= 232448, "smem budget (2-CTA)");
@@ -925,7 +1000,11 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
-      store_accumulator<EPI>(taddr, out, static_cast<size_t>(sg.x + row), row < sg.y, c.n, out_ld);
+      if (MOE_EPI_STAGED)
+        store_accumulator_staged<EPI>(taddr, out, static_cast<size_t>(sg.x + row), row < sg.y, c.n, out_ld,
+                                      smem_u32(smem + SmemLayout2::epi_stage) + (warp - 2) * kStageWarp);
+      else
+        store_accumulator<EPI>(taddr, out, static_cast<size_t>(sg.x + row), row < sg.y, c.n, out_ld);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
