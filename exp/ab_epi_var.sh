@@ -1,5 +1,7 @@
 #!/bin/bash
 # 2-SM K4 epilogue variants under ncu: time, SM clock, tensor-pipe activity, DRAM bytes
+# (the diagnostic flags of session 4 — MOE_EPI_SCRATCH, MOE_DIAG_A_SAME / B_SAME, MOE_DIAG_RED, MOE_EPI_STREAM,
+#  MOE_EPI_PACE_NS — were removed from ffn_gemm.cu after the runs; results in profiles/ab_epi_store_r02.md)
 o=gpurun_out/$1; mkdir -p $o; : > $o/ab.txt
 for fl in "-DMOE_EPI_STAGED=1" "-DMOE_EPI_SCRATCH=4" "-DMOE_EPI_STAGED=1" "-DMOE_EPI_SCRATCH=4"; do
   touch paper_2603_06350_b200/csrc/kernels/ffn_gemm.cu
