@@ -660,6 +660,11 @@ def main():
     if args.workload != "cfg2":
         CFG, WORKLOAD = OTHER_WORKLOADS[args.workload]
     if args.impl == "reference":
+        # all host threads for the CPU path: torchrun (N > 1) exports OMP_NUM_THREADS=1 to every
+        # rank, and only rank 0 runs this arm; set before numpy / OpenBLAS / the oracle load
+        threads = os.environ.get("MOE_REF_THREADS") or str(os.cpu_count() or 1)
+        for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
+            os.environ[var] = threads
         return run_reference(args)
     return run_ours(args)
 
