@@ -369,8 +369,12 @@ __device__ __forceinline__ uint32_t tc_token_topk(const uint32_t (&r)[32], const
   uint64_t key[W];
 #pragma unroll
   for (int c = 0; c < W; ++c) {
+    if (c >= E) {
+      key[c] = 0ull;  // out of the race
+      continue;
+    }
     const float v = gi == 0 ? __uint_as_float(r[c]) : row[gi * E + c];
-    key[c] = c < E ? (static_cast<uint64_t>(logit_key(v)) << 32) | static_cast<uint32_t>(W - 1 - c) : 0ull;
+    key[c] = (static_cast<uint64_t>(logit_key(v)) << 32) | static_cast<uint32_t>(W - 1 - c);
   }
   uint32_t chosen = 0;
 #pragma unroll
