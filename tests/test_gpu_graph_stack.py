@@ -99,3 +99,45 @@ def test_graph_capture_errors(cuda):
     m.forward(0, x, y, MOE_PLAN_FIXED, 1, stats=True)  # eager forwards still work after a capture
     torch.cuda.synchronize()
     m.close()
+
+
+@pytest.mark.parametrize("T,mlp", [(256, False), (256, True), (8192, False)])
+def test_graph_with_fused_predictor(cuda, T, mlp):
+    """Layers whose gate kernel also scores the layer-aware predictor (K2: a
+    linear slot, or an MLP slot) replay as one graph bit-identically to eager
+    forwards, predictor histograms included (decode front end at T = 256, the
+    tcgen05 prefill gate at T = 8192)."""
+    import torch
+    E, k, d, ff, n_layers = 16, 2, 1024, 256, 2
+    rng = np.random.default_rng(5)
+    m = MoELayer(n_layers, E, k, d, ff, max_tokens=T, num_predictor_targets=1)
+    for l in range(n_layers):
+        m.set_gate(l, wl.gate_weights(E, d, 1.2, 1, l, 0))
+        wp = wl.gate_weights(E, d, 1.2, 1, 10 + l, 0)
+        if mlp:
+            m.set_predictor_mlp(l, 0, wp, rng.standard_normal((E, E)).astype(np.float32))
+        else:
+            m.set_predictor(l, 0, wp)
+        for e in range(E):
+            m.load_expert(l, e, *wl.expert_weights(d, ff, 1, l, e))
+    xd = [torch.from_numpy(wl.tokens(T, d, E, 1, 40 + l).view(np.int16)).to(cuda) for l in range(n_layers)]
+
+    def run(graph):
+        ys = [torch.zeros((T, d), dtype=torch.int16, device=cuda) for _ in range(n_layers)]
+        if graph:
+            m.graph_begin()
+        for l in range(n_layers):
+            m.forward(l, xd[l], ys[l], MOE_PLAN_FIXED, 0)
+        if graph:
+            m.graph_launch(m.graph_end())
+        torch.cuda.synchronize()
+        counts = m.read_buffer(7, np.int32, (2 * E,)).copy()  # the last layer's gate + predictor histograms
+        return [y.cpu().numpy().copy() for y in ys], counts
+
+    ye, ce = run(False)
+    yg, cg = run(True)
+    for l in range(n_layers):
+        assert np.array_equal(ye[l], yg[l]), l
+    assert np.array_equal(ce, cg)
+    assert ce[E:].sum() == T * k  # the predictor slot's histogram covers every token
+    m.close()
