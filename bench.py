@@ -201,7 +201,9 @@ def single_gpu_launches(T, k, E, d=4096):
         return 1 + k4 + 1 + prefetch
     tc_gate = T >= 8192 and d % 256 == 0  # tcgen05 gate (+ its side-stream histogram copy to the host)
     split = not tc_gate and nblk * 4 <= 2 * 148  # small batches split K (+ finish kernel)
-    return 1 + (1 if tc_gate else 0) + split + 1 + 1 + k4 + 1 + prefetch
+    # top-2 on the 2-SM kernel: GEMM2 writes y itself (FusedY), no combine launch
+    combine = 0 if (not swap and k == 2 and os.environ.get("MOE_FUSED_Y", "1") != "0") else 1
+    return 1 + (1 if tc_gate else 0) + split + 1 + 1 + k4 + combine + prefetch
 
 
 PLANNER = {"sync": "MOE_PLAN_SYNC (scale_experts + place_experts on actual loads)",

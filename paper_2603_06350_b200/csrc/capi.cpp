@@ -258,7 +258,7 @@ int use_swap(const moe_ctx* c, int T) {
 }
 
 void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t rows = 0, bool gather = false,
-                     uint16_t* fused_y = nullptr) {
+                     uint16_t* fused_y = nullptr, uint16_t* y2 = nullptr) {
   Layer& L = c->layers[layer];
   const int sn = gather || fused_y ? 0 : use_swap(c, c->gemm_T);
   if (sn) {
@@ -310,7 +310,8 @@ void launch_ffn_gemm(moe_ctx* c, int layer, int which, cudaStream_t s, int64_t r
     else
       CU_CHECK(launch_grouped_gemm_2sm(1, &c->tmA2, &L.tmB2h, c->dplan.p->segs, &c->dplan.p->nseg, c->d, c->ff, c->d,
                                        reinterpret_cast<__nv_bfloat16*>(c->yp.p), c->d, c->num_sms, s, c->use_pdl,
-                                       c->group_m[1], c->sched_2sm() ? c->gemm_sched.p + 2 : nullptr));
+                                       c->group_m[1], c->sched_2sm() ? c->gemm_sched.p + 2 : nullptr,
+                                       c->row_owner.p, c->wts.p, reinterpret_cast<__nv_bfloat16*>(y2), c->comb_cnt.p));
     return;
   }
   if (m256) {
@@ -400,6 +401,15 @@ void flush_pending_plan(moe_ctx* c) {
   if (c->pending.gemm_slot >= 0) c->gemm_rows[c->pending.gemm_slot] = c->plan.rows_local;
 }
 
+// GEMM2 writes y itself (combine fused, FusedY in ffn_gemm.cu): top-2 on one
+// GPU on the 2-SM prefill kernel — the same conditions launch_ffn_gemm uses to
+// pick that kernel, decided once per forward for dispatch, GEMM2 and combine.
+bool fused_y_2sm(moe_ctx* c, int T, bool gather, bool fused) {
+  return c->fuse_y && c->G == 1 && !c->p2p && !c->fp32 && c->k == 2 && T > 0 && !gather && !fused &&
+         !c->ext_route && (c->gemm_variant == 0 || c->gemm_variant == 2) && use_swap(c, T) == 0 &&
+         static_cast<int64_t>(T) <= c->Tmax;
+}
+
 // Enqueue one forward.  Three planning paths:
 //   local : G == 1 — the device builds the dispatch plan from its own
 //           histogram (plan_local_kernel);
@@ -448,6 +458,8 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   const bool front = c->frontend && c->G == 1 && !c->fp32 && !c->ext_route && !gather && !fused && L.has_gate &&
                      frontend_applies(T, c->d, Etot, c->k, c->num_sms);
   const bool inline_prefetch = prefetch && front && c->front_prefetch_inline;
+  // (the fused front end does not write the row owners the fused GEMM2 epilogue reads)
+  const bool fy = !front && fused_y_2sm(c, T, gather, fused);
   if (prefetch && !inline_prefetch) {
     CU_CHECK(cudaEventRecord(c->ev_pf_fork, s));
     CU_CHECK(cudaStreamWaitEvent(c->pstream, c->ev_pf_fork, 0));
@@ -507,7 +519,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
       mark(1);
       if (c->G > 1) CU_CHECK(launch_plan_exchange(c->counts_all.p, stride, c->G, c->rank, L.ptab.p, c->dplan.p, s));
       mark(2);
-      stage_dispatch(c, x, T, s, /*upload_plan=*/false, gather, fused, /*local_plan=*/c->G == 1);
+      stage_dispatch(c, x, T, s, /*upload_plan=*/false, gather, fused || fy, /*local_plan=*/c->G == 1);
     } else {
       mark(1);
       CU_CHECK(cudaStreamSynchronize(s));  // the host plans on the real histogram
@@ -533,7 +545,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   // then timed as one interval, reported as GEMM1 with GEMM2 = 0)
   if (!capturing && !c->use_pdl) CU_CHECK(cudaEventRecord(c->gemm_ev[gslot][1], s));
   mark(5);
-  launch_ffn_gemm(c, layer, 1, s, rows, false, fused ? y : nullptr);
+  launch_ffn_gemm(c, layer, 1, s, rows, false, fused ? y : nullptr, fy ? y : nullptr);
   // (after GEMM2, not between the GEMMs: an event there would serialise the PDL pair)
   if (x_consumed && gather) CU_CHECK(cudaEventRecordWithFlags(x_consumed, s, rec));
   if (c->placed) {  // the layer's slots may be overwritten once these GEMMs are done
@@ -548,7 +560,7 @@ void enqueue_forward(moe_ctx* c, Layer& L, int layer, const uint16_t* x, int T, 
   mark(6);
   stage_exchange(c, false, s);
   mark(7);
-  if (!fused && !c->skip_combine) stage_combine(c, y, T, s);
+  if (!fused && !fy && !c->skip_combine) stage_combine(c, y, T, s);
   if (prefetch || front || side_mirror) CU_CHECK(cudaStreamWaitEvent(s, c->ev_pf_join, 0));  // the side stream rejoins
   mark(8);
   if (deferred && !capturing) c->pending = PendingPlan{true, layer, plan_mode, iteration, stride, ahead ? gslot : -1};

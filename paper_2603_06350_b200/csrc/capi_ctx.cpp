@@ -274,6 +274,7 @@ int moe_ctx_create(const moe_ctx_desc* desc, moe_ctx** out) {
     if (const char* v = std::getenv("MOE_PDL")) c->use_pdl = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_GATHER")) c->gather = std::string(v) == "1";
     if (const char* v = std::getenv("MOE_FUSED_COMBINE")) c->fuse_combine = std::string(v) == "1";
+    if (const char* v = std::getenv("MOE_FUSED_Y")) c->fuse_y = std::string(v) != "0";
     if (const char* v = std::getenv("MOE_GEMM_GROUP_M")) std::sscanf(v, "%d,%d", &c->group_m[0], &c->group_m[1]);
     if (const char* v = std::getenv("MOE_GEMM_VARIANT")) {
       const std::string s(v);

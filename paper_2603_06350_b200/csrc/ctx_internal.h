@@ -101,7 +101,9 @@ cudaError_t launch_grouped_gemm_m256(int epi, const CUtensorMap* tmA, const CUte
 cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                     __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl = false,
-                                    int group_m = 0, int* sched = nullptr);
+                                    int group_m = 0, int* sched = nullptr, const int32_t* fy_row_owner = nullptr,
+                                    const float* fy_wts = nullptr, __nv_bfloat16* fy_y = nullptr,
+                                    int32_t* fy_cnt = nullptr);
 cudaError_t launch_grouped_gemm_mc(int epi, const CUtensorMap* tmA, const CUtensorMap* tmBh, const GemmSeg* segs,
                                    const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                    __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl,
@@ -381,6 +383,7 @@ struct moe_ctx {
   // short-K shapes (the late rows' sums serialise on 4 epilogue warps),
   // profiles/ab_fused_combine_r01.md
   bool fuse_combine = false;
+  bool fuse_y = true;  // 2-SM GEMM2 writes y directly at top-2 on one GPU (MOE_FUSED_Y=0: yp + combine kernel)
   bool skip_combine = false;  // MOE_DEBUG_SKIP_COMBINE=1: timing experiments only (y is not written)
   DevBuf<unsigned> gate_ticket;  // CTAs of the gate grid done (histogram mirror, self-resetting)
   DevBuf<int32_t> row_owner;  // [rows_cap] row -> t * k + j

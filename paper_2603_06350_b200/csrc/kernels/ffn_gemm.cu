@@ -526,6 +526,120 @@ __device__ __forceinline__ void store_accumulator_staged(uint32_t taddr, __nv_bf
   }
 }
 
+// GEMM2 with the combine fused for top-2 on one GPU (FusedY, MOE_FUSED_Y): no
+// expert-output rows (yp) are written and no combine kernel runs.  Of a
+// token's two rows, the first to reach its (token, n tile) counter parks its
+// bf16 output (the value yp would hold) in y[t]; the second waits for it and
+// writes fmaf(w1, v1, fmaf(w0, v0, 0)) in slot order — the combine kernel's
+// arithmetic on the same bf16 rows, so y is bit-identical to the unfused path
+// whichever row arrives first.  GEMM2's written footprint halves
+// (profiles/ab_epi_store_r02.md).  Two passes over the tile's columns: first
+// arrivals park and publish (+2) without waiting; only then do second
+// arrivals wait — every awaited publish comes from an epilogue that waits for
+// nothing, so no cycle of waits can form.  The second arrival resets the
+// counter for the next forward.
+struct FusedY {
+  const int32_t* row_owner;  // [rows] t * 2 + slot (dispatch)
+  const float* wts;          // [T * 2] routing weights
+  __nv_bfloat16* y;          // [T, d]
+  int32_t* cnt;              // [T * n_tiles], zero between forwards
+  int d, n_tiles;
+};
+__device__ __forceinline__ int4 ld_cg_v4(const void* p) {
+  int4 r;
+  asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ int ld_acquire_gpu_i32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void store_fused_y(uint32_t taddr, size_t grow, bool valid, int n, uint32_t stage,
+                                              const FusedY& fy) {
+  const int lane = lane_id();
+  int t = 0, slot = 0;
+  float w0 = 0.0f, w1 = 0.0f;
+  bool first = false;
+  int32_t* cnt = nullptr;
+  if (valid) {
+    const int own = __ldg(fy.row_owner + grow);
+    t = own >> 1;
+    slot = own & 1;
+    w0 = __ldg(fy.wts + 2 * t);
+    w1 = __ldg(fy.wts + 2 * t + 1);
+    cnt = fy.cnt + static_cast<size_t>(t) * fy.n_tiles + n;
+    first = atomicAdd(cnt, 1) == 0;
+  }
+  const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+  const uint32_t fmask = __ballot_sync(0xffffffffu, first);
+  const uint32_t my_row = stage + lane * kStageRow;
+  const int jr = lane >> 3, c = lane & 7;
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      // publish the first arrivals (all lanes' stores before the owners' release), then wait
+      __threadfence();
+      __syncwarp();
+      if (valid && first) asm volatile("red.release.gpu.global.add.s32 [%0], 2;" ::"l"(cnt) : "memory");
+      if (valid && !first)
+        while (ld_acquire_gpu_i32(cnt) < 4) __nanosleep(64);
+      __syncwarp();
+    }
+    const uint32_t mine = pass == 0 ? (vmask & fmask) : (vmask & ~fmask);
+    if (mine == 0u) continue;
+#pragma unroll 1
+    for (int g = 0; g < BN / 64; ++g) {
+      uint32_t r0[32], r1[32];
+      tmem_ld_32x32b_x32(taddr + g * 64, r0);
+      tmem_ld_32x32b_x32(taddr + g * 64 + 32, r1);
+      tc_wait_ld();
+      uint32_t packed[32];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        packed[i] = pack_bf16(__uint_as_float(r0[2 * i]), __uint_as_float(r0[2 * i + 1]));
+        packed[16 + i] = pack_bf16(__uint_as_float(r1[2 * i]), __uint_as_float(r1[2 * i + 1]));
+      }
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        st_shared_v4(my_row + 16 * v, packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int j = 4 * i + jr;
+        const int tj = __shfl_sync(0xffffffffu, t, j);
+        const int sj = __shfl_sync(0xffffffffu, slot, j);
+        const float a0 = __shfl_sync(0xffffffffu, w0, j), a1 = __shfl_sync(0xffffffffu, w1, j);
+        if ((mine >> j) & 1u) {
+          int4 v4 = ld_shared_v4(stage + j * kStageRow + 16 * c);
+          __nv_bfloat16* dst = fy.y + static_cast<size_t>(tj) * fy.d + n * BN + g * 64 + c * 8;
+          if (pass == 1) {  // slot order: the parked row is the other slot's
+            const int4 o = ld_cg_v4(dst);
+            const uint32_t own4[4] = {static_cast<uint32_t>(v4.x), static_cast<uint32_t>(v4.y),
+                                      static_cast<uint32_t>(v4.z), static_cast<uint32_t>(v4.w)};
+            const uint32_t park4[4] = {static_cast<uint32_t>(o.x), static_cast<uint32_t>(o.y),
+                                       static_cast<uint32_t>(o.z), static_cast<uint32_t>(o.w)};
+            uint32_t res[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t s0 = sj == 0 ? own4[q] : park4[q], s1 = sj == 0 ? park4[q] : own4[q];
+              const float lo = fmaf(a1, bf16lo(s1), fmaf(a0, bf16lo(s0), 0.0f));
+              const float hi = fmaf(a1, bf16hi(s1), fmaf(a0, bf16hi(s0), 0.0f));
+              res[q] = pack_bf16(lo, hi);
+            }
+            v4 = make_int4(static_cast<int>(res[0]), static_cast<int>(res[1]), static_cast<int>(res[2]),
+                           static_cast<int>(res[3]));
+          }
+          st_v4(dst, v4);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  if (valid && !first) *cnt = 0;  // the pair is closed: ready for the next forward
+}
+
 template <int EPI>
 __device__ __forceinline__ void store_accumulator(uint32_t taddr, __nv_bfloat16* __restrict__ out, size_t grow,
                                                   bool valid, int n, int out_ld) {
@@ -822,7 +936,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const GemmSeg* __restrict__ segs_g, const int* __restrict__ nseg_g, int n_total, int k_total,
                         int b_rows_per_slot, __nv_bfloat16* __restrict__ out, int out_ld, int group_m, int l2pol,
-                        int* __restrict__ sched) {
+                        int* __restrict__ sched, const __grid_constant__ FusedY fy) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout2::bars);
@@ -1000,7 +1114,10 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
-      if (MOE_EPI_STAGED)
+      if (EPI == EPI_STORE && fy.y)
+        store_fused_y(taddr, static_cast<size_t>(sg.x + row), row < sg.y, c.n,
+                      smem_u32(smem + SmemLayout2::epi_stage) + (warp - 2) * kStageWarp, fy);
+      else if (MOE_EPI_STAGED)
         store_accumulator_staged<EPI>(taddr, out, static_cast<size_t>(sg.x + row), row < sg.y, c.n, out_ld,
                                       smem_u32(smem + SmemLayout2::epi_stage) + (warp - 2) * kStageWarp);
       else
@@ -1617,7 +1734,9 @@ static_assert(kSmemBytes <= 232448, "smem budget");
 cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmSeg* segs,
                                     const int* nseg, int n_total, int k_total, int b_rows_per_slot,
                                     __nv_bfloat16* out, int out_ld, int num_ctas, cudaStream_t stream, bool pdl,
-                                    int group_m, int* sched) {
+                                    int group_m, int* sched, const int32_t* fy_row_owner, const float* fy_wts,
+                                    __nv_bfloat16* fy_y, int32_t* fy_cnt) {
+  const FusedY fy{fy_y ? fy_row_owner : nullptr, fy_wts, fy_y, fy_cnt, n_total, n_total / BN};
   if (n_total % BN || k_total % BK) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_ctas & ~1);
@@ -1634,9 +1753,9 @@ cudaError_t launch_grouped_gemm_2sm(int epi, const CUtensorMap* tmA, const CUten
   const int l2pol = pol >= 0 ? (epi == EPI_SWIGLU ? pol & 15 : (pol >> 4) & 15) : 1 << 2;
   if (epi == EPI_SWIGLU)
     return cudaLaunchKernelEx(&cfg, grouped_gemm_2sm_kernel<EPI_SWIGLU>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                              b_rows_per_slot, out, out_ld, gp, l2pol, sched);
+                              b_rows_per_slot, out, out_ld, gp, l2pol, sched, FusedY{});
   return cudaLaunchKernelEx(&cfg, grouped_gemm_2sm_kernel<EPI_STORE>, *tmA, *tmB, segs, nseg, n_total, k_total,
-                            b_rows_per_slot, out, out_ld, gp, l2pol, sched);
+                            b_rows_per_slot, out, out_ld, gp, l2pol, sched, fy);
 }
 
 cudaError_t launch_grouped_gemm_mc(int epi, const CUtensorMap* tmA, const CUtensorMap* tmBh, const GemmSeg* segs,
