@@ -582,8 +582,17 @@ __device__ __forceinline__ void store_fused_y(uint32_t taddr, size_t grow, bool 
       __threadfence();
       __syncwarp();
       if (valid && first) asm volatile("red.release.gpu.global.add.s32 [%0], 2;" ::"l"(cnt) : "memory");
-      if (valid && !first)
-        while (ld_acquire_gpu_i32(cnt) < 4) __nanosleep(64);
+      if (valid && !first) {
+        // bounded: a counter left non-zero by an aborted forward must fail loudly, not hang
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while (ld_acquire_gpu_i32(cnt) < 4) {
+          __nanosleep(64);
+          unsigned long long t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          if (t1 - t0 > 2000000000ull) __trap();
+        }
+      }
       __syncwarp();
     }
     const uint32_t mine = pass == 0 ? (vmask & fmask) : (vmask & ~fmask);
