@@ -10,6 +10,7 @@
   gatetcpred the tcgen05 gate with a linear predictor slot (tree top-k over the smem row)
   2smbig   the 2-SM K4 on 256-row tiles with staged epilogue stores (mean rows > 1024)
   graph    two forwards recorded as one CUDA graph (moe_graph_begin/end) and replayed
+  fusedy   top-2 prefill on the 2-SM K4 with the combine fused into GEMM2 (> 148 blocks)
   python profiles/sanitize_forward_r02.py <scenario>"""
 import os
 import sys
@@ -33,6 +34,8 @@ if scenario in ("gatetc", "gatetcpred"):
     T = 8192 + 17
 if scenario == "2smbig":
     d, ff, T = 512, 256, 4096 + 40
+if scenario == "fusedy":
+    d, ff, T = 512, 256, 8192 + 40
 if scenario == "threek":
     os.environ["MOE_FRONTEND"] = "0"
 npred = 2 if scenario == "frontpred" else (1 if scenario == "gatetcpred" else 0)
