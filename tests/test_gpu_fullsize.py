@@ -14,6 +14,8 @@ the C-ABI (straggler replicas added by the host planner):
     cfg5): max_c |y[t,c] - y_ref[t,c]| / max_c |y_ref[t,c]| for every sampled
     token t, against the oracle that mirrors the device's bf16 rounding of h.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -42,7 +44,7 @@ def check_plan(m, counts, E):
     assert rows_local == int(counts.sum())
 
 
-def _run(cuda, E, k, d, ff, T, extra, s, sample, seed=1, iteration=7):
+def _run(cuda, E, k, d, ff, T, extra, s, sample, seed=1, iteration=7, compare_unfused=False):
     import torch
     mem = 3.0 * d * ff * 2 / 1e6
     m = MoELayer(1, E, k, d, ff, max_tokens=T, expert_mem_mb=mem, layer_mem_cap_mb=extra * mem)
@@ -83,16 +85,30 @@ def _run(cuda, E, k, d, ff, T, extra, s, sample, seed=1, iteration=7):
     err = row_rel_err(y[idx], y_ref)
     assert float(err.max()) <= TOL_ROW, (float(err.max()), int(idx[int(err.argmax())]))
     m.close()
+    if compare_unfused:  # the same forward through expert-output rows + the combine kernel
+        os.environ["MOE_FUSED_Y"] = "0"
+        try:
+            m2 = MoELayer(1, E, k, d, ff, max_tokens=T, expert_mem_mb=mem, layer_mem_cap_mb=extra * mem)
+        finally:
+            del os.environ["MOE_FUSED_Y"]
+        m2.set_gate(0, wg)
+        for e, w in enumerate(experts):
+            m2.load_expert(0, e, *w)
+        y2 = torch.zeros((T, d), dtype=torch.int16, device=cuda)
+        m2.forward(0, xd, y2, MOE_PLAN_SYNC, iteration)
+        torch.cuda.synchronize()
+        assert torch.equal(y2, yd), "fused-combine GEMM2 differs from the combine kernel"
+        m2.close()
     return st, rc
 
 
 def test_cfg2_mixtral_full(cuda):
-    st, rc = _run(cuda, E=8, k=2, d=4096, ff=14336, T=16384, extra=4, s=1.2, sample=1024)
+    st, rc = _run(cuda, E=8, k=2, d=4096, ff=14336, T=16384, extra=4, s=1.2, sample=1024, compare_unfused=True)
     assert st.replica_count > 8 and int(rc.max()) > 1  # the planner added straggler replicas
 
 
 def test_cfg3_phi_shape_single_gpu(cuda):
-    _run(cuda, E=16, k=2, d=4096, ff=6400, T=16384, extra=8, s=1.2, sample=1024)
+    _run(cuda, E=16, k=2, d=4096, ff=6400, T=16384, extra=8, s=1.2, sample=1024, compare_unfused=True)
 
 
 @pytest.mark.parametrize("s", [1.2, 2.0])
